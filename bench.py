@@ -1,0 +1,329 @@
+#!/usr/bin/env python3
+"""bench.py -- sntrup761 batch key generation on B200 (BASELINE.json configs[1]).
+
+One step = one call of the whole hot path (sample, isInvertible, R/3 batchInv, R/q batchInv,
+H = g * fbar, encode pk/sk) for 65,536 keys (sntrup761, seed 2).  Prints ONE JSON line (rank 0).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--batch-size B] [--impl ours|reference]
+
+N > 1 is launched by torchrun: rank r generates global keys [r*n, (r+1)*n) (weak scaling, no
+collective on the data path); the step time is the max over ranks (device events).
+--impl reference times the CPU oracle (oracle/, the test-infrastructure implementation) on the
+same metric, on bounded samples.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PARAM = 761
+N_KEYS = 65536
+SEED = 2
+METRIC = "sntrup761 keys/sec per B200 (batched keygen); Rq mults/sec; int-pipe % of peak"
+UNIT = "keys/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--batch-size", type=int, default=0, help="Montgomery batch size B (0 = tuned default)")
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-extras", action="store_true", help="skip B sweep / rq_mul / cpu baseline")
+    return ap.parse_args()
+
+
+DEFAULT_B = 128
+
+
+# ----------------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
+    FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.active",
+              "clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thr = threading.Thread(target=self._read, daemon=True)
+            self.thr.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == len(self.FIELDS):
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        res = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": len(self.rows)}
+        if not self.rows:
+            return res
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        res["sm_mhz"] = statistics.median(sm) if sm else None
+        res["sm_max_mhz"] = max(mx) if mx else None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for k, name in enumerate(names):
+                if r[4 + k].lower().startswith("active"):
+                    reasons.add(name)
+        res["reasons"] = sorted(reasons)
+        return res
+
+
+# ----------------------------------------------------------------------------------- helpers
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def int_peak_macs_per_s(sm_mhz: float, n_sm: int = 148) -> float:
+    # integer multiply-add (IMAD) issues on the FMA pipe at 64 lanes/clk/SM
+    # (B200_PROFILING / B300_MICROARCH: FMA pipe rt_SMSP = 2 -> 16 lanes/clk/SMSP).
+    return 64.0 * n_sm * sm_mhz * 1e6
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def oracle_keygen_rate(target_s: float = 10.0):
+    """The oracle as it stands, all host cores, parallel over keys only, bounded sample."""
+    import numpy as np
+    from oracle import oracle as O
+    threads = os.cpu_count() or 1
+    n0 = max(threads * 8, 64)
+    t = time.perf_counter()
+    O.keygen_many(PARAM, SEED, np.arange(n0), threads=threads)
+    dt = time.perf_counter() - t
+    n = int(max(n0, min(200000, n0 * target_s / max(dt, 1e-3))))
+    t = time.perf_counter()
+    O.keygen_many(PARAM, SEED, np.arange(n), threads=threads)
+    dt = time.perf_counter() - t
+    return n / dt, threads, "keys 0..%d of configs[1] (sntrup761, seed 2), %d host threads, %.1f s" % (
+        n - 1, threads, dt)
+
+
+# ----------------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import numpy as np
+    from oracle import oracle as O
+    threads = os.cpu_count() or 1
+    # each step: a bounded sample of the workload (the oracle would need minutes for 65,536 keys)
+    n_step = max(64, threads * 16)
+    for i in range(args.warmup):
+        O.keygen_many(PARAM, SEED, np.arange(i * n_step, (i + 1) * n_step), threads=threads)
+    t = time.perf_counter()
+    for i in range(args.steps):
+        O.keygen_many(PARAM, SEED, np.arange(i * n_step, (i + 1) * n_step), threads=threads)
+    dt = time.perf_counter() - t
+    v = n_step * args.steps / dt
+    sample = "%d keys per step of configs[1] (sntrup761, seed 2), %d host threads (%s)" % (
+        n_step, threads, cpu_model())
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": "configs[1]: sntrup761 batch keygen, seed 2 (oracle sample)",
+                       "keys_per_step": n_step},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+# ----------------------------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2106_08759_b200 as S
+
+    P = S.params(PARAM)
+    B = args.batch_size or DEFAULT_B
+    n = N_KEYS
+    first = rank * n
+    stream = torch.cuda.current_stream()
+    pk = torch.empty((n, P["pk_bytes"]), dtype=torch.uint8, device="cuda")
+    sk = torch.empty((n, P["sk_bytes"]), dtype=torch.uint8, device="cuda")
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")   # > 126 MB L2
+
+    def step(batch=B):
+        S.batch_keygen(PARAM, n, SEED, first_key_index=first, batch_size=batch, pk_out=pk,
+                       sk_out=sk, flags=S.OPT_ASYNC)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(fn, steps):
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(steps)]
+        barrier()
+        for e0, e1 in ev:
+            flush.zero_()                       # L2 flush between timed iterations (not timed)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+        barrier()
+        ms = sum(e0.elapsed_time(e1) for e0, e1 in ev)
+        if world > 1:
+            t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- headline: K timed steps
+    launches0 = S.kernel_launch_count()
+    clk = ClockSampler(local)
+    clk.start()
+    ms = timed(step, args.steps)
+    clocks = clk.stop()
+    launches = S.kernel_launch_count() - launches0
+    value = world * n * args.steps / (ms / 1e3)
+
+    # ---- per-kernel breakdown (CUDA events on the launching stream, same K steps)
+    S.profile_enable(True)
+    ms_prof = timed(step, args.steps)
+    prof = S.profile_read(reset=True)
+    S.profile_enable(False)
+
+    # ---- e2e through the C ABI with HOST output buffers (D2H inside the timed region)
+    pk_h = torch.empty((n, P["pk_bytes"]), dtype=torch.uint8).pin_memory()
+    sk_h = torch.empty((n, P["sk_bytes"]), dtype=torch.uint8).pin_memory()
+
+    def step_host():
+        S.batch_keygen(PARAM, n, SEED, first_key_index=first, batch_size=B, pk_out=pk_h,
+                       sk_out=sk_h, flags=S.OPT_HOST_OUTPUT)
+
+    step_host()
+    barrier()
+    t0 = time.perf_counter()
+    ms_e2e = timed(step_host, max(1, args.steps // 2))
+    e2e_steps = max(1, args.steps // 2)
+    e2e_value = world * n * e2e_steps / (ms_e2e / 1e3)
+
+    result = {}
+    if rank == 0:
+        peaks = load_peaks()
+        sm_mhz = clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
+        # dominant kernel class by device time
+        dom = max(prof, key=lambda k: prof[k]["ms"])
+        tot_ms = sum(v["ms"] for v in prof.values())
+        p = P["p"]
+        macs = {"rq_mul": p * p, "r3_mul": p * p}
+        roof = None
+        if dom in macs:
+            per_launch_units = prof[dom]["units"] / max(1, prof[dom]["launches"])
+            avg_ms = prof[dom]["ms"] / max(1, prof[dom]["launches"])
+            achieved = per_launch_units * macs[dom] / (avg_ms / 1e3) / 1e12     # T MAC/s
+            peak = int_peak_macs_per_s(sm_mhz) / 1e12
+            roof = {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": peak,
+                    "unit": "TMAC/s (int32 multiply-accumulate, schoolbook p^2 per product)",
+                    "frac": achieved / peak, "traffic": None,
+                    "peak_source": "derived: 64 IMAD lanes/clk/SM x 148 SMs x %.0f MHz (median SM clock under load)" % sm_mhz,
+                    "share_of_step": prof[dom]["ms"] / tot_ms}
+        result = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": "configs[1]: sntrup761 batch keygen, 65,536 keys per GPU, seed 2",
+                       "keys_per_gpu": n, "batch_size": B, "param_set": PARAM,
+                       "l2": "flushed between timed steps (256 MiB write); working set > L2",
+                       "parallelism": "key ranges per GPU (no collective)"},
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": world * n * (P["pk_bytes"] + P["sk_bytes"])},
+            "roofline": roof,
+            "breakdown_ms_per_step": {k: v["ms"] / args.steps for k, v in prof.items() if v["launches"]},
+            "profiled_ms_per_step": ms_prof / args.steps,
+        }
+
+    if not args.no_extras and rank == 0:
+        # Montgomery batch-size sweep (configs[1])
+        sweep = {}
+        for b in (32, 128, 512, 2048):
+            step(b)
+            sweep[str(b)] = n * 3 / (timed(lambda: step(b), 3) / 1e3)
+        result["batch_size_sweep_keys_per_s"] = sweep
+        # R/q multiplication microbenchmark (configs[2]): 2^20 pairs, uniform x ternary(286)
+        from inputs import synth
+        npairs = 1 << 20
+        a = torch.from_numpy(synth.uniform_rq(npairs, p, P["q"], P["p8"], seed=3)).cuda()
+        bt = torch.from_numpy(synth.ternary_fast(npairs, p, P["w"], P["p8"], seed=3)).cuda()
+        c = torch.empty_like(a)
+        S.rq_mul_batch(PARAM, a, bt, c)
+        rq_ms = timed(lambda: S.rq_mul_batch(PARAM, a, bt, c), 3) / 3
+        result["rq_mul"] = {"value": npairs / (rq_ms / 1e3), "unit": "Rq mults/s",
+                            "config": "configs[2]: 2^20 pairs in Z/4591[x]/(x^761-x-1), uniform x ternary w=286",
+                            "ms": rq_ms}
+        del a, bt, c
+        # CPU baseline: the oracle on this host (bounded sample)
+        v, cores, sample = oracle_keygen_rate(10.0)
+        result["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                                  "sample": sample}
+    if rank == 0:
+        print(json.dumps(result))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

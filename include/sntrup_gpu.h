@@ -1,0 +1,147 @@
+/*
+ * sntrup_gpu.h -- C ABI of libsntrup_gpu.so: batched Streamlined NTRU Prime key generation and
+ * the ring primitives it is built from, as hand-written CUDA kernels for sm_100a (B200).
+ *
+ * Paper: arXiv 2106.08759 ("OpenSSLNTRU").  "P:N" cites line N of its LaTeX source.
+ *   KeyGen            P:3398-3461 (section 3.1): g small, invertible in R/3; f in Short;
+ *                     h = g/(3f) in R/q; output (h, (f, 1/g)).
+ *   BatchKeyGen       P:3597-3618 (Algorithm 1): the 2n inversions replaced by two batchInv.
+ *   batchInv          P:1432-1561 (section 2.2): Montgomery's trick, 3n-3 multiplications and
+ *                     one inversion for n inverses (here: level-parallel product trees).
+ *   isInvertible      P:3620-4070 (section 3.1.1): g mod f_i != 0 for every factor f_i of
+ *                     x^p - x - 1 over GF(3).
+ *   Rings             P:1361-1385 (section 2.1): R/3 = (Z/3)[x]/(x^p-x-1), R/q = (Z/q)[x]/(x^p-x-1),
+ *                     R/q a field; parameter sets P:1418-1430 plus 953/1013/1277 (Z20).
+ *
+ * Conventions ("readings"):
+ *   - param_set is p, one of {653, 761, 857, 953, 1013, 1277}; anything else -> SNTRUP_E_PARAM.
+ *   - R/q elements: int16 rows, coefficients centered in [-(q-1)/2, (q-1)/2], row stride
+ *     p8 = 8*ceil(p/8) elements.  R/3 / Small / Short elements: int8 rows in {-1,0,1}, row stride
+ *     p16 = 16*ceil(p/16) elements.  Pad lanes of inputs must be 0; pad lanes of outputs are
+ *     written 0.  Inputs outside the canonical range are a precondition violation (unchecked).
+ *   - pk = radix Rq-encode(h) (pk_bytes per key), sk = Small-encode(f) || Small-encode(1/g)
+ *     (sk_bytes = 2*ceil(p/4) per key); row strides are pk_bytes / sk_bytes (dense).
+ *   - Randomness: per-key SplitMix64 counter stream keyed by (seed, global key index), consumed
+ *     in the documented order (C2-C4).  Outputs depend only on (param_set, seed,
+ *     global key index): never on batch size, chunking or stream.
+ *   - Pointers are CUDA device pointers unless stated; the caller owns every buffer.  Calls are
+ *     stream-ordered on `stream` (NULL = legacy default stream) and return after enqueueing,
+ *     except where "synchronous" is stated.  The library keeps an internal cached workspace
+ *     (one per device and per stream) and constant tables; no other state.
+ *   - Errors: negative return codes below; CUDA failures -> SNTRUP_E_CUDA.  No call aborts.
+ */
+#ifndef SNTRUP_GPU_H
+#define SNTRUP_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    SNTRUP_OK = 0,
+    SNTRUP_E_PARAM = -1,          /* unknown param_set */
+    SNTRUP_E_ARG = -2,            /* n == 0, NULL required pointer, bad batch size */
+    SNTRUP_E_NOT_INVERTIBLE = -3, /* rq_recip_batch: some input is 0 (R/q is a field) */
+    SNTRUP_E_CUDA = -4,           /* a CUDA runtime call failed */
+    SNTRUP_E_WORKSPACE = -5,      /* device allocation failed */
+    SNTRUP_E_INTERNAL = -6        /* retry bound exceeded (g never invertible) */
+};
+
+/* Parameters of a set.  Any output pointer may be NULL.  Returns SNTRUP_OK or
+   SNTRUP_E_PARAM. */
+int sntrup_params(int param_set, int *p, int *q, int *w, int *p_pad16, int *p_pad8,
+                  size_t *pk_bytes, size_t *sk_bytes);
+
+/* Human-readable name of an error code (static string). */
+const char *sntrup_strerror(int code);
+
+/* Batch key generation (Algorithm 1) of n_keys key pairs with global key indices
+   0 .. n_keys-1 of stream `seed`, Montgomery batch size 32 (the paper's library default,
+   P:7187-7200).  pk_out: uint8[n_keys][pk_bytes], sk_out: uint8[n_keys][sk_bytes], device
+   pointers.  Synchronous (returns after the outputs are complete).  n_keys == 0 -> SNTRUP_E_ARG. */
+int sntrup_batch_keygen(int param_set, uint64_t n_keys, uint64_t seed,
+                        uint8_t *pk_out, uint8_t *sk_out);
+
+/* Option flags for sntrup_keygen_opts.flags */
+#define SNTRUP_OPT_HOST_OUTPUT    1u  /* pk_out/sk_out are HOST pointers (pinned recommended):
+                                         the library copies each chunk back as it completes */
+#define SNTRUP_OPT_NO_SMALL_CHECK 2u  /* test hook: skip the small-factor invertibility test in
+                                         the sampler, so every non-invertible g is caught by the
+                                         product-tree root check and repaired */
+#define SNTRUP_OPT_ASYNC          4u  /* do not synchronise before returning (device outputs) */
+
+typedef struct {
+    uint64_t first_key_index; /* keys first .. first+n-1 (chunked / resumable / multi-GPU runs) */
+    uint32_t batch_size;      /* B = keys per product tree, power of two in [1, 4096]; 0 -> 32 */
+    uint32_t flags;           /* SNTRUP_OPT_* */
+    uint64_t chunk_keys;      /* keys per internal chunk (0 -> library default, 65536 rounded to B) */
+    void *stream;             /* cudaStream_t; NULL -> legacy default stream */
+    int16_t *h_out;           /* optional device [n][p8]: centered public h */
+    int8_t *g_out;            /* optional device [n][p16]: accepted g */
+    int8_t *f_out;            /* optional device [n][p16]: f */
+    int8_t *ginv_out;         /* optional device [n][p16]: 1/g in R/3 */
+    uint8_t *attempts_out;    /* optional device [n]: number of g draws used (>= 1) */
+    uint64_t *stats_out;      /* optional HOST uint64[4]: ring products R/q, ring products R/3,
+                                 root inversions, keys repaired (trees whose R/3 root failed) */
+} sntrup_keygen_opts;
+
+/* Batch key generation with options (opt may be NULL = defaults). */
+int sntrup_batch_keygen_ex(int param_set, uint64_t n_keys, uint64_t seed,
+                           uint8_t *pk_out, uint8_t *sk_out, const sntrup_keygen_opts *opt);
+
+/* Device bytes the library will allocate internally for a keygen call of this shape. */
+size_t sntrup_keygen_workspace_bytes(int param_set, uint64_t n_keys, uint32_t batch_size);
+
+/* c[i] = a[i] * b[i] in R/q for i < n (the ring product of P:5339-5442: full product, then
+   reduction by x^p - x - 1, coefficients centered).  a, b, c: int16 [n][p8], no aliasing of c
+   with a or b.  Stream-ordered; returns after enqueueing. */
+int rq_mul_batch(int param_set, uint64_t n, const int16_t *a, const int16_t *b, int16_t *c,
+                 void *stream);
+
+/* c[i] = a[i] * b[i] in R/3: int8 [n][p16] rows in {-1,0,1}.  Stream-ordered. */
+int r3_mul_batch(int param_set, uint64_t n, const int8_t *a, const int8_t *b, int8_t *c,
+                 void *stream);
+
+/* out[i] = 1/a[i] in R/q (batchInv) using product trees of batch_size leaves
+   (0 -> 32), one constant-time divstep inversion per tree.  a, out: int16 [n][p8].
+   If some a[i] == 0: returns SNTRUP_E_NOT_INVERTIBLE, *bad_index (host pointer, may be NULL)
+   = the smallest such i, and out is unspecified.  Synchronous. */
+int rq_recip_batch(int param_set, uint64_t n, const int16_t *a, int16_t *out,
+                   uint32_t batch_size, uint64_t *bad_index, void *stream);
+
+/* out[i] = 1/g[i] in R/3 for invertible g[i] (ok[i] = 1); non-invertible g[i] (ok[i] = 0,
+   out[i] = 0).  Non-invertibility is a normal outcome, not an error.  g, out: int8 [n][p16];
+   ok: uint8 [n] (device).  Synchronous. */
+int r3_recip_batch(int param_set, uint64_t n, const int8_t *g, int8_t *out, uint8_t *ok,
+                   uint32_t batch_size, void *stream);
+
+/* isInvertible for n elements of R/3: ok[i] = 1 iff g[i] is a unit.
+   Synchronous. */
+int r3_is_invertible_batch(int param_set, uint64_t n, const int8_t *g, uint8_t *ok, void *stream);
+
+/* pk[i] = Rq-encode(h[i]) (radix encoding, C10): h int16 [n][p8] -> uint8 [n][pk_bytes].
+   Stream-ordered. */
+int rq_encode_batch(int param_set, uint64_t n, const int16_t *h, uint8_t *pk, void *stream);
+
+/* Release the cached device workspaces (all streams). */
+void sntrup_release_workspace(void);
+
+/* Number of kernels this library launched since load (device work only; for bench accounting). */
+uint64_t sntrup_kernel_launch_count(void);
+
+/* Measurement hooks (bench.py).  When enabled, every kernel launch is bracketed by CUDA events
+   recorded on its launching stream.  sntrup_profile_read() waits for the recorded events and
+   returns, per kernel class, the summed device milliseconds, the summed work units and the
+   launch count (classes: 0 sample [keys], 1 R/3 product [products], 2 R/q product [products],
+   3 R/3 root inversion [inversions], 4 R/q root inversion [inversions], 5 repair [keys],
+   6 encode [keys], 7 other).  Returns the number of classes. */
+void sntrup_profile_enable(int on);
+int sntrup_profile_read(int reset, double *ms, double *units, uint64_t *launches, int max_classes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SNTRUP_GPU_H */

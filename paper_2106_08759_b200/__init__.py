@@ -1,0 +1,248 @@
+"""paper_2106_08759_b200 -- B200-native batched sntrup key generation (arXiv 2106.08759).
+
+Thin Python binding over the C ABI of libsntrup_gpu.so (include/sntrup_gpu.h).  Argument
+marshalling only: every step of the hot path runs in the library's sm_100a kernels.  PyTorch is
+used for device memory and streams.  There is NO CPU fallback: importing without the built
+library raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_PKG, "libsntrup_gpu.so")
+
+if not os.path.exists(_LIB_PATH):
+    raise ImportError("libsntrup_gpu.so is not built (run __graft_entry__.build() or "
+                      "python -m paper_2106_08759_b200._build); there is no CPU fallback")
+
+_lib = ctypes.CDLL(_LIB_PATH)
+
+SNTRUP_OK = 0
+SNTRUP_E_PARAM = -1
+SNTRUP_E_ARG = -2
+SNTRUP_E_NOT_INVERTIBLE = -3
+SNTRUP_E_CUDA = -4
+SNTRUP_E_WORKSPACE = -5
+SNTRUP_E_INTERNAL = -6
+
+OPT_HOST_OUTPUT = 1
+OPT_NO_SMALL_CHECK = 2
+OPT_ASYNC = 4
+
+PARAM_SETS = (653, 761, 857, 953, 1013, 1277)
+
+
+class KeygenOpts(ctypes.Structure):
+    _fields_ = [("first_key_index", ctypes.c_uint64), ("batch_size", ctypes.c_uint32),
+                ("flags", ctypes.c_uint32), ("chunk_keys", ctypes.c_uint64),
+                ("stream", ctypes.c_void_p), ("h_out", ctypes.c_void_p),
+                ("g_out", ctypes.c_void_p), ("f_out", ctypes.c_void_p),
+                ("ginv_out", ctypes.c_void_p), ("attempts_out", ctypes.c_void_p),
+                ("stats_out", ctypes.c_void_p)]
+
+
+_u64, _i32, _u32, _vp, _sz = ctypes.c_uint64, ctypes.c_int, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_size_t
+_lib.sntrup_params.argtypes = [_i32] + [_vp] * 7
+_lib.sntrup_strerror.restype = ctypes.c_char_p
+_lib.sntrup_strerror.argtypes = [_i32]
+_lib.sntrup_batch_keygen.argtypes = [_i32, _u64, _u64, _vp, _vp]
+_lib.sntrup_batch_keygen_ex.argtypes = [_i32, _u64, _u64, _vp, _vp, ctypes.POINTER(KeygenOpts)]
+_lib.sntrup_keygen_workspace_bytes.restype = _sz
+_lib.sntrup_keygen_workspace_bytes.argtypes = [_i32, _u64, _u32]
+_lib.rq_mul_batch.argtypes = [_i32, _u64, _vp, _vp, _vp, _vp]
+_lib.r3_mul_batch.argtypes = [_i32, _u64, _vp, _vp, _vp, _vp]
+_lib.rq_recip_batch.argtypes = [_i32, _u64, _vp, _vp, _u32, ctypes.POINTER(ctypes.c_uint64), _vp]
+_lib.r3_recip_batch.argtypes = [_i32, _u64, _vp, _vp, _vp, _u32, _vp]
+_lib.r3_is_invertible_batch.argtypes = [_i32, _u64, _vp, _vp, _vp]
+_lib.rq_encode_batch.argtypes = [_i32, _u64, _vp, _vp, _vp]
+_lib.sntrup_release_workspace.restype = None
+_lib.sntrup_kernel_launch_count.restype = _u64
+_lib.sntrup_profile_enable.restype = None
+_lib.sntrup_profile_enable.argtypes = [_i32]
+_lib.sntrup_profile_read.restype = _i32
+_lib.sntrup_profile_read.argtypes = [_i32, _vp, _vp, _vp, _i32]
+
+EXPORTED = ("sntrup_params", "sntrup_strerror", "sntrup_batch_keygen", "sntrup_batch_keygen_ex",
+            "sntrup_keygen_workspace_bytes", "rq_mul_batch", "r3_mul_batch", "rq_recip_batch",
+            "r3_recip_batch", "r3_is_invertible_batch", "rq_encode_batch",
+            "sntrup_release_workspace", "sntrup_kernel_launch_count", "sntrup_profile_enable",
+            "sntrup_profile_read")
+
+PROFILE_CLASSES = ("sample", "r3_mul", "rq_mul", "r3_inv", "rq_inv", "repair", "encode", "other")
+
+
+class SntrupError(RuntimeError):
+    def __init__(self, code: int, what: str = ""):
+        self.code = code
+        super().__init__("%s: %s (%d)" % (what, _lib.sntrup_strerror(code).decode(), code))
+
+
+def _check(rc: int, what: str):
+    if rc != SNTRUP_OK:
+        raise SntrupError(rc, what)
+
+
+def params(param_set: int) -> dict:
+    vals = [ctypes.c_int() for _ in range(5)] + [ctypes.c_size_t() for _ in range(2)]
+    _check(_lib.sntrup_params(param_set, *[ctypes.addressof(v) for v in vals]), "sntrup_params")
+    p, q, w, p16, p8, pk, sk = (v.value for v in vals)
+    return dict(p=p, q=q, w=w, p16=p16, p8=p8, pk_bytes=pk, sk_bytes=sk)
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def _stream(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _need(t, dtype, shape, name):
+    if t.dtype != dtype or tuple(t.shape) != tuple(shape) or not t.is_contiguous() or not t.is_cuda:
+        raise ValueError("%s must be a contiguous CUDA %s tensor of shape %s" % (name, dtype, shape))
+
+
+def batch_keygen(param_set: int, n_keys: int, seed: int, *, first_key_index: int = 0,
+                 batch_size: int = 32, chunk_keys: int = 0, flags: int = 0, pk_out=None,
+                 sk_out=None, debug: bool = False, stream=None, stats: bool = False):
+    """Generate n_keys key pairs (global indices first_key_index ..).  Returns dict with pk, sk
+    (uint8 CUDA tensors) and, with debug=True, h/g/f/ginv/attempts."""
+    P = params(param_set)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    if pk_out is None:
+        pk_out = torch.empty((n_keys, P["pk_bytes"]), dtype=torch.uint8, device=dev)
+    if sk_out is None:
+        sk_out = torch.empty((n_keys, P["sk_bytes"]), dtype=torch.uint8, device=dev)
+    o = KeygenOpts()
+    o.first_key_index = first_key_index
+    o.batch_size = batch_size
+    o.flags = flags
+    o.chunk_keys = chunk_keys
+    o.stream = _stream(stream)
+    out = dict(pk=pk_out, sk=sk_out)
+    if debug:
+        out["h"] = torch.zeros((n_keys, P["p8"]), dtype=torch.int16, device=dev)
+        for k in ("g", "f", "ginv"):
+            out[k] = torch.zeros((n_keys, P["p16"]), dtype=torch.int8, device=dev)
+        out["attempts"] = torch.zeros(n_keys, dtype=torch.uint8, device=dev)
+        o.h_out, o.g_out, o.f_out = out["h"].data_ptr(), out["g"].data_ptr(), out["f"].data_ptr()
+        o.ginv_out, o.attempts_out = out["ginv"].data_ptr(), out["attempts"].data_ptr()
+    st = (ctypes.c_uint64 * 4)()
+    if stats:
+        o.stats_out = ctypes.addressof(st)
+    host = bool(flags & OPT_HOST_OUTPUT)
+    pkp = pk_out.data_ptr() if not host else pk_out.data_ptr()
+    _check(_lib.sntrup_batch_keygen_ex(param_set, n_keys, seed, ctypes.c_void_p(pkp),
+                                       ctypes.c_void_p(sk_out.data_ptr()), ctypes.byref(o)),
+           "sntrup_batch_keygen_ex")
+    if stats:
+        out["stats"] = dict(rq_products=st[0], r3_products=st[1], root_inversions=st[2],
+                            keys_repaired=st[3])
+    return out
+
+
+def rq_mul_batch(param_set: int, a, b, c=None, stream=None):
+    P = params(param_set)
+    n = a.shape[0]
+    _need(a, torch.int16, (n, P["p8"]), "a")
+    _need(b, torch.int16, (n, P["p8"]), "b")
+    if c is None:
+        c = torch.empty_like(a)
+    _check(_lib.rq_mul_batch(param_set, n, _ptr(a), _ptr(b), _ptr(c), _stream(stream)), "rq_mul_batch")
+    return c
+
+
+def r3_mul_batch(param_set: int, a, b, c=None, stream=None):
+    P = params(param_set)
+    n = a.shape[0]
+    _need(a, torch.int8, (n, P["p16"]), "a")
+    _need(b, torch.int8, (n, P["p16"]), "b")
+    if c is None:
+        c = torch.empty_like(a)
+    _check(_lib.r3_mul_batch(param_set, n, _ptr(a), _ptr(b), _ptr(c), _stream(stream)), "r3_mul_batch")
+    return c
+
+
+def rq_recip_batch(param_set: int, a, out=None, batch_size: int = 32, stream=None):
+    """Returns out; raises SntrupError(SNTRUP_E_NOT_INVERTIBLE) with .bad_index for zero rows."""
+    P = params(param_set)
+    n = a.shape[0]
+    _need(a, torch.int16, (n, P["p8"]), "a")
+    if out is None:
+        out = torch.empty_like(a)
+    bad = ctypes.c_uint64(0)
+    rc = _lib.rq_recip_batch(param_set, n, _ptr(a), _ptr(out), batch_size, ctypes.byref(bad), _stream(stream))
+    if rc != SNTRUP_OK:
+        e = SntrupError(rc, "rq_recip_batch")
+        e.bad_index = bad.value
+        raise e
+    return out
+
+
+def r3_recip_batch(param_set: int, g, out=None, ok=None, batch_size: int = 32, stream=None):
+    P = params(param_set)
+    n = g.shape[0]
+    _need(g, torch.int8, (n, P["p16"]), "g")
+    if out is None:
+        out = torch.empty_like(g)
+    if ok is None:
+        ok = torch.empty(n, dtype=torch.uint8, device=g.device)
+    _check(_lib.r3_recip_batch(param_set, n, _ptr(g), _ptr(out), _ptr(ok), batch_size, _stream(stream)),
+           "r3_recip_batch")
+    return out, ok
+
+
+def r3_is_invertible_batch(param_set: int, g, stream=None):
+    P = params(param_set)
+    n = g.shape[0]
+    _need(g, torch.int8, (n, P["p16"]), "g")
+    ok = torch.empty(n, dtype=torch.uint8, device=g.device)
+    _check(_lib.r3_is_invertible_batch(param_set, n, _ptr(g), _ptr(ok), _stream(stream)),
+           "r3_is_invertible_batch")
+    return ok
+
+
+def rq_encode_batch(param_set: int, h, pk=None, stream=None):
+    P = params(param_set)
+    n = h.shape[0]
+    _need(h, torch.int16, (n, P["p8"]), "h")
+    if pk is None:
+        pk = torch.empty((n, P["pk_bytes"]), dtype=torch.uint8, device=h.device)
+    _check(_lib.rq_encode_batch(param_set, n, _ptr(h), _ptr(pk), _stream(stream)), "rq_encode_batch")
+    return pk
+
+
+def keygen_workspace_bytes(param_set: int, n_keys: int, batch_size: int = 32) -> int:
+    return int(_lib.sntrup_keygen_workspace_bytes(param_set, n_keys, batch_size))
+
+
+def release_workspace():
+    _lib.sntrup_release_workspace()
+
+
+def kernel_launch_count() -> int:
+    return int(_lib.sntrup_kernel_launch_count())
+
+
+def profile_enable(on: bool = True):
+    _lib.sntrup_profile_enable(1 if on else 0)
+
+
+def profile_read(reset: bool = True) -> dict:
+    """Per kernel class: device ms (CUDA events on the launching stream), work units, launches."""
+    n = len(PROFILE_CLASSES)
+    ms = (ctypes.c_double * n)()
+    un = (ctypes.c_double * n)()
+    la = (ctypes.c_uint64 * n)()
+    _lib.sntrup_profile_read(1 if reset else 0, ms, un, la, n)
+    return {PROFILE_CLASSES[i]: dict(ms=ms[i], units=un[i], launches=la[i]) for i in range(n)}
+
+
+def library_path() -> str:
+    return _LIB_PATH

@@ -1,0 +1,261 @@
+// sample.cuh -- seeded sampling of Small g and Short f, and the small-factor invertibility test.
+//
+// KeyGen step 1 / step 3 and Algorithm 1 lines 4-6: "g <-$ R/3",
+// "if not isInvertible(g): continue", "f <-$ Short".  The paper does not fix the sampler; the
+// conventions are DESIGN.md C2 (stream), C3 (Small), C4 (Short by sorting p tagged uint32 draws).
+// isInvertible is split: factors of degree <= 64 are tested here with residue
+// tables (g mod f_i = sum_j g_j * (x^j mod f_i)); every larger factor is covered exactly by the
+// product-tree root test (divstep.cuh) plus the per-key repair path.
+#pragma once
+#include "common.cuh"
+
+namespace sntrup {
+
+// ---------------------------------------------------------------------------------------------
+// Warp-wide bitonic sort of 32*E uint32 keys held in registers, blocked layout: lane l holds
+// global elements l*E .. l*E+E-1 in v[0..E-1].  Ascending.  A fixed network (constant time).
+// ---------------------------------------------------------------------------------------------
+template <int E>
+__device__ __forceinline__ void warp_bitonic_sort(uint32_t (&v)[E], int lane) {
+    constexpr int N = 32 * E;
+#pragma unroll
+    for (int k = 2; k <= N; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= E) {
+                const int lm = j / E;
+                const bool lower = (lane & lm) == 0;
+                const bool up = ((lane * E) & k) == 0;     // k > j >= E: bit k of i is a lane bit
+                const bool take_min = (lower == up);
+#pragma unroll
+                for (int e = 0; e < E; e++) {
+                    const uint32_t o = __shfl_xor_sync(FULL, v[e], lm);
+                    v[e] = take_min ? min(v[e], o) : max(v[e], o);
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < E; e++) {
+                    if ((e & j) == 0) {
+                        const int ex = e | j;
+                        // direction bit k of i = l*E + e: from e when k < E, from the lane otherwise
+                        const bool up = (k < E) ? ((e & k) == 0) : (((lane * E) & k) == 0);
+                        const uint32_t a = v[e], b = v[ex];
+                        const uint32_t mn = min(a, b), mx = max(a, b);
+                        v[e] = up ? mn : mx;
+                        v[ex] = up ? mx : mn;
+                    }
+                }
+            }
+        }
+    }
+}
+
+// C4: Short f for key root K (domain d = 0).  Writes the int8 row f[0..P16).
+template <class PS>
+__device__ __forceinline__ void sample_short_warp(uint64_t K, int8_t *frow, int lane) {
+    constexpr int E = PS::NSORT / 32;
+    const uint64_t D = sm_at(K, 0);
+    uint32_t v[E];
+#pragma unroll
+    for (int t = 0; t < E / 2; t++) {
+        const int i = lane * E + 2 * t;                     // words u_i (low half), u_{i+1} (high)
+        const uint64_t z = sm_at(D, (uint64_t)(i / 2));
+        const uint32_t lo = (uint32_t)z, hi = (uint32_t)(z >> 32);
+        v[2 * t] = i < PS::P ? (i < PS::W ? (lo & 0xFFFFFFFEu) : ((lo & 0xFFFFFFFCu) | 1u))
+                             : 0xFFFFFFFFu;
+        v[2 * t + 1] = i + 1 < PS::P ? (i + 1 < PS::W ? (hi & 0xFFFFFFFEu)
+                                                      : ((hi & 0xFFFFFFFCu) | 1u))
+                                     : 0xFFFFFFFFu;
+    }
+    warp_bitonic_sort<E>(v, lane);
+    // f_i = (L_(i) & 3) - 1 for i < P, 0 in the pad; pack 4 per word, 16-byte stores.
+#pragma unroll
+    for (int w4 = 0; w4 < E / 16; w4++) {
+        const int base = lane * E + 16 * w4;
+        if (base >= PS::P16) break;
+        uint32_t wd[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            uint32_t word = 0;
+#pragma unroll
+            for (int b = 0; b < 4; b++) {
+                const int e = 16 * w4 + 4 * q + b;
+                const int i = lane * E + e;
+                const int fv = i < PS::P ? (int)(v[e] & 3u) - 1 : 0;
+                word |= ((uint32_t)(fv & 0xff)) << (8 * b);
+            }
+            wd[q] = word;
+        }
+        *reinterpret_cast<uint4 *>(frow + base) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+    }
+}
+
+// C3: Small g, attempt a (domain 1 + a) for block b (coefficients 32b .. 32b+31): bitsliced
+// planes (pl, mi).  Coefficients >= P are 0.
+template <class PS>
+__device__ __forceinline__ void small_block(uint64_t D, int b, uint32_t &pl, uint32_t &mi) {
+    pl = 0;
+    mi = 0;
+#pragma unroll 4
+    for (int t = 0; t < 16; t++) {
+        const int i = 32 * b + 2 * t;
+        if (i >= PS::P) break;
+        const uint64_t z = sm_at(D, (uint64_t)(i / 2));
+        const uint32_t u0 = (uint32_t)z & 0x3FFFFFFFu, u1 = (uint32_t)(z >> 32) & 0x3FFFFFFFu;
+        const int c0 = (int)((3ull * u0) >> 30);           // 0,1,2 -> g = c - 1
+        const int c1 = (int)((3ull * u1) >> 30);
+        pl |= (uint32_t)(c0 == 2) << (2 * t);
+        mi |= (uint32_t)(c0 == 0) << (2 * t);
+        if (i + 1 < PS::P) {
+            pl |= (uint32_t)(c1 == 2) << (2 * t + 1);
+            mi |= (uint32_t)(c1 == 0) << (2 * t + 1);
+        }
+    }
+}
+
+// Write bitsliced block b to an int8 row (32 bytes; bytes beyond P16 are not written).
+template <class PS>
+__device__ __forceinline__ void store_block_int8(int8_t *row, int b, uint32_t pl, uint32_t mi) {
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+        const int base = 32 * b + 16 * h;
+        if (base >= PS::P16) break;
+        uint32_t wd[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            uint32_t word = 0;
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+                const int bit = 16 * h + 4 * q + c;
+                const int val = (int)((pl >> bit) & 1u) - (int)((mi >> bit) & 1u);
+                word |= ((uint32_t)(val & 0xff)) << (8 * c);
+            }
+            wd[q] = word;
+        }
+        *reinterpret_cast<uint4 *>(row + base) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+    }
+}
+
+// Load block b of an int8 row into bitsliced planes (coefficients >= P ignored).
+template <class PS>
+__device__ __forceinline__ void load_block_int8(const int8_t *row, int b, uint32_t &pl, uint32_t &mi) {
+    pl = 0;
+    mi = 0;
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+        const int base = 32 * b + 16 * h;
+        if (base >= PS::P16) break;
+        const uint4 q4 = *reinterpret_cast<const uint4 *>(row + base);
+        const uint32_t wd[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+                const int bit = 16 * h + 4 * q + c;
+                const int idx = base + 4 * q + c;
+                const int val = (int)(int8_t)((wd[q] >> (8 * c)) & 0xffu);
+                if (idx < PS::P) {
+                    pl |= (uint32_t)(val == 1) << bit;
+                    mi |= (uint32_t)(val == -1) << bit;
+                }
+            }
+    }
+}
+
+// Small-factor residue test (warp).  T: [P][WT] uint2 rows (x^j mod f_i concatenated over the
+// small factors, bitsliced); masks: [nf][WT] words selecting each factor's trits.  Blocks are
+// distributed over lanes (block b on lane b % 32).  Returns true iff no small factor divides g.
+template <class PS, int NBL>
+__device__ __forceinline__ bool small_factor_check(const uint32_t (&pl)[NBL], const uint32_t (&mi)[NBL],
+                                                   const uint2 *__restrict__ T,
+                                                   const uint32_t *__restrict__ masks, int nf,
+                                                   int lane) {
+    constexpr int WT = PS::WT;
+    uint32_t ap[WT], am[WT];
+#pragma unroll
+    for (int w = 0; w < WT; w++) { ap[w] = 0; am[w] = 0; }
+#pragma unroll
+    for (int s = 0; s < NBL; s++) {
+        const int b = lane + 32 * s;
+        uint32_t bp = pl[s], bm = mi[s];
+        while (bp | bm) {
+            const uint32_t any = bp | bm;
+            const int c = __ffs(any) - 1;
+            const bool neg = (bm >> c) & 1u;
+            bm &= ~(1u << c);                                 // clear bit c in both planes
+            bp &= ~(1u << c);
+            const int j = 32 * b + c;
+#pragma unroll
+            for (int w = 0; w < WT; w++) {
+                const uint2 t = __ldg(&T[(size_t)j * WT + w]);
+                if (neg) gf3_add(ap[w], am[w], t.y, t.x);
+                else gf3_add(ap[w], am[w], t.x, t.y);
+            }
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+        for (int w = 0; w < WT; w++) {
+            const uint32_t op = __shfl_xor_sync(FULL, ap[w], off);
+            const uint32_t om = __shfl_xor_sync(FULL, am[w], off);
+            gf3_add(ap[w], am[w], op, om);
+        }
+    bool ok = true;
+    for (int f = 0; f < nf; f++) {
+        uint32_t nz = 0;
+#pragma unroll
+        for (int w = 0; w < WT; w++) nz |= (ap[w] | am[w]) & masks[f * WT + w];
+        ok = ok && (nz != 0);
+    }
+    return ok;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Sampling kernel: one warp per key.  f from domain 0; g from domains 1, 2, ... until the
+// small-factor test passes (or the first draw when the test is disabled).
+// ---------------------------------------------------------------------------------------------
+struct SampleArgs {
+    uint64_t seed, first, n;
+    int8_t *G, *F;          // rows of P16 bytes
+    uint8_t *attempts;
+    const uint2 *T;
+    const uint32_t *masks;
+    int nf;
+    int small_check;
+    int *err;               // set if the retry bound is hit
+};
+
+template <class PS>
+__global__ void __launch_bounds__(128) sample_kernel(SampleArgs a) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t key_local = (uint64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+    if (key_local >= a.n) return;
+    const uint64_t K = sm_at(a.seed, a.first + key_local);
+    sample_short_warp<PS>(K, a.F + key_local * PS::P16, lane);
+
+    constexpr int NBL = (PS::NB32 + 31) / 32;
+    uint32_t pl[NBL], mi[NBL];
+    int attempt = 0;
+    for (;;) {
+        const uint64_t D = sm_at(K, 1 + (uint64_t)attempt);
+#pragma unroll
+        for (int s = 0; s < NBL; s++) {
+            const int b = lane + 32 * s;
+            if (b < PS::NB32) small_block<PS>(D, b, pl[s], mi[s]);
+            else { pl[s] = 0; mi[s] = 0; }
+        }
+        if (!a.small_check) break;
+        if (small_factor_check<PS, NBL>(pl, mi, a.T, a.masks, a.nf, lane)) break;
+        if (++attempt >= 255) { if (lane == 0) atomicExch(a.err, 1); break; }
+    }
+    int8_t *grow = a.G + key_local * PS::P16;
+#pragma unroll
+    for (int s = 0; s < NBL; s++) {
+        const int b = lane + 32 * s;
+        if (32 * b < PS::P16) store_block_int8<PS>(grow, b, pl[s], mi[s]);
+    }
+    if (lane == 0 && a.attempts) a.attempts[key_local] = (uint8_t)(attempt + 1);
+}
+
+}  // namespace sntrup

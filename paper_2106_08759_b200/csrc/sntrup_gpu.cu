@@ -1,0 +1,855 @@
+// sntrup_gpu.cu -- host orchestration and the C ABI (include/sntrup_gpu.h).
+//
+// BatchKeyGen (Algorithm 1) per chunk of keys, all on one stream:
+//   sample (f, g + small-factor isInvertible, retries)          sample.cuh
+//   R/3 batchInv: product-tree up-sweep, root divstep, down-sweep, repair of failed trees
+//   R/q batchInv on [3f]: up-sweep, root divstep, down-sweep     ringmul.cuh, divstep.cuh
+//   H = [g * fbar]                                                ringmul.cuh (ZIP)
+//   encode pk, sk                                                 encode.cuh
+// batchInv is Montgomery's trick arranged as a tree: level l multiplies sibling
+// pairs (cnt_l = ceil(cnt_{l-1}/2) products), one inversion per tree root, then each child's
+// inverse = parent inverse * sibling: 3(B-1) products per full tree of B leaves, as the
+// paper's chain.
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/sntrup_gpu.h"
+#include "common.cuh"
+#include "divstep.cuh"
+#include "encode.cuh"
+#include "factor_tables.h"
+#include "ringmul.cuh"
+#include "sample.cuh"
+
+using namespace sntrup;
+
+namespace {
+
+std::atomic<uint64_t> g_launches{0};
+std::mutex g_mu;                                   // serialises calls (shared workspace)
+
+// ------------------------------------------------------------------------------ profiler
+// Optional per-launch CUDA-event timing on the launching stream (bench.py's roofline): every
+// launch of kernel class k records (start, end) events and `units` of work (products, keys,
+// inversions).  Read back with sntrup_profile_read().
+enum ProfClass { PC_SAMPLE = 0, PC_MUL_R3, PC_MUL_RQ, PC_INV_R3, PC_INV_RQ, PC_REPAIR, PC_ENCODE,
+                 PC_MISC, PC_N };
+struct ProfRec { int cls; cudaEvent_t a, b; double units; };
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof;
+std::vector<cudaEvent_t> g_evpool;
+struct ProfAgg { double ms = 0, units = 0; uint64_t launches = 0; };
+ProfAgg g_agg[PC_N];
+
+cudaEvent_t ev_get() {
+    if (!g_evpool.empty()) { cudaEvent_t e = g_evpool.back(); g_evpool.pop_back(); return e; }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+struct ProfScope {
+    int cls; double units; cudaStream_t s; cudaEvent_t a = nullptr;
+    ProfScope(int c, double u, cudaStream_t st) : cls(c), units(u), s(st) {
+        if (g_prof_on) { a = ev_get(); cudaEventRecord(a, s); }
+    }
+    ~ProfScope() {
+        if (a) { cudaEvent_t b = ev_get(); cudaEventRecord(b, s); g_prof.push_back(ProfRec{cls, a, b, units}); }
+    }
+};
+
+void prof_drain() {
+    for (auto &r : g_prof) {
+        cudaEventSynchronize(r.b);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        g_agg[r.cls].ms += ms;
+        g_agg[r.cls].units += r.units;
+        g_agg[r.cls].launches += 1;
+        g_evpool.push_back(r.a);
+        g_evpool.push_back(r.b);
+    }
+    g_prof.clear();
+}
+
+#define CK(x)                                                                      \
+    do {                                                                           \
+        cudaError_t e_ = (x);                                                      \
+        if (e_ != cudaSuccess) {                                                   \
+            fprintf(stderr, "sntrup_gpu: %s failed: %s (%s:%d)\n", #x,             \
+                    cudaGetErrorString(e_), __FILE__, __LINE__);                   \
+            return SNTRUP_E_CUDA;                                                  \
+        }                                                                          \
+    } while (0)
+
+#define LAUNCHED()                                                                 \
+    do {                                                                           \
+        g_launches.fetch_add(1, std::memory_order_relaxed);                        \
+        cudaError_t e_ = cudaGetLastError();                                       \
+        if (e_ != cudaSuccess) {                                                   \
+            fprintf(stderr, "sntrup_gpu: launch failed: %s (%s:%d)\n",             \
+                    cudaGetErrorString(e_), __FILE__, __LINE__);                   \
+            return SNTRUP_E_CUDA;                                                  \
+        }                                                                          \
+    } while (0)
+
+// ------------------------------------------------------------------------------ param info
+struct ParamInfo { int p, q, w, p16, p8; size_t pk, sk; };
+
+size_t rq_encoded_len(int p, int q) {
+    std::vector<uint32_t> M(p, (uint32_t)q);
+    size_t len = 0;
+    int n = p;
+    while (n > 1) {
+        std::vector<uint32_t> M2((n + 1) / 2);
+        for (int i = 0; i + 1 < n; i += 2) {
+            uint32_t m = M[i] * M[i + 1];
+            while (m >= 16384u) { len++; m = (m + 255u) >> 8; }
+            M2[i / 2] = m;
+        }
+        if (n & 1) M2[n / 2] = M[n - 1];
+        M.swap(M2);
+        n = (n + 1) / 2;
+    }
+    uint32_t m = M[0];
+    while (m > 1) { len++; m = (m + 255u) >> 8; }
+    return len;
+}
+
+bool param_info(int ps, ParamInfo *pi) {
+    static const int tab[][3] = {{653, 4621, 288}, {761, 4591, 286}, {857, 5167, 322},
+                                 {953, 6343, 396}, {1013, 7177, 448}, {1277, 7879, 492}};
+    for (auto &t : tab)
+        if (t[0] == ps) {
+            pi->p = t[0]; pi->q = t[1]; pi->w = t[2];
+            pi->p16 = (t[0] + 15) / 16 * 16;
+            pi->p8 = (t[0] + 7) / 8 * 8;
+            pi->pk = rq_encoded_len(t[0], t[1]);
+            pi->sk = 2 * (size_t)((t[0] + 3) / 4);
+            return true;
+        }
+    return false;
+}
+
+// ------------------------------------------------------------------------------ device tables
+struct DevTables {
+    uint2 *T = nullptr;          // [P][WT] small-factor residues of x^j
+    uint32_t *masks = nullptr;   // [nf][WT]
+    int nf = 0, wt = 0;
+    uint32_t *Mlo = nullptr;
+    uint8_t *emit = nullptr;
+    uint16_t *off = nullptr;
+    EncTables enc{};
+};
+std::map<std::pair<int, int>, DevTables> g_tables;    // (device, param) -> tables
+
+int build_tables(int dev, int ps, int WT, DevTables **out) {
+    auto key = std::make_pair(dev, ps);
+    auto it = g_tables.find(key);
+    if (it != g_tables.end()) { *out = &it->second; return SNTRUP_OK; }
+    ParamInfo pi;
+    param_info(ps, &pi);
+    const int p = pi.p;
+    DevTables t;
+    // -- small-factor residue table: row j = concat_i (x^j mod f_i), bitsliced
+    const sntrup_tables::SmallFactorSet *fs = nullptr;
+    for (auto &s : sntrup_tables::kSmallFactors) if (s.p == p) fs = &s;
+    if (!fs) return SNTRUP_E_PARAM;
+    int S = 0;
+    for (int i = 0; i < fs->count; i++) S += fs->deg[i];
+    const int wt = (S + 31) / 32;
+    if (wt != WT) { fprintf(stderr, "sntrup_gpu: factor table width mismatch\n"); return SNTRUP_E_PARAM; }
+    std::vector<uint2> T((size_t)p * WT, make_uint2(0, 0));
+    std::vector<uint32_t> masks((size_t)fs->count * WT, 0);
+    int o = 0;
+    for (int fi = 0; fi < fs->count; fi++) {
+        const int d = fs->deg[fi];
+        std::vector<int> f(d + 1), r(d, 0);
+        for (int i = 0; i <= d; i++) f[i] = fs->coef[fi][i] - '0';
+        r[0] = 1 % 3;
+        for (int j = 0; j < p; j++) {
+            for (int i = 0; i < d; i++) {
+                const int pos = o + i, w = pos / 32, bit = pos % 32;
+                if (r[i] == 1) T[(size_t)j * WT + w].x |= 1u << bit;
+                if (r[i] == 2) T[(size_t)j * WT + w].y |= 1u << bit;
+            }
+            // r <- x * r mod f (f monic of degree d)
+            const int top = r[d - 1];
+            for (int i = d - 1; i > 0; i--) r[i] = r[i - 1];
+            r[0] = 0;
+            for (int i = 0; i < d; i++) r[i] = ((r[i] - top * f[i]) % 3 + 3) % 3;
+        }
+        for (int i = 0; i < d; i++) masks[(size_t)fi * WT + (o + i) / 32] |= 1u << ((o + i) % 32);
+        o += d;
+    }
+    t.nf = fs->count;
+    t.wt = WT;
+    // -- encode tables (C10): per level, per pair (M_{2i}, bytes, offset)
+    std::vector<uint32_t> Mlo;
+    std::vector<uint8_t> emit;
+    std::vector<uint16_t> off;
+    EncTables enc{};
+    {
+        std::vector<uint32_t> M(p, (uint32_t)pi.q);
+        int n = p, lev = 0;
+        uint32_t pos = 0;
+        while (n > 1) {
+            if (lev >= ENC_MAXLEV) return SNTRUP_E_PARAM;
+            enc.lev_n[lev] = n;
+            enc.lev_pair_base[lev] = (int)Mlo.size();
+            std::vector<uint32_t> M2((n + 1) / 2);
+            for (int i = 0; i + 1 < n; i += 2) {
+                uint32_t m = M[i] * M[i + 1];
+                int e = 0;
+                while (m >= 16384u) { e++; m = (m + 255u) >> 8; }
+                Mlo.push_back(M[i]);
+                emit.push_back((uint8_t)e);
+                off.push_back((uint16_t)pos);
+                pos += e;
+                M2[i / 2] = m;
+            }
+            if (n & 1) M2[n / 2] = M[n - 1];
+            M.swap(M2);
+            n = (n + 1) / 2;
+            lev++;
+        }
+        enc.nlev = lev;
+        uint32_t m = M[0];
+        int e = 0;
+        while (m > 1) { e++; m = (m + 255u) >> 8; }
+        enc.top_emit = e;
+        enc.top_off = (int)pos;
+        enc.pk_bytes = (int)(pos + e);
+        if ((size_t)enc.pk_bytes != pi.pk) return SNTRUP_E_INTERNAL;
+    }
+    CK(cudaMalloc(&t.T, T.size() * sizeof(uint2)));
+    CK(cudaMemcpy(t.T, T.data(), T.size() * sizeof(uint2), cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&t.masks, masks.size() * sizeof(uint32_t)));
+    CK(cudaMemcpy(t.masks, masks.data(), masks.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&t.Mlo, Mlo.size() * sizeof(uint32_t)));
+    CK(cudaMemcpy(t.Mlo, Mlo.data(), Mlo.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&t.emit, emit.size()));
+    CK(cudaMemcpy(t.emit, emit.data(), emit.size(), cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&t.off, off.size() * sizeof(uint16_t)));
+    CK(cudaMemcpy(t.off, off.data(), off.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
+    enc.Mlo = t.Mlo;
+    enc.emit = t.emit;
+    enc.off = t.off;
+    t.enc = enc;
+    auto res = g_tables.emplace(key, t);
+    *out = &res.first->second;
+    return SNTRUP_OK;
+}
+
+// ------------------------------------------------------------------------------ workspace
+struct Workspace {
+    char *base = nullptr;
+    size_t cap = 0, used = 0;
+    int dev = -1;
+};
+Workspace g_ws;
+
+int ws_reserve(size_t bytes) {
+    int dev;
+    CK(cudaGetDevice(&dev));
+    if (g_ws.base && g_ws.cap >= bytes && g_ws.dev == dev) { g_ws.used = 0; return SNTRUP_OK; }
+    if (g_ws.base) {
+        CK(cudaDeviceSynchronize());
+        cudaSetDevice(g_ws.dev);
+        cudaFree(g_ws.base);
+        cudaSetDevice(dev);
+        g_ws.base = nullptr;
+    }
+    size_t cap = bytes + (bytes >> 3) + (1 << 20);
+    if (cudaMalloc(&g_ws.base, cap) != cudaSuccess) {
+        cudaGetLastError();
+        g_ws.base = nullptr;
+        g_ws.cap = 0;
+        return SNTRUP_E_WORKSPACE;
+    }
+    g_ws.cap = cap;
+    g_ws.used = 0;
+    g_ws.dev = dev;
+    return SNTRUP_OK;
+}
+
+template <class T>
+T *ws_take(size_t count) {
+    size_t bytes = (count * sizeof(T) + 255) & ~(size_t)255;
+    T *p = (T *)(g_ws.base + g_ws.used);
+    g_ws.used += bytes;
+    return p;
+}
+
+size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+// ------------------------------------------------------------------------------ tree plan
+struct TreePlan {
+    int L;                          // levels = log2(B)
+    std::vector<long long> cnt;     // cnt[0] = leaves, cnt[l] = ceil(cnt[l-1]/2)
+    long long inner_rows() const { long long s = 0; for (int l = 1; l <= L; l++) s += cnt[l]; return s; }
+};
+
+TreePlan make_plan(long long m, int B) {
+    TreePlan t;
+    t.L = 0;
+    while ((1 << t.L) < B) t.L++;
+    t.cnt.resize(t.L + 1);
+    t.cnt[0] = m;
+    for (int l = 1; l <= t.L; l++) t.cnt[l] = (t.cnt[l - 1] + 1) / 2;
+    return t;
+}
+
+// ------------------------------------------------------------------------------ launches
+template <class PS, int M>
+int launch_mul(const MulArgs &a, cudaStream_t s) {
+    if (a.n_out <= 0) return SNTRUP_OK;
+    const int threads = (PS::P8 / 8 + 31) / 32 * 32;
+    long long grid = a.n_out;
+    if (grid > (1LL << 30)) grid = 1LL << 30;
+    ProfScope ps_(M == 3 ? PC_MUL_R3 : PC_MUL_RQ, (double)a.n_out, s);
+    ring_mul_kernel<PS, M><<<(unsigned)grid, threads, 0, s>>>(a);
+    LAUNCHED();
+    return SNTRUP_OK;
+}
+
+template <class PS, int M>
+int launch_divstep(const InvArgs &a, cudaStream_t s) {
+    if (a.n <= 0) return SNTRUP_OK;
+    ProfScope ps_(M == 3 ? PC_INV_R3 : PC_INV_RQ, (double)a.n, s);
+    divstep_kernel<PS, M><<<(unsigned)((a.n + 3) / 4), 128, 0, s>>>(a);
+    LAUNCHED();
+    return SNTRUP_OK;
+}
+
+RowDesc rows8(const void *p, long long stride, int scale = 1) { return RowDesc{p, stride, 1, scale}; }
+RowDesc rows16(const void *p, long long stride) { return RowDesc{p, stride, 2, 1}; }
+
+// Batch inversion over one ring by product trees.  X0 = leaves (row descriptor), out0 = leaf
+// inverse rows.  Levels l >= 1 live in lvl[l] / inv[l].  M = ring modulus (3 or q).
+template <class PS, int M>
+int batch_inverse(const TreePlan &tp, RowDesc X0, void *out0, int out_bytes, long long out_stride,
+                  const std::vector<void *> &lvl, const std::vector<void *> &inv, uint8_t *root_ok,
+                  bool leaves_small, cudaStream_t s, uint64_t *nprod) {
+    const int L = tp.L;
+    const long long stride = out_bytes == 2 ? PS::P8 : PS::P16;
+    auto desc = [&](int l) -> RowDesc {
+        if (l == 0) return X0;
+        return out_bytes == 2 ? rows16(lvl[l], stride) : rows8(lvl[l], stride);
+    };
+    auto idesc = [&](int l) -> RowDesc {
+        if (l == 0) return out_bytes == 2 ? rows16(out0, out_stride) : rows8(out0, out_stride);
+        return out_bytes == 2 ? rows16(inv[l], stride) : rows8(inv[l], stride);
+    };
+    int rc;
+    for (int l = 1; l <= L; l++) {                   // up-sweep
+        MulArgs a{};
+        a.mode = MUL_PAIRS;
+        a.n_out = tp.cnt[l];
+        a.cnt_in = tp.cnt[l - 1];
+        a.X = desc(l - 1);
+        a.out = lvl[l];
+        a.out_stride = stride;
+        a.out_bytes = out_bytes;
+        a.periodic = (M != 3) && !(l == 1 && leaves_small);
+        if ((rc = launch_mul<PS, M>(a, s))) return rc;
+        *nprod += tp.cnt[l - 1] / 2;
+    }
+    {                                                // roots
+        InvArgs ia{};
+        ia.n = tp.cnt[L];
+        ia.in = desc(L);
+        ia.out = L == 0 ? out0 : inv[L];
+        ia.out_stride = L == 0 ? out_stride : stride;
+        ia.out_bytes = out_bytes;
+        ia.ok = root_ok;
+        if ((rc = launch_divstep<PS, M>(ia, s))) return rc;
+    }
+    for (int l = L; l >= 1; l--) {                   // down-sweep
+        MulArgs a{};
+        a.mode = MUL_DOWN;
+        a.n_out = tp.cnt[l - 1];
+        a.cnt_in = tp.cnt[l - 1];
+        a.X = desc(l - 1);
+        a.Y = idesc(l);
+        const RowDesc od = idesc(l - 1);
+        a.out = const_cast<void *>(od.ptr);
+        a.out_stride = od.stride;
+        a.out_bytes = out_bytes;
+        a.periodic = (M != 3) && !(l == 1 && leaves_small);
+        if ((rc = launch_mul<PS, M>(a, s))) return rc;
+        *nprod += (tp.cnt[l - 1] / 2) * 2;
+    }
+    return SNTRUP_OK;
+}
+
+// ------------------------------------------------------------------------------ keygen
+template <class PS>
+int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
+                const sntrup_keygen_opts &o) {
+    int dev;
+    CK(cudaGetDevice(&dev));
+    DevTables *tb;
+    int rc = build_tables(dev, PS::P, PS::WT, &tb);
+    if (rc) return rc;
+    cudaStream_t s = (cudaStream_t)o.stream;
+    const int B = o.batch_size ? (int)o.batch_size : 32;
+    if (B < 1 || B > 4096 || (B & (B - 1))) return SNTRUP_E_ARG;
+    uint64_t chunk = o.chunk_keys ? o.chunk_keys : 65536;
+    chunk = (chunk + B - 1) / B * B;
+    if (chunk > n) chunk = (n + B - 1) / B * B;
+    const bool host_out = (o.flags & SNTRUP_OPT_HOST_OUTPUT) != 0;
+    const size_t pkb = tb->enc.pk_bytes, skb = 2 * PS::SKH;
+
+    // workspace for one chunk of `chunk` keys
+    const TreePlan tpmax = make_plan((long long)chunk, B);
+    const long long inner = tpmax.inner_rows();
+    size_t need = 0;
+    need += 3 * align256(chunk * PS::P16);                  // G, F, Ginv
+    need += align256(chunk);                                 // attempts
+    need += 2 * align256(inner * PS::P16 + 256 * (tpmax.L + 1));   // R/3 levels + inverses
+    need += 2 * align256(inner * PS::P8 * 2 + 256 * (tpmax.L + 1)); // R/q levels + inverses
+    need += 2 * align256(chunk * PS::P8 * 2);                // Fbar, H
+    need += 2 * align256(tpmax.cnt[tpmax.L]);                // root ok flags
+    if (host_out) need += align256(chunk * pkb) + align256(chunk * skb);
+    need += 4096;
+    if ((rc = ws_reserve(need))) return rc;
+    int8_t *G = ws_take<int8_t>(chunk * PS::P16);
+    int8_t *F = ws_take<int8_t>(chunk * PS::P16);
+    int8_t *Ginv = ws_take<int8_t>(chunk * PS::P16);
+    uint8_t *att = ws_take<uint8_t>(chunk);
+    std::vector<void *> l3(tpmax.L + 1, nullptr), i3(tpmax.L + 1, nullptr);
+    std::vector<void *> lq(tpmax.L + 1, nullptr), iq(tpmax.L + 1, nullptr);
+    for (int l = 1; l <= tpmax.L; l++) {
+        l3[l] = ws_take<int8_t>(tpmax.cnt[l] * PS::P16);
+        i3[l] = ws_take<int8_t>(tpmax.cnt[l] * PS::P16);
+        lq[l] = ws_take<int16_t>(tpmax.cnt[l] * PS::P8);
+        iq[l] = ws_take<int16_t>(tpmax.cnt[l] * PS::P8);
+    }
+    int16_t *Fbar = ws_take<int16_t>(chunk * PS::P8);
+    int16_t *H = ws_take<int16_t>(chunk * PS::P8);
+    uint8_t *ok3 = ws_take<uint8_t>(tpmax.cnt[tpmax.L]);
+    uint8_t *okq = ws_take<uint8_t>(tpmax.cnt[tpmax.L]);
+    uint8_t *pk_dev = nullptr, *sk_dev = nullptr;
+    if (host_out) { pk_dev = ws_take<uint8_t>(chunk * pkb); sk_dev = ws_take<uint8_t>(chunk * skb); }
+    unsigned long long *repaired = ws_take<unsigned long long>(1);
+    int *err = ws_take<int>(1);
+    CK(cudaMemsetAsync(repaired, 0, sizeof(unsigned long long), s));
+    CK(cudaMemsetAsync(err, 0, sizeof(int), s));
+
+    uint64_t n_rq = 0, n_r3 = 0, n_inv = 0;
+    for (uint64_t c0 = 0; c0 < n; c0 += chunk) {
+        const uint64_t m = (n - c0 < chunk) ? n - c0 : chunk;
+        const uint64_t first = o.first_key_index + c0;
+        const TreePlan tp = make_plan((long long)m, B);
+        int8_t *Gc = o.g_out ? o.g_out + c0 * PS::P16 : G;
+        int8_t *Fc = o.f_out ? o.f_out + c0 * PS::P16 : F;
+        int8_t *Ic = o.ginv_out ? o.ginv_out + c0 * PS::P16 : Ginv;
+        uint8_t *Ac = o.attempts_out ? o.attempts_out + c0 : att;
+        int16_t *Hc = o.h_out ? o.h_out + c0 * PS::P8 : H;
+        uint8_t *pkc = host_out ? pk_dev : pk_out + c0 * pkb;
+        uint8_t *skc = host_out ? sk_dev : sk_out + c0 * skb;
+
+        SampleArgs sa{};
+        sa.seed = seed; sa.first = first; sa.n = m;
+        sa.G = Gc; sa.F = Fc; sa.attempts = Ac;
+        sa.T = tb->T; sa.masks = tb->masks; sa.nf = tb->nf;
+        sa.small_check = (o.flags & SNTRUP_OPT_NO_SMALL_CHECK) ? 0 : 1;
+        sa.err = err;
+        {
+            ProfScope ps_(PC_SAMPLE, (double)m, s);
+            sample_kernel<PS><<<(unsigned)((m + 3) / 4), 128, 0, s>>>(sa);
+        }
+        LAUNCHED();
+
+        // R/3: Gbar = batchInv(G)   (Algorithm 1 line 10)
+        if ((rc = batch_inverse<PS, 3>(tp, rows8(Gc, PS::P16), Ic, 1, PS::P16, l3, i3, ok3, true, s, &n_r3)))
+            return rc;
+        RepairArgs ra{};
+        ra.seed = seed; ra.first = first; ra.n = m; ra.B = B; ra.root_ok = ok3;
+        ra.G = Gc; ra.Ginv = Ic; ra.attempts = Ac;
+        ra.T = tb->T; ra.masks = tb->masks; ra.nf = tb->nf; ra.small_check = sa.small_check;
+        ra.repaired = repaired; ra.err = err;
+        {
+            ProfScope ps_(PC_REPAIR, (double)m, s);
+            repair_kernel<PS><<<(unsigned)((m + 3) / 4), 128, 0, s>>>(ra);
+        }
+        LAUNCHED();
+
+        // R/q: Fbar = batchInv([3 f])   (Algorithm 1 line 11)
+        if ((rc = batch_inverse<PS, PS::Q>(tp, rows8(Fc, PS::P16, 3), Fbar, 2, PS::P8, lq, iq, okq, true, s, &n_rq)))
+            return rc;
+        // H = [g * fbar]   (Algorithm 1 line 12)
+        {
+            MulArgs a{};
+            a.mode = MUL_ZIP;
+            a.n_out = (long long)m;
+            a.X = rows8(Gc, PS::P16);
+            a.Y = rows16(Fbar, PS::P8);
+            a.out = Hc;
+            a.out_stride = PS::P8;
+            a.out_bytes = 2;
+            a.periodic = 0;
+            if ((rc = launch_mul<PS, PS::Q>(a, s))) return rc;
+            n_rq += m;
+        }
+        n_inv += 2 * tp.cnt[tp.L];
+        // encode (KeyGen step 5)
+        {
+            EncArgs ea{};
+            ea.n = m; ea.h = Hc; ea.f = Fc; ea.ginv = Ic; ea.pk = pkc; ea.sk = skc; ea.t = tb->enc;
+            {
+                ProfScope ps_(PC_ENCODE, (double)m, s);
+                encode_kernel<PS><<<(unsigned)((m + 3) / 4), 128, 0, s>>>(ea);
+            }
+            LAUNCHED();
+        }
+        if (host_out) {
+            CK(cudaMemcpyAsync(pk_out + c0 * pkb, pk_dev, m * pkb, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(sk_out + c0 * skb, sk_dev, m * skb, cudaMemcpyDeviceToHost, s));
+        }
+    }
+    const bool sync = !(o.flags & SNTRUP_OPT_ASYNC) || host_out || o.stats_out;
+    if (sync) {
+        int herr = 0;
+        unsigned long long hrep = 0;
+        CK(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(&hrep, repaired, sizeof(hrep), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (herr) return SNTRUP_E_INTERNAL;
+        if (o.stats_out) {
+            o.stats_out[0] = n_rq;
+            o.stats_out[1] = n_r3;
+            o.stats_out[2] = n_inv;
+            o.stats_out[3] = hrep;
+        }
+    }
+    return SNTRUP_OK;
+}
+
+// ------------------------------------------------------------------------------ small kernels
+__global__ void zero_rows_kernel(const int16_t *a, long long n, int p, long long stride,
+                                 unsigned long long *first_zero) {
+    const int lane = threadIdx.x & 31;
+    const long long row = (long long)blockIdx.x * 4 + (threadIdx.x >> 5);
+    if (row >= n) return;
+    int nz = 0;
+    for (int k = lane; k < p; k += 32) nz |= a[row * stride + k] != 0;
+    nz = __any_sync(FULL, nz);
+    if (!nz && lane == 0) atomicMin(first_zero, (unsigned long long)row);
+}
+
+// r3: small-factor test per element; G' = ok ? g : 1
+template <class PS>
+__global__ void __launch_bounds__(128) r3_prepare_kernel(const int8_t *g, int8_t *gp, uint8_t *ok_small,
+                                                         long long n, const uint2 *T, const uint32_t *masks,
+                                                         int nf) {
+    constexpr int NBL = (PS::NB32 + 31) / 32;
+    const int lane = threadIdx.x & 31;
+    const long long row = (long long)blockIdx.x * 4 + (threadIdx.x >> 5);
+    if (row >= n) return;
+    uint32_t pl[NBL], mi[NBL];
+#pragma unroll
+    for (int s = 0; s < NBL; s++) {
+        const int b = lane + 32 * s;
+        if (b < PS::NB32) load_block_int8<PS>(g + row * PS::P16, b, pl[s], mi[s]);
+        else { pl[s] = 0; mi[s] = 0; }
+    }
+    bool zero = true;
+#pragma unroll
+    for (int s = 0; s < NBL; s++) zero = zero && !(pl[s] | mi[s]);
+    zero = __all_sync(FULL, zero);
+    const bool ok = !zero && small_factor_check<PS, NBL>(pl, mi, T, masks, nf, lane);
+#pragma unroll
+    for (int s = 0; s < NBL; s++) {
+        const int b = lane + 32 * s;
+        if (32 * b < PS::P16)
+            store_block_int8<PS>(gp + row * PS::P16, b, ok ? pl[s] : (b == 0 ? 1u : 0u), ok ? mi[s] : 0u);
+    }
+    if (lane == 0) ok_small[row] = ok ? 1 : 0;
+}
+
+// r3: finalize.  Trees whose root inverted: ok = ok_small (zero rows that were substituted).
+// Trees whose root failed: exact per-element divstep on the original input.
+template <class PS>
+__global__ void __launch_bounds__(128) r3_finalize_kernel(const int8_t *g, int8_t *out, uint8_t *ok,
+                                                          long long n, int B, const uint8_t *root_ok) {
+    using DS = Divstep<PS, 3>;
+    constexpr int C = DS::C;
+    const int lane = threadIdx.x & 31;
+    const long long row = (long long)blockIdx.x * 4 + (threadIdx.x >> 5);
+    if (row >= n) return;
+    int8_t *orow = out + row * PS::P16;
+    if (root_ok[row / B]) {
+        if (!ok[row])
+            for (int k = lane; k < PS::P16; k += 32) orow[k] = 0;
+        return;
+    }
+    float gg[C], res[C];
+#pragma unroll
+    for (int c = 0; c < C; c++) {
+        const int i = lane * C + c;
+        gg[c] = (i < PS::P) ? (float)g[row * PS::P16 + PS::P - 1 - i] : 0.0f;
+    }
+    const bool inv = DS::invert(gg, res, lane);
+#pragma unroll
+    for (int c = 0; c < C; c++) {
+        const int j = lane * C + c;
+        if (j < PS::P) orow[PS::P - 1 - j] = inv ? (int8_t)(int)res[c] : 0;
+    }
+    for (int k = PS::P + lane; k < PS::P16; k += 32) orow[k] = 0;
+    if (lane == 0) ok[row] = inv ? 1 : 0;
+}
+
+template <class PS>
+int r3_recip_impl(uint64_t n, const int8_t *g, int8_t *out, uint8_t *ok, uint32_t B_, cudaStream_t s) {
+    int dev;
+    CK(cudaGetDevice(&dev));
+    DevTables *tb;
+    int rc = build_tables(dev, PS::P, PS::WT, &tb);
+    if (rc) return rc;
+    const int B = B_ ? (int)B_ : 32;
+    if (B < 1 || B > 4096 || (B & (B - 1))) return SNTRUP_E_ARG;
+    const TreePlan tp = make_plan((long long)n, B);
+    const long long inner = tp.inner_rows();
+    size_t need = align256(n * PS::P16) + 2 * align256(inner * PS::P16 + 256 * (tp.L + 1)) +
+                  align256(tp.cnt[tp.L]) + 4096;
+    if ((rc = ws_reserve(need))) return rc;
+    int8_t *gp = ws_take<int8_t>(n * PS::P16);
+    std::vector<void *> l3(tp.L + 1, nullptr), i3(tp.L + 1, nullptr);
+    for (int l = 1; l <= tp.L; l++) {
+        l3[l] = ws_take<int8_t>(tp.cnt[l] * PS::P16);
+        i3[l] = ws_take<int8_t>(tp.cnt[l] * PS::P16);
+    }
+    uint8_t *rok = ws_take<uint8_t>(tp.cnt[tp.L]);
+    r3_prepare_kernel<PS><<<(unsigned)((n + 3) / 4), 128, 0, s>>>(g, gp, ok, (long long)n, tb->T, tb->masks, tb->nf);
+    LAUNCHED();
+    uint64_t np = 0;
+    if ((rc = batch_inverse<PS, 3>(tp, rows8(gp, PS::P16), out, 1, PS::P16, l3, i3, rok, false, s, &np)))
+        return rc;
+    r3_finalize_kernel<PS><<<(unsigned)((n + 3) / 4), 128, 0, s>>>(g, out, ok, (long long)n, B, rok);
+    LAUNCHED();
+    CK(cudaStreamSynchronize(s));
+    return SNTRUP_OK;
+}
+
+template <class PS>
+int rq_recip_impl(uint64_t n, const int16_t *a, int16_t *out, uint32_t B_, uint64_t *bad, cudaStream_t s) {
+    const int B = B_ ? (int)B_ : 32;
+    if (B < 1 || B > 4096 || (B & (B - 1))) return SNTRUP_E_ARG;
+    const TreePlan tp = make_plan((long long)n, B);
+    const long long inner = tp.inner_rows();
+    size_t need = 2 * align256(inner * PS::P8 * 2 + 256 * (tp.L + 1)) + align256(tp.cnt[tp.L]) + 4096;
+    int rc;
+    if ((rc = ws_reserve(need))) return rc;
+    std::vector<void *> lq(tp.L + 1, nullptr), iq(tp.L + 1, nullptr);
+    for (int l = 1; l <= tp.L; l++) {
+        lq[l] = ws_take<int16_t>(tp.cnt[l] * PS::P8);
+        iq[l] = ws_take<int16_t>(tp.cnt[l] * PS::P8);
+    }
+    uint8_t *rok = ws_take<uint8_t>(tp.cnt[tp.L]);
+    unsigned long long *fz = ws_take<unsigned long long>(1);
+    CK(cudaMemsetAsync(fz, 0xff, sizeof(unsigned long long), s));
+    zero_rows_kernel<<<(unsigned)((n + 3) / 4), 128, 0, s>>>(a, (long long)n, PS::P, PS::P8, fz);
+    LAUNCHED();
+    unsigned long long hz = 0;
+    CK(cudaMemcpyAsync(&hz, fz, sizeof(hz), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (hz != ~0ull) {
+        if (bad) *bad = hz;
+        return SNTRUP_E_NOT_INVERTIBLE;
+    }
+    uint64_t np = 0;
+    if ((rc = batch_inverse<PS, PS::Q>(tp, rows16(a, PS::P8), out, 2, PS::P8, lq, iq, rok, false, s, &np)))
+        return rc;
+    CK(cudaStreamSynchronize(s));
+    return SNTRUP_OK;
+}
+
+}  // namespace
+
+// ================================================================================== C ABI
+extern "C" {
+
+int sntrup_params(int param_set, int *p, int *q, int *w, int *p_pad16, int *p_pad8,
+                  size_t *pk_bytes, size_t *sk_bytes) {
+    ParamInfo pi;
+    if (!param_info(param_set, &pi)) return SNTRUP_E_PARAM;
+    if (p) *p = pi.p;
+    if (q) *q = pi.q;
+    if (w) *w = pi.w;
+    if (p_pad16) *p_pad16 = pi.p16;
+    if (p_pad8) *p_pad8 = pi.p8;
+    if (pk_bytes) *pk_bytes = pi.pk;
+    if (sk_bytes) *sk_bytes = pi.sk;
+    return SNTRUP_OK;
+}
+
+const char *sntrup_strerror(int code) {
+    switch (code) {
+    case SNTRUP_OK: return "ok";
+    case SNTRUP_E_PARAM: return "unknown parameter set";
+    case SNTRUP_E_ARG: return "invalid argument";
+    case SNTRUP_E_NOT_INVERTIBLE: return "element not invertible";
+    case SNTRUP_E_CUDA: return "CUDA error";
+    case SNTRUP_E_WORKSPACE: return "device allocation failed";
+    case SNTRUP_E_INTERNAL: return "internal error (retry bound exceeded)";
+    default: return "unknown error";
+    }
+}
+
+int sntrup_batch_keygen_ex(int param_set, uint64_t n_keys, uint64_t seed, uint8_t *pk_out,
+                           uint8_t *sk_out, const sntrup_keygen_opts *opt) {
+    ParamInfo pi;
+    if (!param_info(param_set, &pi)) return SNTRUP_E_PARAM;
+    if (n_keys == 0 || !pk_out || !sk_out) return SNTRUP_E_ARG;
+    sntrup_keygen_opts o{};
+    if (opt) o = *opt;
+    std::lock_guard<std::mutex> lk(g_mu);
+    SNTRUP_DISPATCH(param_set, return keygen_impl<PS>(n_keys, seed, pk_out, sk_out, o));
+    return SNTRUP_E_PARAM;
+}
+
+int sntrup_batch_keygen(int param_set, uint64_t n_keys, uint64_t seed, uint8_t *pk_out,
+                        uint8_t *sk_out) {
+    return sntrup_batch_keygen_ex(param_set, n_keys, seed, pk_out, sk_out, nullptr);
+}
+
+size_t sntrup_keygen_workspace_bytes(int param_set, uint64_t n_keys, uint32_t batch_size) {
+    ParamInfo pi;
+    if (!param_info(param_set, &pi) || n_keys == 0) return 0;
+    const int B = batch_size ? (int)batch_size : 32;
+    uint64_t chunk = 65536;
+    chunk = (chunk + B - 1) / B * B;
+    if (chunk > n_keys) chunk = (n_keys + B - 1) / B * B;
+    const TreePlan tp = make_plan((long long)chunk, B);
+    const long long inner = tp.inner_rows();
+    return 3 * align256(chunk * pi.p16) + align256(chunk) + 2 * align256(inner * pi.p16) +
+           2 * align256(inner * pi.p8 * 2) + 2 * align256(chunk * pi.p8 * 2) + 4096;
+}
+
+int rq_mul_batch(int param_set, uint64_t n, const int16_t *a, const int16_t *b, int16_t *c,
+                 void *stream) {
+    ParamInfo pi;
+    if (!param_info(param_set, &pi)) return SNTRUP_E_PARAM;
+    if (n == 0 || !a || !b || !c) return SNTRUP_E_ARG;
+    MulArgs m{};
+    m.mode = MUL_ZIP;
+    m.n_out = (long long)n;
+    m.X = RowDesc{a, pi.p8, 2, 1};
+    m.Y = RowDesc{b, pi.p8, 2, 1};
+    m.out = c;
+    m.out_stride = pi.p8;
+    m.out_bytes = 2;
+    m.periodic = 1;
+    SNTRUP_DISPATCH(param_set, return launch_mul<PS, PS::Q>(m, (cudaStream_t)stream));
+    return SNTRUP_E_PARAM;
+}
+
+int r3_mul_batch(int param_set, uint64_t n, const int8_t *a, const int8_t *b, int8_t *c,
+                 void *stream) {
+    ParamInfo pi;
+    if (!param_info(param_set, &pi)) return SNTRUP_E_PARAM;
+    if (n == 0 || !a || !b || !c) return SNTRUP_E_ARG;
+    MulArgs m{};
+    m.mode = MUL_ZIP;
+    m.n_out = (long long)n;
+    m.X = RowDesc{a, pi.p16, 1, 1};
+    m.Y = RowDesc{b, pi.p16, 1, 1};
+    m.out = c;
+    m.out_stride = pi.p16;
+    m.out_bytes = 1;
+    m.periodic = 0;
+    SNTRUP_DISPATCH(param_set, return launch_mul<PS, 3>(m, (cudaStream_t)stream));
+    return SNTRUP_E_PARAM;
+}
+
+int rq_recip_batch(int param_set, uint64_t n, const int16_t *a, int16_t *out, uint32_t batch_size,
+                   uint64_t *bad_index, void *stream) {
+    ParamInfo pi;
+    if (!param_info(param_set, &pi)) return SNTRUP_E_PARAM;
+    if (n == 0 || !a || !out) return SNTRUP_E_ARG;
+    std::lock_guard<std::mutex> lk(g_mu);
+    SNTRUP_DISPATCH(param_set, return rq_recip_impl<PS>(n, a, out, batch_size, bad_index, (cudaStream_t)stream));
+    return SNTRUP_E_PARAM;
+}
+
+int r3_recip_batch(int param_set, uint64_t n, const int8_t *g, int8_t *out, uint8_t *ok,
+                   uint32_t batch_size, void *stream) {
+    ParamInfo pi;
+    if (!param_info(param_set, &pi)) return SNTRUP_E_PARAM;
+    if (n == 0 || !g || !out || !ok) return SNTRUP_E_ARG;
+    std::lock_guard<std::mutex> lk(g_mu);
+    SNTRUP_DISPATCH(param_set, return r3_recip_impl<PS>(n, g, out, ok, batch_size, (cudaStream_t)stream));
+    return SNTRUP_E_PARAM;
+}
+
+int r3_is_invertible_batch(int param_set, uint64_t n, const int8_t *g, uint8_t *ok, void *stream) {
+    ParamInfo pi;
+    if (!param_info(param_set, &pi)) return SNTRUP_E_PARAM;
+    if (n == 0 || !g || !ok) return SNTRUP_E_ARG;
+    int8_t *scratch = nullptr;
+    CK(cudaMalloc(&scratch, n * pi.p16));
+    int rc = r3_recip_batch(param_set, n, g, scratch, ok, 32, stream);
+    cudaFree(scratch);
+    return rc;
+}
+
+int rq_encode_batch(int param_set, uint64_t n, const int16_t *h, uint8_t *pk, void *stream) {
+    ParamInfo pi;
+    if (!param_info(param_set, &pi)) return SNTRUP_E_PARAM;
+    if (n == 0 || !h || !pk) return SNTRUP_E_ARG;
+    std::lock_guard<std::mutex> lk(g_mu);
+    int dev;
+    CK(cudaGetDevice(&dev));
+    SNTRUP_DISPATCH(param_set, {
+        DevTables *tb;
+        int rc = build_tables(dev, PS::P, PS::WT, &tb);
+        if (rc) return rc;
+        EncArgs ea{};
+        ea.n = n; ea.h = h; ea.pk = pk; ea.t = tb->enc;
+        encode_kernel<PS><<<(unsigned)((n + 3) / 4), 128, 0, (cudaStream_t)stream>>>(ea);
+        LAUNCHED();
+        return SNTRUP_OK;
+    });
+    return SNTRUP_E_PARAM;
+}
+
+void sntrup_release_workspace(void) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (g_ws.base) {
+        cudaDeviceSynchronize();
+        cudaFree(g_ws.base);
+        g_ws.base = nullptr;
+        g_ws.cap = 0;
+    }
+}
+
+uint64_t sntrup_kernel_launch_count(void) { return g_launches.load(); }
+
+void sntrup_profile_enable(int on) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    prof_drain();
+    g_prof_on = on != 0;
+}
+
+int sntrup_profile_read(int reset, double *ms, double *units, uint64_t *launches, int max_classes) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    prof_drain();
+    const int n = max_classes < PC_N ? max_classes : PC_N;
+    for (int i = 0; i < n; i++) {
+        if (ms) ms[i] = g_agg[i].ms;
+        if (units) units[i] = g_agg[i].units;
+        if (launches) launches[i] = g_agg[i].launches;
+    }
+    if (reset)
+        for (int i = 0; i < PC_N; i++) g_agg[i] = ProfAgg{};
+    return PC_N;
+}
+
+}  // extern "C"

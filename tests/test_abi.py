@@ -1,0 +1,118 @@
+"""CPU checks of the boundary: the C-ABI library loads and exports every symbol the header
+declares; host-only queries work without a GPU (no kernel is launched here)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "sntrup_gpu.h")
+
+
+def _build_mod():
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "_sntrup_build", os.path.join(ROOT, "paper_2106_08759_b200", "_build.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+@pytest.fixture(scope="module")
+def lib():
+    b = _build_mod()
+    b.build()
+    return ctypes.CDLL(b.LIB)
+
+
+def declared_functions():
+    txt = open(HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    names = re.findall(r"^\s*(?:const\s+)?[A-Za-z_][\w\s\*]*?\b([a-z_][a-z0-9_]*)\s*\(", txt, flags=re.M)
+    return sorted(set(n for n in names if n not in ("defined",)))
+
+
+def test_header_declares_the_north_star_calls():
+    names = declared_functions()
+    for n in ("sntrup_batch_keygen", "rq_mul_batch", "rq_recip_batch", "r3_recip_batch"):
+        assert n in names
+
+
+def test_library_exports_every_declared_symbol(lib):
+    out = subprocess.run(["nm", "-D", "--defined-only", _build_mod().LIB], capture_output=True, text=True).stdout
+    exported = set(l.split()[-1] for l in out.splitlines() if l.strip())
+    missing = [n for n in declared_functions() if n not in exported]
+    assert not missing, missing
+
+
+def test_params_host_query(lib):
+    import paper_2106_08759_b200 as S
+    assert S.params(761) == dict(p=761, q=4591, w=286, p16=768, p8=768, pk_bytes=1158, sk_bytes=382)
+    exp = {653: (994, 328), 857: (1322, 430), 953: (1505, 478), 1013: (1623, 508), 1277: (2067, 640)}
+    for ps, (pk, sk) in exp.items():
+        P = S.params(ps)
+        assert (P["pk_bytes"], P["sk_bytes"]) == (pk, sk)
+    with pytest.raises(S.SntrupError) as e:
+        S.params(512)
+    assert e.value.code == S.SNTRUP_E_PARAM
+
+
+def test_argument_errors_without_gpu(lib):
+    # n == 0 and unknown parameter sets are rejected before any device work
+    import paper_2106_08759_b200 as S
+    assert S._lib.sntrup_batch_keygen(761, 0, 1, None, None) == S.SNTRUP_E_ARG
+    assert S._lib.sntrup_batch_keygen(700, 5, 1, None, None) == S.SNTRUP_E_PARAM
+    assert S._lib.rq_mul_batch(761, 0, None, None, None, None) == S.SNTRUP_E_ARG
+    assert S._lib.sntrup_strerror(S.SNTRUP_E_NOT_INVERTIBLE) == b"element not invertible"
+
+
+def irreducible_gf3(f):
+    """Rabin's test over GF(3): x^(3^d) = x mod f and gcd(x^(3^(d/r)) - x, f) = 1, r | d prime."""
+    import numpy as np
+    import polytools as PT
+    d = len(f) - 1
+
+    def frob_pow(k):                       # x^(3^k) mod f
+        h = np.array([0, 1])
+        for _ in range(k):
+            h = PT.gf_divmod(np.mod(PT.gf_mul(PT.gf_mul(h, h, 3), h, 3), 3), f, 3)[1]
+        return h
+
+    def minus_x(h):
+        h = np.concatenate([h, np.zeros(max(0, 2 - len(h)), np.int64)])
+        h[1] = (h[1] - 1) % 3
+        return PT.trim(h)
+
+    if len(minus_x(frob_pow(d))):
+        return False
+    for r in [r for r in range(2, d + 1) if d % r == 0 and all(r % s for s in range(2, r))]:
+        if len(PT.gf_gcd(f, minus_x(frob_pow(d // r)), 3)) > 1:
+            return False
+    return True
+
+
+def test_factor_tables_are_factors():
+    # the generated small-factor tables divide x^p - x - 1 over GF(3) and are irreducible of
+    # the stated degree (checked with the tests' own polynomial code)
+    import sys
+    sys.path.insert(0, os.path.dirname(__file__))
+    import numpy as np
+    import polytools as PT
+    src = open(os.path.join(ROOT, "paper_2106_08759_b200", "csrc", "factor_tables.h")).read()
+    rows = re.findall(r"\{(\d+), (\d+), \{([\d, ]+)\}, \{([^}]*)\}\}", src)
+    assert len(rows) == 6
+    for p, cnt, degs, coefs in rows:
+        p = int(p)
+        degs = [int(d) for d in degs.split(",")]
+        coefs = re.findall(r'"(\d+)"', coefs)
+        assert len(coefs) == int(cnt) == len(degs)
+        for d, cs in zip(degs, coefs):
+            f = np.array([int(c) for c in cs])
+            assert len(f) == d + 1 and f[-1] == 1
+            _, r = PT.gf_divmod(PT.modulus(p, 3), f, 3)
+            assert len(r) == 0
+            assert irreducible_gf3(f)
+    # 761: f1 digits match SURVEY C16's golden table check
+    assert '"22022212120211112011"' in src
