@@ -132,6 +132,11 @@ void sntrup_release_workspace(void);
 /* Number of kernels this library launched since load (device work only; for bench accounting). */
 uint64_t sntrup_kernel_launch_count(void);
 
+/* Select the ring-product implementation used by every call (measurement / A-B evidence):
+   0 = tensor cores (tcgen05.mma kind::i8 Hankel GEMM, the default), 1 = int32 schoolbook on the
+   integer pipes (v1).  Both are exact.  Returns SNTRUP_OK or SNTRUP_E_ARG. */
+int sntrup_set_mul_impl(int impl);
+
 /* Measurement hooks (bench.py).  When enabled, every kernel launch is bracketed by CUDA events
    recorded on its launching stream.  sntrup_profile_read() waits for the recorded events and
    returns, per kernel class, the summed device milliseconds, the summed work units and the

@@ -61,6 +61,7 @@ _lib.r3_is_invertible_batch.argtypes = [_i32, _u64, _vp, _vp, _vp]
 _lib.rq_encode_batch.argtypes = [_i32, _u64, _vp, _vp, _vp]
 _lib.sntrup_release_workspace.restype = None
 _lib.sntrup_kernel_launch_count.restype = _u64
+_lib.sntrup_set_mul_impl.argtypes = [_i32]
 _lib.sntrup_profile_enable.restype = None
 _lib.sntrup_profile_enable.argtypes = [_i32]
 _lib.sntrup_profile_read.restype = _i32
@@ -69,7 +70,8 @@ _lib.sntrup_profile_read.argtypes = [_i32, _vp, _vp, _vp, _i32]
 EXPORTED = ("sntrup_params", "sntrup_strerror", "sntrup_batch_keygen", "sntrup_batch_keygen_ex",
             "sntrup_keygen_workspace_bytes", "rq_mul_batch", "r3_mul_batch", "rq_recip_batch",
             "r3_recip_batch", "r3_is_invertible_batch", "rq_encode_batch",
-            "sntrup_release_workspace", "sntrup_kernel_launch_count", "sntrup_profile_enable",
+            "sntrup_release_workspace", "sntrup_kernel_launch_count", "sntrup_set_mul_impl",
+            "sntrup_profile_enable",
             "sntrup_profile_read")
 
 PROFILE_CLASSES = ("sample", "r3_mul", "rq_mul", "r3_inv", "rq_inv", "repair", "encode", "other")
@@ -228,6 +230,15 @@ def release_workspace():
 
 def kernel_launch_count() -> int:
     return int(_lib.sntrup_kernel_launch_count())
+
+
+MUL_TENSOR_CORE = 0
+MUL_SCHOOLBOOK = 1
+
+
+def set_mul_impl(impl: int):
+    """0 = tcgen05 int8 Hankel-GEMM ring product (default), 1 = int32 schoolbook (v1)."""
+    _check(_lib.sntrup_set_mul_impl(int(impl)), "sntrup_set_mul_impl")
 
 
 def profile_enable(on: bool = True):

@@ -27,6 +27,7 @@ struct MulArgs {
     long long out_stride;   // elements
     int out_bytes;          // 1 or 2
     int periodic;           // both operands full-size -> lazy reductions inside the tile loop
+    int swap;               // tensor-core path: the second operand takes the A (Hankel) role
 };
 
 template <int NP>

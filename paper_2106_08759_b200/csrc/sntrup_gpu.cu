@@ -25,6 +25,7 @@
 #include "factor_tables.h"
 #include "ringmul.cuh"
 #include "sample.cuh"
+#include "tcmul.cuh"
 
 using namespace sntrup;
 
@@ -306,16 +307,67 @@ TreePlan make_plan(long long m, int B) {
 }
 
 // ------------------------------------------------------------------------------ launches
-template <class PS, int M>
-int launch_mul(const MulArgs &a, cudaStream_t s) {
-    if (a.n_out <= 0) return SNTRUP_OK;
-    const int threads = (PS::P8 / 8 + 31) / 32 * 32;
-    long long grid = a.n_out;
-    if (grid > (1LL << 30)) grid = 1LL << 30;
-    ProfScope ps_(M == 3 ? PC_MUL_R3 : PC_MUL_RQ, (double)a.n_out, s);
-    ring_mul_kernel<PS, M><<<(unsigned)grid, threads, 0, s>>>(a);
+int g_mul_impl = 0;                                 // 0 = tensor cores (tcmul.cuh), 1 = int32 schoolbook
+
+struct DevInfo { int sms = 0; };
+DevInfo &dev_info() {
+    static std::map<int, DevInfo> m;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    DevInfo &d = m[dev];
+    if (!d.sms) cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
+    return d;
+}
+
+template <class PS, int M, int LA, int LB>
+int launch_tc(const MulArgs &a, cudaStream_t s) {
+    using G = TcGeom<PS, LA, LB>;
+    auto kern = tc_mul_kernel<PS, M, LA, LB>;
+    static std::map<int, int> per_sm;                 // device -> resident CTAs per SM
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    auto it = per_sm.find(dev);
+    if (it == per_sm.end()) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        int nb = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 128, G::SMEM));
+        const int by_smem = (227 * 1024) / (G::SMEM + 1024);    // 1 KB reserved per CTA
+        if (nb < by_smem) nb = by_smem;
+        if (nb < 1) nb = 1;
+        if (nb * G::TCOLS > 512) nb = 512 / G::TCOLS;   // TMEM columns per SM
+        it = per_sm.emplace(dev, nb).first;
+    }
+    long long grid = (long long)it->second * dev_info().sms;
+    if (grid > a.n_out) grid = a.n_out;
+    kern<<<(unsigned)grid, 128, G::SMEM, s>>>(a);
     LAUNCHED();
     return SNTRUP_OK;
+}
+
+// la / lb: int8 limbs of the first / second operand (1 = small: R/3, 3f, g; 2 = R/q element).
+template <class PS, int M>
+int launch_mul(MulArgs a, cudaStream_t s, int la = 2, int lb = 2) {
+    if (a.n_out <= 0) return SNTRUP_OK;
+    ProfScope ps_(M == 3 ? PC_MUL_R3 : PC_MUL_RQ, (double)a.n_out, s);
+    if (g_mul_impl == 1) {
+        const int threads = (PS::P8 / 8 + 31) / 32 * 32;
+        long long grid = a.n_out;
+        if (grid > (1LL << 30)) grid = 1LL << 30;
+        ring_mul_kernel<PS, M><<<(unsigned)grid, threads, 0, s>>>(a);
+        LAUNCHED();
+        return SNTRUP_OK;
+    }
+    if constexpr (M == 3) {
+        a.swap = 0;
+        return launch_tc<PS, M, 1, 1>(a, s);
+    } else {
+        if (la == 1 && lb == 1) { a.swap = 0; return launch_tc<PS, M, 1, 1>(a, s); }
+        if (la == 1) { a.swap = 0; return launch_tc<PS, M, 1, 2>(a, s); }
+        if (lb == 1) { a.swap = 1; return launch_tc<PS, M, 1, 2>(a, s); }
+        a.swap = 0;
+        return launch_tc<PS, M, 2, 2>(a, s);
+    }
 }
 
 template <class PS, int M>
@@ -357,7 +409,8 @@ int batch_inverse(const TreePlan &tp, RowDesc X0, void *out0, int out_bytes, lon
         a.out_stride = stride;
         a.out_bytes = out_bytes;
         a.periodic = (M != 3) && !(l == 1 && leaves_small);
-        if ((rc = launch_mul<PS, M>(a, s))) return rc;
+        const int lx = (M == 3 || (l == 1 && leaves_small)) ? 1 : 2;
+        if ((rc = launch_mul<PS, M>(a, s, lx, lx))) return rc;
         *nprod += tp.cnt[l - 1] / 2;
     }
     {                                                // roots
@@ -382,7 +435,9 @@ int batch_inverse(const TreePlan &tp, RowDesc X0, void *out0, int out_bytes, lon
         a.out_stride = od.stride;
         a.out_bytes = out_bytes;
         a.periodic = (M != 3) && !(l == 1 && leaves_small);
-        if ((rc = launch_mul<PS, M>(a, s))) return rc;
+        // operands: (inverse of the parent: big) x (sibling: small at level 1 over small leaves)
+        const int lsib = (M == 3 || (l == 1 && leaves_small)) ? 1 : 2;
+        if ((rc = launch_mul<PS, M>(a, s, M == 3 ? 1 : 2, lsib))) return rc;
         *nprod += (tp.cnt[l - 1] / 2) * 2;
     }
     return SNTRUP_OK;
@@ -495,7 +550,7 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
             a.out_stride = PS::P8;
             a.out_bytes = 2;
             a.periodic = 0;
-            if ((rc = launch_mul<PS, PS::Q>(a, s))) return rc;
+            if ((rc = launch_mul<PS, PS::Q>(a, s, 1, 2))) return rc;       // g small, fbar big
             n_rq += m;
         }
         n_inv += 2 * tp.cnt[tp.L];
@@ -765,7 +820,7 @@ int r3_mul_batch(int param_set, uint64_t n, const int8_t *a, const int8_t *b, in
     m.out_stride = pi.p16;
     m.out_bytes = 1;
     m.periodic = 0;
-    SNTRUP_DISPATCH(param_set, return launch_mul<PS, 3>(m, (cudaStream_t)stream));
+    SNTRUP_DISPATCH(param_set, return launch_mul<PS, 3>(m, (cudaStream_t)stream, 1, 1));
     return SNTRUP_E_PARAM;
 }
 
@@ -831,6 +886,13 @@ void sntrup_release_workspace(void) {
 }
 
 uint64_t sntrup_kernel_launch_count(void) { return g_launches.load(); }
+
+int sntrup_set_mul_impl(int impl) {
+    if (impl != 0 && impl != 1) return SNTRUP_E_ARG;
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_mul_impl = impl;
+    return SNTRUP_OK;
+}
 
 void sntrup_profile_enable(int on) {
     std::lock_guard<std::mutex> lk(g_mu);

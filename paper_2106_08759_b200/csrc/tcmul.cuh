@@ -1,0 +1,415 @@
+// tcmul.cuh -- batched ring products in R/q and R/3 on the 5th-generation tensor cores
+// (tcgen05.mma kind::i8, int32 accumulators in TMEM).
+//
+// The ring product of section 3.3: full product c = a*b of two length-p
+// polynomials, then reduction by x^p - x - 1 (x^p = x + 1), coefficients centered mod q (or 3).
+// The paper computes it with Karatsuba / Schoenhage-Nussbaumer on 16-bit AVX2 lanes
+// (P:4072-6339); on B200 the full product is a dense integer contraction, so it is posed as one
+// GEMM per product on the int8 tensor cores:
+//
+//   raw[128 t + r] = sum_k A[r][k] * B[t][k],   A[r][k] = a[r + k - 127],  B[t][k] = b[128 t + 127 - k]
+//
+// (M = 128 output coefficients per block r, N = output blocks t, K = p + 127 rounded up to 32).
+// A is a Hankel matrix.  In the no-swizzle K-major UMMA layout, core matrices are 8 rows x 16 B
+// at SBO = 128 B (M direction) and LBO = 256 B (K direction); with those strides the tensor core
+// reads element (r, k) of the descriptor's tile at byte 16*(r + k) + (k mod 16) of a "sliding
+// window" buffer whose 16-byte row rho holds hA[rho .. rho+15] (hA = a shifted by 127).  So the
+// whole 128 x K Hankel operand costs 16 B per row of a (16*(K+112) B) instead of 128*K B.
+// B is materialised (N rows of K bytes) from aligned 16-byte chunks of the reversed b.
+//
+// Coefficients of R/q do not fit int8: a big operand is split into limbs v = 64*hi + lo with
+// lo in [-32, 31] and hi in [-62, 62] (|v| <= (q-1)/2 <= 3939).  A-limbs are separate MMAs into
+// separate TMEM accumulators; B-limbs are stacked along N.  Small operands (R/3 elements, 3f,
+// g, the unit) are one limb.  Exactness: every accumulator is an exact int32 sum
+// (|sum| <= p * 62 * 62 < 2^23), combined mod q in the epilogue.
+//
+// One CTA (4 warps) per product, persistent over the grid; thread r owns TMEM lane r (output
+// coefficient r of every block) in the epilogue.  Several CTAs per SM overlap one CTA's operand
+// build / epilogue with another's MMAs.
+#pragma once
+#include "common.cuh"
+#include "ringmul.cuh"
+
+namespace sntrup {
+
+// ----------------------------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// UMMA shared-memory descriptor, SWIZZLE_NONE, K-major (version 1 for sm_100).
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+    d |= (uint64_t)1 << 46;                 // version
+    return d;                               // base_offset 0, lbo_mode 0, layout SWIZZLE_NONE (0)
+}
+
+// Instruction descriptor: kind::i8, D = s32, A = B = signed int8, both K-major, M = 128, N.
+__host__ __device__ constexpr uint32_t umma_idesc_i8(int N) {
+    return (2u << 4)                        // c_format S32
+         | (1u << 7)                        // a_format signed int8
+         | (1u << 10)                       // b_format signed int8
+         | ((uint32_t)(N >> 3) << 17)       // n_dim
+         | ((uint32_t)(128 >> 4) << 24);    // m_dim
+}
+
+__device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t phase) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+    return ok != 0;
+}
+
+// Bounded wait: a descriptor or protocol bug must not hang the GPU (trap after ~2^31 cycles).
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+    const long long t0 = clock64();
+    while (!mbar_try_wait(bar, phase)) {
+        if (clock64() - t0 > (1LL << 31)) __trap();
+    }
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, int (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+          "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// ----------------------------------------------------------------------------------- geometry
+template <class PS, int LA, int LB>
+struct TcGeom {
+    static constexpr int P = PS::P;
+    static constexpr int NKS = (P + 127 + 31) / 32;          // K steps of 32
+    static constexpr int K = 32 * NKS;
+    static constexpr int NBLK = (2 * P - 1 + 127) / 128;     // output blocks of 128 coefficients
+    static constexpr int NL = (NBLK + 7) / 8 * 8;            // B rows per limb
+    static constexpr int NB = (LB * NL + 15) / 16 * 16;      // N of the MMA
+    static constexpr int AROWS = 32 * NKS + 113;             // window rows 0..AROWS-1 (row 0 unused)
+    static constexpr int A_BYTES = (AROWS + 7) / 8 * 128;    // 16 B per row, 128-aligned
+    static constexpr int HA_LEN = (AROWS + 16 + 127) / 128 * 128;   // hA[128 + j] = limb(a_j)
+    static constexpr int ZR_LEN = (128 * NL + K + 127) / 128 * 128; // zr[128 NL - 1 - j] = limb(b_j)
+    static constexpr int B_BYTES = 2 * NKS * NB * 16;
+    static constexpr int RAW_BYTES = 128 * NBLK * 4;
+    static constexpr int TCOLS_USED = LA * NB;
+    static constexpr int TCOLS = TCOLS_USED <= 32 ? 32 : TCOLS_USED <= 64 ? 64 : TCOLS_USED <= 128 ? 128 : 256;
+    static constexpr int NCHK = PS::P8 / 8;                   // 8-coefficient input chunks
+    static constexpr int CH = (NCHK + 127) / 128;             // chunks per thread
+    // smem carve-up (bytes, all 128-aligned); raw aliases the A windows (dead after the MMAs)
+    static constexpr int OFF_A = 0;
+    static constexpr int OFF_B = OFF_A + LA * A_BYTES;
+    static constexpr int OFF_HA = OFF_B + B_BYTES;
+    static constexpr int OFF_ZR = OFF_HA + LA * HA_LEN;
+    static constexpr int OFF_BAR = OFF_ZR + LB * ZR_LEN;
+    static constexpr int SMEM = OFF_BAR + 128;
+    static_assert(RAW_BYTES <= LA * A_BYTES, "raw buffer must fit in the A region");
+    static_assert(NB <= 256, "N too large");
+    static_assert(128 + PS::P8 <= HA_LEN, "hA too short");
+};
+
+// limb l (0 = hi, 1 = lo) of a centered coefficient when the operand has L limbs
+template <int L>
+__device__ __forceinline__ int limb_of(int v, int l) {
+    if (L == 1) return v;
+    const int lo = ((v + 32) & 63) - 32;
+    return l == 0 ? (v - lo) >> 6 : lo;
+}
+
+// 16 raw bytes of chunk c (coefficients 8c .. 8c+7) of row `row` (int16: 16 B, int8: 8 B)
+__device__ __forceinline__ uint4 load_chunk(const RowDesc &d, long long row, int c) {
+    if (d.bytes == 2)
+        return __ldg(reinterpret_cast<const uint4 *>((const int16_t *)d.ptr + row * d.stride) + c);
+    const uint2 v = __ldg(reinterpret_cast<const uint2 *>((const int8_t *)d.ptr + row * d.stride) + c);
+    return make_uint4(v.x, v.y, 0, 0);
+}
+
+__device__ __forceinline__ void decode_chunk(const uint4 r, int bytes, int scale, bool unit, int c, int (&v)[8]) {
+    if (bytes == 2) {
+        const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+        for (int i = 0; i < 8; i++) v[i] = scale * (int)(int16_t)(w[i >> 1] >> (16 * (i & 1)));
+    } else {
+        const uint32_t w[2] = {r.x, r.y};
+#pragma unroll
+        for (int i = 0; i < 8; i++) v[i] = scale * (int)(int8_t)(w[i >> 2] >> (8 * (i & 3)));
+    }
+    if (unit) {
+#pragma unroll
+        for (int i = 0; i < 8; i++) v[i] = (c == 0 && i == 0) ? 1 : 0;
+    }
+}
+
+__device__ __forceinline__ uint32_t pack4(int a, int b, int c, int d) {
+    return (uint32_t)(a & 0xff) | ((uint32_t)(b & 0xff) << 8) | ((uint32_t)(c & 0xff) << 16) |
+           ((uint32_t)(d & 0xff) << 24);
+}
+
+// M = modulus (3 or q); LA / LB = limbs of the A-role / B-role operand.
+template <class PS, int M, int LA, int LB>
+__global__ void __launch_bounds__(128) tc_mul_kernel(MulArgs a) {
+    using G = TcGeom<PS, LA, LB>;
+    constexpr int P = PS::P;
+    constexpr int CH = G::CH;
+    extern __shared__ __align__(1024) uint8_t sm[];
+    uint8_t *sA = sm + G::OFF_A;
+    uint8_t *sB = sm + G::OFF_B;
+    uint8_t *sHA = sm + G::OFF_HA;
+    uint8_t *sZR = sm + G::OFF_ZR;
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sm + G::OFF_BAR);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sm + G::OFF_BAR + 64);
+    int *raw = reinterpret_cast<int *>(sm + G::OFF_A);
+    const int tid = threadIdx.x, warp = tid >> 5;
+
+    // ---- one-time setup: zero staging + B (pads stay zero forever), barrier, TMEM
+    for (int i = tid; i < (G::OFF_BAR - G::OFF_B) / 16; i += 128)
+        reinterpret_cast<uint4 *>(sB)[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"((uint32_t)G::TCOLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    constexpr uint32_t IDESC = umma_idesc_i8(G::NB);
+    uint32_t phase = 0;
+
+    // operand sources of product `prod`: u -> A role, v -> B role (a.swap exchanges them)
+    auto operands = [&](long long prod, RowDesc &du, long long &ru, bool &unit_u, RowDesc &dv,
+                        long long &rv, bool &unit_v) {
+        unit_u = false;
+        unit_v = false;
+        if (a.mode == MUL_ZIP) {
+            du = a.X; ru = prod; dv = a.Y; rv = prod;
+        } else if (a.mode == MUL_PAIRS) {
+            du = a.X; ru = 2 * prod; dv = a.X; rv = 2 * prod + 1;
+            unit_v = rv >= a.cnt_in;
+        } else {
+            du = a.Y; ru = prod >> 1; dv = a.X; rv = prod ^ 1;
+            unit_v = rv >= a.cnt_in;
+        }
+        if (a.swap) {
+            const RowDesc td = du; du = dv; dv = td;
+            const long long tr = ru; ru = rv; rv = tr;
+            unit_u = unit_v; unit_v = false;
+        }
+    };
+    // register prefetch of the next product's rows (in flight during the MMAs / epilogue)
+    uint4 pu[CH], pv[CH];
+    auto prefetch = [&](long long prod) {
+        if (prod >= a.n_out) return;
+        RowDesc du, dv; long long ru, rv; bool uu, uv;
+        operands(prod, du, ru, uu, dv, rv, uv);
+#pragma unroll
+        for (int h = 0; h < CH; h++) {
+            const int c = tid + 128 * h;
+            if (c < G::NCHK) {
+                pu[h] = uu ? make_uint4(0, 0, 0, 0) : load_chunk(du, ru, c);
+                pv[h] = uv ? make_uint4(0, 0, 0, 0) : load_chunk(dv, rv, c);
+            }
+        }
+    };
+    prefetch(blockIdx.x);
+
+    for (long long prod = blockIdx.x; prod < a.n_out; prod += gridDim.x) {
+        RowDesc du, dv; long long ru, rv; bool unit_u, unit_v;
+        operands(prod, du, ru, unit_u, dv, rv, unit_v);
+        // ---- stage limbs (8-byte aligned groups): hA_l[128 + j] = limb_l(u_j),
+        //      zr_l[128 NL - 1 - j] = limb_l(v_j) (reversed within the group)
+#pragma unroll
+        for (int h = 0; h < CH; h++) {
+            const int c = tid + 128 * h;
+            if (c < G::NCHK) {
+                int uv8[8], vv8[8];
+                decode_chunk(pu[h], du.bytes, du.scale, unit_u, c, uv8);
+                decode_chunk(pv[h], dv.bytes, dv.scale, unit_v, c, vv8);
+#pragma unroll
+                for (int l = 0; l < LA; l++) {
+                    int x[8];
+#pragma unroll
+                    for (int i = 0; i < 8; i++) x[i] = limb_of<LA>(uv8[i], l);
+                    *reinterpret_cast<uint2 *>(sHA + l * G::HA_LEN + 128 + 8 * c) =
+                        make_uint2(pack4(x[0], x[1], x[2], x[3]), pack4(x[4], x[5], x[6], x[7]));
+                }
+#pragma unroll
+                for (int l = 0; l < LB; l++) {
+                    int x[8];
+#pragma unroll
+                    for (int i = 0; i < 8; i++) x[i] = limb_of<LB>(vv8[i], l);
+                    *reinterpret_cast<uint2 *>(sZR + l * G::ZR_LEN + 128 * G::NL - 8 - 8 * c) =
+                        make_uint2(pack4(x[7], x[6], x[5], x[4]), pack4(x[3], x[2], x[1], x[0]));
+                }
+            }
+        }
+        __syncthreads();
+        // ---- A: sliding windows, row rho = hA[rho .. rho+15] (descriptor starts at row 1)
+#pragma unroll 1
+        for (int w = tid; w < LA * G::AROWS; w += 128) {
+            const int l = w / G::AROWS, rho = w - l * G::AROWS;
+            const uint32_t *src = reinterpret_cast<const uint32_t *>(sHA + l * G::HA_LEN) + (rho >> 2);
+            const uint32_t s = (uint32_t)(rho & 3);
+            const uint32_t w0 = src[0], w1 = src[1], w2 = src[2], w3 = src[3], w4 = src[4];
+            const uint32_t sel = 0x3210u + s * 0x1111u;       // bytes s..s+3 of (hi:lo)
+            uint4 o;
+            o.x = __byte_perm(w0, w1, sel);
+            o.y = __byte_perm(w1, w2, sel);
+            o.z = __byte_perm(w2, w3, sel);
+            o.w = __byte_perm(w3, w4, sel);
+            reinterpret_cast<uint4 *>(sA + l * G::A_BYTES)[rho] = o;
+        }
+        // ---- B: row (l*NL + t), K-chunk c = zr_l chunk 8(NL-1-t) + c
+        {
+            constexpr int NCH = 2 * G::NKS;
+            constexpr int C_HI_N = (NCH + 7) / 8;
+            constexpr int T_HI_N = G::NL / 8;
+            constexpr int TOT = LB * G::NL * 8 * C_HI_N;
+#pragma unroll 1
+            for (int w = tid; w < TOT; w += 128) {
+                // bank-spread order: 8 consecutive items differ in both t mod 8 and c mod 8
+                const int lo6 = w & 63, hi = w >> 6;
+                const int t_lo = lo6 & 7, c_lo = ((lo6 >> 3) + t_lo) & 7;
+                const int l = hi / (T_HI_N * C_HI_N);
+                const int rem = hi - l * (T_HI_N * C_HI_N);
+                const int t = (rem % T_HI_N) * 8 + t_lo;
+                const int c = (rem / T_HI_N) * 8 + c_lo;
+                if (c >= NCH) continue;
+                const uint4 v = reinterpret_cast<const uint4 *>(sZR + l * G::ZR_LEN)[8 * (G::NL - 1 - t) + c];
+                reinterpret_cast<uint4 *>(sB)[c * G::NB + l * G::NL + t] = v;
+            }
+        }
+        fence_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        // ---- MMAs (one thread)
+        if (tid == 0) {
+            tc_fence_after();
+            const uint32_t a0 = smem_u32(sA) + 16, b0 = smem_u32(sB);
+#pragma unroll 1
+            for (int ks = 0; ks < G::NKS; ks++) {
+                const uint64_t bd = umma_desc(b0 + ks * 32 * G::NB, G::NB * 16, 128);
+#pragma unroll
+                for (int l = 0; l < LA; l++) {
+                    const uint64_t ad = umma_desc(a0 + l * G::A_BYTES + ks * 512, 256, 128);
+                    umma_i8(tmem + l * G::NB, ad, bd, IDESC, ks > 0 ? 1u : 0u);
+                }
+            }
+            umma_commit(bar);
+        }
+        __syncwarp();
+        prefetch(prod + gridDim.x);
+        mbar_wait(bar, phase);
+        phase ^= 1;
+        tc_fence_after();
+        // ---- epilogue: thread tid = TMEM lane = coefficient r of every block
+        int acc[LA][LB][G::NL];
+        {
+            const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
+#pragma unroll
+            for (int l = 0; l < LA; l++)
+#pragma unroll
+                for (int c16 = 0; c16 < G::NB / 16; c16++) {
+                    int v[16];
+                    tmem_ld16(lane_addr + l * G::NB + 16 * c16, v);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int i = 0; i < 16; i++) {
+                        const int col = 16 * c16 + i;
+                        const int lb = col / G::NL, t = col - lb * G::NL;
+                        if (lb < LB) acc[l][lb][t] = v[i];
+                    }
+                }
+        }
+        tc_fence_before();
+        __syncthreads();     // all TMEM reads done (next MMAs may overwrite); A region now free
+#pragma unroll
+        for (int t = 0; t < G::NBLK; t++) {
+            int v;
+            if (LA == 1 && LB == 1) {
+                v = acc[0][0][t];
+            } else if (LA == 1) {
+                v = (64 * acc[0][0][t] + acc[0][1][t]) % M;
+            } else if (LB == 1) {
+                v = (64 * acc[0][0][t] + acc[1][0][t]) % M;
+            } else {
+                v = (4096 * (acc[0][0][t] % M) + 64 * (acc[0][1][t] + acc[1][0][t]) + acc[1][1][t]) % M;
+            }
+            raw[128 * t + tid] = v;
+        }
+        __syncthreads();
+        // ---- fold with x^p = x + 1, center, store 8 coefficients per thread and chunk
+        {
+            const int ostride_elems = a.out_bytes == 2 ? PS::P8 : PS::P16;
+            for (int c = tid; c < ostride_elems / 8; c += 128) {
+                int o[8];
+#pragma unroll
+                for (int i = 0; i < 8; i++) {
+                    const int k = 8 * c + i;
+                    int v = 0;
+                    if (k < P) {
+                        v = raw[k] + raw[k + P] + (k >= 1 ? raw[k + P - 1] : 0);
+                        v = canon<M>(v);
+                    }
+                    o[i] = v;
+                }
+                if (a.out_bytes == 2) {
+                    uint4 st;
+                    st.x = (uint32_t)(o[0] & 0xffff) | ((uint32_t)o[1] << 16);
+                    st.y = (uint32_t)(o[2] & 0xffff) | ((uint32_t)o[3] << 16);
+                    st.z = (uint32_t)(o[4] & 0xffff) | ((uint32_t)o[5] << 16);
+                    st.w = (uint32_t)(o[6] & 0xffff) | ((uint32_t)o[7] << 16);
+                    reinterpret_cast<uint4 *>((int16_t *)a.out + prod * a.out_stride)[c] = st;
+                } else {
+                    reinterpret_cast<uint2 *>((int8_t *)a.out + prod * a.out_stride)[c] =
+                        make_uint2(pack4(o[0], o[1], o[2], o[3]), pack4(o[4], o[5], o[6], o[7]));
+                }
+            }
+        }
+        // the next iteration's first __syncthreads orders these raw reads before A rewrites
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)G::TCOLS));
+}
+
+}  // namespace sntrup

@@ -1,6 +1,9 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 nvidia-smi > gpurun_out/smi.txt 2>&1
+timeout 300 python -m pytest tests/test_gpu_parity.py -x -q -k "rq_mul or r3_mul" -p no:cacheprovider > gpurun_out/pytest_mul.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_mul.log
+tail -3 gpurun_out/pytest_mul.log
+grep -q "rc=0" gpurun_out/pytest_mul.log || exit 1
 timeout 1200 python -m pytest tests -m gpu -q --timeout 400 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "rc=$?" >> gpurun_out/smoke.log
 timeout 600 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.log 2>&1; echo "rc=$?" >> gpurun_out/bench.log

@@ -66,6 +66,11 @@ def test_argument_errors_without_gpu(lib):
     assert S._lib.sntrup_batch_keygen(700, 5, 1, None, None) == S.SNTRUP_E_PARAM
     assert S._lib.rq_mul_batch(761, 0, None, None, None, None) == S.SNTRUP_E_ARG
     assert S._lib.sntrup_strerror(S.SNTRUP_E_NOT_INVERTIBLE) == b"element not invertible"
+    assert S._lib.sntrup_set_mul_impl(7) == S.SNTRUP_E_ARG
+    with pytest.raises(S.SntrupError):
+        S.set_mul_impl(-1)
+    S.set_mul_impl(S.MUL_SCHOOLBOOK)
+    S.set_mul_impl(S.MUL_TENSOR_CORE)
 
 
 def irreducible_gf3(f):

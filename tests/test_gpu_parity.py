@@ -17,6 +17,14 @@ from inputs import synth  # noqa: E402
 PSETS = [653, 761, 857, 953, 1013, 1277]
 
 
+@pytest.fixture(params=[S.MUL_TENSOR_CORE, S.MUL_SCHOOLBOOK], ids=["tc", "schoolbook"])
+def mul_impl(request):
+    """Run a test under both ring-product implementations (tcgen05 Hankel GEMM, int32 schoolbook)."""
+    S.set_mul_impl(request.param)
+    yield request.param
+    S.set_mul_impl(S.MUL_TENSOR_CORE)
+
+
 def oracle_keys(O, param, seed, idx):
     return O.keygen_many(param, seed, np.asarray(idx, dtype=np.uint64), want_polys=True)
 
@@ -42,7 +50,7 @@ def check_keys(O, param, seed, res, idx, offset=0):
 
 
 # --------------------------------------------------------------------------------- keygen
-def test_cfg1_all_32_keys(O):
+def test_cfg1_all_32_keys(O, mul_impl):
     # BASELINE configs[0]: sntrup761, 32 keys, seed 1, one tree of 32
     res = S.batch_keygen(761, 32, 1, batch_size=32, debug=True, stats=True)
     torch.cuda.synchronize()
@@ -73,7 +81,7 @@ def test_chunking_and_first_index(O):
 
 
 @pytest.mark.parametrize("param,seed", [(653, 4), (761, 2), (857, 4), (953, 4), (1013, 4), (1277, 5)])
-def test_param_sets(O, param, seed):
+def test_param_sets(O, param, seed, mul_impl):
     n = 160                                       # covers 653/1277 keys with two g draws
     res = S.batch_keygen(param, n, seed, batch_size=32, debug=True)
     torch.cuda.synchronize()
@@ -134,7 +142,7 @@ def edge_cases(p, p8, q):
 
 
 @pytest.mark.parametrize("param", PSETS)
-def test_rq_mul(O, param):
+def test_rq_mul(O, param, mul_impl):
     P = S.params(param)
     p, q, p8 = P["p"], P["q"], P["p8"]
     a = synth.uniform_rq(203, p, q, p8, seed=1)
@@ -148,8 +156,8 @@ def test_rq_mul(O, param):
     assert np.array_equal(c, ref)
 
 
-@pytest.mark.parametrize("param", [653, 761, 1277])
-def test_r3_mul(O, param):
+@pytest.mark.parametrize("param", PSETS)
+def test_r3_mul(O, param, mul_impl):
     P = S.params(param)
     p, p16 = P["p"], P["p16"]
     a = synth.small(150, p, p16, seed=4)
