@@ -120,7 +120,8 @@ struct TcGeom {
     static constexpr int NB = (LB * NL + 15) / 16 * 16;      // N of the MMA
     static constexpr int AROWS = 32 * NKS + 113;             // window rows 0..AROWS-1 (row 0 unused)
     static constexpr int A_BYTES = (AROWS + 7) / 8 * 128;    // 16 B per row, 128-aligned
-    static constexpr int HA_LEN = (AROWS + 16 + 127) / 128 * 128;   // hA[128 + j] = limb(a_j)
+    static constexpr int AROWS4 = (AROWS + 3) / 4;            // window rows are built 4 at a time
+    static constexpr int HA_LEN = (4 * AROWS4 + 20 + 127) / 128 * 128;   // hA[128 + j] = limb(a_j)
     static constexpr int ZR_LEN = (128 * NL + K + 127) / 128 * 128; // zr[128 NL - 1 - j] = limb(b_j)
     static constexpr int B_BYTES = 2 * NKS * NB * 16;
     static constexpr int RAW_BYTES = 128 * NBLK * 4;
@@ -138,6 +139,12 @@ struct TcGeom {
     static_assert(RAW_BYTES <= LA * A_BYTES, "raw buffer must fit in the A region");
     static_assert(NB <= 256, "N too large");
     static_assert(128 + PS::P8 <= HA_LEN, "hA too short");
+    static_assert(4 * AROWS4 * 16 <= A_BYTES, "A region too short");
+    // B build: (row, residue mod 8) work items; row = l*NL + t, K-chunks c = residue + 8i
+    static constexpr int BROWS = LB * NL;
+    static constexpr int NCHB = 2 * NKS;                      // 16-byte K-chunks per B row
+    static constexpr int BITEMS = BROWS * 8;
+    static constexpr int BPER = (BITEMS + 127) / 128;
 };
 
 // limb l (0 = hi, 1 = lo) of a centered coefficient when the operand has L limbs
@@ -213,6 +220,21 @@ __global__ void __launch_bounds__(128) tc_mul_kernel(MulArgs a) {
     const uint32_t tmem = *tmem_slot;
     constexpr uint32_t IDESC = umma_idesc_i8(G::NB);
     uint32_t phase = 0;
+    // fixed per-thread B-build items (product independent): 16-byte-unit offsets
+    int bsrc[G::BPER], bdst[G::BPER], bres[G::BPER];
+#pragma unroll
+    for (int h = 0; h < G::BPER; h++) {
+        const int w = tid + 128 * h;
+        if (w < G::BITEMS) {
+            const int row = w % G::BROWS, grp = w / G::BROWS;
+            const int l = row / G::NL, t = row - l * G::NL;
+            bres[h] = (grp + row) & 7;
+            bsrc[h] = l * (G::ZR_LEN / 16) + 8 * (G::NL - 1 - t);
+            bdst[h] = row;
+        } else {
+            bsrc[h] = -1; bdst[h] = 0; bres[h] = 0;
+        }
+    }
 
     // operand sources of product `prod`: u -> A role, v -> B role (a.swap exchanges them)
     auto operands = [&](long long prod, RowDesc &du, long long &ru, bool &unit_u, RowDesc &dv,
@@ -282,82 +304,83 @@ __global__ void __launch_bounds__(128) tc_mul_kernel(MulArgs a) {
             }
         }
         __syncthreads();
-        // ---- A: sliding windows, row rho = hA[rho .. rho+15] (descriptor starts at row 1)
+        // ---- A: sliding windows, row rho = hA[rho .. rho+15] (descriptor starts at row 1);
+        //      each work item builds rows 4m .. 4m+3 from 5 words, stores rotated by m (banks)
 #pragma unroll 1
-        for (int w = tid; w < LA * G::AROWS; w += 128) {
-            const int l = w / G::AROWS, rho = w - l * G::AROWS;
-            const uint32_t *src = reinterpret_cast<const uint32_t *>(sHA + l * G::HA_LEN) + (rho >> 2);
-            const uint32_t s = (uint32_t)(rho & 3);
-            const uint32_t w0 = src[0], w1 = src[1], w2 = src[2], w3 = src[3], w4 = src[4];
-            const uint32_t sel = 0x3210u + s * 0x1111u;       // bytes s..s+3 of (hi:lo)
-            uint4 o;
-            o.x = __byte_perm(w0, w1, sel);
-            o.y = __byte_perm(w1, w2, sel);
-            o.z = __byte_perm(w2, w3, sel);
-            o.w = __byte_perm(w3, w4, sel);
-            reinterpret_cast<uint4 *>(sA + l * G::A_BYTES)[rho] = o;
-        }
-        // ---- B: row (l*NL + t), K-chunk c = zr_l chunk 8(NL-1-t) + c
-        {
-            constexpr int NCH = 2 * G::NKS;
-            constexpr int C_HI_N = (NCH + 7) / 8;
-            constexpr int T_HI_N = G::NL / 8;
-            constexpr int TOT = LB * G::NL * 8 * C_HI_N;
-#pragma unroll 1
-            for (int w = tid; w < TOT; w += 128) {
-                // bank-spread order: 8 consecutive items differ in both t mod 8 and c mod 8
-                const int lo6 = w & 63, hi = w >> 6;
-                const int t_lo = lo6 & 7, c_lo = ((lo6 >> 3) + t_lo) & 7;
-                const int l = hi / (T_HI_N * C_HI_N);
-                const int rem = hi - l * (T_HI_N * C_HI_N);
-                const int t = (rem % T_HI_N) * 8 + t_lo;
-                const int c = (rem / T_HI_N) * 8 + c_lo;
-                if (c >= NCH) continue;
-                const uint4 v = reinterpret_cast<const uint4 *>(sZR + l * G::ZR_LEN)[8 * (G::NL - 1 - t) + c];
-                reinterpret_cast<uint4 *>(sB)[c * G::NB + l * G::NL + t] = v;
+        for (int w = tid; w < LA * G::AROWS4; w += 128) {
+            const int l = w / G::AROWS4, m = w - l * G::AROWS4;
+            const uint32_t *src = reinterpret_cast<const uint32_t *>(sHA + l * G::HA_LEN) + m;
+            uint32_t wd[5];
+#pragma unroll
+            for (int i = 0; i < 5; i++) wd[i] = src[i];
+            uint4 *dst = reinterpret_cast<uint4 *>(sA + l * G::A_BYTES) + 4 * m;
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                const int s_ = (i + m) & 3;
+                const uint32_t sel = 0x3210u + (uint32_t)s_ * 0x1111u;   // bytes s..s+3 of (hi:lo)
+                uint4 o;
+                o.x = __byte_perm(wd[0], wd[1], sel);
+                o.y = __byte_perm(wd[1], wd[2], sel);
+                o.z = __byte_perm(wd[2], wd[3], sel);
+                o.w = __byte_perm(wd[3], wd[4], sel);
+                dst[s_] = o;
             }
+        }
+        // ---- B: row (l*NL + t), K-chunk c = zr_l chunk 8(NL-1-t) + c.  Work item (row, res):
+        //      chunks c = res + 8i; res = (item/BROWS + row) mod 8 keeps 8 consecutive lanes on
+        //      distinct banks for both the load and the store.
+#pragma unroll
+        for (int h = 0; h < G::BPER; h++) {
+            if (bsrc[h] < 0) continue;
+            const uint4 *src = reinterpret_cast<const uint4 *>(sZR) + bsrc[h];
+            uint4 *dst = reinterpret_cast<uint4 *>(sB) + bdst[h];
+#pragma unroll 4
+            for (int c = bres[h]; c < G::NCHB; c += 8) dst[c * G::NB] = src[c];
         }
         fence_async_smem();
         tc_fence_before();
         __syncthreads();
-        // ---- MMAs (one thread)
+        // ---- MMAs (one thread).  Descriptors advance by adding to the start-address field.
         if (tid == 0) {
             tc_fence_after();
-            const uint32_t a0 = smem_u32(sA) + 16, b0 = smem_u32(sB);
-#pragma unroll 1
+            const uint64_t bd0 = umma_desc(smem_u32(sB), G::NB * 16, 128);
+            const uint64_t ad0 = umma_desc(smem_u32(sA) + 16, 256, 128);
+#pragma unroll
             for (int ks = 0; ks < G::NKS; ks++) {
-                const uint64_t bd = umma_desc(b0 + ks * 32 * G::NB, G::NB * 16, 128);
+                const uint64_t bd = bd0 + (uint64_t)((ks * 32 * G::NB) >> 4);
 #pragma unroll
                 for (int l = 0; l < LA; l++) {
-                    const uint64_t ad = umma_desc(a0 + l * G::A_BYTES + ks * 512, 256, 128);
+                    const uint64_t ad = ad0 + (uint64_t)((l * G::A_BYTES + ks * 512) >> 4);
                     umma_i8(tmem + l * G::NB, ad, bd, IDESC, ks > 0 ? 1u : 0u);
                 }
             }
             umma_commit(bar);
         }
-        __syncwarp();
         prefetch(prod + gridDim.x);
-        mbar_wait(bar, phase);
+        if (tid == 0) mbar_wait(bar, phase);
         phase ^= 1;
+        __syncthreads();
         tc_fence_after();
         // ---- epilogue: thread tid = TMEM lane = coefficient r of every block
         int acc[LA][LB][G::NL];
         {
             const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
+            int v[LA][G::NB / 16][16];
 #pragma unroll
             for (int l = 0; l < LA; l++)
 #pragma unroll
-                for (int c16 = 0; c16 < G::NB / 16; c16++) {
-                    int v[16];
-                    tmem_ld16(lane_addr + l * G::NB + 16 * c16, v);
-                    tmem_ld_wait();
+                for (int c16 = 0; c16 < G::NB / 16; c16++) tmem_ld16(lane_addr + l * G::NB + 16 * c16, v[l][c16]);
+            tmem_ld_wait();
+#pragma unroll
+            for (int l = 0; l < LA; l++)
+#pragma unroll
+                for (int c16 = 0; c16 < G::NB / 16; c16++)
 #pragma unroll
                     for (int i = 0; i < 16; i++) {
                         const int col = 16 * c16 + i;
                         const int lb = col / G::NL, t = col - lb * G::NL;
-                        if (lb < LB) acc[l][lb][t] = v[i];
+                        if (lb < LB) acc[l][lb][t] = v[l][c16][i];
                     }
-                }
         }
         tc_fence_before();
         __syncthreads();     // all TMEM reads done (next MMAs may overwrite); A region now free
@@ -376,32 +399,17 @@ __global__ void __launch_bounds__(128) tc_mul_kernel(MulArgs a) {
             raw[128 * t + tid] = v;
         }
         __syncthreads();
-        // ---- fold with x^p = x + 1, center, store 8 coefficients per thread and chunk
+        // ---- fold with x^p = x + 1, center, store (lane-consecutive coefficients: no bank conflicts)
         {
             const int ostride_elems = a.out_bytes == 2 ? PS::P8 : PS::P16;
-            for (int c = tid; c < ostride_elems / 8; c += 128) {
-                int o[8];
-#pragma unroll
-                for (int i = 0; i < 8; i++) {
-                    const int k = 8 * c + i;
-                    int v = 0;
-                    if (k < P) {
-                        v = raw[k] + raw[k + P] + (k >= 1 ? raw[k + P - 1] : 0);
-                        v = canon<M>(v);
-                    }
-                    o[i] = v;
+            for (int k = tid; k < ostride_elems; k += 128) {
+                int v = 0;
+                if (k < P) {
+                    v = raw[k] + raw[k + P] + (k >= 1 ? raw[k + P - 1] : 0);
+                    v = canon<M>(v);
                 }
-                if (a.out_bytes == 2) {
-                    uint4 st;
-                    st.x = (uint32_t)(o[0] & 0xffff) | ((uint32_t)o[1] << 16);
-                    st.y = (uint32_t)(o[2] & 0xffff) | ((uint32_t)o[3] << 16);
-                    st.z = (uint32_t)(o[4] & 0xffff) | ((uint32_t)o[5] << 16);
-                    st.w = (uint32_t)(o[6] & 0xffff) | ((uint32_t)o[7] << 16);
-                    reinterpret_cast<uint4 *>((int16_t *)a.out + prod * a.out_stride)[c] = st;
-                } else {
-                    reinterpret_cast<uint2 *>((int8_t *)a.out + prod * a.out_stride)[c] =
-                        make_uint2(pack4(o[0], o[1], o[2], o[3]), pack4(o[4], o[5], o[6], o[7]));
-                }
+                if (a.out_bytes == 2) ((int16_t *)a.out)[prod * a.out_stride + k] = (int16_t)v;
+                else ((int8_t *)a.out)[prod * a.out_stride + k] = (int8_t)v;
             }
         }
         // the next iteration's first __syncthreads orders these raw reads before A rewrites
