@@ -40,10 +40,14 @@ def parse():
     ap.add_argument("--batch-size", type=int, default=0, help="Montgomery batch size B (0 = tuned default)")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-extras", action="store_true", help="skip B sweep / rq_mul / cpu baseline")
+    ap.add_argument("--mul-impl", choices=["tc", "schoolbook"], default="tc",
+                    help="ring products: tcgen05 int8 Hankel GEMM (default) or int32 schoolbook")
     return ap.parse_args()
 
 
 DEFAULT_B = 128
+MUL_IMPL = "tc"          # ring products on the tensor cores (see --mul-impl)
+TRAFFIC = {}             # dram bytes per launch of the dominant kernel, from profiles/ (ncu)
 
 
 # ----------------------------------------------------------------------------------- clocks
@@ -108,9 +112,27 @@ def load_peaks():
 
 
 def int_peak_macs_per_s(sm_mhz: float, n_sm: int = 148) -> float:
-    # DESIGN.md "Roofline": integer multiply-add (IMAD) issues on the FMA pipe at 64 lanes/clk/SM
-    # (B200_PROFILING / B300_MICROARCH: FMA pipe rt_SMSP = 2 -> 16 lanes/clk/SMSP).
+    # DESIGN.md section 6: integer multiply-add (IMAD) issues on the FMA pipe at 64 lanes/clk/SM
+    # (B300_MICROARCH: FMA pipe rt_SMSP = 2 -> 16 lanes/clk/SMSP).
     return 64.0 * n_sm * sm_mhz * 1e6
+
+
+def int8_tc_peak_tops(peaks: dict):
+    """Dense int8 tensor peak: the measured bf16 cuBLAS peak x the nominal int8/bf16 ratio
+    (4.5 / 2.25 PF dense, B200_PROFILING.md).  The ring-product kernels run inside a multi-ms step,
+    so the sustained bf16 figure is the base."""
+    if "bf16_tflops_sustained" in peaks:
+        return 2.0 * peaks["bf16_tflops_sustained"], "measured bf16_tflops_sustained %.1f x 2 (nominal int8/bf16 ratio)" % peaks["bf16_tflops_sustained"]
+    return 2.0 * 1400.0, "fallback 1.4 PF/s sustained bf16 (B200_PROFILING.md) x 2"
+
+
+def load_traffic():
+    """Per-launch DRAM bytes of the ring-product kernels from the committed ncu capture summary
+    (profiles/roofline_traffic.json, written by scripts/ncu_traffic.py); {} if absent."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "roofline_traffic.json")))["per_launch_bytes"]
+    except Exception:
+        return {}
 
 
 def cpu_model():
@@ -186,8 +208,13 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import numpy as np
     import paper_2106_08759_b200 as S
 
+    global MUL_IMPL
+    MUL_IMPL = args.mul_impl
+    S.set_mul_impl(S.MUL_TENSOR_CORE if MUL_IMPL == "tc" else S.MUL_SCHOOLBOOK)
+    TRAFFIC.update(load_traffic())
     P = S.params(PARAM)
     B = args.batch_size or DEFAULT_B
     n = N_KEYS
@@ -264,19 +291,27 @@ def main():
         # dominant kernel class by device time
         dom = max(prof, key=lambda k: prof[k]["ms"])
         tot_ms = sum(v["ms"] for v in prof.values())
-        p = P["p"]
-        macs = {"rq_mul": p * p, "r3_mul": p * p}
         roof = None
-        if dom in macs:
-            per_launch_units = prof[dom]["units"] / max(1, prof[dom]["launches"])
-            avg_ms = prof[dom]["ms"] / max(1, prof[dom]["launches"])
-            achieved = per_launch_units * macs[dom] / (avg_ms / 1e3) / 1e12     # T MAC/s
-            peak = int_peak_macs_per_s(sm_mhz) / 1e12
-            roof = {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": peak,
-                    "unit": "TMAC/s (int32 multiply-accumulate, schoolbook p^2 per product)",
-                    "frac": achieved / peak, "traffic": None,
-                    "peak_source": "derived: 64 IMAD lanes/clk/SM x 148 SMs x %.0f MHz (median SM clock under load)" % sm_mhz,
-                    "share_of_step": prof[dom]["ms"] / tot_ms}
+        if dom in ("rq_mul", "r3_mul"):
+            launches_d = max(1, prof[dom]["launches"])
+            avg_ms = prof[dom]["ms"] / launches_d
+            ops_per_launch = prof[dom]["ops"] / launches_d
+            achieved = ops_per_launch / (avg_ms / 1e3) / 1e12                     # T ops/s
+            if MUL_IMPL == "tc":
+                peak, src = int8_tc_peak_tops(peaks)
+                roof = {"bound": "tensor", "kernel": dom + " (tc_mul_kernel: tcgen05.mma kind::i8)",
+                        "achieved": achieved, "peak": peak,
+                        "unit": "TOPS int8 (algorithmic: 2 p^2 per limb-pair product)",
+                        "frac": achieved / peak, "traffic": TRAFFIC.get(dom),
+                        "peak_source": src, "share_of_step": prof[dom]["ms"] / tot_ms}
+            else:
+                peak = 2 * int_peak_macs_per_s(sm_mhz) / 1e12
+                roof = {"bound": "alu", "kernel": dom + " (ring_mul_kernel: int32 schoolbook)",
+                        "achieved": achieved, "peak": peak,
+                        "unit": "TOPS int32 (2 p^2 per product)", "frac": achieved / peak,
+                        "traffic": None,
+                        "peak_source": "derived: 64 IMAD lanes/clk/SM x 2 ops x 148 SMs x %.0f MHz" % sm_mhz,
+                        "share_of_step": prof[dom]["ms"] / tot_ms}
         result = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -291,6 +326,7 @@ def main():
                     "d2h_bytes_per_step": world * n * (P["pk_bytes"] + P["sk_bytes"])},
             "roofline": roof,
             "breakdown_ms_per_step": {k: v["ms"] / args.steps for k, v in prof.items() if v["launches"]},
+            "mul_impl": MUL_IMPL,
             "profiled_ms_per_step": ms_prof / args.steps,
         }
 
@@ -301,18 +337,28 @@ def main():
             step(b)
             sweep[str(b)] = n * 3 / (timed(lambda: step(b), 3) / 1e3)
         result["batch_size_sweep_keys_per_s"] = sweep
-        # R/q multiplication microbenchmark (configs[2]): 2^20 pairs, uniform x ternary(286)
+        # R/q multiplication microbenchmark (configs[2]): 2^20 pairs, uniform x ternary(286),
+        # through the big x small entry point; the int32 schoolbook beside it (A/B evidence)
         from inputs import synth
         npairs = 1 << 20
+        p = P["p"]
         a = torch.from_numpy(synth.uniform_rq(npairs, p, P["q"], P["p8"], seed=3)).cuda()
-        bt = torch.from_numpy(synth.ternary_fast(npairs, p, P["w"], P["p8"], seed=3)).cuda()
+        bt = torch.from_numpy(synth.ternary_fast(npairs, p, P["w"], P["p16"], seed=3, dtype=np.int8)).cuda()
         c = torch.empty_like(a)
-        S.rq_mul_batch(PARAM, a, bt, c)
-        rq_ms = timed(lambda: S.rq_mul_batch(PARAM, a, bt, c), 3) / 3
+        S.rq_mul_small_batch(PARAM, a, bt, c)
+        rq_ms = timed(lambda: S.rq_mul_small_batch(PARAM, a, bt, c), 3) / 3
+        b16 = torch.zeros_like(a)
+        b16[:, :p] = bt[:, :p].to(torch.int16)
+        bb_ms = timed(lambda: S.rq_mul_batch(PARAM, a, b16, c), 3) / 3
+        S.set_mul_impl(S.MUL_SCHOOLBOOK)
+        sb_ms = timed(lambda: S.rq_mul_batch(PARAM, a, b16, c), 2) / 2
+        S.set_mul_impl(S.MUL_TENSOR_CORE if MUL_IMPL == "tc" else S.MUL_SCHOOLBOOK)
         result["rq_mul"] = {"value": npairs / (rq_ms / 1e3), "unit": "Rq mults/s",
-                            "config": "configs[2]: 2^20 pairs in Z/4591[x]/(x^761-x-1), uniform x ternary w=286",
-                            "ms": rq_ms}
-        del a, bt, c
+                            "config": "configs[2]: 2^20 pairs in Z/4591[x]/(x^761-x-1), uniform x ternary w=286 (rq_mul_small_batch)",
+                            "ms": rq_ms,
+                            "big_x_big_path_mults_per_s": npairs / (bb_ms / 1e3),
+                            "int32_schoolbook_mults_per_s": npairs / (sb_ms / 1e3)}
+        del a, bt, c, b16
         # CPU baseline: the oracle on this host (bounded sample)
         v, cores, sample = oracle_keygen_rate(10.0)
         result["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",

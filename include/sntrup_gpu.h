@@ -101,6 +101,12 @@ size_t sntrup_keygen_workspace_bytes(int param_set, uint64_t n_keys, uint32_t ba
 int rq_mul_batch(int param_set, uint64_t n, const int16_t *a, const int16_t *b, int16_t *c,
                  void *stream);
 
+/* Big x small product (the paper's dedicated "big x small" R/q multiplier, P:6856-6866,
+   P:6984-7104): c[i] = a[i] * b[i] in R/q with a int16 [n][p8] centered and b int8 [n][p16]
+   with |b_j| <= 127 (ternary in the method: g, f, 3f); c int16 [n][p8].  Stream-ordered. */
+int rq_mul_small_batch(int param_set, uint64_t n, const int16_t *a, const int8_t *b, int16_t *c,
+                       void *stream);
+
 /* c[i] = a[i] * b[i] in R/3: int8 [n][p16] rows in {-1,0,1}.  Stream-ordered. */
 int r3_mul_batch(int param_set, uint64_t n, const int8_t *a, const int8_t *b, int8_t *c,
                  void *stream);
@@ -139,12 +145,15 @@ int sntrup_set_mul_impl(int impl);
 
 /* Measurement hooks (bench.py).  When enabled, every kernel launch is bracketed by CUDA events
    recorded on its launching stream.  sntrup_profile_read() waits for the recorded events and
-   returns, per kernel class, the summed device milliseconds, the summed work units and the
-   launch count (classes: 0 sample [keys], 1 R/3 product [products], 2 R/q product [products],
-   3 R/3 root inversion [inversions], 4 R/q root inversion [inversions], 5 repair [keys],
-   6 encode [keys], 7 other).  Returns the number of classes. */
+   returns, per kernel class, the summed device milliseconds, the summed work units, the summed
+   algorithmic integer ops (ring products: 2 p^2 per limb-pair product on the tensor path, 2 p^2
+   per product on the schoolbook path; 0 for other classes) and the launch count (classes:
+   0 sample [keys], 1 R/3 product [products], 2 R/q product [products], 3 R/3 root inversion
+   [inversions], 4 R/q root inversion [inversions], 5 repair [keys], 6 encode [keys], 7 other).
+   Any output pointer may be NULL.  Returns the number of classes. */
 void sntrup_profile_enable(int on);
-int sntrup_profile_read(int reset, double *ms, double *units, uint64_t *launches, int max_classes);
+int sntrup_profile_read(int reset, double *ms, double *units, double *ops, uint64_t *launches,
+                        int max_classes);
 
 #ifdef __cplusplus
 }

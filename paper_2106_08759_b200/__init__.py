@@ -65,10 +65,11 @@ _lib.sntrup_set_mul_impl.argtypes = [_i32]
 _lib.sntrup_profile_enable.restype = None
 _lib.sntrup_profile_enable.argtypes = [_i32]
 _lib.sntrup_profile_read.restype = _i32
-_lib.sntrup_profile_read.argtypes = [_i32, _vp, _vp, _vp, _i32]
+_lib.sntrup_profile_read.argtypes = [_i32, _vp, _vp, _vp, _vp, _i32]
+_lib.rq_mul_small_batch.argtypes = [_i32, _u64, _vp, _vp, _vp, _vp]
 
 EXPORTED = ("sntrup_params", "sntrup_strerror", "sntrup_batch_keygen", "sntrup_batch_keygen_ex",
-            "sntrup_keygen_workspace_bytes", "rq_mul_batch", "r3_mul_batch", "rq_recip_batch",
+            "sntrup_keygen_workspace_bytes", "rq_mul_batch", "rq_mul_small_batch", "r3_mul_batch", "rq_recip_batch",
             "r3_recip_batch", "r3_is_invertible_batch", "rq_encode_batch",
             "sntrup_release_workspace", "sntrup_kernel_launch_count", "sntrup_set_mul_impl",
             "sntrup_profile_enable",
@@ -160,6 +161,19 @@ def rq_mul_batch(param_set: int, a, b, c=None, stream=None):
     return c
 
 
+def rq_mul_small_batch(param_set: int, a, b, c=None, stream=None):
+    """Big x small R/q product: a int16 [n][p8] centered, b int8 [n][p16] (|b_j| <= 127)."""
+    P = params(param_set)
+    n = a.shape[0]
+    _need(a, torch.int16, (n, P["p8"]), "a")
+    _need(b, torch.int8, (n, P["p16"]), "b")
+    if c is None:
+        c = torch.empty_like(a)
+    _check(_lib.rq_mul_small_batch(param_set, n, _ptr(a), _ptr(b), _ptr(c), _stream(stream)),
+           "rq_mul_small_batch")
+    return c
+
+
 def r3_mul_batch(param_set: int, a, b, c=None, stream=None):
     P = params(param_set)
     n = a.shape[0]
@@ -246,13 +260,15 @@ def profile_enable(on: bool = True):
 
 
 def profile_read(reset: bool = True) -> dict:
-    """Per kernel class: device ms (CUDA events on the launching stream), work units, launches."""
+    """Per kernel class: device ms (CUDA events on the launching stream), work units, algorithmic
+    integer ops, launches."""
     n = len(PROFILE_CLASSES)
     ms = (ctypes.c_double * n)()
     un = (ctypes.c_double * n)()
+    op = (ctypes.c_double * n)()
     la = (ctypes.c_uint64 * n)()
-    _lib.sntrup_profile_read(1 if reset else 0, ms, un, la, n)
-    return {PROFILE_CLASSES[i]: dict(ms=ms[i], units=un[i], launches=la[i]) for i in range(n)}
+    _lib.sntrup_profile_read(1 if reset else 0, ms, un, op, la, n)
+    return {PROFILE_CLASSES[i]: dict(ms=ms[i], units=un[i], ops=op[i], launches=la[i]) for i in range(n)}
 
 
 def library_path() -> str:

@@ -40,11 +40,11 @@ std::mutex g_mu;                                   // serialises calls (shared w
 // inversions).  Read back with sntrup_profile_read().
 enum ProfClass { PC_SAMPLE = 0, PC_MUL_R3, PC_MUL_RQ, PC_INV_R3, PC_INV_RQ, PC_REPAIR, PC_ENCODE,
                  PC_MISC, PC_N };
-struct ProfRec { int cls; cudaEvent_t a, b; double units; };
+struct ProfRec { int cls; cudaEvent_t a, b; double units, ops; };
 bool g_prof_on = false;
 std::vector<ProfRec> g_prof;
 std::vector<cudaEvent_t> g_evpool;
-struct ProfAgg { double ms = 0, units = 0; uint64_t launches = 0; };
+struct ProfAgg { double ms = 0, units = 0, ops = 0; uint64_t launches = 0; };
 ProfAgg g_agg[PC_N];
 
 cudaEvent_t ev_get() {
@@ -55,12 +55,13 @@ cudaEvent_t ev_get() {
 }
 
 struct ProfScope {
-    int cls; double units; cudaStream_t s; cudaEvent_t a = nullptr;
-    ProfScope(int c, double u, cudaStream_t st) : cls(c), units(u), s(st) {
+    int cls; double units, ops; cudaStream_t s; cudaEvent_t a = nullptr;
+    // units: products / keys / inversions; ops: algorithmic integer ops of the launch (0 if n/a)
+    ProfScope(int c, double u, cudaStream_t st, double o = 0) : cls(c), units(u), ops(o), s(st) {
         if (g_prof_on) { a = ev_get(); cudaEventRecord(a, s); }
     }
     ~ProfScope() {
-        if (a) { cudaEvent_t b = ev_get(); cudaEventRecord(b, s); g_prof.push_back(ProfRec{cls, a, b, units}); }
+        if (a) { cudaEvent_t b = ev_get(); cudaEventRecord(b, s); g_prof.push_back(ProfRec{cls, a, b, units, ops}); }
     }
 };
 
@@ -71,6 +72,7 @@ void prof_drain() {
         cudaEventElapsedTime(&ms, r.a, r.b);
         g_agg[r.cls].ms += ms;
         g_agg[r.cls].units += r.units;
+        g_agg[r.cls].ops += r.ops;
         g_agg[r.cls].launches += 1;
         g_evpool.push_back(r.a);
         g_evpool.push_back(r.b);
@@ -349,7 +351,11 @@ int launch_tc(const MulArgs &a, cudaStream_t s) {
 template <class PS, int M>
 int launch_mul(MulArgs a, cudaStream_t s, int la = 2, int lb = 2) {
     if (a.n_out <= 0) return SNTRUP_OK;
-    ProfScope ps_(M == 3 ? PC_MUL_R3 : PC_MUL_RQ, (double)a.n_out, s);
+    // algorithmic ops: tensor path = 2 p^2 int8 multiply-add ops per limb-pair product (the
+    // limb-decomposed schoolbook contraction); schoolbook path = 2 p^2 int32 ops per product
+    const int limb_pairs = (g_mul_impl == 1 || M == 3) ? 1 : la * lb;
+    ProfScope ps_(M == 3 ? PC_MUL_R3 : PC_MUL_RQ, (double)a.n_out, s,
+                  2.0 * PS::P * PS::P * limb_pairs * (double)a.n_out);
     if (g_mul_impl == 1) {
         const int threads = (PS::P8 / 8 + 31) / 32 * 32;
         long long grid = a.n_out;
@@ -806,6 +812,24 @@ int rq_mul_batch(int param_set, uint64_t n, const int16_t *a, const int16_t *b, 
     return SNTRUP_E_PARAM;
 }
 
+int rq_mul_small_batch(int param_set, uint64_t n, const int16_t *a, const int8_t *b, int16_t *c,
+                       void *stream) {
+    ParamInfo pi;
+    if (!param_info(param_set, &pi)) return SNTRUP_E_PARAM;
+    if (n == 0 || !a || !b || !c) return SNTRUP_E_ARG;
+    MulArgs m{};
+    m.mode = MUL_ZIP;
+    m.n_out = (long long)n;
+    m.X = RowDesc{a, pi.p8, 2, 1};
+    m.Y = RowDesc{b, pi.p16, 1, 1};
+    m.out = c;
+    m.out_stride = pi.p8;
+    m.out_bytes = 2;
+    m.periodic = 0;
+    SNTRUP_DISPATCH(param_set, return launch_mul<PS, PS::Q>(m, (cudaStream_t)stream, 2, 1));
+    return SNTRUP_E_PARAM;
+}
+
 int r3_mul_batch(int param_set, uint64_t n, const int8_t *a, const int8_t *b, int8_t *c,
                  void *stream) {
     ParamInfo pi;
@@ -900,13 +924,15 @@ void sntrup_profile_enable(int on) {
     g_prof_on = on != 0;
 }
 
-int sntrup_profile_read(int reset, double *ms, double *units, uint64_t *launches, int max_classes) {
+int sntrup_profile_read(int reset, double *ms, double *units, double *ops, uint64_t *launches,
+                        int max_classes) {
     std::lock_guard<std::mutex> lk(g_mu);
     prof_drain();
     const int n = max_classes < PC_N ? max_classes : PC_N;
     for (int i = 0; i < n; i++) {
         if (ms) ms[i] = g_agg[i].ms;
         if (units) units[i] = g_agg[i].units;
+        if (ops) ops[i] = g_agg[i].ops;
         if (launches) launches[i] = g_agg[i].launches;
     }
     if (reset)

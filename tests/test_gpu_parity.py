@@ -157,6 +157,25 @@ def test_rq_mul(O, param, mul_impl):
 
 
 @pytest.mark.parametrize("param", PSETS)
+def test_rq_mul_small(O, param, mul_impl):
+    # configs[2] shape: one operand uniform in [-(q-1)/2, (q-1)/2], the other ternary of weight w
+    P = S.params(param)
+    p, q, p8, p16 = P["p"], P["q"], P["p8"], P["p16"]
+    a = synth.uniform_rq(150, p, q, p8, seed=11)
+    b = np.concatenate([synth.ternary(100, p, P["w"], p16, seed=12, dtype=np.int8),
+                        synth.small(50, p, p16, seed=13)])
+    qh = (q - 1) // 2
+    a[0, :p] = qh
+    a[1, :p] = -qh
+    b[0, :p] = 1
+    b[1, :p] = -1
+    b[2] = 0
+    c = S.rq_mul_small_batch(param, torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()).cpu().numpy()
+    ref = O.mul_many(p, q, a, np.pad(b[:, :p].astype(np.int16), ((0, 0), (0, p8 - p))))
+    assert np.array_equal(c, ref)
+
+
+@pytest.mark.parametrize("param", PSETS)
 def test_r3_mul(O, param, mul_impl):
     P = S.params(param)
     p, p16 = P["p"], P["p16"]
