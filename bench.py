@@ -45,7 +45,7 @@ def parse():
     return ap.parse_args()
 
 
-DEFAULT_B = 128
+DEFAULT_B = 512
 MUL_IMPL = "tc"          # ring products on the tensor cores (see --mul-impl)
 TRAFFIC = {}             # dram bytes per launch of the dominant kernel, from profiles/ (ncu)
 

@@ -640,8 +640,6 @@ __global__ void __launch_bounds__(128) r3_prepare_kernel(const int8_t *g, int8_t
 template <class PS>
 __global__ void __launch_bounds__(128) r3_finalize_kernel(const int8_t *g, int8_t *out, uint8_t *ok,
                                                           long long n, int B, const uint8_t *root_ok) {
-    using DS = Divstep<PS, 3>;
-    constexpr int C = DS::C;
     const int lane = threadIdx.x & 31;
     const long long row = (long long)blockIdx.x * 4 + (threadIdx.x >> 5);
     if (row >= n) return;
@@ -651,18 +649,7 @@ __global__ void __launch_bounds__(128) r3_finalize_kernel(const int8_t *g, int8_
             for (int k = lane; k < PS::P16; k += 32) orow[k] = 0;
         return;
     }
-    float gg[C], res[C];
-#pragma unroll
-    for (int c = 0; c < C; c++) {
-        const int i = lane * C + c;
-        gg[c] = (i < PS::P) ? (float)g[row * PS::P16 + PS::P - 1 - i] : 0.0f;
-    }
-    const bool inv = DS::invert(gg, res, lane);
-#pragma unroll
-    for (int c = 0; c < C; c++) {
-        const int j = lane * C + c;
-        if (j < PS::P) orow[PS::P - 1 - j] = inv ? (int8_t)(int)res[c] : 0;
-    }
+    const bool inv = R3Divstep<PS>::invert(g + row * PS::P16, orow, lane);
     for (int k = PS::P + lane; k < PS::P16; k += 32) orow[k] = 0;
     if (lane == 0) ok[row] = inv ? 1 : 0;
 }
