@@ -380,7 +380,16 @@ template <class PS, int M>
 int launch_divstep(const InvArgs &a, cudaStream_t s) {
     if (a.n <= 0) return SNTRUP_OK;
     ProfScope ps_(M == 3 ? PC_INV_R3 : PC_INV_RQ, (double)a.n, s);
-    divstep_kernel<PS, M><<<(unsigned)((a.n + 3) / 4), 128, 0, s>>>(a);
+    if constexpr (M == 3) {
+        divstep_kernel<PS, M><<<(unsigned)((a.n + 3) / 4), 128, 0, s>>>(a);      // bitsliced, warp/root
+    } else {
+        // few roots: latency bound -> one CTA of 8 warps per root; many roots: throughput bound
+        // -> one warp per root (less per-step overhead in total)
+        if (a.n < 2LL * dev_info().sms)
+            divstep_cta_kernel<PS, M, 256><<<(unsigned)a.n, 256, 0, s>>>(a);
+        else
+            divstep_kernel<PS, M><<<(unsigned)((a.n + 3) / 4), 128, 0, s>>>(a);
+    }
     LAUNCHED();
     return SNTRUP_OK;
 }
