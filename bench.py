@@ -337,6 +337,14 @@ def main():
             step(b)
             sweep[str(b)] = n * 3 / (timed(lambda: step(b), 3) / 1e3)
         result["batch_size_sweep_keys_per_s"] = sweep
+        # A/B: the same step without the shared-A down-sweep, and on the int32 schoolbook
+        ab = {}
+        for name, impl in (("tc_no_shared_a", S.MUL_TENSOR_CORE_NO_SHARED_A), ("int32_schoolbook", S.MUL_SCHOOLBOOK)):
+            S.set_mul_impl(impl)
+            step()
+            ab[name] = n * 2 / (timed(step, 2) / 1e3)
+        S.set_mul_impl(S.MUL_TENSOR_CORE if MUL_IMPL == "tc" else S.MUL_SCHOOLBOOK)
+        result["mul_impl_ab_keys_per_s"] = ab
         # R/q multiplication microbenchmark (configs[2]): 2^20 pairs, uniform x ternary(286),
         # through the big x small entry point; the int32 schoolbook beside it (A/B evidence)
         from inputs import synth

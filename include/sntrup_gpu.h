@@ -140,7 +140,8 @@ uint64_t sntrup_kernel_launch_count(void);
 
 /* Select the ring-product implementation used by every call (measurement / A-B evidence):
    0 = tensor cores (tcgen05.mma kind::i8 Hankel GEMM, the default), 1 = int32 schoolbook on the
-   integer pipes (v1).  Both are exact.  Returns SNTRUP_OK or SNTRUP_E_ARG. */
+   integer pipes (v1), 2 = tensor cores without the shared-A down-sweep (one product per work
+   item; for A/B measurement).  All are exact.  Returns SNTRUP_OK or SNTRUP_E_ARG. */
 int sntrup_set_mul_impl(int impl);
 
 /* Measurement hooks (bench.py).  When enabled, every kernel launch is bracketed by CUDA events

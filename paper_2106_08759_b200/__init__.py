@@ -248,6 +248,7 @@ def kernel_launch_count() -> int:
 
 MUL_TENSOR_CORE = 0
 MUL_SCHOOLBOOK = 1
+MUL_TENSOR_CORE_NO_SHARED_A = 2
 
 
 def set_mul_impl(impl: int):

@@ -11,12 +11,13 @@
 //   ZIP   : out[i] = X[i] * Y[i]
 //   PAIRS : out[j] = X[2j] * X[2j+1]          (up-sweep; X[2j] alone if 2j+1 >= cnt_in)
 //   DOWN  : out[i] = Y[i>>1] * X[i^1]         (down-sweep; Y[i>>1] alone if i^1 >= cnt_in)
+//   DOWN2 : DOWN with both children of parent j in one work item (n_out = parents; tensor path)
 #pragma once
 #include "common.cuh"
 
 namespace sntrup {
 
-enum MulMode { MUL_ZIP = 0, MUL_PAIRS = 1, MUL_DOWN = 2 };
+enum MulMode { MUL_ZIP = 0, MUL_PAIRS = 1, MUL_DOWN = 2, MUL_DOWN2 = 3 };
 
 struct MulArgs {
     int mode;

@@ -249,6 +249,26 @@ int build_tables(int dev, int ps, int WT, DevTables **out) {
     return SNTRUP_OK;
 }
 
+// ------------------------------------------------------------------------------ copy stream
+// Host-output keygen: chunk i's pk/sk are copied device->host on a copy stream while chunk i+1
+// computes (double-buffered device staging).  One per device (calls are serialised).
+struct CopyStream { cudaStream_t s = nullptr; cudaEvent_t comp[2] = {}, copy[2] = {}; };
+int copy_stream(CopyStream **out) {
+    static std::map<int, CopyStream> m;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    CopyStream &c = m[dev];
+    if (!c.s) {
+        CK(cudaStreamCreateWithFlags(&c.s, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; i++) {
+            CK(cudaEventCreateWithFlags(&c.comp[i], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&c.copy[i], cudaEventDisableTiming));
+        }
+    }
+    *out = &c;
+    return SNTRUP_OK;
+}
+
 // ------------------------------------------------------------------------------ workspace
 struct Workspace {
     char *base = nullptr;
@@ -309,7 +329,7 @@ TreePlan make_plan(long long m, int B) {
 }
 
 // ------------------------------------------------------------------------------ launches
-int g_mul_impl = 0;                                 // 0 = tensor cores (tcmul.cuh), 1 = int32 schoolbook
+int g_mul_impl = 0;   // 0 = tensor cores (tcmul.cuh), 1 = int32 schoolbook, 2 = tensor cores without shared-A down-sweep
 
 struct DevInfo { int sms = 0; };
 DevInfo &dev_info() {
@@ -321,10 +341,10 @@ DevInfo &dev_info() {
     return d;
 }
 
-template <class PS, int M, int LA, int LB>
+template <class PS, int M, int LA, int LB, int NPR = 1>
 int launch_tc(const MulArgs &a, cudaStream_t s) {
-    using G = TcGeom<PS, LA, LB>;
-    auto kern = tc_mul_kernel<PS, M, LA, LB>;
+    using G = TcGeom<PS, LA, LB, NPR>;
+    auto kern = tc_mul_kernel<PS, M, LA, LB, NPR>;
     static std::map<int, int> per_sm;                 // device -> resident CTAs per SM
     int dev = 0;
     CK(cudaGetDevice(&dev));
@@ -364,15 +384,22 @@ int launch_mul(MulArgs a, cudaStream_t s, int la = 2, int lb = 2) {
         LAUNCHED();
         return SNTRUP_OK;
     }
+    // down-sweep with both operands of one kind: the two children of a parent share the parent's
+    // inverse as the A operand (one work item per parent)
+    const bool down2 = a.mode == MUL_DOWN && (M == 3 || la == lb) && g_mul_impl != 2;
+    if (down2) {
+        a.mode = MUL_DOWN2;
+        a.n_out = (a.cnt_in + 1) / 2;
+    }
     if constexpr (M == 3) {
         a.swap = 0;
-        return launch_tc<PS, M, 1, 1>(a, s);
+        return down2 ? launch_tc<PS, M, 1, 1, 2>(a, s) : launch_tc<PS, M, 1, 1>(a, s);
     } else {
-        if (la == 1 && lb == 1) { a.swap = 0; return launch_tc<PS, M, 1, 1>(a, s); }
+        if (la == 1 && lb == 1) { a.swap = 0; return down2 ? launch_tc<PS, M, 1, 1, 2>(a, s) : launch_tc<PS, M, 1, 1>(a, s); }
         if (la == 1) { a.swap = 0; return launch_tc<PS, M, 1, 2>(a, s); }
         if (lb == 1) { a.swap = 1; return launch_tc<PS, M, 1, 2>(a, s); }
         a.swap = 0;
-        return launch_tc<PS, M, 2, 2>(a, s);
+        return down2 ? launch_tc<PS, M, 2, 2, 2>(a, s) : launch_tc<PS, M, 2, 2>(a, s);
     }
 }
 
@@ -470,10 +497,11 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
     cudaStream_t s = (cudaStream_t)o.stream;
     const int B = o.batch_size ? (int)o.batch_size : 32;
     if (B < 1 || B > 4096 || (B & (B - 1))) return SNTRUP_E_ARG;
-    uint64_t chunk = o.chunk_keys ? o.chunk_keys : 65536;
+    const bool host_out = (o.flags & SNTRUP_OPT_HOST_OUTPUT) != 0;
+    // host outputs: smaller default chunks so the D2H copies overlap the next chunk's compute
+    uint64_t chunk = o.chunk_keys ? o.chunk_keys : (host_out ? 16384 : 65536);
     chunk = (chunk + B - 1) / B * B;
     if (chunk > n) chunk = (n + B - 1) / B * B;
-    const bool host_out = (o.flags & SNTRUP_OPT_HOST_OUTPUT) != 0;
     const size_t pkb = tb->enc.pk_bytes, skb = 2 * PS::SKH;
 
     // workspace for one chunk of `chunk` keys
@@ -486,7 +514,7 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
     need += 2 * align256(inner * PS::P8 * 2 + 256 * (tpmax.L + 1)); // R/q levels + inverses
     need += 2 * align256(chunk * PS::P8 * 2);                // Fbar, H
     need += 2 * align256(tpmax.cnt[tpmax.L]);                // root ok flags
-    if (host_out) need += align256(chunk * pkb) + align256(chunk * skb);
+    if (host_out) need += 2 * (align256(chunk * pkb) + align256(chunk * skb));
     need += 4096;
     if ((rc = ws_reserve(need))) return rc;
     int8_t *G = ws_take<int8_t>(chunk * PS::P16);
@@ -505,8 +533,15 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
     int16_t *H = ws_take<int16_t>(chunk * PS::P8);
     uint8_t *ok3 = ws_take<uint8_t>(tpmax.cnt[tpmax.L]);
     uint8_t *okq = ws_take<uint8_t>(tpmax.cnt[tpmax.L]);
-    uint8_t *pk_dev = nullptr, *sk_dev = nullptr;
-    if (host_out) { pk_dev = ws_take<uint8_t>(chunk * pkb); sk_dev = ws_take<uint8_t>(chunk * skb); }
+    uint8_t *pk_stage[2] = {nullptr, nullptr}, *sk_stage[2] = {nullptr, nullptr};
+    CopyStream *cs = nullptr;
+    if (host_out) {
+        for (int i = 0; i < 2; i++) {
+            pk_stage[i] = ws_take<uint8_t>(chunk * pkb);
+            sk_stage[i] = ws_take<uint8_t>(chunk * skb);
+        }
+        if ((rc = copy_stream(&cs))) return rc;
+    }
     unsigned long long *repaired = ws_take<unsigned long long>(1);
     int *err = ws_take<int>(1);
     CK(cudaMemsetAsync(repaired, 0, sizeof(unsigned long long), s));
@@ -522,8 +557,10 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
         int8_t *Ic = o.ginv_out ? o.ginv_out + c0 * PS::P16 : Ginv;
         uint8_t *Ac = o.attempts_out ? o.attempts_out + c0 : att;
         int16_t *Hc = o.h_out ? o.h_out + c0 * PS::P8 : H;
-        uint8_t *pkc = host_out ? pk_dev : pk_out + c0 * pkb;
-        uint8_t *skc = host_out ? sk_dev : sk_out + c0 * skb;
+        const int buf = (int)((c0 / chunk) & 1);
+        if (host_out && c0 >= 2 * chunk) CK(cudaStreamWaitEvent(s, cs->copy[buf], 0));   // staging free
+        uint8_t *pkc = host_out ? pk_stage[buf] : pk_out + c0 * pkb;
+        uint8_t *skc = host_out ? sk_stage[buf] : sk_out + c0 * skb;
 
         SampleArgs sa{};
         sa.seed = seed; sa.first = first; sa.n = m;
@@ -580,9 +617,15 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
             LAUNCHED();
         }
         if (host_out) {
-            CK(cudaMemcpyAsync(pk_out + c0 * pkb, pk_dev, m * pkb, cudaMemcpyDeviceToHost, s));
-            CK(cudaMemcpyAsync(sk_out + c0 * skb, sk_dev, m * skb, cudaMemcpyDeviceToHost, s));
+            CK(cudaEventRecord(cs->comp[buf], s));
+            CK(cudaStreamWaitEvent(cs->s, cs->comp[buf], 0));
+            CK(cudaMemcpyAsync(pk_out + c0 * pkb, pkc, m * pkb, cudaMemcpyDeviceToHost, cs->s));
+            CK(cudaMemcpyAsync(sk_out + c0 * skb, skc, m * skb, cudaMemcpyDeviceToHost, cs->s));
+            CK(cudaEventRecord(cs->copy[buf], cs->s));
         }
+    }
+    if (host_out) {                       // join the copies into the caller's stream
+        for (int i = 0; i < 2; i++) CK(cudaStreamWaitEvent(s, cs->copy[i], 0));
     }
     const bool sync = !(o.flags & SNTRUP_OPT_ASYNC) || host_out || o.stats_out;
     if (sync) {
@@ -908,7 +951,7 @@ void sntrup_release_workspace(void) {
 uint64_t sntrup_kernel_launch_count(void) { return g_launches.load(); }
 
 int sntrup_set_mul_impl(int impl) {
-    if (impl != 0 && impl != 1) return SNTRUP_E_ARG;
+    if (impl < 0 || impl > 2) return SNTRUP_E_ARG;
     std::lock_guard<std::mutex> lk(g_mu);
     g_mul_impl = impl;
     return SNTRUP_OK;

@@ -110,21 +110,25 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, int (&v)[16]) {
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // ----------------------------------------------------------------------------------- geometry
-template <class PS, int LA, int LB>
+// NPR products share one A operand per iteration (the down-sweep's two children share the
+// parent's inverse): their B rows are stacked along N, so the A tile read by every MMA -- the
+// dominant shared-memory traffic of a small-N GEMM -- is amortised over both products.
+template <class PS, int LA, int LB, int NPR>
 struct TcGeom {
     static constexpr int P = PS::P;
     static constexpr int NKS = (P + 127 + 31) / 32;          // K steps of 32
     static constexpr int K = 32 * NKS;
     static constexpr int NBLK = (2 * P - 1 + 127) / 128;     // output blocks of 128 coefficients
     static constexpr int NL = (NBLK + 7) / 8 * 8;            // B rows per limb
-    static constexpr int NB = (LB * NL + 15) / 16 * 16;      // N of the MMA
+    static constexpr int PCOL = (LB * NL + 15) / 16 * 16;    // B rows (= D columns) per product
+    static constexpr int NB = NPR * PCOL;                    // N of the MMA
     static constexpr int AROWS = 32 * NKS + 113;             // window rows 0..AROWS-1 (row 0 unused)
     static constexpr int A_BYTES = (AROWS + 7) / 8 * 128;    // 16 B per row, 128-aligned
     static constexpr int AROWS4 = (AROWS + 3) / 4;            // window rows are built 4 at a time
     static constexpr int HA_LEN = (4 * AROWS4 + 20 + 127) / 128 * 128;   // hA[128 + j] = limb(a_j)
     static constexpr int ZR_LEN = (128 * NL + K + 127) / 128 * 128; // zr[128 NL - 1 - j] = limb(b_j)
     static constexpr int B_BYTES = 2 * NKS * NB * 16;
-    static constexpr int RAW_BYTES = 128 * NBLK * 4;
+    static constexpr int RAW_INTS = 128 * NBLK;               // per product
     static constexpr int TCOLS_USED = LA * NB;
     static constexpr int TCOLS = TCOLS_USED <= 32 ? 32 : TCOLS_USED <= 64 ? 64 : TCOLS_USED <= 128 ? 128 : 256;
     static constexpr int NCHK = PS::P8 / 8;                   // 8-coefficient input chunks
@@ -134,14 +138,14 @@ struct TcGeom {
     static constexpr int OFF_B = OFF_A + LA * A_BYTES;
     static constexpr int OFF_HA = OFF_B + B_BYTES;
     static constexpr int OFF_ZR = OFF_HA + LA * HA_LEN;
-    static constexpr int OFF_BAR = OFF_ZR + LB * ZR_LEN;
+    static constexpr int OFF_BAR = OFF_ZR + NPR * LB * ZR_LEN;
     static constexpr int SMEM = OFF_BAR + 128;
-    static_assert(RAW_BYTES <= LA * A_BYTES, "raw buffer must fit in the A region");
+    static_assert(NPR * RAW_INTS * 4 <= LA * A_BYTES, "raw buffers must fit in the A region");
     static_assert(NB <= 256, "N too large");
     static_assert(128 + PS::P8 <= HA_LEN, "hA too short");
     static_assert(4 * AROWS4 * 16 <= A_BYTES, "A region too short");
-    // B build: (row, residue mod 8) work items; row = l*NL + t, K-chunks c = residue + 8i
-    static constexpr int BROWS = LB * NL;
+    // B build: (row, residue mod 8) work items; row = pp*PCOL + l*NL + t, K-chunks c = residue + 8i
+    static constexpr int BROWS = NPR * LB * NL;
     static constexpr int NCHB = 2 * NKS;                      // 16-byte K-chunks per B row
     static constexpr int BITEMS = BROWS * 8;
     static constexpr int BPER = (BITEMS + 127) / 128;
@@ -184,10 +188,51 @@ __device__ __forceinline__ uint32_t pack4(int a, int b, int c, int d) {
            ((uint32_t)(d & 0xff) << 24);
 }
 
-// M = modulus (3 or q); LA / LB = limbs of the A-role / B-role operand.
-template <class PS, int M, int LA, int LB>
+// Operands of work item `it`: u -> A role; v[pp] -> B role of product pp, written to out row
+// orow[pp] (orow < 0: no such product).
+template <int NPR>
+struct TcWork {
+    RowDesc du; long long ru; bool unit_u;
+    RowDesc dv[NPR]; long long rv[NPR]; bool unit_v[NPR];
+    long long orow[NPR];
+};
+
+template <int NPR>
+__device__ __forceinline__ void tc_work(const MulArgs &a, long long it, TcWork<NPR> &w) {
+    w.unit_u = false;
+#pragma unroll
+    for (int pp = 0; pp < NPR; pp++) { w.unit_v[pp] = false; w.orow[pp] = -1; w.dv[pp] = a.X; w.rv[pp] = 0; }
+    if constexpr (NPR == 2) {
+        // MUL_DOWN2: parent it; out[2it] = Y[it] * X[2it+1] (unit if absent), out[2it+1] = Y[it] * X[2it]
+        w.du = a.Y; w.ru = it;
+        w.dv[0] = a.X; w.rv[0] = 2 * it + 1; w.unit_v[0] = 2 * it + 1 >= a.cnt_in; w.orow[0] = 2 * it;
+        w.dv[1] = a.X; w.rv[1] = 2 * it;
+        w.orow[1] = (2 * it + 1 < a.cnt_in) ? 2 * it + 1 : -1;
+    } else {
+        RowDesc du, dv; long long ru, rv; bool uv = false, uu = false;
+        if (a.mode == MUL_ZIP) {
+            du = a.X; ru = it; dv = a.Y; rv = it;
+        } else if (a.mode == MUL_PAIRS) {
+            du = a.X; ru = 2 * it; dv = a.X; rv = 2 * it + 1;
+            uv = rv >= a.cnt_in;
+        } else {
+            du = a.Y; ru = it >> 1; dv = a.X; rv = it ^ 1;
+            uv = rv >= a.cnt_in;
+        }
+        if (a.swap) {
+            const RowDesc td = du; du = dv; dv = td;
+            const long long tr = ru; ru = rv; rv = tr;
+            uu = uv; uv = false;
+        }
+        w.du = du; w.ru = ru; w.unit_u = uu;
+        w.dv[0] = dv; w.rv[0] = rv; w.unit_v[0] = uv; w.orow[0] = it;
+    }
+}
+
+// M = modulus (3 or q); LA / LB = limbs of the A-role / B-role operand; NPR products per A.
+template <class PS, int M, int LA, int LB, int NPR>
 __global__ void __launch_bounds__(128) tc_mul_kernel(MulArgs a) {
-    using G = TcGeom<PS, LA, LB>;
+    using G = TcGeom<PS, LA, LB, NPR>;
     constexpr int P = PS::P;
     constexpr int CH = G::CH;
     extern __shared__ __align__(1024) uint8_t sm[];
@@ -227,64 +272,47 @@ __global__ void __launch_bounds__(128) tc_mul_kernel(MulArgs a) {
         const int w = tid + 128 * h;
         if (w < G::BITEMS) {
             const int row = w % G::BROWS, grp = w / G::BROWS;
-            const int l = row / G::NL, t = row - l * G::NL;
+            const int pl = row / G::NL, t = row - pl * G::NL;       // pl = pp * LB + l
+            const int pp = pl / LB, l = pl - pp * LB;
             bres[h] = (grp + row) & 7;
-            bsrc[h] = l * (G::ZR_LEN / 16) + 8 * (G::NL - 1 - t);
-            bdst[h] = row;
+            bsrc[h] = pl * (G::ZR_LEN / 16) + 8 * (G::NL - 1 - t);
+            bdst[h] = pp * G::PCOL + l * G::NL + t;
         } else {
             bsrc[h] = -1; bdst[h] = 0; bres[h] = 0;
         }
     }
 
-    // operand sources of product `prod`: u -> A role, v -> B role (a.swap exchanges them)
-    auto operands = [&](long long prod, RowDesc &du, long long &ru, bool &unit_u, RowDesc &dv,
-                        long long &rv, bool &unit_v) {
-        unit_u = false;
-        unit_v = false;
-        if (a.mode == MUL_ZIP) {
-            du = a.X; ru = prod; dv = a.Y; rv = prod;
-        } else if (a.mode == MUL_PAIRS) {
-            du = a.X; ru = 2 * prod; dv = a.X; rv = 2 * prod + 1;
-            unit_v = rv >= a.cnt_in;
-        } else {
-            du = a.Y; ru = prod >> 1; dv = a.X; rv = prod ^ 1;
-            unit_v = rv >= a.cnt_in;
-        }
-        if (a.swap) {
-            const RowDesc td = du; du = dv; dv = td;
-            const long long tr = ru; ru = rv; rv = tr;
-            unit_u = unit_v; unit_v = false;
-        }
-    };
-    // register prefetch of the next product's rows (in flight during the MMAs / epilogue)
-    uint4 pu[CH], pv[CH];
-    auto prefetch = [&](long long prod) {
-        if (prod >= a.n_out) return;
-        RowDesc du, dv; long long ru, rv; bool uu, uv;
-        operands(prod, du, ru, uu, dv, rv, uv);
+    // register prefetch of the next work item's rows (in flight during the MMAs / epilogue)
+    uint4 pu[CH], pv[NPR][CH];
+    auto prefetch = [&](long long it) {
+        if (it >= a.n_out) return;
+        TcWork<NPR> w;
+        tc_work<NPR>(a, it, w);
 #pragma unroll
         for (int h = 0; h < CH; h++) {
             const int c = tid + 128 * h;
             if (c < G::NCHK) {
-                pu[h] = uu ? make_uint4(0, 0, 0, 0) : load_chunk(du, ru, c);
-                pv[h] = uv ? make_uint4(0, 0, 0, 0) : load_chunk(dv, rv, c);
+                pu[h] = w.unit_u ? make_uint4(0, 0, 0, 0) : load_chunk(w.du, w.ru, c);
+#pragma unroll
+                for (int pp = 0; pp < NPR; pp++)
+                    pv[pp][h] = (w.unit_v[pp] || (pp > 0 && w.orow[pp] < 0)) ? make_uint4(0, 0, 0, 0)
+                                                                         : load_chunk(w.dv[pp], w.rv[pp], c);
             }
         }
     };
     prefetch(blockIdx.x);
 
-    for (long long prod = blockIdx.x; prod < a.n_out; prod += gridDim.x) {
-        RowDesc du, dv; long long ru, rv; bool unit_u, unit_v;
-        operands(prod, du, ru, unit_u, dv, rv, unit_v);
+    for (long long it = blockIdx.x; it < a.n_out; it += gridDim.x) {
+        TcWork<NPR> w;
+        tc_work<NPR>(a, it, w);
         // ---- stage limbs (8-byte aligned groups): hA_l[128 + j] = limb_l(u_j),
-        //      zr_l[128 NL - 1 - j] = limb_l(v_j) (reversed within the group)
+        //      zr_{pp,l}[128 NL - 1 - j] = limb_l(v_pp,j) (reversed within the group)
 #pragma unroll
         for (int h = 0; h < CH; h++) {
             const int c = tid + 128 * h;
             if (c < G::NCHK) {
-                int uv8[8], vv8[8];
-                decode_chunk(pu[h], du.bytes, du.scale, unit_u, c, uv8);
-                decode_chunk(pv[h], dv.bytes, dv.scale, unit_v, c, vv8);
+                int uv8[8];
+                decode_chunk(pu[h], w.du.bytes, w.du.scale, w.unit_u, c, uv8);
 #pragma unroll
                 for (int l = 0; l < LA; l++) {
                     int x[8];
@@ -294,12 +322,17 @@ __global__ void __launch_bounds__(128) tc_mul_kernel(MulArgs a) {
                         make_uint2(pack4(x[0], x[1], x[2], x[3]), pack4(x[4], x[5], x[6], x[7]));
                 }
 #pragma unroll
-                for (int l = 0; l < LB; l++) {
-                    int x[8];
+                for (int pp = 0; pp < NPR; pp++) {
+                    int vv8[8];
+                    decode_chunk(pv[pp][h], w.dv[pp].bytes, w.dv[pp].scale, w.unit_v[pp], c, vv8);
 #pragma unroll
-                    for (int i = 0; i < 8; i++) x[i] = limb_of<LB>(vv8[i], l);
-                    *reinterpret_cast<uint2 *>(sZR + l * G::ZR_LEN + 128 * G::NL - 8 - 8 * c) =
-                        make_uint2(pack4(x[7], x[6], x[5], x[4]), pack4(x[3], x[2], x[1], x[0]));
+                    for (int l = 0; l < LB; l++) {
+                        int x[8];
+#pragma unroll
+                        for (int i = 0; i < 8; i++) x[i] = limb_of<LB>(vv8[i], l);
+                        *reinterpret_cast<uint2 *>(sZR + (pp * LB + l) * G::ZR_LEN + 128 * G::NL - 8 - 8 * c) =
+                            make_uint2(pack4(x[7], x[6], x[5], x[4]), pack4(x[3], x[2], x[1], x[0]));
+                    }
                 }
             }
         }
@@ -307,8 +340,8 @@ __global__ void __launch_bounds__(128) tc_mul_kernel(MulArgs a) {
         // ---- A: sliding windows, row rho = hA[rho .. rho+15] (descriptor starts at row 1);
         //      each work item builds rows 4m .. 4m+3 from 5 words, stores rotated by m (banks)
 #pragma unroll 1
-        for (int w = tid; w < LA * G::AROWS4; w += 128) {
-            const int l = w / G::AROWS4, m = w - l * G::AROWS4;
+        for (int wi = tid; wi < LA * G::AROWS4; wi += 128) {
+            const int l = wi / G::AROWS4, m = wi - l * G::AROWS4;
             const uint32_t *src = reinterpret_cast<const uint32_t *>(sHA + l * G::HA_LEN) + m;
             uint32_t wd[5];
 #pragma unroll
@@ -326,9 +359,9 @@ __global__ void __launch_bounds__(128) tc_mul_kernel(MulArgs a) {
                 dst[s_] = o;
             }
         }
-        // ---- B: row (l*NL + t), K-chunk c = zr_l chunk 8(NL-1-t) + c.  Work item (row, res):
-        //      chunks c = res + 8i; res = (item/BROWS + row) mod 8 keeps 8 consecutive lanes on
-        //      distinct banks for both the load and the store.
+        // ---- B: row (pp*PCOL + l*NL + t), K-chunk c = zr_{pp,l} chunk 8(NL-1-t) + c.  Work item
+        //      (row, res): chunks c = res + 8i; res = (item/BROWS + row) mod 8 keeps 8
+        //      consecutive lanes on distinct banks for both the load and the store.
 #pragma unroll
         for (int h = 0; h < G::BPER; h++) {
             if (bsrc[h] < 0) continue;
@@ -356,60 +389,57 @@ __global__ void __launch_bounds__(128) tc_mul_kernel(MulArgs a) {
             }
             umma_commit(bar);
         }
-        prefetch(prod + gridDim.x);
+        prefetch(it + gridDim.x);
         if (tid == 0) mbar_wait(bar, phase);
         phase ^= 1;
         __syncthreads();
         tc_fence_after();
-        // ---- epilogue: thread tid = TMEM lane = coefficient r of every block
-        int acc[LA][LB][G::NL];
-        {
-            const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
-            int v[LA][G::NB / 16][16];
+        // ---- epilogue: thread tid = TMEM lane = coefficient r of every block, product by product
+        const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
+        int vals[NPR][G::NBLK];
+#pragma unroll
+        for (int pp = 0; pp < NPR; pp++) {
+            int v[LA][G::PCOL / 16][16];
 #pragma unroll
             for (int l = 0; l < LA; l++)
 #pragma unroll
-                for (int c16 = 0; c16 < G::NB / 16; c16++) tmem_ld16(lane_addr + l * G::NB + 16 * c16, v[l][c16]);
+                for (int c16 = 0; c16 < G::PCOL / 16; c16++)
+                    tmem_ld16(lane_addr + l * G::NB + pp * G::PCOL + 16 * c16, v[l][c16]);
             tmem_ld_wait();
 #pragma unroll
-            for (int l = 0; l < LA; l++)
-#pragma unroll
-                for (int c16 = 0; c16 < G::NB / 16; c16++)
-#pragma unroll
-                    for (int i = 0; i < 16; i++) {
-                        const int col = 16 * c16 + i;
-                        const int lb = col / G::NL, t = col - lb * G::NL;
-                        if (lb < LB) acc[l][lb][t] = v[l][c16][i];
-                    }
+            for (int t = 0; t < G::NBLK; t++) {
+                // D[l][lb*NL + t]
+                auto D = [&](int l, int lb) { const int col = lb * G::NL + t; return v[l][col >> 4][col & 15]; };
+                int x;
+                if (LA == 1 && LB == 1) x = D(0, 0);
+                else if (LA == 1) x = (64 * D(0, 0) + D(0, 1)) % M;
+                else if (LB == 1) x = (64 * D(0, 0) + D(1, 0)) % M;
+                else x = (4096 * (D(0, 0) % M) + 64 * (D(0, 1) + D(1, 0)) + D(1, 1)) % M;
+                vals[pp][t] = x;
+            }
         }
         tc_fence_before();
         __syncthreads();     // all TMEM reads done (next MMAs may overwrite); A region now free
 #pragma unroll
-        for (int t = 0; t < G::NBLK; t++) {
-            int v;
-            if (LA == 1 && LB == 1) {
-                v = acc[0][0][t];
-            } else if (LA == 1) {
-                v = (64 * acc[0][0][t] + acc[0][1][t]) % M;
-            } else if (LB == 1) {
-                v = (64 * acc[0][0][t] + acc[1][0][t]) % M;
-            } else {
-                v = (4096 * (acc[0][0][t] % M) + 64 * (acc[0][1][t] + acc[1][0][t]) + acc[1][1][t]) % M;
-            }
-            raw[128 * t + tid] = v;
-        }
+        for (int pp = 0; pp < NPR; pp++)
+#pragma unroll
+            for (int t = 0; t < G::NBLK; t++) raw[pp * G::RAW_INTS + 128 * t + tid] = vals[pp][t];
         __syncthreads();
         // ---- fold with x^p = x + 1, center, store (lane-consecutive coefficients: no bank conflicts)
-        {
-            const int ostride_elems = a.out_bytes == 2 ? PS::P8 : PS::P16;
+        const int ostride_elems = a.out_bytes == 2 ? PS::P8 : PS::P16;
+#pragma unroll
+        for (int pp = 0; pp < NPR; pp++) {
+            const long long orow = w.orow[pp];
+            if (orow < 0) continue;
+            const int *rw = raw + pp * G::RAW_INTS;
             for (int k = tid; k < ostride_elems; k += 128) {
                 int v = 0;
                 if (k < P) {
-                    v = raw[k] + raw[k + P] + (k >= 1 ? raw[k + P - 1] : 0);
+                    v = rw[k] + rw[k + P] + (k >= 1 ? rw[k + P - 1] : 0);
                     v = canon<M>(v);
                 }
-                if (a.out_bytes == 2) ((int16_t *)a.out)[prod * a.out_stride + k] = (int16_t)v;
-                else ((int8_t *)a.out)[prod * a.out_stride + k] = (int8_t)v;
+                if (a.out_bytes == 2) ((int16_t *)a.out)[orow * a.out_stride + k] = (int16_t)v;
+                else ((int8_t *)a.out)[orow * a.out_stride + k] = (int8_t)v;
             }
         }
         // the next iteration's first __syncthreads orders these raw reads before A rewrites
