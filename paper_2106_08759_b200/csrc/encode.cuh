@@ -45,6 +45,13 @@ __device__ __forceinline__ uint8_t small_byte(const int8_t *row, int j) {
     return (uint8_t)v;
 }
 
+// small-encode 4 trits {-1,0,1} packed in a little-endian word -> one byte sum (c+1) 4^t
+__device__ __forceinline__ uint32_t small4(uint32_t w) {
+    // bytes b_t in {0xff, 0, 1}: ((b_t & 3) + 1) & 3 = c + 1 in {0, 1, 2}, carry-free per byte
+    const uint32_t d = ((w & 0x03030303u) + 0x01010101u) & 0x03030303u;
+    return (d & 0xffu) | ((d >> 6) & 0x0cu) | ((d >> 12) & 0x30u) | ((d >> 18) & 0xc0u);
+}
+
 template <class PS>
 __global__ void __launch_bounds__(128) encode_kernel(EncArgs a) {
     constexpr int WPB = 4;
@@ -58,9 +65,35 @@ __global__ void __launch_bounds__(128) encode_kernel(EncArgs a) {
         uint16_t *R = sR[wid][0], *R2 = sR[wid][1];
         uint8_t *out = spk[wid];
         const int16_t *hrow = a.h + key * PS::P8;
-        for (int i = lane; i < PS::P; i += 32) R[i] = (uint16_t)(hrow[i] + PS::QH);
+        // level 0 straight from HBM: 8 coefficients (4 pairs) per lane and 16-byte load; every
+        // level-0 pair has M = q*q and emits the same number of bytes e0 at offset e0*i
+        {
+            const uint32_t m0 = a.t.Mlo[0];
+            const int e0 = a.t.emit[0];
+            const int npairs = a.t.lev_n[0] / 2;
+            for (int c = lane; c < PS::P8 / 8; c += 32) {
+                const uint4 q4 = __ldg(reinterpret_cast<const uint4 *>(hrow) + c);
+                const uint32_t w[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+                for (int t = 0; t < 4; t++) {
+                    const int i = 4 * c + t;                          // pair index
+                    const uint32_t r0 = (uint32_t)((int)(int16_t)(w[t] & 0xffffu) + PS::QH);
+                    const uint32_t r1 = (uint32_t)((int)(int16_t)(w[t] >> 16) + PS::QH);
+                    if (i < npairs) {
+                        uint32_t r = r0 + m0 * r1;
+                        for (int b = 0; b < e0; b++) { out[e0 * i + b] = (uint8_t)(r & 255u); r >>= 8; }
+                        R2[i] = (uint16_t)r;
+                    } else if (2 * i < PS::P) {
+                        R2[i] = (uint16_t)r0;                          // odd last element carried
+                    }
+                }
+            }
+        }
         __syncwarp();
-        for (int lev = 0; lev < a.t.nlev; lev++) {
+        {
+            uint16_t *tmp = R; R = R2; R2 = tmp;
+        }
+        for (int lev = 1; lev < a.t.nlev; lev++) {
             const int n = a.t.lev_n[lev];
             const int base = a.t.lev_pair_base[lev];
             for (int i = lane; i < n / 2; i += 32) {
@@ -84,12 +117,26 @@ __global__ void __launch_bounds__(128) encode_kernel(EncArgs a) {
         for (int k = lane; k < a.t.pk_bytes; k += 32) dst[k] = out[k];
     }
     if (a.f) {
+        // 16 trits per 16-byte load -> 4 sk bytes; trits >= P are 0 (pad) and contribute (0+1)
+        // in the low-level formula, so the last byte is masked to its P mod 4 coefficients
         uint8_t *dst = a.sk + key * (uint64_t)(2 * PS::SKH);
-        const int8_t *frow = a.f + key * PS::P16;
-        const int8_t *grow = a.ginv + key * PS::P16;
-        for (int j = lane; j < PS::SKH; j += 32) {
-            dst[j] = small_byte<PS>(frow, j);
-            dst[PS::SKH + j] = small_byte<PS>(grow, j);
+        const int8_t *rows[2] = {a.f + key * PS::P16, a.ginv + key * PS::P16};
+#pragma unroll
+        for (int which = 0; which < 2; which++) {
+            for (int c = lane; c < PS::P16 / 16; c += 32) {
+                const uint4 q4 = __ldg(reinterpret_cast<const uint4 *>(rows[which]) + c);
+                const uint32_t w[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+                for (int t = 0; t < 4; t++) {
+                    const int j = 4 * c + t;                          // sk byte index
+                    if (j < PS::SKH) {
+                        uint32_t b = small4(w[t]);
+                        const int nvalid = PS::P - 4 * j;             // coefficients present
+                        if (nvalid < 4) b &= (1u << (2 * nvalid)) - 1u;
+                        dst[which * PS::SKH + j] = (uint8_t)b;
+                    }
+                }
+            }
         }
     }
 }

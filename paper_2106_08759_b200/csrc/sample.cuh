@@ -14,35 +14,53 @@ namespace sntrup {
 // ---------------------------------------------------------------------------------------------
 // Warp-wide bitonic sort of 32*E uint32 keys held in registers, blocked layout: lane l holds
 // global elements l*E .. l*E+E-1 in v[0..E-1].  Ascending.  A fixed network (constant time).
+// Variant with every comparator ascending: each merge stage starts with the "mirror" step
+// (i <-> i ^ (k-1)) followed by half-cleaners (i <-> i ^ j), so no direction selects are needed;
+// across lanes a comparator is one SHFL plus one predicated min/max.
 // ---------------------------------------------------------------------------------------------
 template <int E>
 __device__ __forceinline__ void warp_bitonic_sort(uint32_t (&v)[E], int lane) {
     constexpr int N = 32 * E;
 #pragma unroll
     for (int k = 2; k <= N; k <<= 1) {
+        // mirror step
+        if (k <= E) {
 #pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int e = 0; e < E; e++) {
+                const int ex = e ^ (k - 1);
+                if ((e & (k >> 1)) == 0) {
+                    const uint32_t a = v[e], b = v[ex];
+                    v[e] = min(a, b);
+                    v[ex] = max(a, b);
+                }
+            }
+        } else {
+            const int lm = k / E - 1;                      // partner lane = lane ^ lm, element E-1-e
+            const bool lower = (lane & ((k / E) >> 1)) == 0;
+            uint32_t o[E];
+#pragma unroll
+            for (int e = 0; e < E; e++) o[e] = __shfl_xor_sync(FULL, v[E - 1 - e], lm);
+#pragma unroll
+            for (int e = 0; e < E; e++) v[e] = lower ? min(v[e], o[e]) : max(v[e], o[e]);
+        }
+        // half-cleaners
+#pragma unroll
+        for (int j = k >> 2; j > 0; j >>= 1) {
             if (j >= E) {
                 const int lm = j / E;
                 const bool lower = (lane & lm) == 0;
-                const bool up = ((lane * E) & k) == 0;     // k > j >= E: bit k of i is a lane bit
-                const bool take_min = (lower == up);
 #pragma unroll
                 for (int e = 0; e < E; e++) {
                     const uint32_t o = __shfl_xor_sync(FULL, v[e], lm);
-                    v[e] = take_min ? min(v[e], o) : max(v[e], o);
+                    v[e] = lower ? min(v[e], o) : max(v[e], o);
                 }
             } else {
 #pragma unroll
                 for (int e = 0; e < E; e++) {
                     if ((e & j) == 0) {
-                        const int ex = e | j;
-                        // direction bit k of i = l*E + e: from e when k < E, from the lane otherwise
-                        const bool up = (k < E) ? ((e & k) == 0) : (((lane * E) & k) == 0);
-                        const uint32_t a = v[e], b = v[ex];
-                        const uint32_t mn = min(a, b), mx = max(a, b);
-                        v[e] = up ? mn : mx;
-                        v[ex] = up ? mx : mn;
+                        const uint32_t a = v[e], b = v[e | j];
+                        v[e] = min(a, b);
+                        v[e | j] = max(a, b);
                     }
                 }
             }

@@ -114,7 +114,7 @@ def test_cfg2_full_size_sampled(O):
     # BASELINE configs[1]: 65,536 keys, seed 2, in the launch configuration bench.py times;
     # compared on a sample the oracle computes one by one: first and last trees, every 97th key.
     n = 65536
-    for B in (32, 128):
+    for B in (32, 128, 512, 2048):
         res = S.batch_keygen(761, n, 2, batch_size=B)
         torch.cuda.synchronize()
         idx = np.unique(np.concatenate([np.arange(0, 128), np.arange(n - 128, n), np.arange(0, n, 97)]))
@@ -123,6 +123,50 @@ def test_cfg2_full_size_sampled(O):
             first = (res["pk"].clone(), res["sk"].clone())
         else:
             assert torch.equal(first[0], res["pk"]) and torch.equal(first[1], res["sk"])
+
+
+def _rejection_bound(param, att):
+    """Total extra g draws vs the per-draw rejection probability (golden): per key the
+    extra draws are geometric with mean P/(1-P) and variance P/(1-P)^2; accept within 6 sigma."""
+    import json
+    import os
+    rates = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "rejection_rates.json")))
+    P = rates["p_reject_per_draw"][str(param)]
+    n = len(att)
+    extra = float((att.astype(np.int64) - 1).sum())
+    mean, sd = n * P / (1 - P), (n * P) ** 0.5 / (1 - P)
+    assert abs(extra - mean) <= 6 * sd + 1, (param, extra, mean, sd)
+
+
+@pytest.mark.parametrize("param", [653, 857, 953, 1013])
+def test_cfg4_full_size_sampled(O, param):
+    # BASELINE configs[3]: 65,536 keys per set, seed 4.  Compared with the oracle on every key
+    # that needed more than one g draw, the first and last trees, and every 97th key.
+    n = 65536
+    res = S.batch_keygen(param, n, 4, batch_size=512, debug=True)
+    torch.cuda.synchronize()
+    att = res["attempts"].cpu().numpy()
+    assert att.min() >= 1
+    _rejection_bound(param, att)
+    rej = np.nonzero(att > 1)[0]
+    idx = np.unique(np.concatenate([np.arange(0, 64), np.arange(n - 64, n), np.arange(0, n, 97), rej]))
+    check_keys(O, param, 4, res, idx)
+
+
+def test_cfg5_full_size_sampled(O):
+    # BASELINE configs[4]: sntrup1277, 1,048,576 keys, seed 5, 1024 keys per product tree,
+    # streamed in 65,536-key chunks.  Sampled: first/last chunk edges, every 509th key, every
+    # 32nd key that needed more than one g draw; rejection total vs the per-draw probability.
+    n = 1 << 20
+    res = S.batch_keygen(1277, n, 5, batch_size=1024, chunk_keys=65536, debug=True)
+    torch.cuda.synchronize()
+    att = res["attempts"].cpu().numpy()
+    assert att.min() >= 1
+    _rejection_bound(1277, att)
+    rej = np.nonzero(att > 1)[0]
+    idx = np.unique(np.concatenate([np.arange(0, 64), np.arange(65536 - 32, 65536 + 32),
+                                    np.arange(n - 64, n), np.arange(0, n, 509), rej[::32]]))
+    check_keys(O, 1277, 5, res, idx)
 
 
 # --------------------------------------------------------------------------------- ring ops
