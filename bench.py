@@ -267,6 +267,7 @@ def main():
     S.profile_enable(True)
     ms_prof = timed(step, args.steps)
     prof = S.profile_read(reset=True)
+    kinds = S.profile_read_kinds(reset=True)
     S.profile_enable(False)
 
     # ---- e2e through the C ABI with HOST output buffers (D2H inside the timed region)
@@ -288,30 +289,38 @@ def main():
     if rank == 0:
         peaks = load_peaks()
         sm_mhz = clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
-        # dominant kernel class by device time
+        # dominant kernel class by device time; the roofline is taken on the ring-product
+        # kernels of the dominant arithmetic kind (int8 or fp4 tensor, or int32 schoolbook),
+        # each against its own peak
         dom = max(prof, key=lambda k: prof[k]["ms"])
         tot_ms = sum(v["ms"] for v in prof.values())
+        kd = max(kinds, key=lambda k: kinds[k]["ms"])
         roof = None
-        if dom in ("rq_mul", "r3_mul"):
-            launches_d = max(1, prof[dom]["launches"])
-            avg_ms = prof[dom]["ms"] / launches_d
-            ops_per_launch = prof[dom]["ops"] / launches_d
-            achieved = ops_per_launch / (avg_ms / 1e3) / 1e12                     # T ops/s
-            if MUL_IMPL == "tc":
-                peak, src = int8_tc_peak_tops(peaks)
-                roof = {"bound": "tensor", "kernel": dom + " (tc_mul_kernel: tcgen05.mma kind::i8)",
+        if kinds[kd]["launches"]:
+            launches_d = kinds[kd]["launches"]
+            avg_ms = kinds[kd]["ms"] / launches_d
+            achieved = kinds[kd]["ops"] / launches_d / (avg_ms / 1e3) / 1e12          # T ops/s
+            share = kinds[kd]["ms"] / tot_ms
+            if kd in ("tc_int8", "tc_fp4"):
+                peak8, src = int8_tc_peak_tops(peaks)
+                peak = peak8 if kd == "tc_int8" else 2 * peak8
+                roof = {"bound": "tensor",
+                        "kernel": "ring products, " + ("tc_mul_kernel (tcgen05.mma kind::i8)" if kd == "tc_int8"
+                                                        else "tc4_mul_kernel (tcgen05.mma kind::mxf4)"),
                         "achieved": achieved, "peak": peak,
-                        "unit": "TOPS int8 (algorithmic: 2 p^2 per limb-pair product)",
-                        "frac": achieved / peak, "traffic": TRAFFIC.get(dom),
-                        "peak_source": src, "share_of_step": prof[dom]["ms"] / tot_ms}
+                        "unit": "TOPS %s (algorithmic: 2 p^2 per limb/digit-pair product)" % ("int8" if kd == "tc_int8" else "fp4"),
+                        "frac": achieved / peak, "traffic": TRAFFIC.get("tc_int8" if kd == "tc_int8" else "tc_fp4"),
+                        "peak_source": src + ("" if kd == "tc_int8" else " x 2 (nominal fp4/int8 ratio 9/4.5 PF)"),
+                        "share_of_step": share,
+                        "by_kind_ms_per_step": {k: v["ms"] / args.steps for k, v in kinds.items()}}
             else:
                 peak = 2 * int_peak_macs_per_s(sm_mhz) / 1e12
-                roof = {"bound": "alu", "kernel": dom + " (ring_mul_kernel: int32 schoolbook)",
+                roof = {"bound": "alu", "kernel": "ring products, ring_mul_kernel (int32 schoolbook)",
                         "achieved": achieved, "peak": peak,
                         "unit": "TOPS int32 (2 p^2 per product)", "frac": achieved / peak,
                         "traffic": None,
                         "peak_source": "derived: 64 IMAD lanes/clk/SM x 2 ops x 148 SMs x %.0f MHz" % sm_mhz,
-                        "share_of_step": prof[dom]["ms"] / tot_ms}
+                        "share_of_step": share}
         result = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -339,7 +348,10 @@ def main():
         result["batch_size_sweep_keys_per_s"] = sweep
         # A/B: the same step without the shared-A down-sweep, and on the int32 schoolbook
         ab = {}
-        for name, impl in (("tc_no_shared_a", S.MUL_TENSOR_CORE_NO_SHARED_A), ("int32_schoolbook", S.MUL_SCHOOLBOOK)):
+        for name, impl in (("tc_fp4_all_small", S.MUL_TENSOR_CORE_FP4_ALL),
+                           ("tc_int8_shared_a", S.MUL_TENSOR_CORE_INT8),
+                           ("tc_int8_no_shared_a", S.MUL_TENSOR_CORE_NO_SHARED_A),
+                           ("int32_schoolbook", S.MUL_SCHOOLBOOK)):
             S.set_mul_impl(impl)
             step()
             ab[name] = n * 2 / (timed(step, 2) / 1e3)

@@ -139,9 +139,13 @@ void sntrup_release_workspace(void);
 uint64_t sntrup_kernel_launch_count(void);
 
 /* Select the ring-product implementation used by every call (measurement / A-B evidence):
-   0 = tensor cores (tcgen05.mma kind::i8 Hankel GEMM, the default), 1 = int32 schoolbook on the
-   integer pipes (v1), 2 = tensor cores without the shared-A down-sweep (one product per work
-   item; for A/B measurement).  All are exact.  Returns SNTRUP_OK or SNTRUP_E_ARG. */
+   0 = tensor cores (the default): tcgen05.mma kind::mxf4 (e2m1) for small x small products
+       (R/3, 3f x 3f), kind::i8 (int8 limbs) otherwise, the down-sweep's children sharing one A;
+   1 = int32 schoolbook on the integer pipes (v1);
+   2 = int8 tensor cores only, one product per work item (v2);
+   3 = int8 tensor cores only, with the shared-A down-sweep;
+   4 = as 0, plus big x small products on fp4 with balanced base-9 digits (A/B only).
+   All are exact.  Returns SNTRUP_OK or SNTRUP_E_ARG. */
 int sntrup_set_mul_impl(int impl);
 
 /* Measurement hooks (bench.py).  When enabled, every kernel launch is bracketed by CUDA events
@@ -153,6 +157,10 @@ int sntrup_set_mul_impl(int impl);
    [inversions], 4 R/q root inversion [inversions], 5 repair [keys], 6 encode [keys], 7 other).
    Any output pointer may be NULL.  Returns the number of classes. */
 void sntrup_profile_enable(int on);
+/* Ring-product launches by arithmetic kind (0 = int8 tensor, 1 = fp4 tensor, 2 = int32
+   schoolbook): summed device ms, algorithmic ops (2 p^2 per limb/digit-pair product) and launch
+   counts since the last reset.  Returns the number of kinds (3). */
+int sntrup_profile_read_kinds(int reset, double *ms, double *ops, uint64_t *launches);
 int sntrup_profile_read(int reset, double *ms, double *units, double *ops, uint64_t *launches,
                         int max_classes);
 

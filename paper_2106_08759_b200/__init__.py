@@ -66,13 +66,15 @@ _lib.sntrup_profile_enable.restype = None
 _lib.sntrup_profile_enable.argtypes = [_i32]
 _lib.sntrup_profile_read.restype = _i32
 _lib.sntrup_profile_read.argtypes = [_i32, _vp, _vp, _vp, _vp, _i32]
+_lib.sntrup_profile_read_kinds.restype = _i32
+_lib.sntrup_profile_read_kinds.argtypes = [_i32, _vp, _vp, _vp]
 _lib.rq_mul_small_batch.argtypes = [_i32, _u64, _vp, _vp, _vp, _vp]
 
 EXPORTED = ("sntrup_params", "sntrup_strerror", "sntrup_batch_keygen", "sntrup_batch_keygen_ex",
             "sntrup_keygen_workspace_bytes", "rq_mul_batch", "rq_mul_small_batch", "r3_mul_batch", "rq_recip_batch",
             "r3_recip_batch", "r3_is_invertible_batch", "rq_encode_batch",
             "sntrup_release_workspace", "sntrup_kernel_launch_count", "sntrup_set_mul_impl",
-            "sntrup_profile_enable",
+            "sntrup_profile_enable", "sntrup_profile_read_kinds",
             "sntrup_profile_read")
 
 PROFILE_CLASSES = ("sample", "r3_mul", "rq_mul", "r3_inv", "rq_inv", "repair", "encode", "other")
@@ -248,7 +250,9 @@ def kernel_launch_count() -> int:
 
 MUL_TENSOR_CORE = 0
 MUL_SCHOOLBOOK = 1
-MUL_TENSOR_CORE_NO_SHARED_A = 2
+MUL_TENSOR_CORE_NO_SHARED_A = 2   # int8 only, one product per work item
+MUL_TENSOR_CORE_INT8 = 3          # int8 only, shared-A down-sweep
+MUL_TENSOR_CORE_FP4_ALL = 4       # fp4 also for big x small (base-9 digits)
 
 
 def set_mul_impl(impl: int):
@@ -258,6 +262,18 @@ def set_mul_impl(impl: int):
 
 def profile_enable(on: bool = True):
     _lib.sntrup_profile_enable(1 if on else 0)
+
+
+MUL_KINDS = ("tc_int8", "tc_fp4", "int32")
+
+
+def profile_read_kinds(reset: bool = True) -> dict:
+    """Ring-product launches by arithmetic kind: device ms, algorithmic ops, launches."""
+    ms = (ctypes.c_double * 3)()
+    op = (ctypes.c_double * 3)()
+    la = (ctypes.c_uint64 * 3)()
+    _lib.sntrup_profile_read_kinds(1 if reset else 0, ms, op, la)
+    return {MUL_KINDS[i]: dict(ms=ms[i], ops=op[i], launches=la[i]) for i in range(3)}
 
 
 def profile_read(reset: bool = True) -> dict:

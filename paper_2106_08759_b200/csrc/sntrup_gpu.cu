@@ -26,6 +26,7 @@
 #include "ringmul.cuh"
 #include "sample.cuh"
 #include "tcmul.cuh"
+#include "tc4mul.cuh"
 
 using namespace sntrup;
 
@@ -40,12 +41,17 @@ std::mutex g_mu;                                   // serialises calls (shared w
 // inversions).  Read back with sntrup_profile_read().
 enum ProfClass { PC_SAMPLE = 0, PC_MUL_R3, PC_MUL_RQ, PC_INV_R3, PC_INV_RQ, PC_REPAIR, PC_ENCODE,
                  PC_MISC, PC_N };
-struct ProfRec { int cls; cudaEvent_t a, b; double units, ops; };
+struct ProfRec { int cls; cudaEvent_t a, b; double units, ops; int kind; };
 bool g_prof_on = false;
 std::vector<ProfRec> g_prof;
 std::vector<cudaEvent_t> g_evpool;
 struct ProfAgg { double ms = 0, units = 0, ops = 0; uint64_t launches = 0; };
 ProfAgg g_agg[PC_N];
+// ring-product launches by arithmetic kind: 0 = int8 tensor (kind::i8), 1 = fp4 tensor
+// (kind::mxf4), 2 = int32 schoolbook
+enum { PK_I8 = 0, PK_F4 = 1, PK_I32 = 2, PK_N = 3 };
+ProfAgg g_kagg[PK_N];
+int g_cur_kind = -1;                 // set by the launcher inside a ProfScope
 
 cudaEvent_t ev_get() {
     if (!g_evpool.empty()) { cudaEvent_t e = g_evpool.back(); g_evpool.pop_back(); return e; }
@@ -61,7 +67,8 @@ struct ProfScope {
         if (g_prof_on) { a = ev_get(); cudaEventRecord(a, s); }
     }
     ~ProfScope() {
-        if (a) { cudaEvent_t b = ev_get(); cudaEventRecord(b, s); g_prof.push_back(ProfRec{cls, a, b, units, ops}); }
+        if (a) { cudaEvent_t b = ev_get(); cudaEventRecord(b, s); g_prof.push_back(ProfRec{cls, a, b, units, ops, g_cur_kind}); }
+        g_cur_kind = -1;
     }
 };
 
@@ -73,6 +80,12 @@ void prof_drain() {
         g_agg[r.cls].ms += ms;
         g_agg[r.cls].units += r.units;
         g_agg[r.cls].ops += r.ops;
+        if (r.kind >= 0) {
+            g_kagg[r.kind].ms += ms;
+            g_kagg[r.kind].ops += r.ops;
+            g_kagg[r.kind].units += r.units;
+            g_kagg[r.kind].launches += 1;
+        }
         g_agg[r.cls].launches += 1;
         g_evpool.push_back(r.a);
         g_evpool.push_back(r.b);
@@ -329,7 +342,11 @@ TreePlan make_plan(long long m, int B) {
 }
 
 // ------------------------------------------------------------------------------ launches
-int g_mul_impl = 0;   // 0 = tensor cores (tcmul.cuh), 1 = int32 schoolbook, 2 = tensor cores without shared-A down-sweep
+// ring-product implementation (sntrup_set_mul_impl): 0 = tensor cores, fp4 (tc4mul.cuh) where an
+// operand is small + int8 (tcmul.cuh) otherwise, shared-A down-sweep; 1 = int32 schoolbook;
+// 2 = int8 tensor cores only, one product per work item; 3 = int8 tensor cores with shared A;
+// 4 = as 0 but big x small products also on fp4 (base-9 digits; slower, kept for A/B)
+int g_mul_impl = 0;
 
 struct DevInfo { int sms = 0; };
 DevInfo &dev_info() {
@@ -362,6 +379,34 @@ int launch_tc(const MulArgs &a, cudaStream_t s) {
     }
     long long grid = (long long)it->second * dev_info().sms;
     if (grid > a.n_out) grid = a.n_out;
+    g_cur_kind = PK_I8;
+    kern<<<(unsigned)grid, 128, G::SMEM, s>>>(a);
+    LAUNCHED();
+    return SNTRUP_OK;
+}
+
+template <class PS, int M, int LB, int NPR = 1>
+int launch_tc4(const MulArgs &a, cudaStream_t s) {
+    using G = Tc4Geom<PS, LB, NPR>;
+    auto kern = tc4_mul_kernel<PS, M, LB, NPR>;
+    static std::map<int, int> per_sm;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    auto it = per_sm.find(dev);
+    if (it == per_sm.end()) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        int nb = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 128, G::SMEM));
+        const int by_smem = (227 * 1024) / (G::SMEM + 1024);
+        if (nb < by_smem) nb = by_smem;
+        if (nb < 1) nb = 1;
+        if (nb * G::TCOLS > 512) nb = 512 / G::TCOLS;
+        it = per_sm.emplace(dev, nb).first;
+    }
+    long long grid = (long long)it->second * dev_info().sms;
+    if (grid > a.n_out) grid = a.n_out;
+    g_cur_kind = PK_F4;
     kern<<<(unsigned)grid, 128, G::SMEM, s>>>(a);
     LAUNCHED();
     return SNTRUP_OK;
@@ -373,13 +418,18 @@ int launch_mul(MulArgs a, cudaStream_t s, int la = 2, int lb = 2) {
     if (a.n_out <= 0) return SNTRUP_OK;
     // algorithmic ops: tensor path = 2 p^2 int8 multiply-add ops per limb-pair product (the
     // limb-decomposed schoolbook contraction); schoolbook path = 2 p^2 int32 ops per product
-    const int limb_pairs = (g_mul_impl == 1 || M == 3) ? 1 : la * lb;
+    // (fp4 path: digit pairs = LB base-9 digits of the big operand x 1)
+    const bool small_op = (M == 3) || la == 1 || lb == 1;
+    int limb_pairs = (g_mul_impl == 1 || M == 3) ? 1 : la * lb;
+    if (g_mul_impl == 0 && small_op && M != 3) limb_pairs = (la == 1 && lb == 1) ? 1 : 2;
+    if (g_mul_impl == 4 && small_op && M != 3) limb_pairs = (la == 1 && lb == 1) ? 1 : digits9(M);
     ProfScope ps_(M == 3 ? PC_MUL_R3 : PC_MUL_RQ, (double)a.n_out, s,
                   2.0 * PS::P * PS::P * limb_pairs * (double)a.n_out);
     if (g_mul_impl == 1) {
         const int threads = (PS::P8 / 8 + 31) / 32 * 32;
         long long grid = a.n_out;
         if (grid > (1LL << 30)) grid = 1LL << 30;
+        g_cur_kind = PK_I32;
         ring_mul_kernel<PS, M><<<(unsigned)grid, threads, 0, s>>>(a);
         LAUNCHED();
         return SNTRUP_OK;
@@ -391,13 +441,26 @@ int launch_mul(MulArgs a, cudaStream_t s, int la = 2, int lb = 2) {
         a.mode = MUL_DOWN2;
         a.n_out = (a.cnt_in + 1) / 2;
     }
+    const bool fp4 = g_mul_impl == 0 || g_mul_impl == 4;
     if constexpr (M == 3) {
         a.swap = 0;
+        if (fp4) return down2 ? launch_tc4<PS, M, 1, 2>(a, s) : launch_tc4<PS, M, 1, 1>(a, s);
         return down2 ? launch_tc<PS, M, 1, 1, 2>(a, s) : launch_tc<PS, M, 1, 1>(a, s);
     } else {
-        if (la == 1 && lb == 1) { a.swap = 0; return down2 ? launch_tc<PS, M, 1, 1, 2>(a, s) : launch_tc<PS, M, 1, 1>(a, s); }
-        if (la == 1) { a.swap = 0; return launch_tc<PS, M, 1, 2>(a, s); }
-        if (lb == 1) { a.swap = 1; return launch_tc<PS, M, 1, 2>(a, s); }
+        constexpr int D9 = digits9(M);
+        if (la == 1 && lb == 1) {
+            a.swap = 0;
+            if (fp4) return down2 ? launch_tc4<PS, M, 1, 2>(a, s) : launch_tc4<PS, M, 1, 1>(a, s);
+            return down2 ? launch_tc<PS, M, 1, 1, 2>(a, s) : launch_tc<PS, M, 1, 1>(a, s);
+        }
+        if (la == 1 || lb == 1) {
+            // the small operand takes the A (Hankel) role.  int8 with two limbs for the big one:
+            // measured faster than fp4 with D9 base-9 digits (larger N, digit staging), see
+            // DESIGN.md section 6; the fp4 variant stays selectable for A/B (impl 4)
+            a.swap = la == 1 ? 0 : 1;
+            if (g_mul_impl == 4) return launch_tc4<PS, M, D9, 1>(a, s);
+            return launch_tc<PS, M, 1, 2>(a, s);
+        }
         a.swap = 0;
         return down2 ? launch_tc<PS, M, 2, 2, 2>(a, s) : launch_tc<PS, M, 2, 2>(a, s);
     }
@@ -950,8 +1013,21 @@ void sntrup_release_workspace(void) {
 
 uint64_t sntrup_kernel_launch_count(void) { return g_launches.load(); }
 
+int sntrup_profile_read_kinds(int reset, double *ms, double *ops, uint64_t *launches) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    prof_drain();
+    for (int i = 0; i < PK_N; i++) {
+        if (ms) ms[i] = g_kagg[i].ms;
+        if (ops) ops[i] = g_kagg[i].ops;
+        if (launches) launches[i] = g_kagg[i].launches;
+    }
+    if (reset)
+        for (int i = 0; i < PK_N; i++) g_kagg[i] = ProfAgg{};
+    return PK_N;
+}
+
 int sntrup_set_mul_impl(int impl) {
-    if (impl < 0 || impl > 2) return SNTRUP_E_ARG;
+    if (impl < 0 || impl > 4) return SNTRUP_E_ARG;
     std::lock_guard<std::mutex> lk(g_mu);
     g_mul_impl = impl;
     return SNTRUP_OK;

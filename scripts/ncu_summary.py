@@ -33,13 +33,15 @@ def launches(path):
     hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
     h = rows[hi]
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    mi = h.index("Metric Name")
     agg = collections.OrderedDict()
     for r in rows[hi + 1:]:
-        if len(r) <= vi:
+        if len(r) <= vi or r[mi] != "gpu__time_duration.sum":
             continue
-        name = r[ki].split("(")[0]
+        name = r[ki].split("(")[0].replace("sntrup::", "").replace("Params<761, 4591, 286, 3>", "P761")
         v = float(r[vi].replace(",", ""))
-        v *= {"nsecond": 1, "usecond": 1e3, "msecond": 1e6, "second": 1e9}.get(r[ui], 1)
+        v *= {"ns": 1, "us": 1e3, "ms": 1e6, "nsecond": 1, "usecond": 1e3, "msecond": 1e6,
+              "second": 1e9}.get(r[ui], 1)
         a = agg.setdefault(name, [0, 0.0])
         a[0] += 1
         a[1] += v
