@@ -561,8 +561,7 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
     const int B = o.batch_size ? (int)o.batch_size : 32;
     if (B < 1 || B > 4096 || (B & (B - 1))) return SNTRUP_E_ARG;
     const bool host_out = (o.flags & SNTRUP_OPT_HOST_OUTPUT) != 0;
-    // host outputs: smaller default chunks so the D2H copies overlap the next chunk's compute
-    uint64_t chunk = o.chunk_keys ? o.chunk_keys : (host_out ? 16384 : 65536);
+    uint64_t chunk = o.chunk_keys ? o.chunk_keys : 65536;
     chunk = (chunk + B - 1) / B * B;
     if (chunk > n) chunk = (n + B - 1) / B * B;
     const size_t pkb = tb->enc.pk_bytes, skb = 2 * PS::SKH;
@@ -651,41 +650,58 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
         }
         LAUNCHED();
 
-        // R/q: Fbar = batchInv([3 f])   (Algorithm 1 line 11)
-        if ((rc = batch_inverse<PS, PS::Q>(tp, rows8(Fc, PS::P16, 3), Fbar, 2, PS::P8, lq, iq, okq, true, s, &n_rq)))
-            return rc;
-        // H = [g * fbar]   (Algorithm 1 line 12)
-        {
-            MulArgs a{};
-            a.mode = MUL_ZIP;
-            a.n_out = (long long)m;
-            a.X = rows8(Gc, PS::P16);
-            a.Y = rows16(Fbar, PS::P8);
-            a.out = Hc;
-            a.out_stride = PS::P8;
-            a.out_bytes = 2;
-            a.periodic = 0;
-            if ((rc = launch_mul<PS, PS::Q>(a, s, 1, 2))) return rc;       // g small, fbar big
-            n_rq += m;
-        }
-        n_inv += 2 * tp.cnt[tp.L];
-        // encode (KeyGen step 5)
-        {
+        if (host_out) {
+            // sk = Small(f) || Small(1/g) is final here (after repair): encode it and start its
+            // D2H copy while the R/q tree runs
             EncArgs ea{};
-            ea.n = m; ea.h = Hc; ea.f = Fc; ea.ginv = Ic; ea.pk = pkc; ea.sk = skc; ea.t = tb->enc;
+            ea.n = m; ea.h = nullptr; ea.f = Fc; ea.ginv = Ic; ea.pk = nullptr; ea.sk = skc; ea.t = tb->enc;
             {
                 ProfScope ps_(PC_ENCODE, (double)m, s);
                 encode_kernel<PS><<<(unsigned)((m + 3) / 4), 128, 0, s>>>(ea);
             }
             LAUNCHED();
-        }
-        if (host_out) {
             CK(cudaEventRecord(cs->comp[buf], s));
             CK(cudaStreamWaitEvent(cs->s, cs->comp[buf], 0));
-            CK(cudaMemcpyAsync(pk_out + c0 * pkb, pkc, m * pkb, cudaMemcpyDeviceToHost, cs->s));
             CK(cudaMemcpyAsync(sk_out + c0 * skb, skc, m * skb, cudaMemcpyDeviceToHost, cs->s));
-            CK(cudaEventRecord(cs->copy[buf], cs->s));
         }
+        // R/q: Fbar = batchInv([3 f])   (Algorithm 1 line 11)
+        if ((rc = batch_inverse<PS, PS::Q>(tp, rows8(Fc, PS::P16, 3), Fbar, 2, PS::P8, lq, iq, okq, true, s, &n_rq)))
+            return rc;
+        n_inv += 2 * tp.cnt[tp.L];
+        // H = [g * fbar] (Algorithm 1 line 12) and encode (KeyGen step 5).  With host outputs the
+        // tail runs in sub-batches, each pk slice copied D2H while the next slice computes.
+        const int nsub = host_out ? 4 : 1;
+        for (int j = 0; j < nsub; j++) {
+            const uint64_t r0 = m * (uint64_t)j / nsub, r1 = m * (uint64_t)(j + 1) / nsub, rows = r1 - r0;
+            if (!rows) continue;
+            {
+                MulArgs a{};
+                a.mode = MUL_ZIP;
+                a.n_out = (long long)rows;
+                a.X = rows8(Gc + r0 * PS::P16, PS::P16);
+                a.Y = rows16(Fbar + r0 * PS::P8, PS::P8);
+                a.out = Hc + r0 * PS::P8;
+                a.out_stride = PS::P8;
+                a.out_bytes = 2;
+                a.periodic = 0;
+                if ((rc = launch_mul<PS, PS::Q>(a, s, 1, 2))) return rc;   // g small, fbar big
+            }
+            {
+                EncArgs ea{};
+                ea.n = rows; ea.h = Hc + r0 * PS::P8; ea.pk = pkc + r0 * pkb; ea.t = tb->enc;
+                if (!host_out) { ea.f = Fc + r0 * PS::P16; ea.ginv = Ic + r0 * PS::P16; ea.sk = skc + r0 * skb; }
+                ProfScope ps_(PC_ENCODE, (double)rows, s);
+                encode_kernel<PS><<<(unsigned)((rows + 3) / 4), 128, 0, s>>>(ea);
+            }
+            LAUNCHED();
+            if (host_out) {
+                CK(cudaEventRecord(cs->comp[buf], s));
+                CK(cudaStreamWaitEvent(cs->s, cs->comp[buf], 0));
+                CK(cudaMemcpyAsync(pk_out + (c0 + r0) * pkb, pkc + r0 * pkb, rows * pkb, cudaMemcpyDeviceToHost, cs->s));
+            }
+        }
+        n_rq += m;
+        if (host_out) CK(cudaEventRecord(cs->copy[buf], cs->s));
     }
     if (host_out) {                       // join the copies into the caller's stream
         for (int i = 0; i < 2; i++) CK(cudaStreamWaitEvent(s, cs->copy[i], 0));

@@ -1,0 +1,5 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 600 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.log 2>&1; echo "rc=$?" >> gpurun_out/bench.log
+python -c "
+import json;d=json.loads(open('gpurun_out/bench.log').readlines()[0]);print(d['value'],d['ms_per_step']);print(d['breakdown_ms_per_step']);print(d['e2e'])"
