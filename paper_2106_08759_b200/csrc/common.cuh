@@ -80,6 +80,13 @@ __device__ __forceinline__ float fmodc(float t) {
 // canonical centered representative of an int in (-2^30, 2^30)
 template <int M>
 __device__ __forceinline__ int canon(int x) {
+    if constexpr (M == 3) {
+        if (x > -8192 && x < 8192) {              // multiply-shift remainder (exact on this range)
+            const int t = x + 3 * 4096;           // in (4096, 20480): t * 0x5556 / 2^16 - t/3 < 1/3
+            const int r = t - 3 * (int)(((unsigned)t * 0x5556u) >> 16);
+            return r - 3 * (r >> 1);              // {0, 1, 2} -> {0, 1, -1}
+        }
+    }
     x %= M;
     if (x > (M - 1) / 2) x -= M;
     if (x < -(M - 1) / 2) x += M;

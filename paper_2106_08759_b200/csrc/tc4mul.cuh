@@ -27,6 +27,26 @@ __device__ __forceinline__ uint32_t e2m1_code(int d) {
     return ((0x65420u >> (4 * a)) & 0xFu) | (d < 0 ? 8u : 0u);
 }
 
+// SWAR e2m1 packing of 8 int8 coefficients in {-s, 0, s}, s in {1, 3} (bytes of w0 = coefficients
+// 0..3, w1 = 4..7) into one word, nibble i = coefficient i.  Nonzero <=> byte bit 0 (1, 3, 0xff,
+// 0xfd all odd); sign = byte bit 7; e2m1 magnitude code 2 (1.0) or 5 (3.0), sign bit 8.
+__device__ __forceinline__ uint32_t e2m1_pack8_int8(uint32_t w0, uint32_t w1, int scale) {
+    auto nib = [scale](uint32_t w) {
+        const uint32_t m = w & 0x01010101u, s = (w >> 7) & 0x01010101u;
+        const uint32_t mag = scale == 1 ? (m << 1) : ((m << 2) | m);
+        uint32_t x = mag | (s << 3);                  // one nibble value per byte
+        x = (x | (x >> 4)) & 0x00FF00FFu;
+        return (x | (x >> 8)) & 0x0000FFFFu;
+    };
+    return nib(w0) | (nib(w1) << 16);
+}
+
+// nibble order reversal of a word (nibble i -> nibble 7 - i)
+__device__ __forceinline__ uint32_t nibble_reverse(uint32_t x) {
+    const uint32_t y = __byte_perm(x, 0, 0x0123);
+    return ((y >> 4) & 0x0F0F0F0Fu) | ((y << 4) & 0xF0F0F0F0u);
+}
+
 template <class PS, int LB, int NPR>
 struct Tc4Geom {
     static constexpr int P = PS::P;
@@ -166,32 +186,40 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
         for (int h = 0; h < CH; h++) {
             const int c = tid + 128 * h;
             if (c < G::NCHK) {
-                int uv8[8];
-                decode_chunk(pu[h], w.du.bytes, w.du.scale, w.unit_u, c, uv8);
                 uint32_t word = 0;
+                if (w.du.bytes == 1 && !w.unit_u) {
+                    word = e2m1_pack8_int8(pu[h].x, pu[h].y, w.du.scale);
+                } else {
+                    int uv8[8];
+                    decode_chunk(pu[h], w.du.bytes, w.du.scale, w.unit_u, c, uv8);
 #pragma unroll
-                for (int i = 0; i < 8; i++) word |= e2m1_code(uv8[i]) << (4 * i);
+                    for (int i = 0; i < 8; i++) word |= e2m1_code(uv8[i]) << (4 * i);
+                }
                 sHA[16 + c] = word;                                  // nibbles 128 + 8c + i
 #pragma unroll
                 for (int pp = 0; pp < NPR; pp++) {
-                    int vv8[8];
-                    decode_chunk(pv[pp][h], w.dv[pp].bytes, w.dv[pp].scale, w.unit_v[pp], c, vv8);
                     uint32_t dw[LB];
+                    if (LB == 1 && w.dv[pp].bytes == 1 && !w.unit_v[pp]) {
+                        // reversed: coefficient 8c + i -> nibble 7 - i of word 16 NL - 1 - c
+                        dw[0] = nibble_reverse(e2m1_pack8_int8(pv[pp][h].x, pv[pp][h].y, w.dv[pp].scale));
+                    } else {
+                        int vv8[8];
+                        decode_chunk(pv[pp][h], w.dv[pp].bytes, w.dv[pp].scale, w.unit_v[pp], c, vv8);
 #pragma unroll
-                    for (int l = 0; l < LB; l++) dw[l] = 0;
+                        for (int l = 0; l < LB; l++) dw[l] = 0;
 #pragma unroll
-                    for (int i = 0; i < 8; i++) {
-                        int v = vv8[i];
+                        for (int i = 0; i < 8; i++) {
+                            int v = vv8[i];
 #pragma unroll
-                        for (int l = 0; l < LB; l++) {
-                            int d = v;
-                            if (LB > 1) {
-                                const int qd = (v + 4 + 9 * 1024) / 9 - 1024;    // floor((v + 4) / 9)
-                                d = v - 9 * qd;
-                                v = qd;
+                            for (int l = 0; l < LB; l++) {
+                                int d = v;
+                                if (LB > 1) {
+                                    const int qd = (v + 4 + 9 * 1024) / 9 - 1024;    // floor((v + 4) / 9)
+                                    d = v - 9 * qd;
+                                    v = qd;
+                                }
+                                dw[l] |= e2m1_code(d) << (4 * (7 - i));
                             }
-                            // reversed: coefficient 8c + i -> nibble 7 - i of word 16 NL - 1 - c
-                            dw[l] |= e2m1_code(d) << (4 * (7 - i));
                         }
                     }
 #pragma unroll
