@@ -304,18 +304,30 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
 #pragma unroll
             for (int t = 0; t < G::NBLK; t++) raw[pp * G::RAW_INTS + 128 * t + tid] = vals[pp][t];
         __syncthreads();
+        // (all shared-memory reads of a product issued before its arithmetic: one latency)
         const int ostride_elems = a.out_bytes == 2 ? PS::P8 : PS::P16;
+        constexpr int FI = (PS::P16 + 127) / 128;
 #pragma unroll
         for (int pp = 0; pp < NPR; pp++) {
             const long long orow = w.orow[pp];
             if (orow < 0) continue;
             const int *rw = raw + pp * G::RAW_INTS;
-            for (int k = tid; k < ostride_elems; k += 128) {
-                int v = 0;
+            int fa[FI], fb[FI], fc[FI];
+#pragma unroll
+            for (int i = 0; i < FI; i++) {
+                const int k = tid + 128 * i;
+                fa[i] = fb[i] = fc[i] = 0;
                 if (k < P) {
-                    v = rw[k] + rw[k + P] + (k >= 1 ? rw[k + P - 1] : 0);
-                    v = canon<M>(v);
+                    fa[i] = rw[k];
+                    fb[i] = rw[k + P];
+                    fc[i] = k >= 1 ? rw[k + P - 1] : 0;
                 }
+            }
+#pragma unroll
+            for (int i = 0; i < FI; i++) {
+                const int k = tid + 128 * i;
+                if (k >= ostride_elems) break;
+                const int v = k < P ? canon<M>(fa[i] + fb[i] + fc[i]) : 0;
                 if (a.out_bytes == 2) ((int16_t *)a.out)[orow * a.out_stride + k] = (int16_t)v;
                 else ((int8_t *)a.out)[orow * a.out_stride + k] = (int8_t)v;
             }
