@@ -279,7 +279,6 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
         __syncthreads();
         tc_fence_after();
         const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
-        int vals[NPR][G::NBLK];
 #pragma unroll
         for (int pp = 0; pp < NPR; pp++) {
             int v[G::PCOL / 16][16];
@@ -294,15 +293,10 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
                     const int col = l * G::NL + t;
                     x = 9 * x + __float2int_rn(__int_as_float(v[col >> 4][col & 15]));
                 }
-                vals[pp][t] = (LB > 1) ? x % M : x;
+                raw[pp * G::RAW_INTS + 128 * t + tid] = (LB > 1) ? x % M : x;
             }
         }
         tc_fence_before();
-        __syncthreads();     // TMEM reads done; A region (raw) free
-#pragma unroll
-        for (int pp = 0; pp < NPR; pp++)
-#pragma unroll
-            for (int t = 0; t < G::NBLK; t++) raw[pp * G::RAW_INTS + 128 * t + tid] = vals[pp][t];
         __syncthreads();
         // (all shared-memory reads of a product issued before its arithmetic: one latency)
         const int ostride_elems = a.out_bytes == 2 ? PS::P8 : PS::P16;

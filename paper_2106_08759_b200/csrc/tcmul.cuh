@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(128) tc_mul_kernel(MulArgs a) {
         tc_fence_after();
         // ---- epilogue: thread tid = TMEM lane = coefficient r of every block, product by product
         const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
-        int vals[NPR][G::NBLK];
+        // (the MMAs have completed, so the A region is free: combined values go straight to raw)
 #pragma unroll
         for (int pp = 0; pp < NPR; pp++) {
             int v[LA][G::PCOL / 16][16];
@@ -415,15 +415,10 @@ __global__ void __launch_bounds__(128) tc_mul_kernel(MulArgs a) {
                 else if (LA == 1) x = (64 * D(0, 0) + D(0, 1)) % M;
                 else if (LB == 1) x = (64 * D(0, 0) + D(1, 0)) % M;
                 else x = (4096 * (D(0, 0) % M) + 64 * (D(0, 1) + D(1, 0)) + D(1, 1)) % M;
-                vals[pp][t] = x;
+                raw[pp * G::RAW_INTS + 128 * t + tid] = x;
             }
         }
-        tc_fence_before();
-        __syncthreads();     // all TMEM reads done (next MMAs may overwrite); A region now free
-#pragma unroll
-        for (int pp = 0; pp < NPR; pp++)
-#pragma unroll
-            for (int t = 0; t < G::NBLK; t++) raw[pp * G::RAW_INTS + 128 * t + tid] = vals[pp][t];
+        tc_fence_before();   // TMEM reads ordered before the next item's MMAs (issued after later barriers)
         __syncthreads();
         // ---- fold with x^p = x + 1, center, store (lane-consecutive coefficients: no bank conflicts)
         // (all shared-memory reads of a product issued before its arithmetic: one latency)
