@@ -72,6 +72,11 @@ int sntrup_batch_keygen(int param_set, uint64_t n_keys, uint64_t seed,
                                          the sampler, so every non-invertible g is caught by the
                                          product-tree root check and repaired */
 #define SNTRUP_OPT_ASYNC          4u  /* do not synchronise before returning (device outputs) */
+#define SNTRUP_OPT_FORCE_SMALL_CHECK 8u /* always run the sampler's small-factor test (by default it
+                                         is skipped where a tree almost never fails without it:
+                                         B * P(small-factor rejection per draw) <= 1e-4,
+                                         e.g. 761/857;
+                                         outputs are identical either way) */
 
 typedef struct {
     uint64_t first_key_index; /* keys first .. first+n-1 (chunked / resumable / multi-GPU runs) */
@@ -153,8 +158,9 @@ int sntrup_set_mul_impl(int impl);
    returns, per kernel class, the summed device milliseconds, the summed work units, the summed
    algorithmic integer ops (ring products: 2 p^2 per limb-pair product on the tensor path, 2 p^2
    per product on the schoolbook path; 0 for other classes) and the launch count (classes:
-   0 sample [keys], 1 R/3 product [products], 2 R/q product [products], 3 R/3 root inversion
-   [inversions], 4 R/q root inversion [inversions], 5 repair [keys], 6 encode [keys], 7 other).
+   0 sample [keys], 1 R/3 product [products], 2 R/q product [products], 3 root inversions
+   [inversions: R/3 roots, and in keygen both rings' roots in one launch], 4 R/q root inversion
+   [inversions, rq_recip_batch], 5 repair [keys], 6 encode [keys], 7 other).
    Any output pointer may be NULL.  Returns the number of classes. */
 void sntrup_profile_enable(int on);
 /* Ring-product launches by arithmetic kind (0 = int8 tensor, 1 = fp4 tensor, 2 = int32

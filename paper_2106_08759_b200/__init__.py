@@ -32,6 +32,7 @@ SNTRUP_E_INTERNAL = -6
 OPT_HOST_OUTPUT = 1
 OPT_NO_SMALL_CHECK = 2
 OPT_ASYNC = 4
+OPT_FORCE_SMALL_CHECK = 8
 
 PARAM_SETS = (653, 761, 857, 953, 1013, 1277)
 
@@ -77,7 +78,7 @@ EXPORTED = ("sntrup_params", "sntrup_strerror", "sntrup_batch_keygen", "sntrup_b
             "sntrup_profile_enable", "sntrup_profile_read_kinds",
             "sntrup_profile_read")
 
-PROFILE_CLASSES = ("sample", "r3_mul", "rq_mul", "r3_inv", "rq_inv", "repair", "encode", "other")
+PROFILE_CLASSES = ("sample", "r3_mul", "rq_mul", "root_inv", "rq_inv", "repair", "encode", "other")
 
 
 class SntrupError(RuntimeError):

@@ -330,13 +330,12 @@ struct RqDivstepCTA {
     }
 };
 
+// One element per CTA of NT threads (all threads of the block call this).
 template <class PS, int M, int NT>
-__global__ void __launch_bounds__(NT) divstep_cta_kernel(InvArgs a) {
+__device__ __forceinline__ void inv_row_cta(const InvArgs &a, long long row, int t,
+                                            typename RqDivstepCTA<PS, M, NT>::Smem &sm) {
     using DS = RqDivstepCTA<PS, M, NT>;
     constexpr int C = DS::C;
-    __shared__ typename DS::Smem sm;
-    const int t = threadIdx.x;
-    const long long row = blockIdx.x;
     float g[C], out[C];
 #pragma unroll
     for (int c = 0; c < C; c++) {
@@ -362,12 +361,15 @@ __global__ void __launch_bounds__(NT) divstep_cta_kernel(InvArgs a) {
     if (t == 0 && a.ok) a.ok[row] = ok ? 1 : 0;
 }
 
+template <class PS, int M, int NT>
+__global__ void __launch_bounds__(NT) divstep_cta_kernel(InvArgs a) {
+    __shared__ typename RqDivstepCTA<PS, M, NT>::Smem sm;
+    inv_row_cta<PS, M, NT>(a, (long long)blockIdx.x, threadIdx.x, sm);
+}
 
+// One element per warp: row `row` of a.in -> a.out, a.ok.
 template <class PS, int M>
-__global__ void __launch_bounds__(128) divstep_kernel(InvArgs a) {
-    const int lane = threadIdx.x & 31;
-    const long long row = (long long)blockIdx.x * 4 + (threadIdx.x >> 5);
-    if (row >= a.n) return;
+__device__ __forceinline__ void inv_row_warp(const InvArgs &a, long long row, int lane) {
     const int ostride = a.out_bytes == 2 ? PS::P8 : PS::P16;
     bool ok;
     if constexpr (M == 3) {
@@ -402,6 +404,36 @@ __global__ void __launch_bounds__(128) divstep_kernel(InvArgs a) {
         else ((int8_t *)a.out)[row * a.out_stride + k] = 0;
     }
     if (lane == 0 && a.ok) a.ok[row] = ok ? 1 : 0;
+}
+
+template <class PS, int M>
+__global__ void __launch_bounds__(128) divstep_kernel(InvArgs a) {
+    const int lane = threadIdx.x & 31;
+    const long long row = (long long)blockIdx.x * 4 + (threadIdx.x >> 5);
+    if (row >= a.n) return;
+    inv_row_warp<PS, M>(a, row, lane);
+}
+
+// Both rings' tree roots in one launch (keygen): blocks [0, nb3) invert R/3 roots, 8 per block
+// (bitsliced, one warp each); the remaining blocks invert the R/q roots, one per CTA when the
+// roots are few (latency bound) or 8 per block with one warp each.  The two latency-bound
+// chains run side by side instead of one after the other.
+template <class PS>
+__global__ void __launch_bounds__(256) joint_roots_kernel(InvArgs r3, InvArgs rq, int nb3, int rq_cta) {
+    __shared__ typename RqDivstepCTA<PS, PS::Q, 256>::Smem sm;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if ((int)blockIdx.x < nb3) {
+        const long long row = (long long)blockIdx.x * 8 + warp;
+        if (row < r3.n) inv_row_warp<PS, 3>(r3, row, lane);
+        return;
+    }
+    const long long b = (long long)blockIdx.x - nb3;
+    if (rq_cta) {
+        inv_row_cta<PS, PS::Q, 256>(rq, b, threadIdx.x, sm);
+    } else {
+        const long long row = b * 8 + warp;
+        if (row < rq.n) inv_row_warp<PS, PS::Q>(rq, row, lane);
+    }
 }
 
 // ---------------------------------------------------------------------------------------------

@@ -11,6 +11,7 @@
 // inverse = parent inverse * sibling: 3(B-1) products per full tree of B leaves, as the
 // paper's chain.
 #include <atomic>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -161,6 +162,7 @@ struct DevTables {
     uint8_t *emit = nullptr;
     uint16_t *off = nullptr;
     EncTables enc{};
+    double p_small_reject = 0;   // 1 - prod (1 - 3^-d) over the small factors' degrees d
 };
 std::map<std::pair<int, int>, DevTables> g_tables;    // (device, param) -> tables
 
@@ -205,6 +207,11 @@ int build_tables(int dev, int ps, int WT, DevTables **out) {
     }
     t.nf = fs->count;
     t.wt = WT;
+    {
+        double keep = 1.0;
+        for (int fi = 0; fi < fs->count; fi++) keep *= 1.0 - std::pow(3.0, -fs->deg[fi]);
+        t.p_small_reject = 1.0 - keep;
+    }
     // -- encode tables (C10): per level, per pair (M_{2i}, bytes, offset)
     std::vector<uint32_t> Mlo;
     std::vector<uint8_t> emit;
@@ -488,63 +495,100 @@ RowDesc rows8(const void *p, long long stride, int scale = 1) { return RowDesc{p
 RowDesc rows16(const void *p, long long stride) { return RowDesc{p, stride, 2, 1}; }
 
 // Batch inversion over one ring by product trees.  X0 = leaves (row descriptor), out0 = leaf
-// inverse rows.  Levels l >= 1 live in lvl[l] / inv[l].  M = ring modulus (3 or q).
+// inverse rows.  Levels l >= 1 live in lvl[l] / inv[l].  M = ring modulus (3 or q).  Split into
+// up-sweep / roots / down-sweep so that keygen can invert both rings' roots in one launch.
 template <class PS, int M>
-int batch_inverse(const TreePlan &tp, RowDesc X0, void *out0, int out_bytes, long long out_stride,
-                  const std::vector<void *> &lvl, const std::vector<void *> &inv, uint8_t *root_ok,
-                  bool leaves_small, cudaStream_t s, uint64_t *nprod) {
-    const int L = tp.L;
-    const long long stride = out_bytes == 2 ? PS::P8 : PS::P16;
-    auto desc = [&](int l) -> RowDesc {
+struct TreeJob {
+    const TreePlan &tp;
+    RowDesc X0;
+    void *out0;
+    int out_bytes;
+    long long out_stride;
+    const std::vector<void *> &lvl, &inv;
+    uint8_t *root_ok;
+    bool leaves_small;
+
+    long long stride() const { return out_bytes == 2 ? PS::P8 : PS::P16; }
+    RowDesc desc(int l) const {
         if (l == 0) return X0;
-        return out_bytes == 2 ? rows16(lvl[l], stride) : rows8(lvl[l], stride);
-    };
-    auto idesc = [&](int l) -> RowDesc {
-        if (l == 0) return out_bytes == 2 ? rows16(out0, out_stride) : rows8(out0, out_stride);
-        return out_bytes == 2 ? rows16(inv[l], stride) : rows8(inv[l], stride);
-    };
-    int rc;
-    for (int l = 1; l <= L; l++) {                   // up-sweep
-        MulArgs a{};
-        a.mode = MUL_PAIRS;
-        a.n_out = tp.cnt[l];
-        a.cnt_in = tp.cnt[l - 1];
-        a.X = desc(l - 1);
-        a.out = lvl[l];
-        a.out_stride = stride;
-        a.out_bytes = out_bytes;
-        a.periodic = (M != 3) && !(l == 1 && leaves_small);
-        const int lx = (M == 3 || (l == 1 && leaves_small)) ? 1 : 2;
-        if ((rc = launch_mul<PS, M>(a, s, lx, lx))) return rc;
-        *nprod += tp.cnt[l - 1] / 2;
+        return out_bytes == 2 ? rows16(lvl[l], stride()) : rows8(lvl[l], stride());
     }
-    {                                                // roots
+    RowDesc idesc(int l) const {
+        if (l == 0) return out_bytes == 2 ? rows16(out0, out_stride) : rows8(out0, out_stride);
+        return out_bytes == 2 ? rows16(inv[l], stride()) : rows8(inv[l], stride());
+    }
+    int up(cudaStream_t s, uint64_t *nprod) const {
+        int rc;
+        for (int l = 1; l <= tp.L; l++) {
+            MulArgs a{};
+            a.mode = MUL_PAIRS;
+            a.n_out = tp.cnt[l];
+            a.cnt_in = tp.cnt[l - 1];
+            a.X = desc(l - 1);
+            a.out = lvl[l];
+            a.out_stride = stride();
+            a.out_bytes = out_bytes;
+            a.periodic = (M != 3) && !(l == 1 && leaves_small);
+            const int lx = (M == 3 || (l == 1 && leaves_small)) ? 1 : 2;
+            if ((rc = launch_mul<PS, M>(a, s, lx, lx))) return rc;
+            *nprod += tp.cnt[l - 1] / 2;
+        }
+        return SNTRUP_OK;
+    }
+    InvArgs roots() const {
+        const int L = tp.L;
         InvArgs ia{};
         ia.n = tp.cnt[L];
         ia.in = desc(L);
         ia.out = L == 0 ? out0 : inv[L];
-        ia.out_stride = L == 0 ? out_stride : stride;
+        ia.out_stride = L == 0 ? out_stride : stride();
         ia.out_bytes = out_bytes;
         ia.ok = root_ok;
-        if ((rc = launch_divstep<PS, M>(ia, s))) return rc;
+        return ia;
     }
-    for (int l = L; l >= 1; l--) {                   // down-sweep
-        MulArgs a{};
-        a.mode = MUL_DOWN;
-        a.n_out = tp.cnt[l - 1];
-        a.cnt_in = tp.cnt[l - 1];
-        a.X = desc(l - 1);
-        a.Y = idesc(l);
-        const RowDesc od = idesc(l - 1);
-        a.out = const_cast<void *>(od.ptr);
-        a.out_stride = od.stride;
-        a.out_bytes = out_bytes;
-        a.periodic = (M != 3) && !(l == 1 && leaves_small);
-        // operands: (inverse of the parent: big) x (sibling: small at level 1 over small leaves)
-        const int lsib = (M == 3 || (l == 1 && leaves_small)) ? 1 : 2;
-        if ((rc = launch_mul<PS, M>(a, s, M == 3 ? 1 : 2, lsib))) return rc;
-        *nprod += (tp.cnt[l - 1] / 2) * 2;
+    int down(cudaStream_t s, uint64_t *nprod) const {
+        int rc;
+        for (int l = tp.L; l >= 1; l--) {
+            MulArgs a{};
+            a.mode = MUL_DOWN;
+            a.n_out = tp.cnt[l - 1];
+            a.cnt_in = tp.cnt[l - 1];
+            a.X = desc(l - 1);
+            a.Y = idesc(l);
+            const RowDesc od = idesc(l - 1);
+            a.out = const_cast<void *>(od.ptr);
+            a.out_stride = od.stride;
+            a.out_bytes = out_bytes;
+            a.periodic = (M != 3) && !(l == 1 && leaves_small);
+            // operands: (inverse of the parent: big) x (sibling: small at level 1 over small leaves)
+            const int lsib = (M == 3 || (l == 1 && leaves_small)) ? 1 : 2;
+            if ((rc = launch_mul<PS, M>(a, s, M == 3 ? 1 : 2, lsib))) return rc;
+            *nprod += (tp.cnt[l - 1] / 2) * 2;
+        }
+        return SNTRUP_OK;
     }
+};
+
+template <class PS, int M>
+int batch_inverse(const TreePlan &tp, RowDesc X0, void *out0, int out_bytes, long long out_stride,
+                  const std::vector<void *> &lvl, const std::vector<void *> &inv, uint8_t *root_ok,
+                  bool leaves_small, cudaStream_t s, uint64_t *nprod) {
+    const TreeJob<PS, M> j{tp, X0, out0, out_bytes, out_stride, lvl, inv, root_ok, leaves_small};
+    int rc;
+    if ((rc = j.up(s, nprod))) return rc;
+    if ((rc = launch_divstep<PS, M>(j.roots(), s))) return rc;
+    return j.down(s, nprod);
+}
+
+// Both rings' roots in one launch (keygen).
+template <class PS>
+int launch_joint_roots(const InvArgs &r3, const InvArgs &rq, cudaStream_t s) {
+    const int nb3 = (int)((r3.n + 7) / 8);
+    const int rq_cta = rq.n < 2LL * dev_info().sms ? 1 : 0;
+    const long long nbq = rq_cta ? rq.n : (rq.n + 7) / 8;
+    ProfScope ps_(PC_INV_R3, (double)(r3.n + rq.n), s);
+    joint_roots_kernel<PS><<<(unsigned)(nb3 + nbq), 256, 0, s>>>(r3, rq, nb3, rq_cta);
+    LAUNCHED();
     return SNTRUP_OK;
 }
 
@@ -628,7 +672,12 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
         sa.seed = seed; sa.first = first; sa.n = m;
         sa.G = Gc; sa.F = Fc; sa.attempts = Ac;
         sa.T = tb->T; sa.masks = tb->masks; sa.nf = tb->nf;
-        sa.small_check = (o.flags & SNTRUP_OPT_NO_SMALL_CHECK) ? 0 : 1;
+        // The sampler's small-factor test only saves re-draws: the tree-root test + repair decide
+        // invertibility exactly anyway.  Where a tree almost never fails
+        // without it (761: 3^-19 per draw, 857: 3^-25), it is skipped.
+        if (o.flags & SNTRUP_OPT_NO_SMALL_CHECK) sa.small_check = 0;
+        else if (o.flags & SNTRUP_OPT_FORCE_SMALL_CHECK) sa.small_check = 1;
+        else sa.small_check = (tb->p_small_reject * B > 1e-4) ? 1 : 0;
         sa.err = err;
         {
             ProfScope ps_(PC_SAMPLE, (double)m, s);
@@ -637,8 +686,13 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
         LAUNCHED();
 
         // R/3: Gbar = batchInv(G)   (Algorithm 1 line 10)
-        if ((rc = batch_inverse<PS, 3>(tp, rows8(Gc, PS::P16), Ic, 1, PS::P16, l3, i3, ok3, true, s, &n_r3)))
-            return rc;
+        // Both trees up, both rings' roots in one launch, then the down-sweeps.
+        const TreeJob<PS, 3> j3{tp, rows8(Gc, PS::P16), Ic, 1, PS::P16, l3, i3, ok3, true};
+        const TreeJob<PS, PS::Q> jq{tp, rows8(Fc, PS::P16, 3), Fbar, 2, PS::P8, lq, iq, okq, true};
+        if ((rc = j3.up(s, &n_r3))) return rc;
+        if ((rc = jq.up(s, &n_rq))) return rc;
+        if ((rc = launch_joint_roots<PS>(j3.roots(), jq.roots(), s))) return rc;
+        if ((rc = j3.down(s, &n_r3))) return rc;
         RepairArgs ra{};
         ra.seed = seed; ra.first = first; ra.n = m; ra.B = B; ra.root_ok = ok3;
         ra.G = Gc; ra.Ginv = Ic; ra.attempts = Ac;
@@ -665,8 +719,7 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
             CK(cudaMemcpyAsync(sk_out + c0 * skb, skc, m * skb, cudaMemcpyDeviceToHost, cs->s));
         }
         // R/q: Fbar = batchInv([3 f])   (Algorithm 1 line 11)
-        if ((rc = batch_inverse<PS, PS::Q>(tp, rows8(Fc, PS::P16, 3), Fbar, 2, PS::P8, lq, iq, okq, true, s, &n_rq)))
-            return rc;
+        if ((rc = jq.down(s, &n_rq))) return rc;
         n_inv += 2 * tp.cnt[tp.L];
         // H = [g * fbar] (Algorithm 1 line 12) and encode (KeyGen step 5).  With host outputs the
         // tail runs in sub-batches, each pk slice copied D2H while the next slice computes.

@@ -101,6 +101,16 @@ def test_repair_path_without_small_check(O, param, seed):
     assert res["stats"]["keys_repaired"] > 0
 
 
+@pytest.mark.parametrize("flags", [0, S.OPT_FORCE_SMALL_CHECK, S.OPT_NO_SMALL_CHECK])
+def test_small_check_policies_761(O, flags):
+    # the sampler's small-factor test is skipped by default for 761 (3^-19 per draw); forcing it
+    # or disabling it must not change a byte
+    n = 300
+    res = S.batch_keygen(761, n, 17, batch_size=64, debug=True, flags=flags)
+    torch.cuda.synchronize()
+    check_keys(O, 761, 17, res, np.arange(n))
+
+
 def test_host_output(O):
     P = S.params(761)
     n = 100
