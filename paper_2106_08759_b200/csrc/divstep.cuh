@@ -454,7 +454,34 @@ struct RepairArgs {
     int small_check;
     unsigned long long *repaired;
     int *err;
+    const int8_t *F;             // rows of P16: f (for u_i = g_i * 3 f_{i^1}); with U
+    int16_t *U;                  // rows of P8 or NULL: recompute u_i for repaired keys
 };
+
+// u = g * 3 f_sib in R/q for one key (one warp; the rare repair path): folded schoolbook,
+// c_k = s_k + s_{k+p} + s_{k+p-1}, s_t = sum_j g_j * 3 f_{t-j}.  f_sib = NULL means 1.
+template <class PS>
+__device__ void warp_u_product(const int8_t *g, const int8_t *fs, int16_t *u, int lane) {
+    constexpr int P = PS::P;
+    auto conv = [&](int t) {                          // s_t for t in [0, 2p-2]
+        int acc = 0;
+        const int j0 = t - (P - 1) > 0 ? t - (P - 1) : 0, j1 = t < P - 1 ? t : P - 1;
+        for (int j = j0; j <= j1; j++) acc += (int)g[j] * (int)fs[t - j];
+        return 3 * acc;
+    };
+    for (int k = lane; k < PS::P8; k += 32) {
+        int v = 0;
+        if (k < P) {
+            if (fs) {
+                v = conv(k) + conv(k + P) + (k >= 1 ? conv(k + P - 1) : 0);
+                v = canon<PS::Q>(v);
+            } else {
+                v = g[k];
+            }
+        }
+        u[k] = (int16_t)v;
+    }
+}
 
 template <class PS>
 __global__ void __launch_bounds__(128) repair_kernel(RepairArgs a) {
@@ -497,6 +524,11 @@ __global__ void __launch_bounds__(128) repair_kernel(RepairArgs a) {
     }
     if (!ok) { if (lane == 0) atomicExch(a.err, 2); return; }
     for (int k = PS::P + lane; k < PS::P16; k += 32) irow[k] = 0;
+    if (a.U) {
+        __syncwarp();
+        const uint64_t sib = key_local ^ 1;
+        warp_u_product<PS>(grow, sib < a.n ? a.F + sib * PS::P16 : nullptr, a.U + key_local * PS::P8, lane);
+    }
     if (lane == 0) {
         if (a.attempts) a.attempts[key_local] = (uint8_t)(attempt + 1);
         atomicAdd(a.repaired, 1ull);

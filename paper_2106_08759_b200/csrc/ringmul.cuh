@@ -12,12 +12,15 @@
 //   PAIRS : out[j] = X[2j] * X[2j+1]          (up-sweep; X[2j] alone if 2j+1 >= cnt_in)
 //   DOWN  : out[i] = Y[i>>1] * X[i^1]         (down-sweep; Y[i>>1] alone if i^1 >= cnt_in)
 //   DOWN2 : DOWN with both children of parent j in one work item (n_out = parents; tensor path)
+//   SIB   : out[i] = X[i] * Y[i^1]            (Y[i^1] = 1 if i^1 >= cnt_in)
+//   DOWNH : out[i] = Y[i>>1] * X[i]           (no sibling swap)
+//   DOWNH2: DOWNH with both children of parent j in one work item (tensor path)
 #pragma once
 #include "common.cuh"
 
 namespace sntrup {
 
-enum MulMode { MUL_ZIP = 0, MUL_PAIRS = 1, MUL_DOWN = 2, MUL_DOWN2 = 3 };
+enum MulMode { MUL_ZIP = 0, MUL_PAIRS = 1, MUL_DOWN = 2, MUL_DOWN2 = 3, MUL_SIB = 4, MUL_DOWNH = 5, MUL_DOWNH2 = 6 };
 
 struct MulArgs {
     int mode;
@@ -110,6 +113,11 @@ __global__ void __launch_bounds__((PS::P8 / 8 + 31) / 32 * 32) ring_mul_kernel(M
         } else if (a.mode == MUL_PAIRS) {
             da = &a.X; ra = 2 * prod; db = &a.X; rb = 2 * prod + 1;
             unit_b = rb >= a.cnt_in;
+        } else if (a.mode == MUL_SIB) {
+            da = &a.X; ra = prod; db = &a.Y; rb = prod ^ 1;
+            unit_b = rb >= a.cnt_in;
+        } else if (a.mode == MUL_DOWNH) {
+            da = &a.Y; ra = prod >> 1; db = &a.X; rb = prod;
         } else {
             da = &a.Y; ra = prod >> 1; db = &a.X; rb = prod ^ 1;
             unit_b = rb >= a.cnt_in;

@@ -12,6 +12,7 @@
 // paper's chain.
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -289,6 +290,24 @@ int copy_stream(CopyStream **out) {
     return SNTRUP_OK;
 }
 
+// ------------------------------------------------------------------------------ aux stream
+// Keygen's u_i = g_i * 3 f_{i^1} products depend only on the sample: they run on an aux stream
+// concurrently with the (latency-bound) joint root inversion.  One per device.
+struct AuxStream { cudaStream_t s = nullptr; cudaEvent_t go = nullptr, done = nullptr; };
+int aux_stream(AuxStream **out) {
+    static std::map<int, AuxStream> m;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    AuxStream &x = m[dev];
+    if (!x.s) {
+        CK(cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&x.go, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&x.done, cudaEventDisableTiming));
+    }
+    *out = &x;
+    return SNTRUP_OK;
+}
+
 // ------------------------------------------------------------------------------ workspace
 struct Workspace {
     char *base = nullptr;
@@ -443,9 +462,12 @@ int launch_mul(MulArgs a, cudaStream_t s, int la = 2, int lb = 2) {
     }
     // down-sweep with both operands of one kind: the two children of a parent share the parent's
     // inverse as the A operand (one work item per parent)
-    const bool down2 = a.mode == MUL_DOWN && (M == 3 || la == lb) && g_mul_impl != 2;
+    // (R/3 and small x small only: for int8 big x big the stacked-N variant needs 2 CTAs/SM of
+    // smem and measured no faster than one product per item)
+    const bool down2 = (a.mode == MUL_DOWN || a.mode == MUL_DOWNH) && (M == 3 || (la == 1 && lb == 1)) &&
+                       g_mul_impl != 2;
     if (down2) {
-        a.mode = MUL_DOWN2;
+        a.mode = a.mode == MUL_DOWN ? MUL_DOWN2 : MUL_DOWNH2;
         a.n_out = (a.cnt_in + 1) / 2;
     }
     const bool fp4 = g_mul_impl == 0 || g_mul_impl == 4;
@@ -469,7 +491,7 @@ int launch_mul(MulArgs a, cudaStream_t s, int la = 2, int lb = 2) {
             return launch_tc<PS, M, 1, 2>(a, s);
         }
         a.swap = 0;
-        return down2 ? launch_tc<PS, M, 2, 2, 2>(a, s) : launch_tc<PS, M, 2, 2>(a, s);
+        return launch_tc<PS, M, 2, 2>(a, s);
     }
 }
 
@@ -546,9 +568,9 @@ struct TreeJob {
         ia.ok = root_ok;
         return ia;
     }
-    int down(cudaStream_t s, uint64_t *nprod) const {
+    int down(cudaStream_t s, uint64_t *nprod, int stop = 1) const {
         int rc;
-        for (int l = tp.L; l >= 1; l--) {
+        for (int l = tp.L; l >= stop; l--) {
             MulArgs a{};
             a.mode = MUL_DOWN;
             a.n_out = tp.cnt[l - 1];
@@ -618,7 +640,7 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
     need += align256(chunk);                                 // attempts
     need += 2 * align256(inner * PS::P16 + 256 * (tpmax.L + 1));   // R/3 levels + inverses
     need += 2 * align256(inner * PS::P8 * 2 + 256 * (tpmax.L + 1)); // R/q levels + inverses
-    need += 2 * align256(chunk * PS::P8 * 2);                // Fbar, H
+    need += 3 * align256(chunk * PS::P8 * 2);                // Fbar, H, U
     need += 2 * align256(tpmax.cnt[tpmax.L]);                // root ok flags
     if (host_out) need += 2 * (align256(chunk * pkb) + align256(chunk * skb));
     need += 4096;
@@ -637,6 +659,7 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
     }
     int16_t *Fbar = ws_take<int16_t>(chunk * PS::P8);
     int16_t *H = ws_take<int16_t>(chunk * PS::P8);
+    int16_t *U = ws_take<int16_t>(chunk * PS::P8);
     uint8_t *ok3 = ws_take<uint8_t>(tpmax.cnt[tpmax.L]);
     uint8_t *okq = ws_take<uint8_t>(tpmax.cnt[tpmax.L]);
     uint8_t *pk_stage[2] = {nullptr, nullptr}, *sk_stage[2] = {nullptr, nullptr};
@@ -685,19 +708,47 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
         }
         LAUNCHED();
 
-        // R/3: Gbar = batchInv(G)   (Algorithm 1 line 10)
+        // R/3: Gbar = batchInv(G) (Algorithm 1 line 10); R/q: Fbar = batchInv([3 f]) (line 11).
         // Both trees up, both rings' roots in one launch, then the down-sweeps.
+        //
+        // h = g * fbar (line 12) is computed without fbar: at the bottom of the R/q tree
+        // fbar_i = 1/(3 f_i) = P_j * 3 f_{i^1} with P_j the inverse of the leaves' parent, so
+        // h_i = P_j * u_i with u_i = g_i * 3 f_{i^1}.  The u products (small x small, fp4) need only
+        // the sample and run on an aux stream beside the root inversion; the bottom R/q down-sweep
+        // level (1 x 2 limbs per product) disappears, h becomes a 2 x 2-limb product.
+        // (B = 1 has no parents: plain fbar, then h = g * fbar.)
         const TreeJob<PS, 3> j3{tp, rows8(Gc, PS::P16), Ic, 1, PS::P16, l3, i3, ok3, true};
         const TreeJob<PS, PS::Q> jq{tp, rows8(Fc, PS::P16, 3), Fbar, 2, PS::P8, lq, iq, okq, true};
+        const bool utrick = tp.L >= 1;
+        AuxStream *ax = nullptr;
+        if ((rc = aux_stream(&ax))) return rc;
         if ((rc = j3.up(s, &n_r3))) return rc;
         if ((rc = jq.up(s, &n_rq))) return rc;
+        if (utrick) {
+            CK(cudaEventRecord(ax->go, s));
+            CK(cudaStreamWaitEvent(ax->s, ax->go, 0));
+            MulArgs a{};
+            a.mode = MUL_SIB;
+            a.n_out = (long long)m;
+            a.cnt_in = (long long)m;
+            a.X = rows8(Gc, PS::P16);
+            a.Y = rows8(Fc, PS::P16, 3);
+            a.out = U;
+            a.out_stride = PS::P8;
+            a.out_bytes = 2;
+            a.periodic = 0;
+            if ((rc = launch_mul<PS, PS::Q>(a, ax->s, 1, 1))) return rc;
+            CK(cudaEventRecord(ax->done, ax->s));
+        }
         if ((rc = launch_joint_roots<PS>(j3.roots(), jq.roots(), s))) return rc;
         if ((rc = j3.down(s, &n_r3))) return rc;
+        if (utrick) CK(cudaStreamWaitEvent(s, ax->done, 0));    // repair may rewrite u rows
         RepairArgs ra{};
         ra.seed = seed; ra.first = first; ra.n = m; ra.B = B; ra.root_ok = ok3;
         ra.G = Gc; ra.Ginv = Ic; ra.attempts = Ac;
         ra.T = tb->T; ra.masks = tb->masks; ra.nf = tb->nf; ra.small_check = sa.small_check;
         ra.repaired = repaired; ra.err = err;
+        ra.F = Fc; ra.U = utrick ? U : nullptr;
         {
             ProfScope ps_(PC_REPAIR, (double)m, s);
             repair_kernel<PS><<<(unsigned)((m + 3) / 4), 128, 0, s>>>(ra);
@@ -718,26 +769,44 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
             CK(cudaStreamWaitEvent(cs->s, cs->comp[buf], 0));
             CK(cudaMemcpyAsync(sk_out + c0 * skb, skc, m * skb, cudaMemcpyDeviceToHost, cs->s));
         }
-        // R/q: Fbar = batchInv([3 f])   (Algorithm 1 line 11)
-        if ((rc = jq.down(s, &n_rq))) return rc;
+        if ((rc = jq.down(s, &n_rq, utrick ? 2 : 1))) return rc;
+        if (utrick) n_rq += m;                                     // the u products replace level 1
         n_inv += 2 * tp.cnt[tp.L];
-        // H = [g * fbar] (Algorithm 1 line 12) and encode (KeyGen step 5).  With host outputs the
-        // tail runs in sub-batches, each pk slice copied D2H while the next slice computes.
+        // H and encode (KeyGen step 5).  With host outputs the tail runs in sub-batches (an even
+        // number of rows each, so parents are not split), each pk slice copied D2H while the next
+        // slice computes.
         const int nsub = host_out ? 4 : 1;
         for (int j = 0; j < nsub; j++) {
-            const uint64_t r0 = m * (uint64_t)j / nsub, r1 = m * (uint64_t)(j + 1) / nsub, rows = r1 - r0;
+            const uint64_t r0 = (m * (uint64_t)j / nsub) & ~1ull;
+            const uint64_t r1 = (j + 1 == nsub) ? m : ((m * (uint64_t)(j + 1) / nsub) & ~1ull);
+            const uint64_t rows = r1 - r0;
             if (!rows) continue;
             {
                 MulArgs a{};
-                a.mode = MUL_ZIP;
-                a.n_out = (long long)rows;
-                a.X = rows8(Gc + r0 * PS::P16, PS::P16);
-                a.Y = rows16(Fbar + r0 * PS::P8, PS::P8);
-                a.out = Hc + r0 * PS::P8;
-                a.out_stride = PS::P8;
-                a.out_bytes = 2;
-                a.periodic = 0;
-                if ((rc = launch_mul<PS, PS::Q>(a, s, 1, 2))) return rc;   // g small, fbar big
+                if (utrick) {
+                    // h_i = P_{i/2} * u_i
+                    const RowDesc P1 = jq.idesc(1);
+                    a.mode = MUL_DOWNH;
+                    a.n_out = (long long)rows;
+                    a.cnt_in = (long long)rows;
+                    a.X = rows16(U + r0 * PS::P8, PS::P8);
+                    a.Y = rows16((const int16_t *)P1.ptr + (r0 / 2) * P1.stride, P1.stride);
+                    a.periodic = 1;
+                    a.out = Hc + r0 * PS::P8;
+                    a.out_stride = PS::P8;
+                    a.out_bytes = 2;
+                    if ((rc = launch_mul<PS, PS::Q>(a, s, 2, 2))) return rc;
+                } else {
+                    a.mode = MUL_ZIP;
+                    a.n_out = (long long)rows;
+                    a.X = rows8(Gc + r0 * PS::P16, PS::P16);
+                    a.Y = rows16(Fbar + r0 * PS::P8, PS::P8);
+                    a.periodic = 0;
+                    a.out = Hc + r0 * PS::P8;
+                    a.out_stride = PS::P8;
+                    a.out_bytes = 2;
+                    if ((rc = launch_mul<PS, PS::Q>(a, s, 1, 2))) return rc;   // g small, fbar big
+                }
             }
             {
                 EncArgs ea{};

@@ -204,9 +204,12 @@ __device__ __forceinline__ void tc_work(const MulArgs &a, long long it, TcWork<N
     for (int pp = 0; pp < NPR; pp++) { w.unit_v[pp] = false; w.orow[pp] = -1; w.dv[pp] = a.X; w.rv[pp] = 0; }
     if constexpr (NPR == 2) {
         // MUL_DOWN2: parent it; out[2it] = Y[it] * X[2it+1] (unit if absent), out[2it+1] = Y[it] * X[2it]
+        // MUL_DOWNH2: parent it; out[2it] = Y[it] * X[2it], out[2it+1] = Y[it] * X[2it+1] (if present)
+        const bool noswap = a.mode == MUL_DOWNH2;
         w.du = a.Y; w.ru = it;
-        w.dv[0] = a.X; w.rv[0] = 2 * it + 1; w.unit_v[0] = 2 * it + 1 >= a.cnt_in; w.orow[0] = 2 * it;
-        w.dv[1] = a.X; w.rv[1] = 2 * it;
+        w.dv[0] = a.X; w.rv[0] = noswap ? 2 * it : 2 * it + 1;
+        w.unit_v[0] = !noswap && 2 * it + 1 >= a.cnt_in; w.orow[0] = 2 * it;
+        w.dv[1] = a.X; w.rv[1] = noswap ? 2 * it + 1 : 2 * it;
         w.orow[1] = (2 * it + 1 < a.cnt_in) ? 2 * it + 1 : -1;
     } else {
         RowDesc du, dv; long long ru, rv; bool uv = false, uu = false;
@@ -215,6 +218,11 @@ __device__ __forceinline__ void tc_work(const MulArgs &a, long long it, TcWork<N
         } else if (a.mode == MUL_PAIRS) {
             du = a.X; ru = 2 * it; dv = a.X; rv = 2 * it + 1;
             uv = rv >= a.cnt_in;
+        } else if (a.mode == MUL_SIB) {
+            du = a.X; ru = it; dv = a.Y; rv = it ^ 1;
+            uv = rv >= a.cnt_in;
+        } else if (a.mode == MUL_DOWNH) {
+            du = a.Y; ru = it >> 1; dv = a.X; rv = it;
         } else {
             du = a.Y; ru = it >> 1; dv = a.X; rv = it ^ 1;
             uv = rv >= a.cnt_in;
