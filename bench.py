@@ -357,7 +357,8 @@ def main():
         result["batch_size_sweep_keys_per_s"] = sweep
         # A/B: the same step without the shared-A down-sweep, and on the int32 schoolbook
         ab = {}
-        for name, impl in (("tc_fp4_all_small", S.MUL_TENSOR_CORE_FP4_ALL),
+        for name, impl in (("tc_int8_m64", S.MUL_TENSOR_CORE_M64),
+                           ("tc_fp4_all_small", S.MUL_TENSOR_CORE_FP4_ALL),
                            ("tc_int8_shared_a", S.MUL_TENSOR_CORE_INT8),
                            ("tc_int8_no_shared_a", S.MUL_TENSOR_CORE_NO_SHARED_A),
                            ("int32_schoolbook", S.MUL_SCHOOLBOOK)):

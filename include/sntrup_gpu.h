@@ -150,7 +150,8 @@ uint64_t sntrup_kernel_launch_count(void);
    1 = int32 schoolbook on the integer pipes (v1);
    2 = int8 tensor cores only, one product per work item (v2);
    3 = int8 tensor cores only, with the shared-A R/3 down-sweep;
-   4 = as 0, plus big x small products on fp4 with balanced base-9 digits (A/B only).
+   4 = as 0, plus big x small products on fp4 with balanced base-9 digits (A/B only);
+   5 = as 0, with the int8 products at MMA M = 64 instead of 128 (A/B only).
    All are exact.  Returns SNTRUP_OK or SNTRUP_E_ARG. */
 int sntrup_set_mul_impl(int impl);
 

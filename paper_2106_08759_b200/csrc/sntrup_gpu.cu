@@ -371,7 +371,8 @@ TreePlan make_plan(long long m, int B) {
 // ring-product implementation (sntrup_set_mul_impl): 0 = tensor cores, fp4 (tc4mul.cuh) where an
 // operand is small + int8 (tcmul.cuh) otherwise, shared-A down-sweep; 1 = int32 schoolbook;
 // 2 = int8 tensor cores only, one product per work item; 3 = int8 tensor cores with shared A;
-// 4 = as 0 but big x small products also on fp4 (base-9 digits; slower, kept for A/B)
+// 4 = as 0 but big x small products also on fp4 (base-9 digits; slower, kept for A/B);
+// 5 = as 0 but int8 products with MMA M = 64 (A/B for the M = 128 choice)
 int g_mul_impl = 0;
 
 struct DevInfo { int sms = 0; };
@@ -384,10 +385,10 @@ DevInfo &dev_info() {
     return d;
 }
 
-template <class PS, int M, int LA, int LB, int NPR = 1>
+template <class PS, int M, int LA, int LB, int NPR = 1, int MM = 128>
 int launch_tc(const MulArgs &a, cudaStream_t s) {
-    using G = TcGeom<PS, LA, LB, NPR>;
-    auto kern = tc_mul_kernel<PS, M, LA, LB, NPR>;
+    using G = TcGeom<PS, LA, LB, NPR, MM>;
+    auto kern = tc_mul_kernel<PS, M, LA, LB, NPR, MM>;
     static std::map<int, int> per_sm;                 // device -> resident CTAs per SM
     int dev = 0;
     CK(cudaGetDevice(&dev));
@@ -447,7 +448,7 @@ int launch_mul(MulArgs a, cudaStream_t s, int la = 2, int lb = 2) {
     // (fp4 path: digit pairs = LB base-9 digits of the big operand x 1)
     const bool small_op = (M == 3) || la == 1 || lb == 1;
     int limb_pairs = (g_mul_impl == 1 || M == 3) ? 1 : la * lb;
-    if (g_mul_impl == 0 && small_op && M != 3) limb_pairs = (la == 1 && lb == 1) ? 1 : 2;
+    if ((g_mul_impl == 0 || g_mul_impl == 5) && small_op && M != 3) limb_pairs = (la == 1 && lb == 1) ? 1 : 2;
     if (g_mul_impl == 4 && small_op && M != 3) limb_pairs = (la == 1 && lb == 1) ? 1 : digits9(M);
     ProfScope ps_(M == 3 ? PC_MUL_R3 : PC_MUL_RQ, (double)a.n_out, s,
                   2.0 * PS::P * PS::P * limb_pairs * (double)a.n_out);
@@ -470,7 +471,7 @@ int launch_mul(MulArgs a, cudaStream_t s, int la = 2, int lb = 2) {
         a.mode = a.mode == MUL_DOWN ? MUL_DOWN2 : MUL_DOWNH2;
         a.n_out = (a.cnt_in + 1) / 2;
     }
-    const bool fp4 = g_mul_impl == 0 || g_mul_impl == 4;
+    const bool fp4 = g_mul_impl == 0 || g_mul_impl == 4 || g_mul_impl == 5;
     if constexpr (M == 3) {
         a.swap = 0;
         if (fp4) return down2 ? launch_tc4<PS, M, 1, 2>(a, s) : launch_tc4<PS, M, 1, 1>(a, s);
@@ -482,16 +483,19 @@ int launch_mul(MulArgs a, cudaStream_t s, int la = 2, int lb = 2) {
             if (fp4) return down2 ? launch_tc4<PS, M, 1, 2>(a, s) : launch_tc4<PS, M, 1, 1>(a, s);
             return down2 ? launch_tc<PS, M, 1, 1, 2>(a, s) : launch_tc<PS, M, 1, 1>(a, s);
         }
+        // int8 products at MMA M = 128; M = 64 (half the A bytes per MMA, twice the N) is kept
+        // as an A/B mode (impl 5): measured slower
+        const bool m128 = g_mul_impl != 5;
         if (la == 1 || lb == 1) {
             // the small operand takes the A (Hankel) role.  int8 with two limbs for the big one:
             // measured faster than fp4 with D9 base-9 digits (larger N, digit staging), see
             // DESIGN.md section 6; the fp4 variant stays selectable for A/B (impl 4)
             a.swap = la == 1 ? 0 : 1;
             if (g_mul_impl == 4) return launch_tc4<PS, M, D9, 1>(a, s);
-            return launch_tc<PS, M, 1, 2>(a, s);
+            return m128 ? launch_tc<PS, M, 1, 2>(a, s) : launch_tc<PS, M, 1, 2, 1, 64>(a, s);
         }
         a.swap = 0;
-        return launch_tc<PS, M, 2, 2>(a, s);
+        return m128 ? launch_tc<PS, M, 2, 2>(a, s) : launch_tc<PS, M, 2, 2, 1, 64>(a, s);
     }
 }
 
@@ -1165,7 +1169,7 @@ int sntrup_profile_read_kinds(int reset, double *ms, double *ops, uint64_t *laun
 }
 
 int sntrup_set_mul_impl(int impl) {
-    if (impl < 0 || impl > 4) return SNTRUP_E_ARG;
+    if (impl < 0 || impl > 5) return SNTRUP_E_ARG;
     std::lock_guard<std::mutex> lk(g_mu);
     g_mul_impl = impl;
     return SNTRUP_OK;

@@ -48,12 +48,12 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
 }
 
 // Instruction descriptor: kind::i8, D = s32, A = B = signed int8, both K-major, M = 128, N.
-__host__ __device__ constexpr uint32_t umma_idesc_i8(int N) {
+__host__ __device__ constexpr uint32_t umma_idesc_i8(int N, int M = 128) {
     return (2u << 4)                        // c_format S32
          | (1u << 7)                        // a_format signed int8
          | (1u << 10)                       // b_format signed int8
          | ((uint32_t)(N >> 3) << 17)       // n_dim
-         | ((uint32_t)(128 >> 4) << 24);    // m_dim
+         | ((uint32_t)(M >> 4) << 24);      // m_dim
 }
 
 __device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
@@ -113,22 +113,23 @@ __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.
 // NPR products share one A operand per iteration (the down-sweep's two children share the
 // parent's inverse): their B rows are stacked along N, so the A tile read by every MMA -- the
 // dominant shared-memory traffic of a small-N GEMM -- is amortised over both products.
-template <class PS, int LA, int LB, int NPR>
+template <class PS, int LA, int LB, int NPR, int MM = 128>
 struct TcGeom {
+    static_assert(MM == 64 || MM == 128, "M is 64 or 128");
     static constexpr int P = PS::P;
-    static constexpr int NKS = (P + 127 + 31) / 32;          // K steps of 32
+    static constexpr int NKS = (P + MM - 1 + 31) / 32;       // K steps of 32
     static constexpr int K = 32 * NKS;
-    static constexpr int NBLK = (2 * P - 1 + 127) / 128;     // output blocks of 128 coefficients
+    static constexpr int NBLK = (2 * P - 1 + MM - 1) / MM;   // output blocks of MM coefficients
     static constexpr int NL = (NBLK + 7) / 8 * 8;            // B rows per limb
     static constexpr int PCOL = (LB * NL + 15) / 16 * 16;    // B rows (= D columns) per product
     static constexpr int NB = NPR * PCOL;                    // N of the MMA
-    static constexpr int AROWS = 32 * NKS + 113;             // window rows 0..AROWS-1 (row 0 unused)
+    static constexpr int AROWS = 32 * NKS + MM - 15;         // window rows 0..AROWS-1 (row 0 unused)
     static constexpr int A_BYTES = (AROWS + 7) / 8 * 128;    // 16 B per row, 128-aligned
     static constexpr int AROWS4 = (AROWS + 3) / 4;            // window rows are built 4 at a time
-    static constexpr int HA_LEN = (4 * AROWS4 + 20 + 127) / 128 * 128;   // hA[128 + j] = limb(a_j)
-    static constexpr int ZR_LEN = (128 * NL + K + 127) / 128 * 128; // zr[128 NL - 1 - j] = limb(b_j)
+    static constexpr int HA_LEN = (4 * AROWS4 + 20 + 127) / 128 * 128;   // hA[MM + j] = limb(a_j)
+    static constexpr int ZR_LEN = (MM * NL + K + 127) / 128 * 128;  // zr[MM NL - 1 - j] = limb(b_j)
     static constexpr int B_BYTES = 2 * NKS * NB * 16;
-    static constexpr int RAW_INTS = 128 * NBLK;               // per product
+    static constexpr int RAW_INTS = MM * NBLK;                // per product
     static constexpr int TCOLS_USED = LA * NB;
     static constexpr int TCOLS = TCOLS_USED <= 32 ? 32 : TCOLS_USED <= 64 ? 64 : TCOLS_USED <= 128 ? 128 : 256;
     static constexpr int NCHK = PS::P8 / 8;                   // 8-coefficient input chunks
@@ -142,7 +143,7 @@ struct TcGeom {
     static constexpr int SMEM = OFF_BAR + 128;
     static_assert(NPR * RAW_INTS * 4 <= LA * A_BYTES, "raw buffers must fit in the A region");
     static_assert(NB <= 256, "N too large");
-    static_assert(128 + PS::P8 <= HA_LEN, "hA too short");
+    static_assert(MM + PS::P8 <= HA_LEN, "hA too short");
     static_assert(4 * AROWS4 * 16 <= A_BYTES, "A region too short");
     // B build: (row, residue mod 8) work items; row = pp*PCOL + l*NL + t, K-chunks c = residue + 8i
     static constexpr int BROWS = NPR * LB * NL;
@@ -237,10 +238,12 @@ __device__ __forceinline__ void tc_work(const MulArgs &a, long long it, TcWork<N
     }
 }
 
-// M = modulus (3 or q); LA / LB = limbs of the A-role / B-role operand; NPR products per A.
-template <class PS, int M, int LA, int LB, int NPR>
+// M = modulus (3 or q); LA / LB = limbs of the A-role / B-role operand; NPR products per A;
+// MM = MMA M (output coefficients per block).  With MM = 64 each MMA reads half the A bytes and
+// the accumulator row r lives in TMEM lane 32(r/16) + r%16 (probed: scripts/probe/tmem_m64_probe.cu).
+template <class PS, int M, int LA, int LB, int NPR, int MM = 128>
 __global__ void __launch_bounds__(128) tc_mul_kernel(MulArgs a) {
-    using G = TcGeom<PS, LA, LB, NPR>;
+    using G = TcGeom<PS, LA, LB, NPR, MM>;
     constexpr int P = PS::P;
     constexpr int CH = G::CH;
     extern __shared__ __align__(1024) uint8_t sm[];
@@ -271,7 +274,7 @@ __global__ void __launch_bounds__(128) tc_mul_kernel(MulArgs a) {
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    constexpr uint32_t IDESC = umma_idesc_i8(G::NB);
+    constexpr uint32_t IDESC = umma_idesc_i8(G::NB, MM);
     uint32_t phase = 0;
     // fixed per-thread B-build items (product independent): 16-byte-unit offsets
     int bsrc[G::BPER], bdst[G::BPER], bres[G::BPER];
@@ -283,7 +286,7 @@ __global__ void __launch_bounds__(128) tc_mul_kernel(MulArgs a) {
             const int pl = row / G::NL, t = row - pl * G::NL;       // pl = pp * LB + l
             const int pp = pl / LB, l = pl - pp * LB;
             bres[h] = (grp + row) & 7;
-            bsrc[h] = pl * (G::ZR_LEN / 16) + 8 * (G::NL - 1 - t);
+            bsrc[h] = pl * (G::ZR_LEN / 16) + (MM / 16) * (G::NL - 1 - t);
             bdst[h] = pp * G::PCOL + l * G::NL + t;
         } else {
             bsrc[h] = -1; bdst[h] = 0; bres[h] = 0;
@@ -326,7 +329,7 @@ __global__ void __launch_bounds__(128) tc_mul_kernel(MulArgs a) {
                     int x[8];
 #pragma unroll
                     for (int i = 0; i < 8; i++) x[i] = limb_of<LA>(uv8[i], l);
-                    *reinterpret_cast<uint2 *>(sHA + l * G::HA_LEN + 128 + 8 * c) =
+                    *reinterpret_cast<uint2 *>(sHA + l * G::HA_LEN + MM + 8 * c) =
                         make_uint2(pack4(x[0], x[1], x[2], x[3]), pack4(x[4], x[5], x[6], x[7]));
                 }
 #pragma unroll
@@ -338,7 +341,7 @@ __global__ void __launch_bounds__(128) tc_mul_kernel(MulArgs a) {
                         int x[8];
 #pragma unroll
                         for (int i = 0; i < 8; i++) x[i] = limb_of<LB>(vv8[i], l);
-                        *reinterpret_cast<uint2 *>(sZR + (pp * LB + l) * G::ZR_LEN + 128 * G::NL - 8 - 8 * c) =
+                        *reinterpret_cast<uint2 *>(sZR + (pp * LB + l) * G::ZR_LEN + MM * G::NL - 8 - 8 * c) =
                             make_uint2(pack4(x[7], x[6], x[5], x[4]), pack4(x[3], x[2], x[1], x[0]));
                     }
                 }
@@ -404,6 +407,10 @@ __global__ void __launch_bounds__(128) tc_mul_kernel(MulArgs a) {
         tc_fence_after();
         // ---- epilogue: thread tid = TMEM lane = coefficient r of every block, product by product
         const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
+        // accumulator row of this thread (MM = 64: lanes 16..31 of each warp hold nothing)
+        const int lane = tid & 31;
+        const int rrow = MM == 128 ? tid : 16 * warp + lane;
+        const bool rowok = MM == 128 || lane < 16;
         // (the MMAs have completed, so the A region is free: combined values go straight to raw)
 #pragma unroll
         for (int pp = 0; pp < NPR; pp++) {
@@ -414,16 +421,18 @@ __global__ void __launch_bounds__(128) tc_mul_kernel(MulArgs a) {
                 for (int c16 = 0; c16 < G::PCOL / 16; c16++)
                     tmem_ld16(lane_addr + l * G::NB + pp * G::PCOL + 16 * c16, v[l][c16]);
             tmem_ld_wait();
+            if (rowok) {
 #pragma unroll
-            for (int t = 0; t < G::NBLK; t++) {
-                // D[l][lb*NL + t]
-                auto D = [&](int l, int lb) { const int col = lb * G::NL + t; return v[l][col >> 4][col & 15]; };
-                int x;
-                if (LA == 1 && LB == 1) x = D(0, 0);
-                else if (LA == 1) x = (64 * D(0, 0) + D(0, 1)) % M;
-                else if (LB == 1) x = (64 * D(0, 0) + D(1, 0)) % M;
-                else x = (4096 * (D(0, 0) % M) + 64 * (D(0, 1) + D(1, 0)) + D(1, 1)) % M;
-                raw[pp * G::RAW_INTS + 128 * t + tid] = x;
+                for (int t = 0; t < G::NBLK; t++) {
+                    // D[l][lb*NL + t]
+                    auto D = [&](int l, int lb) { const int col = lb * G::NL + t; return v[l][col >> 4][col & 15]; };
+                    int x;
+                    if (LA == 1 && LB == 1) x = D(0, 0);
+                    else if (LA == 1) x = (64 * D(0, 0) + D(0, 1)) % M;
+                    else if (LB == 1) x = (64 * D(0, 0) + D(1, 0)) % M;
+                    else x = (4096 * (D(0, 0) % M) + 64 * (D(0, 1) + D(1, 0)) + D(1, 1)) % M;
+                    raw[pp * G::RAW_INTS + MM * t + rrow] = x;
+                }
             }
         }
         tc_fence_before();   // TMEM reads ordered before the next item's MMAs (issued after later barriers)

@@ -1,8 +1,9 @@
 #!/usr/bin/env python3
 """From an ncu launch list with gpu__time_duration.sum, dram__bytes_read.sum and
-dram__bytes_write.sum, write profiles/roofline_traffic.json: per kernel class (R/q or R/3 ring
-product, ...) the average DRAM bytes and device time per launch, and each class's share of the
-step.  bench.py reads per_launch_bytes for its roofline "traffic" field.
+dram__bytes_write.sum, write profiles/roofline_traffic.json: per kernel kind (int8 / fp4 tensor
+ring products, sampler, divsteps, encoder, ...) the average DRAM bytes and device time per launch,
+and each kind's share of the device time.  bench.py reads per_launch_bytes for its roofline
+"traffic" field.
 
   ncu_traffic.py <launches.csv> <out.json> [--skip-launches N]
 """
@@ -40,10 +41,15 @@ def main():
         d[r[mi]] = v
     agg = collections.defaultdict(lambda: {"launches": 0, "bytes": 0.0, "s": 0.0})
     for d in per.values():
-        if "tc_mul_kernel" in d["name"] or "ring_mul_kernel" in d["name"]:
-            c = "r3_mul" if "Params<761, 4591, 286, 3>, 3" in d["name"] or ">, 3, " in d["name"] else "rq_mul"
+        name = d["name"]
+        if "tc4_mul_kernel" in name:
+            c = "tc_fp4"
+        elif "tc_mul_kernel" in name:
+            c = "tc_int8"
+        elif "ring_mul_kernel" in name:
+            c = "int32"
         else:
-            c = klass(d["name"])
+            c = klass(name)
         a = agg[c]
         a["launches"] += 1
         a["bytes"] += d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0)
