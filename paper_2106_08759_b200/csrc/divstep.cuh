@@ -414,24 +414,25 @@ __global__ void __launch_bounds__(128) divstep_kernel(InvArgs a) {
     inv_row_warp<PS, M>(a, row, lane);
 }
 
-// Both rings' tree roots in one launch (keygen): blocks [0, nb3) invert R/3 roots, 8 per block
-// (bitsliced, one warp each); the remaining blocks invert the R/q roots, one per CTA when the
-// roots are few (latency bound) or 8 per block with one warp each.  The two latency-bound
+// Both rings' tree roots in one launch (keygen): blocks [0, nb3) invert R/3 roots, NT/32 per
+// block (bitsliced, one warp each); the remaining blocks invert the R/q roots, one per CTA when
+// the roots are few (latency bound) or NT/32 per block with one warp each.  The two latency-bound
 // chains run side by side instead of one after the other.
-template <class PS>
-__global__ void __launch_bounds__(256) joint_roots_kernel(InvArgs r3, InvArgs rq, int nb3, int rq_cta) {
-    __shared__ typename RqDivstepCTA<PS, PS::Q, 256>::Smem sm;
+template <class PS, int NT>
+__global__ void __launch_bounds__(NT) joint_roots_kernel(InvArgs r3, InvArgs rq, int nb3, int rq_cta) {
+    __shared__ typename RqDivstepCTA<PS, PS::Q, NT>::Smem sm;
+    constexpr int WPB = NT / 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if ((int)blockIdx.x < nb3) {
-        const long long row = (long long)blockIdx.x * 8 + warp;
+        const long long row = (long long)blockIdx.x * WPB + warp;
         if (row < r3.n) inv_row_warp<PS, 3>(r3, row, lane);
         return;
     }
     const long long b = (long long)blockIdx.x - nb3;
     if (rq_cta) {
-        inv_row_cta<PS, PS::Q, 256>(rq, b, threadIdx.x, sm);
+        inv_row_cta<PS, PS::Q, NT>(rq, b, threadIdx.x, sm);
     } else {
-        const long long row = b * 8 + warp;
+        const long long row = b * WPB + warp;
         if (row < rq.n) inv_row_warp<PS, PS::Q>(rq, row, lane);
     }
 }

@@ -607,13 +607,15 @@ int batch_inverse(const TreePlan &tp, RowDesc X0, void *out0, int out_bytes, lon
 }
 
 // Both rings' roots in one launch (keygen).
+// (256 threads per block measured best against 128 and 512: profiles/)
 template <class PS>
 int launch_joint_roots(const InvArgs &r3, const InvArgs &rq, cudaStream_t s) {
-    const int nb3 = (int)((r3.n + 7) / 8);
+    constexpr int NT = 256, WPB = NT / 32;
+    const int nb3 = (int)((r3.n + WPB - 1) / WPB);
     const int rq_cta = rq.n < 2LL * dev_info().sms ? 1 : 0;
-    const long long nbq = rq_cta ? rq.n : (rq.n + 7) / 8;
+    const long long nbq = rq_cta ? rq.n : (rq.n + WPB - 1) / WPB;
     ProfScope ps_(PC_INV_R3, (double)(r3.n + rq.n), s);
-    joint_roots_kernel<PS><<<(unsigned)(nb3 + nbq), 256, 0, s>>>(r3, rq, nb3, rq_cta);
+    joint_roots_kernel<PS, NT><<<(unsigned)(nb3 + nbq), NT, 0, s>>>(r3, rq, nb3, rq_cta);
     LAUNCHED();
     return SNTRUP_OK;
 }
