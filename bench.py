@@ -126,6 +126,17 @@ def int8_tc_peak_tops(peaks: dict):
     return 2.0 * 1400.0, "fallback 1.4 PF/s sustained bf16 (B200_PROFILING.md) x 2"
 
 
+def load_ncu_pipes():
+    """Time-weighted pipe utilisation per kernel of the step from the committed ncu capture
+    (profiles/ncu_pipes.json, written by scripts/ncu_pipes.py); {} if absent."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_pipes.json")))
+        return {"source": "profiles/ncu_pipes.json (" + d.get("_source", "")[:60] + "...)",
+                "per_kernel_pct": {k.replace("void ", ""): v["time_weighted"] for k, v in d["kernels"].items()}}
+    except Exception:
+        return {}
+
+
 def load_traffic():
     """Per-launch DRAM bytes of the ring-product kernels from the committed ncu capture summary
     (profiles/roofline_traffic.json, written by scripts/ncu_traffic.py); {} if absent."""
@@ -345,6 +356,7 @@ def main():
             "roofline": roof,
             "breakdown_ms_per_step": {k: v["ms"] / args.steps for k, v in prof.items() if v["launches"]},
             "mul_impl": MUL_IMPL,
+            "ncu_pipes": load_ncu_pipes(),
             "profiled_ms_per_step": ms_prof / args.steps,
         }
 

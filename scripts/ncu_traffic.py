@@ -16,7 +16,7 @@ import sys
 def klass(name):
     if "tc_mul_kernel" in name or "ring_mul_kernel" in name:
         return "r3_mul" if ("Params<761, 4591, 286, 3>, 3," in name or ", 3, " in name.split(">, ")[1][:4]) else "rq_mul"
-    for k in ("sample_kernel", "divstep", "encode_kernel", "repair_kernel"):
+    for k in ("sample_kernel", "divstep", "joint_roots", "encode_kernel", "repair_kernel"):
         if k in name:
             return k
     return "other"
