@@ -38,6 +38,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--batch-size", type=int, default=0, help="Montgomery batch size B (0 = tuned default)")
+    ap.add_argument("--chunk-keys", type=int, default=0, help="keys per internal chunk (0 = tuned default); "
+                    "two or more chunks run on two pipelined streams")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-extras", action="store_true", help="skip B sweep / rq_mul / cpu baseline")
     ap.add_argument("--mul-impl", choices=["tc", "schoolbook"], default="tc",
@@ -46,6 +48,7 @@ def parse():
 
 
 DEFAULT_B = 512
+DEFAULT_CHUNK = 65536
 MUL_IMPL = "tc"          # ring products on the tensor cores (see --mul-impl)
 TRAFFIC = {}             # dram bytes per launch of the dominant kernel, from profiles/ (ncu)
 
@@ -235,9 +238,11 @@ def main():
     sk = torch.empty((n, P["sk_bytes"]), dtype=torch.uint8, device="cuda")
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")   # > 126 MB L2
 
-    def step(batch=B):
+    CHUNK = args.chunk_keys or DEFAULT_CHUNK
+
+    def step(batch=B, chunk=None):
         S.batch_keygen(PARAM, n, SEED, first_key_index=first, batch_size=batch, pk_out=pk,
-                       sk_out=sk, flags=S.OPT_ASYNC)
+                       sk_out=sk, flags=S.OPT_ASYNC, chunk_keys=CHUNK if chunk is None else chunk)
 
     def barrier():
         if world > 1:
@@ -328,7 +333,12 @@ def main():
                         "frac": achieved / peak, "traffic": TRAFFIC.get("tc_int8" if kd == "tc_int8" else "tc_fp4"),
                         "peak_source": src + ("" if kd == "tc_int8" else " x 2 (nominal fp4/int8 ratio 9/4.5 PF)"),
                         "share_of_step": share,
-                        "by_kind_ms_per_step": {k: v["ms"] / args.steps for k, v in kinds.items()}}
+                        "by_kind_ms_per_step": {k: v["ms"] / args.steps for k, v in kinds.items()},
+                        "binding_resource": "the UMMA operand fetch from shared memory (every MMA of a "
+                                            "small-N GEMM re-reads its 128x32-byte A tile): ncu "
+                                            "sm__pipe_tc_cycles_active ~93% time-weighted over the "
+                                            "step's int8 launches vs tensor math ~33% "
+                                            "(profiles/ncu_pipes.json, DESIGN.md section 6.1)"}
             else:
                 peak = 2 * int_peak_macs_per_s(sm_mhz) / 1e12
                 roof = {"bound": "alu", "kernel": "ring products, ring_mul_kernel (int32 schoolbook)",
@@ -342,7 +352,7 @@ def main():
             "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
             "config": {"workload": "configs[1]: sntrup761 batch keygen, 65,536 keys per GPU, seed 2",
-                       "keys_per_gpu": n, "batch_size": B, "param_set": PARAM,
+                       "keys_per_gpu": n, "batch_size": B, "chunk_keys": CHUNK, "param_set": PARAM,
                        "l2": "flushed between timed steps (256 MiB write); working set > L2",
                        "parallelism": "key ranges per GPU (no collective)"},
             "gpu_launches": launches,
@@ -367,6 +377,12 @@ def main():
             step(b)
             sweep[str(b)] = n * 3 / (timed(lambda: step(b), 3) / 1e3)
         result["batch_size_sweep_keys_per_s"] = sweep
+        # chunking: one chunk, or 2/4 chunks pipelined on two streams
+        csweep = {}
+        for ck in (65536, 32768, 16384):
+            step(chunk=ck)
+            csweep[str(ck)] = n * 3 / (timed(lambda: step(chunk=ck), 3) / 1e3)
+        result["chunk_sweep_keys_per_s"] = csweep
         # A/B: the same step without the shared-A down-sweep, and on the int32 schoolbook
         ab = {}
         for name, impl in (("tc_int8_m64", S.MUL_TENSOR_CORE_M64),

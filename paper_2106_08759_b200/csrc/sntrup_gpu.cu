@@ -621,6 +621,53 @@ int launch_joint_roots(const InvArgs &r3, const InvArgs &rq, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------------------ keygen
+// Per pipeline lane: a stream, an aux stream (u products) and one chunk's workspace.  With two
+// or more chunks, consecutive chunks alternate between two lanes (the caller's stream and an
+// internal stream), so one chunk's latency-bound phases (sampling, tree tops, root inversion)
+// overlap the other chunk's tensor-core products.
+struct Lane {
+    cudaStream_t s = nullptr;
+    AuxStream *ax = nullptr;
+    int8_t *G = nullptr, *F = nullptr, *Ginv = nullptr;
+    uint8_t *att = nullptr;
+    std::vector<void *> l3, i3, lq, iq;
+    int16_t *Fbar = nullptr, *H = nullptr, *U = nullptr;
+    uint8_t *ok3 = nullptr, *okq = nullptr;
+    unsigned long long *repaired = nullptr;
+    int *err = nullptr;
+};
+
+// internal second lane: a stream and its own aux stream (per device)
+int lane2_streams(cudaStream_t *s2, AuxStream **ax2) {
+    static std::map<int, std::pair<cudaStream_t, AuxStream>> m;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    auto &e = m[dev];
+    if (!e.first) {
+        CK(cudaStreamCreateWithFlags(&e.first, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&e.second.s, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&e.second.go, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&e.second.done, cudaEventDisableTiming));
+    }
+    *s2 = e.first;
+    *ax2 = &e.second;
+    return SNTRUP_OK;
+}
+
+struct LaneJoin { cudaEvent_t start = nullptr, end = nullptr; };
+int lane_join_events(LaneJoin **out) {
+    static std::map<int, LaneJoin> m;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    LaneJoin &j = m[dev];
+    if (!j.start) {
+        CK(cudaEventCreateWithFlags(&j.start, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&j.end, cudaEventDisableTiming));
+    }
+    *out = &j;
+    return SNTRUP_OK;
+}
+
 template <class PS>
 int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
                 const sntrup_keygen_opts &o) {
@@ -629,7 +676,7 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
     DevTables *tb;
     int rc = build_tables(dev, PS::P, PS::WT, &tb);
     if (rc) return rc;
-    cudaStream_t s = (cudaStream_t)o.stream;
+    const cudaStream_t s0 = (cudaStream_t)o.stream;
     const int B = o.batch_size ? (int)o.batch_size : 32;
     if (B < 1 || B > 4096 || (B & (B - 1))) return SNTRUP_E_ARG;
     const bool host_out = (o.flags & SNTRUP_OPT_HOST_OUTPUT) != 0;
@@ -637,37 +684,52 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
     chunk = (chunk + B - 1) / B * B;
     if (chunk > n) chunk = (n + B - 1) / B * B;
     const size_t pkb = tb->enc.pk_bytes, skb = 2 * PS::SKH;
+    const uint64_t nchunks = (n + chunk - 1) / chunk;
+    const int nl = nchunks >= 2 ? 2 : 1;
 
-    // workspace for one chunk of `chunk` keys
+    // workspace: one chunk's buffers per lane (+ shared host-output staging)
     const TreePlan tpmax = make_plan((long long)chunk, B);
     const long long inner = tpmax.inner_rows();
-    size_t need = 0;
-    need += 3 * align256(chunk * PS::P16);                  // G, F, Ginv
-    need += align256(chunk);                                 // attempts
-    need += 2 * align256(inner * PS::P16 + 256 * (tpmax.L + 1));   // R/3 levels + inverses
-    need += 2 * align256(inner * PS::P8 * 2 + 256 * (tpmax.L + 1)); // R/q levels + inverses
-    need += 3 * align256(chunk * PS::P8 * 2);                // Fbar, H, U
-    need += 2 * align256(tpmax.cnt[tpmax.L]);                // root ok flags
+    size_t per_lane = 0;
+    per_lane += 3 * align256(chunk * PS::P16);                  // G, F, Ginv
+    per_lane += align256(chunk);                                 // attempts
+    per_lane += 2 * (inner * PS::P16 + 256 * (tpmax.L + 1)) + 2 * 256 * (tpmax.L + 1);  // R/3 levels + inverses
+    per_lane += 2 * (inner * PS::P8 * 2 + 256 * (tpmax.L + 1)) + 2 * 256 * (tpmax.L + 1); // R/q levels + inverses
+    per_lane += 3 * align256(chunk * PS::P8 * 2);                // Fbar, H, U
+    per_lane += 2 * align256(tpmax.cnt[tpmax.L]);                // root ok flags
+    per_lane += 2 * 256;                                         // counters
+    size_t need = nl * per_lane + 4096;
     if (host_out) need += 2 * (align256(chunk * pkb) + align256(chunk * skb));
-    need += 4096;
     if ((rc = ws_reserve(need))) return rc;
-    int8_t *G = ws_take<int8_t>(chunk * PS::P16);
-    int8_t *F = ws_take<int8_t>(chunk * PS::P16);
-    int8_t *Ginv = ws_take<int8_t>(chunk * PS::P16);
-    uint8_t *att = ws_take<uint8_t>(chunk);
-    std::vector<void *> l3(tpmax.L + 1, nullptr), i3(tpmax.L + 1, nullptr);
-    std::vector<void *> lq(tpmax.L + 1, nullptr), iq(tpmax.L + 1, nullptr);
-    for (int l = 1; l <= tpmax.L; l++) {
-        l3[l] = ws_take<int8_t>(tpmax.cnt[l] * PS::P16);
-        i3[l] = ws_take<int8_t>(tpmax.cnt[l] * PS::P16);
-        lq[l] = ws_take<int16_t>(tpmax.cnt[l] * PS::P8);
-        iq[l] = ws_take<int16_t>(tpmax.cnt[l] * PS::P8);
+    Lane lanes[2];
+    for (int li = 0; li < nl; li++) {
+        Lane &L = lanes[li];
+        if (li == 0) {
+            L.s = s0;
+            if ((rc = aux_stream(&L.ax))) return rc;
+        } else {
+            if ((rc = lane2_streams(&L.s, &L.ax))) return rc;
+        }
+        L.G = ws_take<int8_t>(chunk * PS::P16);
+        L.F = ws_take<int8_t>(chunk * PS::P16);
+        L.Ginv = ws_take<int8_t>(chunk * PS::P16);
+        L.att = ws_take<uint8_t>(chunk);
+        L.l3.assign(tpmax.L + 1, nullptr); L.i3.assign(tpmax.L + 1, nullptr);
+        L.lq.assign(tpmax.L + 1, nullptr); L.iq.assign(tpmax.L + 1, nullptr);
+        for (int l = 1; l <= tpmax.L; l++) {
+            L.l3[l] = ws_take<int8_t>(tpmax.cnt[l] * PS::P16);
+            L.i3[l] = ws_take<int8_t>(tpmax.cnt[l] * PS::P16);
+            L.lq[l] = ws_take<int16_t>(tpmax.cnt[l] * PS::P8);
+            L.iq[l] = ws_take<int16_t>(tpmax.cnt[l] * PS::P8);
+        }
+        L.Fbar = ws_take<int16_t>(chunk * PS::P8);
+        L.H = ws_take<int16_t>(chunk * PS::P8);
+        L.U = ws_take<int16_t>(chunk * PS::P8);
+        L.ok3 = ws_take<uint8_t>(tpmax.cnt[tpmax.L]);
+        L.okq = ws_take<uint8_t>(tpmax.cnt[tpmax.L]);
+        L.repaired = ws_take<unsigned long long>(1);
+        L.err = ws_take<int>(1);
     }
-    int16_t *Fbar = ws_take<int16_t>(chunk * PS::P8);
-    int16_t *H = ws_take<int16_t>(chunk * PS::P8);
-    int16_t *U = ws_take<int16_t>(chunk * PS::P8);
-    uint8_t *ok3 = ws_take<uint8_t>(tpmax.cnt[tpmax.L]);
-    uint8_t *okq = ws_take<uint8_t>(tpmax.cnt[tpmax.L]);
     uint8_t *pk_stage[2] = {nullptr, nullptr}, *sk_stage[2] = {nullptr, nullptr};
     CopyStream *cs = nullptr;
     if (host_out) {
@@ -677,23 +739,34 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
         }
         if ((rc = copy_stream(&cs))) return rc;
     }
-    unsigned long long *repaired = ws_take<unsigned long long>(1);
-    int *err = ws_take<int>(1);
-    CK(cudaMemsetAsync(repaired, 0, sizeof(unsigned long long), s));
-    CK(cudaMemsetAsync(err, 0, sizeof(int), s));
+    LaneJoin *lj = nullptr;
+    if (nl > 1) {                          // lane 1 starts after everything enqueued before the call
+        if ((rc = lane_join_events(&lj))) return rc;
+        CK(cudaEventRecord(lj->start, s0));
+        CK(cudaStreamWaitEvent(lanes[1].s, lj->start, 0));
+    }
+    for (int li = 0; li < nl; li++) {
+        CK(cudaMemsetAsync(lanes[li].repaired, 0, sizeof(unsigned long long), lanes[li].s));
+        CK(cudaMemsetAsync(lanes[li].err, 0, sizeof(int), lanes[li].s));
+    }
 
     uint64_t n_rq = 0, n_r3 = 0, n_inv = 0;
     for (uint64_t c0 = 0; c0 < n; c0 += chunk) {
         const uint64_t m = (n - c0 < chunk) ? n - c0 : chunk;
         const uint64_t first = o.first_key_index + c0;
         const TreePlan tp = make_plan((long long)m, B);
-        int8_t *Gc = o.g_out ? o.g_out + c0 * PS::P16 : G;
-        int8_t *Fc = o.f_out ? o.f_out + c0 * PS::P16 : F;
-        int8_t *Ic = o.ginv_out ? o.ginv_out + c0 * PS::P16 : Ginv;
-        uint8_t *Ac = o.attempts_out ? o.attempts_out + c0 : att;
-        int16_t *Hc = o.h_out ? o.h_out + c0 * PS::P8 : H;
-        const int buf = (int)((c0 / chunk) & 1);
-        if (host_out && c0 >= 2 * chunk) CK(cudaStreamWaitEvent(s, cs->copy[buf], 0));   // staging free
+        const uint64_t ci = c0 / chunk;
+        Lane &L = lanes[ci % nl];
+        const cudaStream_t s = L.s;                          // this chunk's stream
+        // host outputs: staging buffer pair indexed by chunk parity (both lanes share the copy
+        // stream); a pair is reused two chunks later, after its copies
+        const int buf = (int)(ci & 1);
+        int8_t *Gc = o.g_out ? o.g_out + c0 * PS::P16 : L.G;
+        int8_t *Fc = o.f_out ? o.f_out + c0 * PS::P16 : L.F;
+        int8_t *Ic = o.ginv_out ? o.ginv_out + c0 * PS::P16 : L.Ginv;
+        uint8_t *Ac = o.attempts_out ? o.attempts_out + c0 : L.att;
+        int16_t *Hc = o.h_out ? o.h_out + c0 * PS::P8 : L.H;
+        if (host_out && ci >= 2) CK(cudaStreamWaitEvent(s, cs->copy[buf], 0));   // staging free
         uint8_t *pkc = host_out ? pk_stage[buf] : pk_out + c0 * pkb;
         uint8_t *skc = host_out ? sk_stage[buf] : sk_out + c0 * skb;
 
@@ -707,7 +780,7 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
         if (o.flags & SNTRUP_OPT_NO_SMALL_CHECK) sa.small_check = 0;
         else if (o.flags & SNTRUP_OPT_FORCE_SMALL_CHECK) sa.small_check = 1;
         else sa.small_check = (tb->p_small_reject * B > 1e-4) ? 1 : 0;
-        sa.err = err;
+        sa.err = L.err;
         {
             ProfScope ps_(PC_SAMPLE, (double)m, s);
             sample_kernel<PS><<<(unsigned)((m + 3) / 4), 128, 0, s>>>(sa);
@@ -723,11 +796,10 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
         // the sample and run on an aux stream beside the root inversion; the bottom R/q down-sweep
         // level (1 x 2 limbs per product) disappears, h becomes a 2 x 2-limb product.
         // (B = 1 has no parents: plain fbar, then h = g * fbar.)
-        const TreeJob<PS, 3> j3{tp, rows8(Gc, PS::P16), Ic, 1, PS::P16, l3, i3, ok3, true};
-        const TreeJob<PS, PS::Q> jq{tp, rows8(Fc, PS::P16, 3), Fbar, 2, PS::P8, lq, iq, okq, true};
+        const TreeJob<PS, 3> j3{tp, rows8(Gc, PS::P16), Ic, 1, PS::P16, L.l3, L.i3, L.ok3, true};
+        const TreeJob<PS, PS::Q> jq{tp, rows8(Fc, PS::P16, 3), L.Fbar, 2, PS::P8, L.lq, L.iq, L.okq, true};
         const bool utrick = tp.L >= 1;
-        AuxStream *ax = nullptr;
-        if ((rc = aux_stream(&ax))) return rc;
+        AuxStream *ax = L.ax;
         if ((rc = j3.up(s, &n_r3))) return rc;
         if ((rc = jq.up(s, &n_rq))) return rc;
         if (utrick) {
@@ -739,7 +811,7 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
             a.cnt_in = (long long)m;
             a.X = rows8(Gc, PS::P16);
             a.Y = rows8(Fc, PS::P16, 3);
-            a.out = U;
+            a.out = L.U;
             a.out_stride = PS::P8;
             a.out_bytes = 2;
             a.periodic = 0;
@@ -750,11 +822,11 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
         if ((rc = j3.down(s, &n_r3))) return rc;
         if (utrick) CK(cudaStreamWaitEvent(s, ax->done, 0));    // repair may rewrite u rows
         RepairArgs ra{};
-        ra.seed = seed; ra.first = first; ra.n = m; ra.B = B; ra.root_ok = ok3;
+        ra.seed = seed; ra.first = first; ra.n = m; ra.B = B; ra.root_ok = L.ok3;
         ra.G = Gc; ra.Ginv = Ic; ra.attempts = Ac;
         ra.T = tb->T; ra.masks = tb->masks; ra.nf = tb->nf; ra.small_check = sa.small_check;
-        ra.repaired = repaired; ra.err = err;
-        ra.F = Fc; ra.U = utrick ? U : nullptr;
+        ra.repaired = L.repaired; ra.err = L.err;
+        ra.F = Fc; ra.U = utrick ? L.U : nullptr;
         {
             ProfScope ps_(PC_REPAIR, (double)m, s);
             repair_kernel<PS><<<(unsigned)((m + 3) / 4), 128, 0, s>>>(ra);
@@ -795,7 +867,7 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
                     a.mode = MUL_DOWNH;
                     a.n_out = (long long)rows;
                     a.cnt_in = (long long)rows;
-                    a.X = rows16(U + r0 * PS::P8, PS::P8);
+                    a.X = rows16(L.U + r0 * PS::P8, PS::P8);
                     a.Y = rows16((const int16_t *)P1.ptr + (r0 / 2) * P1.stride, P1.stride);
                     a.periodic = 1;
                     a.out = Hc + r0 * PS::P8;
@@ -806,7 +878,7 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
                     a.mode = MUL_ZIP;
                     a.n_out = (long long)rows;
                     a.X = rows8(Gc + r0 * PS::P16, PS::P16);
-                    a.Y = rows16(Fbar + r0 * PS::P8, PS::P8);
+                    a.Y = rows16(L.Fbar + r0 * PS::P8, PS::P8);
                     a.periodic = 0;
                     a.out = Hc + r0 * PS::P8;
                     a.out_stride = PS::P8;
@@ -830,23 +902,29 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
         }
         n_rq += m;
         if (host_out) CK(cudaEventRecord(cs->copy[buf], cs->s));
+        }
+    if (nl > 1) {                          // join lane 1 into the caller's stream
+        CK(cudaEventRecord(lj->end, lanes[1].s));
+        CK(cudaStreamWaitEvent(s0, lj->end, 0));
     }
-    if (host_out) {                       // join the copies into the caller's stream
-        for (int i = 0; i < 2; i++) CK(cudaStreamWaitEvent(s, cs->copy[i], 0));
+    if (host_out) {                        // join the copies into the caller's stream
+        for (int i = 0; i < 2; i++) CK(cudaStreamWaitEvent(s0, cs->copy[i], 0));
     }
     const bool sync = !(o.flags & SNTRUP_OPT_ASYNC) || host_out || o.stats_out;
     if (sync) {
-        int herr = 0;
-        unsigned long long hrep = 0;
-        CK(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(&hrep, repaired, sizeof(hrep), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        if (herr) return SNTRUP_E_INTERNAL;
+        int herr[2] = {0, 0};
+        unsigned long long hrep[2] = {0, 0};
+        for (int li = 0; li < nl; li++) {
+            CK(cudaMemcpyAsync(&herr[li], lanes[li].err, sizeof(int), cudaMemcpyDeviceToHost, s0));
+            CK(cudaMemcpyAsync(&hrep[li], lanes[li].repaired, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s0));
+        }
+        CK(cudaStreamSynchronize(s0));
+        if (herr[0] || herr[1]) return SNTRUP_E_INTERNAL;
         if (o.stats_out) {
             o.stats_out[0] = n_rq;
             o.stats_out[1] = n_r3;
             o.stats_out[2] = n_inv;
-            o.stats_out[3] = hrep;
+            o.stats_out[3] = hrep[0] + hrep[1];
         }
     }
     return SNTRUP_OK;
