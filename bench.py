@@ -176,6 +176,56 @@ def oracle_keygen_rate(target_s: float = 10.0):
         n - 1, threads, dt)
 
 
+def other_configs(S, torch, timed):
+    """configs[0]: latency of one 32-key call (launch-bound; synchronous C-ABI call, host
+    wall clock around it, and device time); configs[3]: keys/s per parameter set at 65,536 keys
+    (B = 512); configs[4]: sntrup1277, 2^20 keys, B = 1024, streamed in 65,536-key chunks."""
+    out = {}
+    # configs[0]: 761, 32 keys, seed 1, one tree of 32
+    P = S.params(761)
+    pk = torch.empty((32, P["pk_bytes"]), dtype=torch.uint8, device="cuda")
+    sk = torch.empty((32, P["sk_bytes"]), dtype=torch.uint8, device="cuda")
+    for _ in range(5):
+        S.batch_keygen(761, 32, 1, batch_size=32, pk_out=pk, sk_out=sk)
+    torch.cuda.synchronize()
+    lat = []
+    for _ in range(20):
+        t0 = time.perf_counter()
+        S.batch_keygen(761, 32, 1, batch_size=32, pk_out=pk, sk_out=sk)   # synchronous call
+        lat.append((time.perf_counter() - t0) * 1e6)
+    dev_ms = timed(lambda: S.batch_keygen(761, 32, 1, batch_size=32, pk_out=pk, sk_out=sk,
+                                          flags=S.OPT_ASYNC), 10) / 10
+    out["configs[0]"] = {"workload": "sntrup761, 32 keys, seed 1, B = 32",
+                         "latency_us_median": statistics.median(lat), "device_us": dev_ms * 1e3,
+                         "keys_per_s": 32 / (statistics.median(lat) / 1e6)}
+    # configs[3]: parameter sweep at 65,536 keys, seed 4
+    sweep = {}
+    for ps in (653, 857, 953, 1013):
+        P = S.params(ps)
+        n = 65536
+        pk = torch.empty((n, P["pk_bytes"]), dtype=torch.uint8, device="cuda")
+        sk = torch.empty((n, P["sk_bytes"]), dtype=torch.uint8, device="cuda")
+        f = lambda: S.batch_keygen(ps, n, 4, batch_size=512, pk_out=pk, sk_out=sk, flags=S.OPT_ASYNC)
+        f()
+        ms = timed(f, 3) / 3
+        sweep[str(ps)] = {"keys_per_s": n / (ms / 1e3), "ms": ms}
+        del pk, sk
+    out["configs[3]"] = {"workload": "65,536 keys per set, seed 4, B = 512", "by_param_set": sweep}
+    # configs[4]: 1277, 2^20 keys, B = 1024, 65,536-key chunks (two pipelined lanes)
+    P = S.params(1277)
+    n = 1 << 20
+    pk = torch.empty((n, P["pk_bytes"]), dtype=torch.uint8, device="cuda")
+    sk = torch.empty((n, P["sk_bytes"]), dtype=torch.uint8, device="cuda")
+    f = lambda: S.batch_keygen(1277, n, 5, batch_size=1024, chunk_keys=65536, pk_out=pk, sk_out=sk,
+                               flags=S.OPT_ASYNC)
+    f()
+    ms = timed(f, 2) / 2
+    out["configs[4]"] = {"workload": "sntrup1277, 2^20 keys, seed 5, B = 1024, 65,536-key chunks",
+                         "keys_per_s": n / (ms / 1e3), "ms": ms}
+    del pk, sk
+    return out
+
+
 # ----------------------------------------------------------------------------------- reference arm
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
@@ -417,6 +467,9 @@ def main():
                             "big_x_big_path_mults_per_s": npairs / (bb_ms / 1e3),
                             "int32_schoolbook_mults_per_s": npairs / (sb_ms / 1e3)}
         del a, bt, c, b16
+        # the other configs' reported quantities; parity for each is in
+        # tests/test_gpu_parity.py
+        result["other_configs"] = other_configs(S, torch, timed)
         # CPU baseline: the oracle on this host (bounded sample)
         v, cores, sample = oracle_keygen_rate(10.0)
         result["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
