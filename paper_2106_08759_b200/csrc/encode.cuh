@@ -22,6 +22,11 @@ struct EncTables {
     const uint8_t *emit;              // per pair: bytes emitted
     const uint16_t *off;              // per pair: byte offset of the first emitted byte
     int pk_bytes;
+    // Per level (host-verified): M_{2i} is the same for every pair of a level (only the last
+    // element can be a carried odd one), so every pair but the last emits lev_e bytes at
+    // lev_off + lev_e * i; the last pair emits lev_elast bytes.
+    uint32_t lev_M[ENC_MAXLEV];
+    int lev_e[ENC_MAXLEV], lev_elast[ENC_MAXLEV], lev_off[ENC_MAXLEV];
 };
 
 struct EncArgs {
@@ -56,20 +61,20 @@ template <class PS>
 __global__ void __launch_bounds__(128) encode_kernel(EncArgs a) {
     constexpr int WPB = 4;
     __shared__ uint16_t sR[WPB][2][PS::P8];
-    __shared__ uint8_t spk[WPB][2112];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint64_t key = (uint64_t)blockIdx.x * WPB + wid;
     if (key >= a.n) return;
 
     if (a.h) {
         uint16_t *R = sR[wid][0], *R2 = sR[wid][1];
-        uint8_t *out = spk[wid];
+        uint8_t *dst = a.pk + key * (uint64_t)a.t.pk_bytes;
         const int16_t *hrow = a.h + key * PS::P8;
         // level 0 straight from HBM: 8 coefficients (4 pairs) per lane and 16-byte load; every
-        // level-0 pair has M = q*q and emits the same number of bytes e0 at offset e0*i
+        // level-0 pair has M = q*q and emits the same number of bytes e0 at offset e0*i.
+        // Emitted bytes go straight to the pk row (consecutive lanes, consecutive bytes).
         {
-            const uint32_t m0 = a.t.Mlo[0];
-            const int e0 = a.t.emit[0];
+            const uint32_t m0 = a.t.lev_M[0];
+            const int e0 = a.t.lev_e[0];
             const int npairs = a.t.lev_n[0] / 2;
             for (int c = lane; c < PS::P8 / 8; c += 32) {
                 const uint4 q4 = __ldg(reinterpret_cast<const uint4 *>(hrow) + c);
@@ -81,7 +86,7 @@ __global__ void __launch_bounds__(128) encode_kernel(EncArgs a) {
                     const uint32_t r1 = (uint32_t)((int)(int16_t)(w[t] >> 16) + PS::QH);
                     if (i < npairs) {
                         uint32_t r = r0 + m0 * r1;
-                        for (int b = 0; b < e0; b++) { out[e0 * i + b] = (uint8_t)(r & 255u); r >>= 8; }
+                        for (int b = 0; b < e0; b++) { dst[e0 * i + b] = (uint8_t)(r & 255u); r >>= 8; }
                         R2[i] = (uint16_t)r;
                     } else if (2 * i < PS::P) {
                         R2[i] = (uint16_t)r0;                          // odd last element carried
@@ -95,13 +100,14 @@ __global__ void __launch_bounds__(128) encode_kernel(EncArgs a) {
         }
         for (int lev = 1; lev < a.t.nlev; lev++) {
             const int n = a.t.lev_n[lev];
-            const int base = a.t.lev_pair_base[lev];
-            for (int i = lane; i < n / 2; i += 32) {
-                const uint32_t m0 = a.t.Mlo[base + i];
+            const uint32_t m0 = a.t.lev_M[lev];
+            const int e = a.t.lev_e[lev], el = a.t.lev_elast[lev], ob = a.t.lev_off[lev];
+            const int npairs = n / 2;
+            for (int i = lane; i < npairs; i += 32) {
                 uint32_t r = (uint32_t)R[2 * i] + m0 * (uint32_t)R[2 * i + 1];
-                const int e = a.t.emit[base + i];
-                const int o = a.t.off[base + i];
-                for (int t = 0; t < e; t++) { out[o + t] = (uint8_t)(r & 255u); r >>= 8; }
+                const int ee = (i == npairs - 1) ? el : e;
+                const int o = ob + e * i;
+                for (int t = 0; t < ee; t++) { dst[o + t] = (uint8_t)(r & 255u); r >>= 8; }
                 R2[i] = (uint16_t)r;
             }
             if ((n & 1) && lane == 0) R2[n / 2] = R[n - 1];
@@ -110,11 +116,8 @@ __global__ void __launch_bounds__(128) encode_kernel(EncArgs a) {
         }
         if (lane == 0) {
             uint32_t r = R[0];
-            for (int t = 0; t < a.t.top_emit; t++) { out[a.t.top_off + t] = (uint8_t)(r & 255u); r >>= 8; }
+            for (int t = 0; t < a.t.top_emit; t++) { dst[a.t.top_off + t] = (uint8_t)(r & 255u); r >>= 8; }
         }
-        __syncwarp();
-        uint8_t *dst = a.pk + key * (uint64_t)a.t.pk_bytes;
-        for (int k = lane; k < a.t.pk_bytes; k += 32) dst[k] = out[k];
     }
     if (a.f) {
         // 16 trits per 16-byte load -> 4 sk bytes; trits >= P are 0 (pad) and contribute (0+1)

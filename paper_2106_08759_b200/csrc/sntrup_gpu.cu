@@ -226,6 +226,7 @@ int build_tables(int dev, int ps, int WT, DevTables **out) {
             if (lev >= ENC_MAXLEV) return SNTRUP_E_PARAM;
             enc.lev_n[lev] = n;
             enc.lev_pair_base[lev] = (int)Mlo.size();
+            enc.lev_off[lev] = (int)pos;
             std::vector<uint32_t> M2((n + 1) / 2);
             for (int i = 0; i + 1 < n; i += 2) {
                 uint32_t m = M[i] * M[i + 1];
@@ -243,6 +244,18 @@ int build_tables(int dev, int ps, int WT, DevTables **out) {
             lev++;
         }
         enc.nlev = lev;
+        // per-level uniform form used by the kernel (checked here)
+        for (int l = 0; l < lev; l++) {
+            const int base = enc.lev_pair_base[l], np = enc.lev_n[l] / 2;
+            enc.lev_M[l] = Mlo[base];
+            enc.lev_e[l] = emit[base];
+            enc.lev_elast[l] = emit[base + np - 1];
+            for (int i = 0; i < np; i++) {
+                if (Mlo[base + i] != enc.lev_M[l]) return SNTRUP_E_INTERNAL;
+                if (i < np - 1 && emit[base + i] != enc.lev_e[l]) return SNTRUP_E_INTERNAL;
+                if (off[base + i] != enc.lev_off[l] + enc.lev_e[l] * i) return SNTRUP_E_INTERNAL;
+            }
+        }
         uint32_t m = M[0];
         int e = 0;
         while (m > 1) { e++; m = (m + 255u) >> 8; }
