@@ -287,11 +287,11 @@ int build_tables(int dev, int ps, int WT, DevTables **out) {
 // Host-output keygen: chunk i's pk/sk are copied device->host on a copy stream while chunk i+1
 // computes (double-buffered device staging).  One per device (calls are serialised).
 struct CopyStream { cudaStream_t s = nullptr; cudaEvent_t comp[2] = {}, copy[2] = {}; };
-int copy_stream(CopyStream **out) {
-    static std::map<int, CopyStream> m;
+int copy_stream(CopyStream **out, int which = 0) {   // which: pipeline lane (0 or 1)
+    static std::map<std::pair<int, int>, CopyStream> m;
     int dev = 0;
     CK(cudaGetDevice(&dev));
-    CopyStream &c = m[dev];
+    CopyStream &c = m[std::make_pair(dev, which)];
     if (!c.s) {
         CK(cudaStreamCreateWithFlags(&c.s, cudaStreamNonBlocking));
         for (int i = 0; i < 2; i++) {
@@ -744,13 +744,15 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
         L.err = ws_take<int>(1);
     }
     uint8_t *pk_stage[2] = {nullptr, nullptr}, *sk_stage[2] = {nullptr, nullptr};
-    CopyStream *cs = nullptr;
+    CopyStream *csl[2] = {nullptr, nullptr};       // one copy stream per lane: copies follow readiness
     if (host_out) {
         for (int i = 0; i < 2; i++) {
             pk_stage[i] = ws_take<uint8_t>(chunk * pkb);
             sk_stage[i] = ws_take<uint8_t>(chunk * skb);
         }
-        if ((rc = copy_stream(&cs))) return rc;
+        for (int li = 0; li < nl; li++)
+            if ((rc = copy_stream(&csl[li], li))) return rc;
+        if (nl == 1) csl[1] = csl[0];
     }
     LaneJoin *lj = nullptr;
     if (nl > 1) {                          // lane 1 starts after everything enqueued before the call
@@ -779,6 +781,7 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
         int8_t *Ic = o.ginv_out ? o.ginv_out + c0 * PS::P16 : L.Ginv;
         uint8_t *Ac = o.attempts_out ? o.attempts_out + c0 : L.att;
         int16_t *Hc = o.h_out ? o.h_out + c0 * PS::P8 : L.H;
+        CopyStream *cs = csl[ci % nl];
         if (host_out && ci >= 2) CK(cudaStreamWaitEvent(s, cs->copy[buf], 0));   // staging free
         uint8_t *pkc = host_out ? pk_stage[buf] : pk_out + c0 * pkb;
         uint8_t *skc = host_out ? sk_stage[buf] : sk_out + c0 * skb;
@@ -921,7 +924,8 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
         CK(cudaStreamWaitEvent(s0, lj->end, 0));
     }
     if (host_out) {                        // join the copies into the caller's stream
-        for (int i = 0; i < 2; i++) CK(cudaStreamWaitEvent(s0, cs->copy[i], 0));
+        for (int li = 0; li < nl; li++)
+            for (int i = 0; i < 2; i++) CK(cudaStreamWaitEvent(s0, csl[li]->copy[i], 0));
     }
     const bool sync = !(o.flags & SNTRUP_OPT_ASYNC) || host_out || o.stats_out;
     if (sync) {
