@@ -137,6 +137,26 @@ int r3_is_invertible_batch(int param_set, uint64_t n, const int8_t *g, uint8_t *
    Stream-ordered. */
 int rq_encode_batch(int param_set, uint64_t n, const int16_t *h, uint8_t *pk, void *stream);
 
+/* ---- Key pool: the paper's engNTRU batch_lib provider (section 4.2) on the GPU.
+   A pinned host ring of `capacity` key pairs (a multiple of batch_keys, at least two batches),
+   filled by sntrup_batch_keygen_ex calls of batch_keys keys (product trees of batch_size, 0 ->
+   32) on a private stream, with consecutive global key indices first_key_index, +1, ... of
+   `seed`.  The first take() fills lazily and waits; every take() that leaves the ring at most
+   half full starts the next batch asynchronously, so a steady consumer does not wait for the GPU
+   (the paper's "first key 2.5 ms, then 0 ms").  Thread-safe; one pool per device
+   and parameter set as the caller chooses.  Handed-out slots are erased. */
+typedef struct sntrup_pool sntrup_pool;
+int sntrup_pool_create(int param_set, uint64_t seed, uint64_t first_key_index, uint64_t capacity,
+                       uint64_t batch_keys, uint32_t batch_size, sntrup_pool **out);
+/* Next key pair into HOST buffers pk (pk_bytes) and sk (sk_bytes); *key_index (may be NULL) =
+   its global key index.  Blocks only if no generated key is left. */
+int sntrup_pool_take(sntrup_pool *pool, uint8_t *pk, uint8_t *sk, uint64_t *key_index);
+/* Counters: keys handed out, keys generated (incl. in flight), takes that had to wait for the
+   GPU, keys ready or in flight.  Any pointer may be NULL. */
+int sntrup_pool_stats(sntrup_pool *pool, uint64_t *taken, uint64_t *generated, uint64_t *waits,
+                      uint64_t *ready);
+void sntrup_pool_destroy(sntrup_pool *pool);
+
 /* Release the cached device workspaces (all streams). */
 void sntrup_release_workspace(void);
 

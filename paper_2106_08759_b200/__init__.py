@@ -69,13 +69,19 @@ _lib.sntrup_profile_read.restype = _i32
 _lib.sntrup_profile_read.argtypes = [_i32, _vp, _vp, _vp, _vp, _i32]
 _lib.sntrup_profile_read_kinds.restype = _i32
 _lib.sntrup_profile_read_kinds.argtypes = [_i32, _vp, _vp, _vp]
+_lib.sntrup_pool_create.argtypes = [_i32, _u64, _u64, _u64, _u64, _u32, ctypes.POINTER(_vp)]
+_lib.sntrup_pool_take.argtypes = [_vp, _vp, _vp, ctypes.POINTER(ctypes.c_uint64)]
+_lib.sntrup_pool_stats.argtypes = [_vp] + [ctypes.POINTER(ctypes.c_uint64)] * 4
+_lib.sntrup_pool_destroy.argtypes = [_vp]
+_lib.sntrup_pool_destroy.restype = None
 _lib.rq_mul_small_batch.argtypes = [_i32, _u64, _vp, _vp, _vp, _vp]
 
 EXPORTED = ("sntrup_params", "sntrup_strerror", "sntrup_batch_keygen", "sntrup_batch_keygen_ex",
             "sntrup_keygen_workspace_bytes", "rq_mul_batch", "rq_mul_small_batch", "r3_mul_batch", "rq_recip_batch",
             "r3_recip_batch", "r3_is_invertible_batch", "rq_encode_batch",
             "sntrup_release_workspace", "sntrup_kernel_launch_count", "sntrup_set_mul_impl",
-            "sntrup_profile_enable", "sntrup_profile_read_kinds",
+            "sntrup_profile_enable", "sntrup_profile_read_kinds", "sntrup_pool_create",
+            "sntrup_pool_take", "sntrup_pool_stats", "sntrup_pool_destroy",
             "sntrup_profile_read")
 
 PROFILE_CLASSES = ("sample", "r3_mul", "rq_mul", "root_inv", "rq_inv", "repair", "encode", "other")
@@ -264,6 +270,41 @@ def set_mul_impl(impl: int):
 
 def profile_enable(on: bool = True):
     _lib.sntrup_profile_enable(1 if on else 0)
+
+
+class KeyPool:
+    """GPU-backed key pool (sntrup_pool_*): take() returns (pk, sk, key_index) as host bytes."""
+
+    def __init__(self, param_set: int, seed: int, capacity: int, batch_keys: int,
+                 batch_size: int = 32, first_key_index: int = 0):
+        self.P = params(param_set)
+        h = ctypes.c_void_p()
+        _check(_lib.sntrup_pool_create(param_set, seed, first_key_index, capacity, batch_keys,
+                                       batch_size, ctypes.byref(h)), "sntrup_pool_create")
+        self._h = h
+        self._pk = (ctypes.c_uint8 * self.P["pk_bytes"])()
+        self._sk = (ctypes.c_uint8 * self.P["sk_bytes"])()
+
+    def take(self):
+        idx = ctypes.c_uint64()
+        _check(_lib.sntrup_pool_take(self._h, self._pk, self._sk, ctypes.byref(idx)), "sntrup_pool_take")
+        return bytes(self._pk), bytes(self._sk), idx.value
+
+    def stats(self) -> dict:
+        v = [ctypes.c_uint64() for _ in range(4)]
+        _check(_lib.sntrup_pool_stats(self._h, *[ctypes.byref(x) for x in v]), "sntrup_pool_stats")
+        return dict(taken=v[0].value, generated=v[1].value, waits=v[2].value, ready=v[3].value)
+
+    def close(self):
+        if self._h:
+            _lib.sntrup_pool_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 MUL_KINDS = ("tc_int8", "tc_fp4", "int32")

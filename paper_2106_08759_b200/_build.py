@@ -6,7 +6,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsntrup_gpu.so")
-SOURCES = [os.path.join(CSRC, "sntrup_gpu.cu")]
+SOURCES = [os.path.join(CSRC, "sntrup_gpu.cu"), os.path.join(CSRC, "pool.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))] + \
     [os.path.join(ROOT, "include", "sntrup_gpu.h")]
 

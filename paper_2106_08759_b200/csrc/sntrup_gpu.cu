@@ -322,42 +322,47 @@ int aux_stream(AuxStream **out) {
 }
 
 // ------------------------------------------------------------------------------ workspace
+// One cached workspace per (device, caller stream): calls on different streams never share
+// scratch memory, so asynchronous calls on different streams are independent (the header's
+// promise).  The workspace of the current call is selected by ws_reserve (under g_mu).
 struct Workspace {
     char *base = nullptr;
     size_t cap = 0, used = 0;
     int dev = -1;
 };
-Workspace g_ws;
+std::map<std::pair<int, uintptr_t>, Workspace> g_wsmap;
+Workspace *g_ws = nullptr;
 
-int ws_reserve(size_t bytes) {
+int ws_reserve(size_t bytes, cudaStream_t stream) {
     int dev;
     CK(cudaGetDevice(&dev));
-    if (g_ws.base && g_ws.cap >= bytes && g_ws.dev == dev) { g_ws.used = 0; return SNTRUP_OK; }
-    if (g_ws.base) {
-        CK(cudaDeviceSynchronize());
-        cudaSetDevice(g_ws.dev);
-        cudaFree(g_ws.base);
-        cudaSetDevice(dev);
-        g_ws.base = nullptr;
+    Workspace &w = g_wsmap[std::make_pair(dev, (uintptr_t)stream)];
+    g_ws = &w;
+    if (w.base && w.cap >= bytes) { w.used = 0; return SNTRUP_OK; }
+    if (w.base) {
+        CK(cudaDeviceSynchronize());          // in-flight work (any internal stream) may use it
+        cudaFree(w.base);
+        w.base = nullptr;
+        w.cap = 0;
     }
     size_t cap = bytes + (bytes >> 3) + (1 << 20);
-    if (cudaMalloc(&g_ws.base, cap) != cudaSuccess) {
+    if (cudaMalloc(&w.base, cap) != cudaSuccess) {
         cudaGetLastError();
-        g_ws.base = nullptr;
-        g_ws.cap = 0;
+        w.base = nullptr;
+        w.cap = 0;
         return SNTRUP_E_WORKSPACE;
     }
-    g_ws.cap = cap;
-    g_ws.used = 0;
-    g_ws.dev = dev;
+    w.cap = cap;
+    w.used = 0;
+    w.dev = dev;
     return SNTRUP_OK;
 }
 
 template <class T>
 T *ws_take(size_t count) {
     size_t bytes = (count * sizeof(T) + 255) & ~(size_t)255;
-    T *p = (T *)(g_ws.base + g_ws.used);
-    g_ws.used += bytes;
+    T *p = (T *)(g_ws->base + g_ws->used);
+    g_ws->used += bytes;
     return p;
 }
 
@@ -713,7 +718,7 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
     per_lane += 2 * 256;                                         // counters
     size_t need = nl * per_lane + 4096;
     if (host_out) need += 2 * (align256(chunk * pkb) + align256(chunk * skb));
-    if ((rc = ws_reserve(need))) return rc;
+    if ((rc = ws_reserve(need, s0))) return rc;
     Lane lanes[2];
     for (int li = 0; li < nl; li++) {
         Lane &L = lanes[li];
@@ -1021,7 +1026,7 @@ int r3_recip_impl(uint64_t n, const int8_t *g, int8_t *out, uint8_t *ok, uint32_
     const long long inner = tp.inner_rows();
     size_t need = align256(n * PS::P16) + 2 * align256(inner * PS::P16 + 256 * (tp.L + 1)) +
                   align256(tp.cnt[tp.L]) + 4096;
-    if ((rc = ws_reserve(need))) return rc;
+    if ((rc = ws_reserve(need, s))) return rc;
     int8_t *gp = ws_take<int8_t>(n * PS::P16);
     std::vector<void *> l3(tp.L + 1, nullptr), i3(tp.L + 1, nullptr);
     for (int l = 1; l <= tp.L; l++) {
@@ -1048,7 +1053,7 @@ int rq_recip_impl(uint64_t n, const int16_t *a, int16_t *out, uint32_t B_, uint6
     const long long inner = tp.inner_rows();
     size_t need = 2 * align256(inner * PS::P8 * 2 + 256 * (tp.L + 1)) + align256(tp.cnt[tp.L]) + 4096;
     int rc;
-    if ((rc = ws_reserve(need))) return rc;
+    if ((rc = ws_reserve(need, s))) return rc;
     std::vector<void *> lq(tp.L + 1, nullptr), iq(tp.L + 1, nullptr);
     for (int l = 1; l <= tp.L; l++) {
         lq[l] = ws_take<int16_t>(tp.cnt[l] * PS::P8);
@@ -1242,12 +1247,18 @@ int rq_encode_batch(int param_set, uint64_t n, const int16_t *h, uint8_t *pk, vo
 
 void sntrup_release_workspace(void) {
     std::lock_guard<std::mutex> lk(g_mu);
-    if (g_ws.base) {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (auto &kv : g_wsmap) {
+        if (!kv.second.base) continue;
+        cudaSetDevice(kv.second.dev);
         cudaDeviceSynchronize();
-        cudaFree(g_ws.base);
-        g_ws.base = nullptr;
-        g_ws.cap = 0;
+        cudaFree(kv.second.base);
+        kv.second.base = nullptr;
+        kv.second.cap = 0;
     }
+    cudaSetDevice(cur);
+    g_ws = nullptr;
 }
 
 uint64_t sntrup_kernel_launch_count(void) { return g_launches.load(); }

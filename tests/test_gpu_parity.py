@@ -181,6 +181,37 @@ def test_cfg5_full_size_sampled(O):
     check_keys(O, 1277, 5, res, idx)
 
 
+# --------------------------------------------------------------------------------- key pool
+def test_key_pool_hands_out_oracle_keys_in_order(O):
+    # engNTRU batch_lib analogue: consecutive global key indices from first_key_index,
+    # each pair byte-identical to the oracle's; refills happen ahead of the consumer
+    import time
+    pool = S.KeyPool(761, seed=21, capacity=256, batch_keys=64, batch_size=32, first_key_index=1000)
+    got = [pool.take() for _ in range(300)]                  # tight loop: crosses several refills
+    st = pool.stats()
+    idx = np.array([g[2] for g in got], dtype=np.uint64)
+    assert np.array_equal(idx, np.arange(1000, 1300, dtype=np.uint64))
+    ref = oracle_keys(O, 761, 21, idx)
+    for i, (pk, sk, _) in enumerate(got):
+        assert pk == ref["pk"][i].tobytes() and sk == ref["sk"][i].tobytes(), i
+    assert st["taken"] == 300 and st["generated"] >= 300 and st["waits"] >= 1
+    # a paced consumer (1 ms between takes, like sporadic handshakes) never waits for the GPU:
+    # each 64-key refill completes long before the ring's ready half is used up
+    w0 = st["waits"]
+    for _ in range(200):
+        time.sleep(0.001)
+        pool.take()
+    assert pool.stats()["waits"] == w0
+    pool.close()
+
+
+def test_key_pool_arguments():
+    with pytest.raises(S.SntrupError):
+        S.KeyPool(761, seed=1, capacity=100, batch_keys=64)      # not a multiple of the batch
+    with pytest.raises(S.SntrupError):
+        S.KeyPool(700, seed=1, capacity=128, batch_keys=64)      # unknown parameter set
+
+
 # --------------------------------------------------------------------------------- ring ops
 def edge_cases(p, p8, q):
     qh = (q - 1) // 2
