@@ -47,8 +47,8 @@ def parse():
     return ap.parse_args()
 
 
-DEFAULT_B = 512
-DEFAULT_CHUNK = 65536
+DEFAULT_B = 1024
+DEFAULT_CHUNK = 32768      # two pipelined lanes (measured best with B = 1024; sweeps in the line)
 MUL_IMPL = "tc"          # ring products on the tensor cores (see --mul-impl)
 TRAFFIC = {}             # dram bytes per launch of the dominant kernel, from profiles/ (ncu)
 
@@ -442,7 +442,7 @@ def main():
     if not args.no_extras and rank == 0:
         # Montgomery batch-size sweep (configs[1])
         sweep = {}
-        for b in (32, 128, 512, 2048):
+        for b in (32, 128, 512, 1024, 2048):
             step(b)
             sweep[str(b)] = n * 3 / (timed(lambda: step(b), 3) / 1e3)
         result["batch_size_sweep_keys_per_s"] = sweep

@@ -126,8 +126,8 @@ def test_cfg2_full_size_sampled(O):
     # BASELINE configs[1]: 65,536 keys, seed 2, in the launch configuration bench.py times;
     # compared on a sample the oracle computes one by one: first and last trees, every 97th key.
     n = 65536
-    for B in (32, 128, 512, 2048):
-        res = S.batch_keygen(761, n, 2, batch_size=B)
+    for B, chunk in ((32, 0), (128, 0), (512, 0), (2048, 0), (1024, 32768)):   # last: bench.py's config
+        res = S.batch_keygen(761, n, 2, batch_size=B, chunk_keys=chunk)
         torch.cuda.synchronize()
         idx = np.unique(np.concatenate([np.arange(0, 128), np.arange(n - 128, n), np.arange(0, n, 97)]))
         check_keys(O, 761, 2, res, idx)
