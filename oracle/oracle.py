@@ -74,6 +74,10 @@ def lib():
         L.or_keygen_many.restype = i32
         L.or_keygen_many.argtypes = [i32, i32, i32, u64, vp, u64, i32, vp, sz, vp, sz,
                                      vp, vp, vp, vp, sz, vp]
+        L.or_encap_core.restype = None
+        L.or_encap_core.argtypes = [i32, i32, vp, vp, vp]
+        L.or_decap_core.restype = i32
+        L.or_decap_core.argtypes = [i32, i32, i32, vp, vp, vp, vp]
         L.or_mul_many.restype = None
         L.or_mul_many.argtypes = [i32, i64, u64, vp, vp, vp, sz, i32]
         _lib = L
@@ -134,6 +138,26 @@ def mul_many(p: int, m: int, a: np.ndarray, b: np.ndarray, threads: int = 0) -> 
     c = np.zeros_like(a)
     lib().or_mul_many(p, m, n, _p(a), _p(b), _p(c), row, threads or (os.cpu_count() or 1))
     return c
+
+
+# ----------------------------------------------------------------------------- encap / decap core
+def encap_core(p: int, q: int, h, r) -> np.ndarray:
+    """c = Round(h * r) in R/q (SPEC encrypt_core): int16 [p], every coefficient = 0 mod 3."""
+    H = np.ascontiguousarray(np.asarray(h, dtype=np.int16)[:p])
+    R = np.ascontiguousarray(np.asarray(r, dtype=np.int8)[:p])
+    C = np.zeros(p, dtype=np.int16)
+    lib().or_encap_core(p, q, _p(H), _p(R), _p(C))
+    return C
+
+
+def decap_core(p: int, q: int, w: int, f, ginv, c):
+    """(ok, r') with r' = ((3f * c) mod 3) * (1/g) in R/3 and ok = weight(r') == w."""
+    F = np.ascontiguousarray(np.asarray(f, dtype=np.int8)[:p])
+    G = np.ascontiguousarray(np.asarray(ginv, dtype=np.int8)[:p])
+    C = np.ascontiguousarray(np.asarray(c, dtype=np.int16)[:p])
+    R = np.zeros(p, dtype=np.int8)
+    ok = lib().or_decap_core(p, q, w, _p(F), _p(G), _p(C), _p(R))
+    return bool(ok), R
 
 
 # ----------------------------------------------------------------------------- encodings (C10-C11)

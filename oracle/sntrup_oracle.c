@@ -468,3 +468,43 @@ void or_mul_many(int p, int64_t m, uint64_t n, const int16_t *a, const int16_t *
     for (int t = 0; t < n_threads; t++) pthread_join(th[t], NULL);
     free(th);
 }
+
+/* ------------------------------------------------------------------------------------------ */
+/* Encapsulation / decapsulation core (SPEC.md encrypt_core /    */
+/* decrypt_core, S:405-422 -- the paper only benchmarks enc/dec, Table 1, and names the */
+/* key shape (h, (f, 1/g)) of section 3.1).  Plain definitions, one key at a time.  */
+/*   encap: c = Round(h * r) in R/q, Round = each centered coefficient x to the nearest multiple   */
+/*          of 3, x - (x mods 3) (unique: x is within 1 of exactly one multiple of 3; stays in   */
+/*          range because (q-1)/2 = 0 mod 3 for every set, C1).                                 */
+/*   decap: e = 3 f * c in R/q (centered); e3 = e mod 3 lifted to {-1,0,1}; r' = e3 * (1/g) in    */
+/*          R/3; valid iff weight(r') = w.                                                        */
+/* ------------------------------------------------------------------------------------------ */
+void or_encap_core(int p, int q, const int16_t *h, const int8_t *r, int16_t *c)
+{
+    int64_t *H = calloc((size_t)p, sizeof(int64_t)), *R = calloc((size_t)p, sizeof(int64_t));
+    int64_t *X = calloc((size_t)p, sizeof(int64_t));
+    for (int i = 0; i < p; i++) { H[i] = h[i]; R[i] = r[i]; }
+    or_poly_mul(p, q, H, R, X);
+    for (int i = 0; i < p; i++) {
+        const int64_t x = X[i];                     /* centered in [-(q-1)/2, (q-1)/2] */
+        const int64_t m3 = mod_center(x, 3);        /* x - m3 is the nearest multiple of 3 */
+        c[i] = (int16_t)(x - m3);
+    }
+    free(H); free(R); free(X);
+}
+
+int or_decap_core(int p, int q, int w, const int8_t *f, const int8_t *ginv, const int16_t *c,
+                  int8_t *r_out)
+{
+    int64_t *F3 = calloc((size_t)p, sizeof(int64_t)), *C = calloc((size_t)p, sizeof(int64_t));
+    int64_t *E = calloc((size_t)p, sizeof(int64_t)), *G = calloc((size_t)p, sizeof(int64_t));
+    int64_t *R = calloc((size_t)p, sizeof(int64_t));
+    for (int i = 0; i < p; i++) { F3[i] = 3 * (int64_t)f[i]; C[i] = c[i]; G[i] = ginv[i]; }
+    or_poly_mul(p, q, F3, C, E);                    /* e = 3f * c in R/q, centered */
+    for (int i = 0; i < p; i++) E[i] = mod_center(E[i], 3);
+    or_poly_mul(p, 3, E, G, R);                     /* r' = e3 * (1/g) in R/3 */
+    int weight = 0;
+    for (int i = 0; i < p; i++) { r_out[i] = (int8_t)R[i]; weight += R[i] != 0; }
+    free(F3); free(C); free(E); free(G); free(R);
+    return weight == w;
+}
