@@ -69,7 +69,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.idx), "--query-gpu=" + ",".join(self.FIELDS),
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "25"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thr = threading.Thread(target=self._read, daemon=True)
             self.thr.start()
@@ -223,6 +223,32 @@ def other_configs(S, torch, timed):
     out["configs[4]"] = {"workload": "sntrup1277, 2^20 keys, seed 5, B = 1024, 65,536-key chunks",
                          "keys_per_s": n / (ms / 1e3), "ms": ms}
     del pk, sk
+    # KEM core: 65,536 encapsulations (r from the encapsulation stream
+    # domain + c = Round(h r)) and decapsulations (r' = ((3f c) mod 3)/g + weight check)
+    n = 65536
+    keys = S.batch_keygen(761, n, 2, batch_size=1024, debug=True)
+    r = torch.empty((n, S.params(761)["p16"]), dtype=torch.int8, device="cuda")
+    c = torch.empty_like(keys["h"])
+    r2 = torch.empty_like(r)
+    okb = torch.empty(n, dtype=torch.uint8, device="cuda")
+
+    def enc():
+        S.sample_short_batch(761, n, 2, 0, out=r)
+        S.encap_core_batch(761, keys["h"], r, c)
+
+    def dec():
+        S.decap_core_batch(761, keys["f"], keys["ginv"], c, r2, okb)
+
+    enc(); dec()
+    torch.cuda.synchronize()
+    assert bool(okb.all()) and torch.equal(r, r2), "KEM core round trip failed"
+    enc_ms = timed(enc, 3) / 3
+    dec_ms = timed(dec, 3) / 3
+    out["kem_core"] = {"workload": "sntrup761, 65,536 keys of configs[1]: encapsulation core (Short r from "
+                                   "the stream + Round(h r)) and decapsulation core (+ weight check)",
+                       "encaps_per_s": n / (enc_ms / 1e3), "decaps_per_s": n / (dec_ms / 1e3),
+                       "paper_context_cycles": {"enc": 46914, "dec": 56241, "hardware": "Haswell, Table 1 P:864-876"}}
+    del keys, r, c, r2, okb
     # key pool (the paper's engNTRU batch_lib provider: "first key 2.5 ms, then
     # 0 ms"): first take (lazy fill), then paced takes served from the pinned ring
     pool = S.KeyPool(761, seed=9, capacity=1 << 15, batch_keys=1 << 13, batch_size=512)
@@ -335,16 +361,17 @@ def main():
             ms = float(t.item())
         return ms
 
+    # clocks are sampled from the warm-up through the timed, profiled and e2e steps (all under
+    # load; the timed region alone can be shorter than nvidia-smi's first sample)
+    clk = ClockSampler(local)
+    clk.start()
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
 
     # ---- headline: K timed steps
     launches0 = S.kernel_launch_count()
-    clk = ClockSampler(local)
-    clk.start()
     ms = timed(step, args.steps)
-    clocks = clk.stop()
     launches = S.kernel_launch_count() - launches0
     value = world * n * args.steps / (ms / 1e3)
 
@@ -374,6 +401,7 @@ def main():
         e2e_by_chunk[chunk] = world * n * e2e_steps / (ms_c / 1e3)
     best_chunk = max(e2e_by_chunk, key=e2e_by_chunk.get)
     e2e_value = e2e_by_chunk[best_chunk]
+    clocks = clk.stop()
 
     result = {}
     if rank == 0:

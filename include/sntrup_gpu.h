@@ -116,6 +116,28 @@ int rq_mul_small_batch(int param_set, uint64_t n, const int16_t *a, const int8_t
 int r3_mul_batch(int param_set, uint64_t n, const int8_t *a, const int8_t *b, int8_t *c,
                  void *stream);
 
+/* ---- Encapsulation / decapsulation core.  The paper benchmarks
+   enc/dec (Table 1) for keys of shape (h, (f, 1/g)) but does not spell
+   them out; the core follows Streamlined NTRU Prime as SPEC.md's encrypt_core/decrypt_core
+   (S:405-422).  Hashing / ciphertext encoding (the KEM wrapper) are out of scope. */
+
+/* r_out[i] = Short element (weight w) from stream domain `domain` of global key index
+   first_key_index + i (C2-C4; domains >= 2^32 are reserved for encapsulation).
+   int8 [n][p16].  Stream-ordered. */
+int sntrup_sample_short_batch(int param_set, uint64_t n, uint64_t seed, uint64_t first_key_index,
+                              uint64_t domain, int8_t *r_out, void *stream);
+
+/* c[i] = Round(h[i] * r[i]) in R/q: each centered coefficient to the nearest multiple of 3.
+   h, c int16 [n][p8] centered; r int8 [n][p16] (weight w).  Stream-ordered. */
+int sntrup_encap_core_batch(int param_set, uint64_t n, const int16_t *h, const int8_t *r, int16_t *c,
+                            void *stream);
+
+/* r_out[i] = ((3 f[i] * c[i] in R/q) mod 3) * ginv[i] in R/3, ok[i] = (weight(r_out[i]) == w).
+   f, ginv, r_out int8 [n][p16]; c int16 [n][p8]; ok uint8 [n].  Uses the stream's workspace.
+   Stream-ordered. */
+int sntrup_decap_core_batch(int param_set, uint64_t n, const int8_t *f, const int8_t *ginv,
+                            const int16_t *c, int8_t *r_out, uint8_t *ok, void *stream);
+
 /* out[i] = 1/a[i] in R/q (batchInv) using product trees of batch_size leaves
    (0 -> 32), one constant-time divstep inversion per tree.  a, out: int16 [n][p8].
    If some a[i] == 0: returns SNTRUP_E_NOT_INVERTIBLE, *bad_index (host pointer, may be NULL)

@@ -75,6 +75,9 @@ _lib.sntrup_pool_stats.argtypes = [_vp] + [ctypes.POINTER(ctypes.c_uint64)] * 4
 _lib.sntrup_pool_destroy.argtypes = [_vp]
 _lib.sntrup_pool_destroy.restype = None
 _lib.rq_mul_small_batch.argtypes = [_i32, _u64, _vp, _vp, _vp, _vp]
+_lib.sntrup_sample_short_batch.argtypes = [_i32, _u64, _u64, _u64, _u64, _vp, _vp]
+_lib.sntrup_encap_core_batch.argtypes = [_i32, _u64, _vp, _vp, _vp, _vp]
+_lib.sntrup_decap_core_batch.argtypes = [_i32, _u64, _vp, _vp, _vp, _vp, _vp, _vp]
 
 EXPORTED = ("sntrup_params", "sntrup_strerror", "sntrup_batch_keygen", "sntrup_batch_keygen_ex",
             "sntrup_keygen_workspace_bytes", "rq_mul_batch", "rq_mul_small_batch", "r3_mul_batch", "rq_recip_batch",
@@ -82,6 +85,7 @@ EXPORTED = ("sntrup_params", "sntrup_strerror", "sntrup_batch_keygen", "sntrup_b
             "sntrup_release_workspace", "sntrup_kernel_launch_count", "sntrup_set_mul_impl",
             "sntrup_profile_enable", "sntrup_profile_read_kinds", "sntrup_pool_create",
             "sntrup_pool_take", "sntrup_pool_stats", "sntrup_pool_destroy",
+            "sntrup_sample_short_batch", "sntrup_encap_core_batch", "sntrup_decap_core_batch",
             "sntrup_profile_read")
 
 PROFILE_CLASSES = ("sample", "r3_mul", "rq_mul", "root_inv", "rq_inv", "repair", "encode", "other")
@@ -181,6 +185,50 @@ def rq_mul_small_batch(param_set: int, a, b, c=None, stream=None):
     _check(_lib.rq_mul_small_batch(param_set, n, _ptr(a), _ptr(b), _ptr(c), _stream(stream)),
            "rq_mul_small_batch")
     return c
+
+
+ENC_DOMAIN = 1 << 32      # C2: stream domains >= 2^32 are reserved for encapsulation draws
+
+
+def sample_short_batch(param_set: int, n: int, seed: int, first_key_index: int = 0,
+                       domain: int = ENC_DOMAIN, out=None, stream=None):
+    """Short elements (weight w) of one stream domain for global key indices first.. (int8 rows)."""
+    P = params(param_set)
+    if out is None:
+        out = torch.empty((n, P["p16"]), dtype=torch.int8, device="cuda")
+    _need(out, torch.int8, (n, P["p16"]), "out")
+    _check(_lib.sntrup_sample_short_batch(param_set, n, seed, first_key_index, domain, _ptr(out),
+                                          _stream(stream)), "sntrup_sample_short_batch")
+    return out
+
+
+def encap_core_batch(param_set: int, h, r, c=None, stream=None):
+    """c = Round(h * r) in R/q (each coefficient to the nearest multiple of 3)."""
+    P = params(param_set)
+    n = h.shape[0]
+    _need(h, torch.int16, (n, P["p8"]), "h")
+    _need(r, torch.int8, (n, P["p16"]), "r")
+    if c is None:
+        c = torch.empty_like(h)
+    _check(_lib.sntrup_encap_core_batch(param_set, n, _ptr(h), _ptr(r), _ptr(c), _stream(stream)),
+           "sntrup_encap_core_batch")
+    return c
+
+
+def decap_core_batch(param_set: int, f, ginv, c, r_out=None, ok=None, stream=None):
+    """(r', ok): r' = ((3f * c) mod 3) * (1/g) in R/3, ok = weight(r') == w."""
+    P = params(param_set)
+    n = c.shape[0]
+    _need(f, torch.int8, (n, P["p16"]), "f")
+    _need(ginv, torch.int8, (n, P["p16"]), "ginv")
+    _need(c, torch.int16, (n, P["p8"]), "c")
+    if r_out is None:
+        r_out = torch.empty_like(f)
+    if ok is None:
+        ok = torch.empty(n, dtype=torch.uint8, device=c.device)
+    _check(_lib.sntrup_decap_core_batch(param_set, n, _ptr(f), _ptr(ginv), _ptr(c), _ptr(r_out), _ptr(ok),
+                                        _stream(stream)), "sntrup_decap_core_batch")
+    return r_out, ok
 
 
 def r3_mul_batch(param_set: int, a, b, c=None, stream=None):

@@ -102,16 +102,21 @@ __host__ __device__ constexpr int inv_mod_const(int a) {   // a^(M-2) mod M, a i
 
 // Row descriptor: element (i, k) at ptr + i*stride + k, elements of `bytes` bytes (1 or 2),
 // multiplied by `scale` on load.  A NULL ptr means the unit polynomial 1.
+// mod3 != 0: each loaded coefficient is reduced to its centered representative mod 3 (an R/q
+// element read as an R/3 element, e.g. decapsulation's e mod 3).
 struct RowDesc {
     const void *ptr;
     long long stride;   // elements
     int bytes;          // 1 (int8) or 2 (int16)
     int scale;
+    int mod3;
 };
 
 __device__ __forceinline__ int load_coef(const RowDesc &d, long long row, int k) {
-    if (d.bytes == 1) return d.scale * (int)((const int8_t *)d.ptr)[row * d.stride + k];
-    return d.scale * (int)((const int16_t *)d.ptr)[row * d.stride + k];
+    int v;
+    if (d.bytes == 1) v = d.scale * (int)((const int8_t *)d.ptr)[row * d.stride + k];
+    else v = d.scale * (int)((const int16_t *)d.ptr)[row * d.stride + k];
+    return d.mod3 ? canon<3>(v) : v;
 }
 
 }  // namespace sntrup

@@ -32,6 +32,7 @@ struct MulArgs {
     int out_bytes;          // 1 or 2
     int periodic;           // both operands full-size -> lazy reductions inside the tile loop
     int swap;               // tensor-core path: the second operand takes the A (Hankel) role
+    int round3;             // post-op: each output coefficient to the nearest multiple of 3
 };
 
 template <int NP>
@@ -142,6 +143,7 @@ __global__ void __launch_bounds__((PS::P8 / 8 + 31) / 32 * 32) ring_mul_kernel(M
             if (k < PS::P) {
                 v = sm.raw[k] + sm.raw[k + PS::P] + (k >= 1 ? sm.raw[k + PS::P - 1] : 0);
                 v = canon<M>(v);
+                if (a.round3) v -= canon<3>(v);
             }
             if (a.out_bytes == 2) ((int16_t *)a.out)[prod * a.out_stride + k] = (int16_t)v;
             else ((int8_t *)a.out)[prod * a.out_stride + k] = (int8_t)v;

@@ -70,9 +70,9 @@ __device__ __forceinline__ void warp_bitonic_sort(uint32_t (&v)[E], int lane) {
 
 // C4: Short f for key root K (domain d = 0).  Writes the int8 row f[0..P16).
 template <class PS>
-__device__ __forceinline__ void sample_short_warp(uint64_t K, int8_t *frow, int lane) {
+__device__ __forceinline__ void sample_short_warp(uint64_t K, int8_t *frow, int lane, uint64_t domain = 0) {
     constexpr int E = PS::NSORT / 32;
-    const uint64_t D = sm_at(K, 0);
+    const uint64_t D = sm_at(K, domain);
     uint32_t v[E];
 #pragma unroll
     for (int t = 0; t < E / 2; t++) {
@@ -274,6 +274,36 @@ __global__ void __launch_bounds__(128) sample_kernel(SampleArgs a) {
         if (32 * b < PS::P16) store_block_int8<PS>(grow, b, pl[s], mi[s]);
     }
     if (lane == 0 && a.attempts) a.attempts[key_local] = (uint8_t)(attempt + 1);
+}
+
+// Short elements of an arbitrary stream domain (C2: domain 0 = f; domains >= 2^32 reserved for
+// encapsulation draws), one warp per global key index.
+template <class PS>
+__global__ void __launch_bounds__(128) short_kernel(uint64_t seed, uint64_t first, uint64_t n,
+                                                    uint64_t domain, int8_t *out) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t row = (uint64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+    if (row >= n) return;
+    sample_short_warp<PS>(sm_at(seed, first + row), out + row * PS::P16, lane, domain);
+}
+
+// ok[row] = (number of nonzero coefficients of row == W) (decapsulation's weight check)
+template <class PS>
+__global__ void __launch_bounds__(128) weight_check_kernel(const int8_t *r, uint64_t n, uint8_t *ok) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t row = (uint64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+    if (row >= n) return;
+    const uint4 *rr = reinterpret_cast<const uint4 *>(r + row * PS::P16);
+    int cnt = 0;
+    for (int c = lane; c < PS::P16 / 16; c += 32) {
+        const uint4 q = rr[c];
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int i = 0; i < 4; i++) cnt += __popc(w[i] & 0x01010101u);   // nonzero trit <=> odd byte
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) cnt += __shfl_xor_sync(FULL, cnt, off);
+    if (lane == 0) ok[row] = cnt == PS::W ? 1 : 0;
 }
 
 }  // namespace sntrup

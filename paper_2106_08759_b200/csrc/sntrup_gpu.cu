@@ -403,10 +403,10 @@ DevInfo &dev_info() {
     return d;
 }
 
-template <class PS, int M, int LA, int LB, int NPR = 1, int MM = 128>
-int launch_tc(const MulArgs &a, cudaStream_t s) {
+template <class PS, int M, int LA, int LB, int NPR = 1, int MM = 128, bool XOPS = false>
+int launch_tc_impl(const MulArgs &a, cudaStream_t s) {
     using G = TcGeom<PS, LA, LB, NPR, MM>;
-    auto kern = tc_mul_kernel<PS, M, LA, LB, NPR, MM>;
+    auto kern = tc_mul_kernel<PS, M, LA, LB, NPR, MM, XOPS>;
     static std::map<int, int> per_sm;                 // device -> resident CTAs per SM
     int dev = 0;
     CK(cudaGetDevice(&dev));
@@ -430,10 +430,19 @@ int launch_tc(const MulArgs &a, cudaStream_t s) {
     return SNTRUP_OK;
 }
 
-template <class PS, int M, int LB, int NPR = 1>
-int launch_tc4(const MulArgs &a, cudaStream_t s) {
+// KEM-core pre/post-ops need the XOPS instantiation (keygen never sets them)
+bool mul_xops(const MulArgs &a) { return a.round3 || a.X.mod3 || a.Y.mod3; }
+
+template <class PS, int M, int LA, int LB, int NPR = 1, int MM = 128>
+int launch_tc(const MulArgs &a, cudaStream_t s) {
+    return mul_xops(a) ? launch_tc_impl<PS, M, LA, LB, NPR, MM, true>(a, s)
+                       : launch_tc_impl<PS, M, LA, LB, NPR, MM, false>(a, s);
+}
+
+template <class PS, int M, int LB, int NPR = 1, bool XOPS = false>
+int launch_tc4_impl(const MulArgs &a, cudaStream_t s) {
     using G = Tc4Geom<PS, LB, NPR>;
-    auto kern = tc4_mul_kernel<PS, M, LB, NPR>;
+    auto kern = tc4_mul_kernel<PS, M, LB, NPR, XOPS>;
     static std::map<int, int> per_sm;
     int dev = 0;
     CK(cudaGetDevice(&dev));
@@ -455,6 +464,12 @@ int launch_tc4(const MulArgs &a, cudaStream_t s) {
     kern<<<(unsigned)grid, 128, G::SMEM, s>>>(a);
     LAUNCHED();
     return SNTRUP_OK;
+}
+
+template <class PS, int M, int LB, int NPR = 1>
+int launch_tc4(const MulArgs &a, cudaStream_t s) {
+    return mul_xops(a) ? launch_tc4_impl<PS, M, LB, NPR, true>(a, s)
+                       : launch_tc4_impl<PS, M, LB, NPR, false>(a, s);
 }
 
 // la / lb: int8 limbs of the first / second operand (1 = small: R/3, 3f, g; 2 = R/q element).
@@ -1173,6 +1188,75 @@ int rq_mul_small_batch(int param_set, uint64_t n, const int16_t *a, const int8_t
     m.out_bytes = 2;
     m.periodic = 0;
     SNTRUP_DISPATCH(param_set, return launch_mul<PS, PS::Q>(m, (cudaStream_t)stream, 2, 1));
+    return SNTRUP_E_PARAM;
+}
+
+int sntrup_sample_short_batch(int param_set, uint64_t n, uint64_t seed, uint64_t first_key_index,
+                              uint64_t domain, int8_t *r_out, void *stream) {
+    ParamInfo pi;
+    if (!param_info(param_set, &pi)) return SNTRUP_E_PARAM;
+    if (n == 0 || !r_out) return SNTRUP_E_ARG;
+    SNTRUP_DISPATCH(param_set, {
+        short_kernel<PS><<<(unsigned)((n + 3) / 4), 128, 0, (cudaStream_t)stream>>>(seed, first_key_index, n,
+                                                                                    domain, r_out);
+        LAUNCHED();
+        return SNTRUP_OK;
+    });
+    return SNTRUP_E_PARAM;
+}
+
+int sntrup_encap_core_batch(int param_set, uint64_t n, const int16_t *h, const int8_t *r, int16_t *c,
+                            void *stream) {
+    ParamInfo pi;
+    if (!param_info(param_set, &pi)) return SNTRUP_E_PARAM;
+    if (n == 0 || !h || !r || !c) return SNTRUP_E_ARG;
+    std::lock_guard<std::mutex> lk(g_mu);
+    MulArgs m{};
+    m.mode = MUL_ZIP;
+    m.n_out = (long long)n;
+    m.X = RowDesc{h, pi.p8, 2, 1};
+    m.Y = RowDesc{r, pi.p16, 1, 1};
+    m.out = c;
+    m.out_stride = pi.p8;
+    m.out_bytes = 2;
+    m.round3 = 1;                                   // c = Round(h * r)
+    SNTRUP_DISPATCH(param_set, return launch_mul<PS, PS::Q>(m, (cudaStream_t)stream, 2, 1));
+    return SNTRUP_E_PARAM;
+}
+
+int sntrup_decap_core_batch(int param_set, uint64_t n, const int8_t *f, const int8_t *ginv,
+                            const int16_t *c, int8_t *r_out, uint8_t *ok, void *stream) {
+    ParamInfo pi;
+    if (!param_info(param_set, &pi)) return SNTRUP_E_PARAM;
+    if (n == 0 || !f || !ginv || !c || !r_out || !ok) return SNTRUP_E_ARG;
+    std::lock_guard<std::mutex> lk(g_mu);
+    cudaStream_t s = (cudaStream_t)stream;
+    int rc;
+    if ((rc = ws_reserve(align256(n * pi.p8 * 2) + 4096, s))) return rc;
+    int16_t *e = ws_take<int16_t>(n * pi.p8);
+    SNTRUP_DISPATCH(param_set, {
+        MulArgs m{};                                 // e = 3f * c in R/q
+        m.mode = MUL_ZIP;
+        m.n_out = (long long)n;
+        m.X = RowDesc{c, pi.p8, 2, 1};
+        m.Y = RowDesc{f, pi.p16, 1, 3};
+        m.out = e;
+        m.out_stride = pi.p8;
+        m.out_bytes = 2;
+        if ((rc = launch_mul<PS, PS::Q>(m, s, 2, 1))) return rc;
+        MulArgs m3{};                                // r' = (e mod 3) * (1/g) in R/3
+        m3.mode = MUL_ZIP;
+        m3.n_out = (long long)n;
+        m3.X = RowDesc{e, pi.p8, 2, 1, 1};
+        m3.Y = RowDesc{ginv, pi.p16, 1, 1};
+        m3.out = r_out;
+        m3.out_stride = pi.p16;
+        m3.out_bytes = 1;
+        if ((rc = launch_mul<PS, 3>(m3, s, 1, 1))) return rc;
+        weight_check_kernel<PS><<<(unsigned)((n + 3) / 4), 128, 0, s>>>(r_out, n, ok);
+        LAUNCHED();
+        return SNTRUP_OK;
+    });
     return SNTRUP_E_PARAM;
 }
 

@@ -100,7 +100,7 @@ __device__ __forceinline__ void umma_mxf4(uint32_t tmem_d, uint64_t adesc, uint6
 }
 
 // M = modulus; A = one digit (the small operand); LB digits for the B operand; NPR products per A.
-template <class PS, int M, int LB, int NPR>
+template <class PS, int M, int LB, int NPR, bool XOPS = false>
 __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
     using G = Tc4Geom<PS, LB, NPR>;
     constexpr int P = PS::P;
@@ -187,11 +187,11 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
             const int c = tid + 128 * h;
             if (c < G::NCHK) {
                 uint32_t word = 0;
-                if (w.du.bytes == 1 && !w.unit_u) {
+                if (w.du.bytes == 1 && !w.unit_u && !(XOPS && w.du.mod3)) {
                     word = e2m1_pack8_int8(pu[h].x, pu[h].y, w.du.scale);
                 } else {
                     int uv8[8];
-                    decode_chunk(pu[h], w.du.bytes, w.du.scale, w.unit_u, c, uv8);
+                    decode_chunk(pu[h], w.du.bytes, w.du.scale, w.unit_u, c, uv8, XOPS ? w.du.mod3 : 0);
 #pragma unroll
                     for (int i = 0; i < 8; i++) word |= e2m1_code(uv8[i]) << (4 * i);
                 }
@@ -199,12 +199,12 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
 #pragma unroll
                 for (int pp = 0; pp < NPR; pp++) {
                     uint32_t dw[LB];
-                    if (LB == 1 && w.dv[pp].bytes == 1 && !w.unit_v[pp]) {
+                    if (LB == 1 && w.dv[pp].bytes == 1 && !w.unit_v[pp] && !(XOPS && w.dv[pp].mod3)) {
                         // reversed: coefficient 8c + i -> nibble 7 - i of word 16 NL - 1 - c
                         dw[0] = nibble_reverse(e2m1_pack8_int8(pv[pp][h].x, pv[pp][h].y, w.dv[pp].scale));
                     } else {
                         int vv8[8];
-                        decode_chunk(pv[pp][h], w.dv[pp].bytes, w.dv[pp].scale, w.unit_v[pp], c, vv8);
+                        decode_chunk(pv[pp][h], w.dv[pp].bytes, w.dv[pp].scale, w.unit_v[pp], c, vv8, XOPS ? w.dv[pp].mod3 : 0);
 #pragma unroll
                         for (int l = 0; l < LB; l++) dw[l] = 0;
 #pragma unroll
@@ -321,7 +321,8 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
             for (int i = 0; i < FI; i++) {
                 const int k = tid + 128 * i;
                 if (k >= ostride_elems) break;
-                const int v = k < P ? canon<M>(fa[i] + fb[i] + fc[i]) : 0;
+                int v = k < P ? canon<M>(fa[i] + fb[i] + fc[i]) : 0;
+                if (XOPS && a.round3) v -= canon<3>(v);      // encapsulation's Round
                 if (a.out_bytes == 2) ((int16_t *)a.out)[orow * a.out_stride + k] = (int16_t)v;
                 else ((int8_t *)a.out)[orow * a.out_stride + k] = (int8_t)v;
             }

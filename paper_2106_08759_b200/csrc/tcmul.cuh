@@ -168,7 +168,8 @@ __device__ __forceinline__ uint4 load_chunk(const RowDesc &d, long long row, int
     return make_uint4(v.x, v.y, 0, 0);
 }
 
-__device__ __forceinline__ void decode_chunk(const uint4 r, int bytes, int scale, bool unit, int c, int (&v)[8]) {
+__device__ __forceinline__ void decode_chunk(const uint4 r, int bytes, int scale, bool unit, int c, int (&v)[8],
+                                             int mod3 = 0) {
     if (bytes == 2) {
         const uint32_t w[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
@@ -177,6 +178,10 @@ __device__ __forceinline__ void decode_chunk(const uint4 r, int bytes, int scale
         const uint32_t w[2] = {r.x, r.y};
 #pragma unroll
         for (int i = 0; i < 8; i++) v[i] = scale * (int)(int8_t)(w[i >> 2] >> (8 * (i & 3)));
+    }
+    if (mod3) {
+#pragma unroll
+        for (int i = 0; i < 8; i++) v[i] = canon<3>(v[i]);
     }
     if (unit) {
 #pragma unroll
@@ -241,7 +246,9 @@ __device__ __forceinline__ void tc_work(const MulArgs &a, long long it, TcWork<N
 // M = modulus (3 or q); LA / LB = limbs of the A-role / B-role operand; NPR products per A;
 // MM = MMA M (output coefficients per block).  With MM = 64 each MMA reads half the A bytes and
 // the accumulator row r lives in TMEM lane 32(r/16) + r%16 (probed: scripts/probe/tmem_m64_probe.cu).
-template <class PS, int M, int LA, int LB, int NPR, int MM = 128>
+// XOPS: honour the operand pre-op (RowDesc.mod3) and the output post-op (MulArgs.round3) of the
+// KEM core; compiled out of the keygen instantiations.
+template <class PS, int M, int LA, int LB, int NPR, int MM = 128, bool XOPS = false>
 __global__ void __launch_bounds__(128) tc_mul_kernel(MulArgs a) {
     using G = TcGeom<PS, LA, LB, NPR, MM>;
     constexpr int P = PS::P;
@@ -323,7 +330,7 @@ __global__ void __launch_bounds__(128) tc_mul_kernel(MulArgs a) {
             const int c = tid + 128 * h;
             if (c < G::NCHK) {
                 int uv8[8];
-                decode_chunk(pu[h], w.du.bytes, w.du.scale, w.unit_u, c, uv8);
+                decode_chunk(pu[h], w.du.bytes, w.du.scale, w.unit_u, c, uv8, XOPS ? w.du.mod3 : 0);
 #pragma unroll
                 for (int l = 0; l < LA; l++) {
                     int x[8];
@@ -335,7 +342,7 @@ __global__ void __launch_bounds__(128) tc_mul_kernel(MulArgs a) {
 #pragma unroll
                 for (int pp = 0; pp < NPR; pp++) {
                     int vv8[8];
-                    decode_chunk(pv[pp][h], w.dv[pp].bytes, w.dv[pp].scale, w.unit_v[pp], c, vv8);
+                    decode_chunk(pv[pp][h], w.dv[pp].bytes, w.dv[pp].scale, w.unit_v[pp], c, vv8, XOPS ? w.dv[pp].mod3 : 0);
 #pragma unroll
                     for (int l = 0; l < LB; l++) {
                         int x[8];
@@ -461,7 +468,8 @@ __global__ void __launch_bounds__(128) tc_mul_kernel(MulArgs a) {
             for (int i = 0; i < FI; i++) {
                 const int k = tid + 128 * i;
                 if (k >= ostride_elems) break;
-                const int v = k < P ? canon<M>(fa[i] + fb[i] + fc[i]) : 0;
+                int v = k < P ? canon<M>(fa[i] + fb[i] + fc[i]) : 0;
+                if (XOPS && a.round3) v -= canon<3>(v);      // encapsulation's Round
                 if (a.out_bytes == 2) ((int16_t *)a.out)[orow * a.out_stride + k] = (int16_t)v;
                 else ((int8_t *)a.out)[orow * a.out_stride + k] = (int8_t)v;
             }

@@ -181,6 +181,39 @@ def test_cfg5_full_size_sampled(O):
     check_keys(O, 1277, 5, res, idx)
 
 
+# --------------------------------------------------------------------------------- KEM core
+@pytest.mark.parametrize("param", PSETS)
+def test_kem_core_parity_and_roundtrip(O, param, mul_impl):
+    # r from the encapsulation stream domain, c = Round(h r), decap recovers r;
+    # every output byte against the oracle (encap_core / decap_core / short_from_words)
+    P = S.params(param)
+    p, q, w = P["p"], P["q"], P["w"]
+    n, seed = 40, 23
+    keys = S.batch_keygen(param, n, seed, batch_size=8, debug=True)
+    r = S.sample_short_batch(param, n, seed, first_key_index=0)
+    c = S.encap_core_batch(param, keys["h"], r)
+    r2, ok = S.decap_core_batch(param, keys["f"], keys["ginv"], c)
+    # a tampered ciphertext row and an all-zero one
+    ct = c.clone()
+    ct[1, 5] += 3
+    ct[2] = 0
+    r3, ok3 = S.decap_core_batch(param, keys["f"], keys["ginv"], ct)
+    torch.cuda.synchronize()
+    h, f, gi = keys["h"].cpu().numpy(), keys["f"].cpu().numpy(), keys["ginv"].cpu().numpy()
+    rr, cc, rr2 = r.cpu().numpy(), c.cpu().numpy(), r2.cpu().numpy()
+    for i in range(n):
+        ref_r = O.short_from_words(p, w, O.stream_words(seed, i, S.ENC_DOMAIN, p))
+        assert np.array_equal(rr[i, :p], ref_r) and not rr[i, p:].any()
+        ref_c = O.encap_core(p, q, h[i, :p], ref_r)
+        assert np.array_equal(cc[i, :p], ref_c) and not cc[i, p:].any()
+        assert ok[i] == 1 and np.array_equal(rr2[i, :p], ref_r) and not rr2[i, p:].any()
+    ctn, r3n, ok3n = ct.cpu().numpy(), r3.cpu().numpy(), ok3.cpu().numpy()
+    for i in (1, 2):
+        ref_ok, ref_r3 = O.decap_core(p, q, w, f[i, :p], gi[i, :p], ctn[i, :p])
+        assert bool(ok3n[i]) == ref_ok and np.array_equal(r3n[i, :p], ref_r3)
+    assert ok3n[2] == 0
+
+
 # --------------------------------------------------------------------------------- key pool
 def test_key_pool_hands_out_oracle_keys_in_order(O):
     # engNTRU batch_lib analogue: consecutive global key indices from first_key_index,
