@@ -42,13 +42,16 @@ def parse():
                     "two or more chunks run on two pipelined streams")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-extras", action="store_true", help="skip B sweep / rq_mul / cpu baseline")
+    ap.add_argument("--ring-streams", type=int, choices=[0, 1], default=-1,
+                    help="R/3 and R/q tree chains on separate streams (default: tuned)")
     ap.add_argument("--mul-impl", choices=["tc", "schoolbook"], default="tc",
                     help="ring products: tcgen05 int8 Hankel GEMM (default) or int32 schoolbook")
     return ap.parse_args()
 
 
-DEFAULT_B = 1024
-DEFAULT_CHUNK = 32768      # two pipelined lanes (measured best with B = 1024; sweeps in the line)
+DEFAULT_B = 512
+DEFAULT_CHUNK = 65536
+DEFAULT_RING_STREAMS = True   # R/3 and R/q chains on two streams (measured best; A/B in DESIGN.md)
 MUL_IMPL = "tc"          # ring products on the tensor cores (see --mul-impl)
 TRAFFIC = {}             # dram bytes per launch of the dominant kernel, from profiles/ (ncu)
 
@@ -335,9 +338,12 @@ def main():
 
     CHUNK = args.chunk_keys or DEFAULT_CHUNK
 
+    RINGS = DEFAULT_RING_STREAMS if args.ring_streams < 0 else bool(args.ring_streams)
+    FLAGS = S.OPT_ASYNC | (S.OPT_RING_STREAMS if RINGS else 0)
+
     def step(batch=B, chunk=None):
         S.batch_keygen(PARAM, n, SEED, first_key_index=first, batch_size=batch, pk_out=pk,
-                       sk_out=sk, flags=S.OPT_ASYNC, chunk_keys=CHUNK if chunk is None else chunk)
+                       sk_out=sk, flags=FLAGS, chunk_keys=CHUNK if chunk is None else chunk)
 
     def barrier():
         if world > 1:
@@ -388,7 +394,7 @@ def main():
 
     def step_host(chunk):
         S.batch_keygen(PARAM, n, SEED, first_key_index=first, batch_size=B, pk_out=pk_h,
-                       sk_out=sk_h, flags=S.OPT_HOST_OUTPUT, chunk_keys=chunk)
+                       sk_out=sk_h, flags=S.OPT_HOST_OUTPUT | (FLAGS & ~S.OPT_ASYNC), chunk_keys=chunk)
 
     # the chunk size trades D2H/compute overlap against per-chunk latency phases: measure the
     # candidates and report the best (all are in the line)
@@ -449,7 +455,8 @@ def main():
             "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
             "config": {"workload": "configs[1]: sntrup761 batch keygen, 65,536 keys per GPU, seed 2",
-                       "keys_per_gpu": n, "batch_size": B, "chunk_keys": CHUNK, "param_set": PARAM,
+                       "keys_per_gpu": n, "batch_size": B, "chunk_keys": CHUNK, "ring_streams": RINGS,
+                       "param_set": PARAM,
                        "l2": "flushed between timed steps (256 MiB write); working set > L2",
                        "parallelism": "key ranges per GPU (no collective)"},
             "gpu_launches": launches,

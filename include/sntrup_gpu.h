@@ -72,6 +72,9 @@ int sntrup_batch_keygen(int param_set, uint64_t n_keys, uint64_t seed,
                                          the sampler, so every non-invertible g is caught by the
                                          product-tree root check and repaired */
 #define SNTRUP_OPT_ASYNC          4u  /* do not synchronise before returning (device outputs) */
+#define SNTRUP_OPT_RING_STREAMS   16u /* run the R/3 tree chain on its own stream beside the R/q
+                                         chain (separate root inversions) instead of one stream
+                                         with a joint root launch; outputs identical */
 #define SNTRUP_OPT_FORCE_SMALL_CHECK 8u /* always run the sampler's small-factor test (by default it
                                          is skipped where a tree almost never fails without it:
                                          B * P(small-factor rejection per draw) <= 1e-4,

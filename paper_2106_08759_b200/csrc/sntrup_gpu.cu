@@ -661,6 +661,7 @@ int launch_joint_roots(const InvArgs &r3, const InvArgs &rq, cudaStream_t s) {
 struct Lane {
     cudaStream_t s = nullptr;
     AuxStream *ax = nullptr;
+    AuxStream *r3 = nullptr;       // SNTRUP_OPT_RING_STREAMS: the R/3 chain's stream + events
     int8_t *G = nullptr, *F = nullptr, *Ginv = nullptr;
     uint8_t *att = nullptr;
     std::vector<void *> l3, i3, lq, iq;
@@ -684,6 +685,21 @@ int lane2_streams(cudaStream_t *s2, AuxStream **ax2) {
     }
     *s2 = e.first;
     *ax2 = &e.second;
+    return SNTRUP_OK;
+}
+
+// R/3-chain stream of a lane (SNTRUP_OPT_RING_STREAMS); go = sample done, done = R/3 chain done
+int ring_stream(int lane, AuxStream **out) {
+    static std::map<std::pair<int, int>, AuxStream> m;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    AuxStream &x = m[std::make_pair(dev, lane)];
+    if (!x.s) {
+        CK(cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&x.go, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&x.done, cudaEventDisableTiming));
+    }
+    *out = &x;
     return SNTRUP_OK;
 }
 
@@ -762,6 +778,8 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
         L.okq = ws_take<uint8_t>(tpmax.cnt[tpmax.L]);
         L.repaired = ws_take<unsigned long long>(1);
         L.err = ws_take<int>(1);
+        if (o.flags & SNTRUP_OPT_RING_STREAMS)
+            if ((rc = ring_stream(li, &L.r3))) return rc;
     }
     uint8_t *pk_stage[2] = {nullptr, nullptr}, *sk_stage[2] = {nullptr, nullptr};
     CopyStream *csl[2] = {nullptr, nullptr};       // one copy stream per lane: copies follow readiness
@@ -835,8 +853,14 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
         const TreeJob<PS, 3> j3{tp, rows8(Gc, PS::P16), Ic, 1, PS::P16, L.l3, L.i3, L.ok3, true};
         const TreeJob<PS, PS::Q> jq{tp, rows8(Fc, PS::P16, 3), L.Fbar, 2, PS::P8, L.lq, L.iq, L.okq, true};
         const bool utrick = tp.L >= 1;
+        const bool rings = L.r3 != nullptr;      // R/3 chain on its own stream
         AuxStream *ax = L.ax;
-        if ((rc = j3.up(s, &n_r3))) return rc;
+        const cudaStream_t s3 = rings ? L.r3->s : s;  // stream of the R/3 chain
+        if (rings) {
+            CK(cudaEventRecord(L.r3->go, s));
+            CK(cudaStreamWaitEvent(s3, L.r3->go, 0));
+        }
+        if ((rc = j3.up(s3, &n_r3))) return rc;
         if ((rc = jq.up(s, &n_rq))) return rc;
         if (utrick) {
             CK(cudaEventRecord(ax->go, s));
@@ -854,9 +878,16 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
             if ((rc = launch_mul<PS, PS::Q>(a, ax->s, 1, 1))) return rc;
             CK(cudaEventRecord(ax->done, ax->s));
         }
-        if ((rc = launch_joint_roots<PS>(j3.roots(), jq.roots(), s))) return rc;
-        if ((rc = j3.down(s, &n_r3))) return rc;
-        if (utrick) CK(cudaStreamWaitEvent(s, ax->done, 0));    // repair may rewrite u rows
+        if (rings) {
+            // each ring's roots on its own chain: one ring's latency-bound inversion overlaps the
+            // other ring's products
+            if ((rc = launch_divstep<PS, 3>(j3.roots(), s3))) return rc;
+            if ((rc = launch_divstep<PS, PS::Q>(jq.roots(), s))) return rc;
+        } else {
+            if ((rc = launch_joint_roots<PS>(j3.roots(), jq.roots(), s))) return rc;
+        }
+        if ((rc = j3.down(s3, &n_r3))) return rc;
+        if (utrick) CK(cudaStreamWaitEvent(s3, ax->done, 0));    // repair may rewrite u rows
         RepairArgs ra{};
         ra.seed = seed; ra.first = first; ra.n = m; ra.B = B; ra.root_ok = L.ok3;
         ra.G = Gc; ra.Ginv = Ic; ra.attempts = Ac;
@@ -864,8 +895,8 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
         ra.repaired = L.repaired; ra.err = L.err;
         ra.F = Fc; ra.U = utrick ? L.U : nullptr;
         {
-            ProfScope ps_(PC_REPAIR, (double)m, s);
-            repair_kernel<PS><<<(unsigned)((m + 3) / 4), 128, 0, s>>>(ra);
+            ProfScope ps_(PC_REPAIR, (double)m, s3);
+            repair_kernel<PS><<<(unsigned)((m + 3) / 4), 128, 0, s3>>>(ra);
         }
         LAUNCHED();
 
@@ -875,13 +906,17 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
             EncArgs ea{};
             ea.n = m; ea.h = nullptr; ea.f = Fc; ea.ginv = Ic; ea.pk = nullptr; ea.sk = skc; ea.t = tb->enc;
             {
-                ProfScope ps_(PC_ENCODE, (double)m, s);
-                encode_kernel<PS><<<(unsigned)((m + 3) / 4), 128, 0, s>>>(ea);
+                ProfScope ps_(PC_ENCODE, (double)m, s3);
+                encode_kernel<PS><<<(unsigned)((m + 3) / 4), 128, 0, s3>>>(ea);
             }
             LAUNCHED();
-            CK(cudaEventRecord(cs->comp[buf], s));
+            CK(cudaEventRecord(cs->comp[buf], s3));
             CK(cudaStreamWaitEvent(cs->s, cs->comp[buf], 0));
             CK(cudaMemcpyAsync(sk_out + c0 * skb, skc, m * skb, cudaMemcpyDeviceToHost, cs->s));
+        }
+        if (rings) {                               // join the R/3 chain (G, 1/g, u final)
+            CK(cudaEventRecord(L.r3->done, s3));
+            CK(cudaStreamWaitEvent(s, L.r3->done, 0));
         }
         if ((rc = jq.down(s, &n_rq, utrick ? 2 : 1))) return rc;
         if (utrick) n_rq += m;                                     // the u products replace level 1

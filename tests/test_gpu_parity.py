@@ -102,7 +102,8 @@ def test_repair_path_without_small_check(O, param, seed):
     assert res["stats"]["keys_repaired"] > 0
 
 
-@pytest.mark.parametrize("flags", [0, S.OPT_FORCE_SMALL_CHECK, S.OPT_NO_SMALL_CHECK])
+@pytest.mark.parametrize("flags", [0, S.OPT_FORCE_SMALL_CHECK, S.OPT_NO_SMALL_CHECK, S.OPT_RING_STREAMS,
+                                   S.OPT_RING_STREAMS | S.OPT_NO_SMALL_CHECK])
 def test_small_check_policies_761(O, flags):
     # the sampler's small-factor test is skipped by default for 761 (3^-19 per draw); forcing it
     # or disabling it must not change a byte
@@ -126,8 +127,9 @@ def test_cfg2_full_size_sampled(O):
     # BASELINE configs[1]: 65,536 keys, seed 2, in the launch configuration bench.py times;
     # compared on a sample the oracle computes one by one: first and last trees, every 97th key.
     n = 65536
-    for B, chunk in ((32, 0), (128, 0), (512, 0), (2048, 0), (1024, 32768)):   # last: bench.py's config
-        res = S.batch_keygen(761, n, 2, batch_size=B, chunk_keys=chunk)
+    for B, chunk, fl in ((32, 0, 0), (128, 0, 0), (2048, 0, 0), (1024, 32768, 0),
+                         (512, 65536, S.OPT_RING_STREAMS)):                 # last: bench.py's config
+        res = S.batch_keygen(761, n, 2, batch_size=B, chunk_keys=chunk, flags=fl)
         torch.cuda.synchronize()
         idx = np.unique(np.concatenate([np.arange(0, 128), np.arange(n - 128, n), np.arange(0, n, 97)]))
         check_keys(O, 761, 2, res, idx)
