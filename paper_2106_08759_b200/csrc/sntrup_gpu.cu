@@ -403,6 +403,22 @@ DevInfo &dev_info() {
     return d;
 }
 
+// Resident 128-thread CTAs per SM of a persistent tensor-core kernel: the minimum of the
+// shared-memory (1 KB reserved per CTA), register-file and TMEM-column (512 per SM) limits.  A
+// persistent grid larger than what is resident runs a second partial wave after the first CTAs
+// finish their whole share, so this must not over-count.
+template <class F>
+int resident_ctas(F kern, int smem, int tcols) {
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, kern) != cudaSuccess) return 1;
+    const int regs = (fa.numRegs + 7) / 8 * 8;                  // allocation granularity
+    const int by_regs = regs > 0 ? 65536 / (regs * 128) : 32;
+    const int by_smem = (227 * 1024) / (smem + 1024);
+    int nb = by_regs < by_smem ? by_regs : by_smem;
+    if (nb * tcols > 512) nb = 512 / tcols;
+    return nb < 1 ? 1 : nb;
+}
+
 template <class PS, int M, int LA, int LB, int NPR = 1, int MM = 128, bool XOPS = false>
 int launch_tc_impl(const MulArgs &a, cudaStream_t s) {
     using G = TcGeom<PS, LA, LB, NPR, MM>;
@@ -415,11 +431,7 @@ int launch_tc_impl(const MulArgs &a, cudaStream_t s) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         int nb = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 128, G::SMEM));
-        const int by_smem = (227 * 1024) / (G::SMEM + 1024);    // 1 KB reserved per CTA
-        if (nb < by_smem) nb = by_smem;
-        if (nb < 1) nb = 1;
-        if (nb * G::TCOLS > 512) nb = 512 / G::TCOLS;   // TMEM columns per SM
+        nb = resident_ctas(kern, G::SMEM, G::TCOLS);
         it = per_sm.emplace(dev, nb).first;
     }
     long long grid = (long long)it->second * dev_info().sms;
@@ -451,11 +463,7 @@ int launch_tc4_impl(const MulArgs &a, cudaStream_t s) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         int nb = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 128, G::SMEM));
-        const int by_smem = (227 * 1024) / (G::SMEM + 1024);
-        if (nb < by_smem) nb = by_smem;
-        if (nb < 1) nb = 1;
-        if (nb * G::TCOLS > 512) nb = 512 / G::TCOLS;
+        nb = resident_ctas(kern, G::SMEM, G::TCOLS);
         it = per_sm.emplace(dev, nb).first;
     }
     long long grid = (long long)it->second * dev_info().sms;

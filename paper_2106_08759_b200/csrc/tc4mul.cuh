@@ -21,10 +21,10 @@ __host__ __device__ constexpr int digits9(int q) {       // balanced base-9 digi
     return n;
 }
 
-// e2m1 code of an integer in [-4, 4]
+// e2m1 code of an integer in [-4, 4] or +-6
 __device__ __forceinline__ uint32_t e2m1_code(int d) {
     const int a = d < 0 ? -d : d;
-    return ((0x65420u >> (4 * a)) & 0xFu) | (d < 0 ? 8u : 0u);
+    return ((0x7065420u >> (4 * a)) & 0xFu) | (d < 0 ? 8u : 0u);   // |d| in {0..4, 6}
 }
 
 // SWAR e2m1 packing of 8 int8 coefficients in {-s, 0, s}, s in {1, 3} (bytes of w0 = coefficients
@@ -41,6 +41,18 @@ __device__ __forceinline__ uint32_t e2m1_pack8_int8(uint32_t w0, uint32_t w1, in
     return nib(w0) | (nib(w1) << 16);
 }
 
+// e2m1 codes of x_i + y_i for nibble-packed x, y with values in {-s, 0, s} (s = 1: code 2;
+// s = 3: code 5): sums in {0, +-s, +-2s}, 2s = 2.0 (code 4) or 6.0 (code 7).  Bitwise on the
+// nonzero / sign bits of each nibble.
+__device__ __forceinline__ uint32_t e2m1_pair_sum(uint32_t x, uint32_t y, int scale) {
+    constexpr uint32_t M1 = 0x11111111u;
+    const uint32_t nx = (scale == 1 ? x >> 1 : x) & M1, ny = (scale == 1 ? y >> 1 : y) & M1;
+    const uint32_t sx = (x >> 3) & M1, sy = (y >> 3) & M1;
+    const uint32_t same = nx & ny & ~(sx ^ sy), one = nx ^ ny;
+    const uint32_t sg = ((nx & sx) | (ny & sy)) & (same | one);
+    return same * (scale == 1 ? 4u : 7u) + one * (scale == 1 ? 2u : 5u) + (sg << 3);
+}
+
 // nibble order reversal of a word (nibble i -> nibble 7 - i)
 __device__ __forceinline__ uint32_t nibble_reverse(uint32_t x) {
     const uint32_t y = __byte_perm(x, 0, 0x0123);
@@ -52,8 +64,8 @@ struct Tc4Geom {
     static constexpr int P = PS::P;
     static constexpr int NKS = (P + 127 + 63) / 64;          // K steps of 64
     static constexpr int K = 64 * NKS;
-    static constexpr int NBLK = (2 * P - 1 + 127) / 128;
-    static constexpr int NL = (NBLK + 7) / 8 * 8;
+    static constexpr int NT = (P + 127) / 128;                // output blocks (folded B, tcmul.cuh)
+    static constexpr int NL = (NT + 1 + 7) / 8 * 8;           // B rows per digit (+ the fix row)
     static constexpr int PCOL = (LB * NL + 15) / 16 * 16;
     static constexpr int NB = NPR * PCOL;
     // window rows: the descriptor starts at row 1 and reads rows up to 127 + 32*(2*NKS-1) + 32
@@ -61,28 +73,38 @@ struct Tc4Geom {
     static constexpr int A_BYTES = AROWS * 16;
     static constexpr int HA_WORDS = AROWS / 8 + 8;           // 8 nibbles per word; nibble 128 + j = digit(a_j)
     static constexpr int HA_BYTES = (HA_WORDS * 4 + 127) / 128 * 128;
-    static constexpr int ZR_BYTES = ((128 * NL + K) / 2 + 127) / 128 * 128;   // nibble 128 NL - 1 - j = digit(b_j)
+    // Z (nibbles): bt reversed, Z[ZMARG + E - m] = digit(bt[m]), E = 128 NT - 1 (tcmul.cuh)
+    static constexpr int PD = P % 8;
+    static constexpr int R0 = (P - 1) % 32;                   // accumulator row of the fix row
+    static constexpr int ZMARG = 128;
+    static constexpr int ZB_END = ZMARG + 128 * NT;
+    static constexpr int Z_NIB = (ZMARG + 128 * NT + P + 64 + 255) / 256 * 256;
+    static constexpr int ZR_BYTES = Z_NIB / 2;
     static constexpr int NCHB = 2 * NKS;                      // 16-byte K-chunks per B row
     static constexpr int B_BYTES = NCHB * NB * 16;
-    static constexpr int RAW_INTS = 128 * NBLK;
     static constexpr int SFCOL = NB;                          // scale-factor columns after the accumulators
     static constexpr int TCOLS_USED = NB + 8;
     static constexpr int TCOLS = TCOLS_USED <= 32 ? 32 : TCOLS_USED <= 64 ? 64 : TCOLS_USED <= 128 ? 128 : 256;
     static constexpr int NCHK = PS::P8 / 8;
-    static constexpr int CH = (NCHK + 127) / 128;
+    static constexpr int CH = (NCHK + 1 + 127) / 128;
     static constexpr int OFF_A = 0;
     static constexpr int OFF_B = OFF_A + A_BYTES;
     static constexpr int OFF_HA = OFF_B + B_BYTES;
     static constexpr int OFF_ZR = OFF_HA + HA_BYTES;
     static constexpr int OFF_BAR = OFF_ZR + NPR * LB * ZR_BYTES;
     static constexpr int SMEM = OFF_BAR + 128;
-    static constexpr int BROWS = NPR * LB * NL;
+    static constexpr int BROWS = NPR * LB * (NT + 1);
     static constexpr int BITEMS = BROWS * 8;
     static constexpr int BPER = (BITEMS + 127) / 128;
-    static_assert(NPR * RAW_INTS * 4 <= A_BYTES, "raw buffers must fit in the A region");
     static_assert(NB <= 256, "N too large");
     static_assert(4 * (16 + NCHK) <= HA_BYTES, "hA too short (staging)");
     static_assert(4 * (AROWS / 8 + 5) <= HA_BYTES, "hA too short (windows)");
+    static_assert(PD != 0 && NCHK * 8 > P, "p odd: the s-groups need the next chunk");
+    static_assert(ZMARG + 128 * NT + 1 - 128 + R0 - P >= 0 && (1 + R0 - P) % 32 == 0, "fix row window");
+    static_assert(ZMARG + 128 * (NT - 1) + K <= Z_NIB, "Z too short");
+    static constexpr __host__ __device__ int zrow(int t) {     // nibble start of B row t's window
+        return t < NT ? ZMARG + 128 * (NT - 1 - t) : ZMARG + 128 * NT + 1 - 128 + R0 - P;
+    }
 };
 
 // idesc for kind::mxf4 (block-scaled layout): A = B = E2M1, scales UE8M0, K = 64, M = 128, N
@@ -99,12 +121,36 @@ __device__ __forceinline__ void umma_mxf4(uint32_t tmem_d, uint64_t adesc, uint6
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(tsf), "r"(tsf));
 }
 
+// 8 B digits (reversed into one word: value i -> nibble 7 - i), digit l of each value
+template <int LB>
+__device__ __forceinline__ void digits_rev8(const int (&vals)[8], uint32_t (&dw)[LB]) {
+#pragma unroll
+    for (int l = 0; l < LB; l++) dw[l] = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        int v = vals[i];
+#pragma unroll
+        for (int l = 0; l < LB; l++) {
+            int d = v;
+            if (LB > 1) {
+                const int qd = (v + 4 + 9 * 1024) / 9 - 1024;    // floor((v + 4) / 9)
+                d = v - 9 * qd;
+                v = qd;
+            }
+            dw[l] |= e2m1_code(d) << (4 * (7 - i));
+        }
+    }
+}
+
 // M = modulus; A = one digit (the small operand); LB digits for the B operand; NPR products per A.
+// The B operand is folded (bt of tcmul.cuh): LB = 1 sums stay in {0, +-s, +-2s} (s = 1 or 3:
+// e2m1-exact up to 6); LB > 1 sums are reduced mod M before their base-9 digits.
 template <class PS, int M, int LB, int NPR, bool XOPS = false>
 __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
     using G = Tc4Geom<PS, LB, NPR>;
     constexpr int P = PS::P;
     constexpr int CH = G::CH;
+    constexpr int PD = G::PD;
     extern __shared__ __align__(1024) uint8_t sm[];
     uint8_t *sA = sm + G::OFF_A;
     uint8_t *sB = sm + G::OFF_B;
@@ -112,7 +158,6 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
     uint8_t *sZR = sm + G::OFF_ZR;
     uint64_t *bar = reinterpret_cast<uint64_t *>(sm + G::OFF_BAR);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sm + G::OFF_BAR + 64);
-    int *raw = reinterpret_cast<int *>(sm + G::OFF_A);
     const int tid = threadIdx.x, warp = tid >> 5;
 
     for (int i = tid; i < (G::OFF_BAR - G::OFF_B) / 16; i += 128)
@@ -149,38 +194,57 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
         const int w = tid + 128 * h;
         if (w < G::BITEMS) {
             const int row = w % G::BROWS, grp = w / G::BROWS;
-            const int pl = row / G::NL, t = row - pl * G::NL;       // pl = pp * LB + l
+            const int pl = row / (G::NT + 1), t = row - pl * (G::NT + 1);   // pl = pp * LB + l
             const int pp = pl / LB, l = pl - pp * LB;
             bres[h] = (grp + row) & 7;
-            bsrc[h] = pl * (G::ZR_BYTES / 16) + 4 * (G::NL - 1 - t);
+            bsrc[h] = pl * (G::ZR_BYTES / 16) + G::zrow(t) / 32;
             bdst[h] = pp * G::PCOL + l * G::NL + t;
         } else {
             bsrc[h] = -1; bdst[h] = 0; bres[h] = 0;
         }
     }
 
-    uint4 pu[CH], pv[NPR][CH];
+    uint4 pu[CH], pv[NPR][CH], pn[NPR][CH];
+    int pa1 = 0, pb1[NPR];
+#pragma unroll
+    for (int pp = 0; pp < NPR; pp++) pb1[pp] = 0;
+    // window rows 4m+s, s = (i + m) mod 4 (rotated by m against bank conflicts), m = tid mod 128:
+    // nibble shifts are per-thread constants
+    uint32_t wsh[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) wsh[i] = 16u * (uint32_t)(tid & 1) + 4u * (uint32_t)((i + tid) & 3);
+    TcWork<NPR> wn;                                       // work item of the prefetched rows
     auto prefetch = [&](long long it) {
         if (it >= a.n_out) return;
-        TcWork<NPR> w;
+        TcWork<NPR> &w = wn;
         tc_work<NPR>(a, it, w);
 #pragma unroll
         for (int h = 0; h < CH; h++) {
             const int c = tid + 128 * h;
-            if (c < G::NCHK) {
-                pu[h] = w.unit_u ? make_uint4(0, 0, 0, 0) : load_chunk(w.du, w.ru, c);
+            if (c < G::NCHK) pu[h] = w.unit_u ? make_uint4(0, 0, 0, 0) : load_chunk(w.du, c);
+            const int cs = c == G::NCHK ? -1 : c;
 #pragma unroll
-                for (int pp = 0; pp < NPR; pp++)
-                    pv[pp][h] = (w.unit_v[pp] || (pp > 0 && w.orow[pp] < 0)) ? make_uint4(0, 0, 0, 0)
-                                                                         : load_chunk(w.dv[pp], w.rv[pp], c);
+            for (int pp = 0; pp < NPR; pp++) {
+                const bool none = w.unit_v[pp] || (pp > 0 && w.orow[pp] < 0);
+                if (c < G::NCHK) pv[pp][h] = none ? make_uint4(0, 0, 0, 0) : load_chunk(w.dv[pp], c);
+                if (c <= G::NCHK && cs < G::NCHK - 1)
+                    pn[pp][h] = none ? make_uint4(0, 0, 0, 0) : load_chunk(w.dv[pp], cs + 1);
             }
+        }
+        if (tid == 0) {
+            pa1 = opnd_coef<XOPS>(w.du, w.unit_u, P - 1);
+#pragma unroll
+            for (int pp = 0; pp < NPR; pp++)
+                pb1[pp] = (pp > 0 && w.orow[pp] < 0) ? 0 : opnd_coef<XOPS>(w.dv[pp], w.unit_v[pp], P - 1);
         }
     };
     prefetch(blockIdx.x);
 
     for (long long it = blockIdx.x; it < a.n_out; it += gridDim.x) {
-        TcWork<NPR> w;
-        tc_work<NPR>(a, it, w);
+        const TcWork<NPR> w = wn;
+        int fixab[NPR];
+#pragma unroll
+        for (int pp = 0; pp < NPR; pp++) fixab[pp] = 0;
         // ---- stage digits: one 32-bit word (8 nibbles) per 8 coefficients
 #pragma unroll
         for (int h = 0; h < CH; h++) {
@@ -196,42 +260,75 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
                     for (int i = 0; i < 8; i++) word |= e2m1_code(uv8[i]) << (4 * i);
                 }
                 sHA[16 + c] = word;                                  // nibbles 128 + 8c + i
+            }
+            if (c <= G::NCHK) {
+                const int cs = c == G::NCHK ? -1 : c;
 #pragma unroll
                 for (int pp = 0; pp < NPR; pp++) {
-                    uint32_t dw[LB];
-                    if (LB == 1 && w.dv[pp].bytes == 1 && !w.unit_v[pp] && !(XOPS && w.dv[pp].mod3)) {
-                        // reversed: coefficient 8c + i -> nibble 7 - i of word 16 NL - 1 - c
-                        dw[0] = nibble_reverse(e2m1_pack8_int8(pv[pp][h].x, pv[pp][h].y, w.dv[pp].scale));
-                    } else {
-                        int vv8[8];
-                        decode_chunk(pv[pp][h], w.dv[pp].bytes, w.dv[pp].scale, w.unit_v[pp], c, vv8, XOPS ? w.dv[pp].mod3 : 0);
-#pragma unroll
-                        for (int l = 0; l < LB; l++) dw[l] = 0;
-#pragma unroll
-                        for (int i = 0; i < 8; i++) {
-                            int v = vv8[i];
-#pragma unroll
-                            for (int l = 0; l < LB; l++) {
-                                int d = v;
-                                if (LB > 1) {
-                                    const int qd = (v + 4 + 9 * 1024) / 9 - 1024;    // floor((v + 4) / 9)
-                                    d = v - 9 * qd;
-                                    v = qd;
-                                }
-                                dw[l] |= e2m1_code(d) << (4 * (7 - i));
-                            }
+                    uint32_t *zr = reinterpret_cast<uint32_t *>(sZR + pp * LB * G::ZR_BYTES);
+                    const bool fast = LB == 1 && w.dv[pp].bytes == 1 && !w.unit_v[pp] && !(XOPS && w.dv[pp].mod3);
+                    const int zws = (G::ZB_END + (P - PD) - 8 - 8 * cs) / 8;    // s-group word
+                    const int zwb = G::ZB_END / 8 - 1 - c;                      // b[8c+i]: nibble ZB_END-1-8c-i
+                    if (c == 0) fixab[pp] = pa1 * pb1[pp];
+                    if (LB == 1 && fast) {
+                        // SWAR: forward-packed chunks, s-group = pairwise sums of two shifted views
+                        const int sc = w.dv[pp].scale;
+                        const uint32_t W0 = c < G::NCHK ? e2m1_pack8_int8(pv[pp][h].x, pv[pp][h].y, sc) : 0u;
+                        if (cs < G::NCHK - 1) {
+                            const uint32_t W1 = e2m1_pack8_int8(pn[pp][h].x, pn[pp][h].y, sc);
+                            zr[zws] = nibble_reverse(e2m1_pair_sum(__funnelshift_r(W0, W1, 4 * PD),
+                                                                   __funnelshift_r(W0, W1, 4 * (PD - 1)), sc));
                         }
+                        if (c < G::NCHK) {
+                            uint32_t fw = W0;
+                            if (c == 0)                                  // bt[0] = b[0] + b[p-1]
+                                fw = (W0 & ~0xFu) | e2m1_code(sc * (int)(int8_t)(pv[pp][h].x & 0xFFu) + pb1[pp]);
+                            zr[zwb] = nibble_reverse(fw);
+                        }
+                        continue;
                     }
+                    int vv8[8], vn8[8];
+                    if (c < G::NCHK)
+                        decode_chunk(pv[pp][h], w.dv[pp].bytes, w.dv[pp].scale, w.unit_v[pp], c, vv8,
+                                     XOPS ? w.dv[pp].mod3 : 0);
+                    else
 #pragma unroll
-                    for (int l = 0; l < LB; l++)
-                        reinterpret_cast<uint32_t *>(sZR + (pp * LB + l) * G::ZR_BYTES)[16 * G::NL - 1 - c] = dw[l];
+                        for (int i = 0; i < 8; i++) vv8[i] = 0;
+                    if (cs < G::NCHK - 1) {
+                        // s-group: s[i] = b[i] + b[i-1], i = 8cs+PD+j, at nibble ZB_END + p - 1 - i
+                        decode_chunk(pn[pp][h], w.dv[pp].bytes, w.dv[pp].scale, w.unit_v[pp], cs + 1, vn8,
+                                     XOPS ? w.dv[pp].mod3 : 0);
+                        int s8[8];
+#pragma unroll
+                        for (int j = 0; j < 8; j++) {
+                            const int i0 = PD + j, i1 = PD + j - 1;
+                            s8[j] = (i0 < 8 ? vv8[i0] : vn8[i0 - 8]) + (i1 < 8 ? vv8[i1] : vn8[i1 - 8]);
+                            if (LB > 1) s8[j] = canon<M>(s8[j]);
+                        }
+                        uint32_t dw[LB];
+                        digits_rev8<LB>(s8, dw);
+#pragma unroll
+                        for (int l = 0; l < LB; l++) zr[l * (G::ZR_BYTES / 4) + zws] = dw[l];
+                    }
+                    if (c < G::NCHK) {
+                        uint32_t dw[LB];
+                        if (c == 0) {
+                            vv8[0] += pb1[pp];                       // bt[0] = b[0] + b[p-1]
+                            if (LB > 1) vv8[0] = canon<M>(vv8[0]);
+                        }
+                        digits_rev8<LB>(vv8, dw);
+#pragma unroll
+                        for (int l = 0; l < LB; l++) zr[l * (G::ZR_BYTES / 4) + zwb] = dw[l];
+                    }
                 }
             }
         }
         __syncthreads();
         // ---- A windows: row rho = nibbles [rho, rho+32); rows 4m..4m+3 share word base m/2
-#pragma unroll 1
-        for (int m = tid; m < G::AROWS / 4; m += 128) {
+#pragma unroll
+        for (int kw = 0; kw < (G::AROWS / 4 + 127) / 128; kw++) {
+            const int m = tid + 128 * kw;
+            if (m >= G::AROWS / 4) break;
             const uint32_t *src = sHA + (m >> 1);
             uint32_t wd[5];
 #pragma unroll
@@ -239,17 +336,15 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
             uint4 *dst = reinterpret_cast<uint4 *>(sA) + 4 * m;
 #pragma unroll
             for (int i = 0; i < 4; i++) {
-                const int s_ = (i + m) & 3;
-                const uint32_t sh = 16u * (uint32_t)(m & 1) + 4u * (uint32_t)s_;
                 uint4 o;
-                o.x = __funnelshift_r(wd[0], wd[1], sh);
-                o.y = __funnelshift_r(wd[1], wd[2], sh);
-                o.z = __funnelshift_r(wd[2], wd[3], sh);
-                o.w = __funnelshift_r(wd[3], wd[4], sh);
-                dst[s_] = o;
+                o.x = __funnelshift_r(wd[0], wd[1], wsh[i]);
+                o.y = __funnelshift_r(wd[1], wd[2], wsh[i]);
+                o.z = __funnelshift_r(wd[2], wd[3], wsh[i]);
+                o.w = __funnelshift_r(wd[3], wd[4], wsh[i]);
+                dst[(i + tid) & 3] = o;
             }
         }
-        // ---- B rows (aligned 16-byte chunks of the reversed digit arrays)
+        // ---- B rows (aligned 16-byte chunks of the rows' Z windows)
 #pragma unroll
         for (int h = 0; h < G::BPER; h++) {
             if (bsrc[h] < 0) continue;
@@ -278,6 +373,7 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
         phase ^= 1;
         __syncthreads();
         tc_fence_after();
+        // ---- epilogue: thread tid = TMEM lane = coefficient r of every block, straight to HBM
         const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
 #pragma unroll
         for (int pp = 0; pp < NPR; pp++) {
@@ -285,48 +381,39 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
 #pragma unroll
             for (int c16 = 0; c16 < G::PCOL / 16; c16++) tmem_ld16(lane_addr + pp * G::PCOL + 16 * c16, v[c16]);
             tmem_ld_wait();
-#pragma unroll
-            for (int t = 0; t < G::NBLK; t++) {
+            auto comb = [&](int t) {
                 int x = 0;
 #pragma unroll
                 for (int l = LB - 1; l >= 0; l--) {
                     const int col = l * G::NL + t;
                     x = 9 * x + __float2int_rn(__int_as_float(v[col >> 4][col & 15]));
                 }
-                raw[pp * G::RAW_INTS + 128 * t + tid] = (LB > 1) ? x % M : x;
-            }
-        }
-        tc_fence_before();
-        __syncthreads();
-        // (all shared-memory reads of a product issued before its arithmetic: one latency)
-        const int ostride_elems = a.out_bytes == 2 ? PS::P8 : PS::P16;
-        constexpr int FI = (PS::P16 + 127) / 128;
-#pragma unroll
-        for (int pp = 0; pp < NPR; pp++) {
+                return LB > 1 ? x % M : x;
+            };
+            int fix = 0;
+            if (warp == 0) fix = __shfl_sync(FULL, comb(G::NT), G::R0);    // = D(p-1)
             const long long orow = w.orow[pp];
             if (orow < 0) continue;
-            const int *rw = raw + pp * G::RAW_INTS;
-            int fa[FI], fb[FI], fc[FI];
+            auto store = [&](auto *op) {
+                constexpr int OSTRIDE = sizeof(*op) == 2 ? PS::P8 : PS::P16;
 #pragma unroll
-            for (int i = 0; i < FI; i++) {
-                const int k = tid + 128 * i;
-                fa[i] = fb[i] = fc[i] = 0;
-                if (k < P) {
-                    fa[i] = rw[k];
-                    fb[i] = rw[k + P];
-                    fc[i] = k >= 1 ? rw[k + P - 1] : 0;
+                for (int t = 0; t < G::NT; t++) {
+                    const int k = 128 * t + tid;
+                    if (k >= OSTRIDE) break;
+                    int vv;
+                    if (k == 0) vv = canon<M>(comb(0) - fix + fixab[pp] % M);
+                    else if (M == 3 && LB == 1) vv = (int)fmodc<3>(__int_as_float(v[t >> 4][t & 15]));  // exact: |D| < 2^20
+                    else vv = canon<M>(comb(t));
+                    if (k >= P) vv = 0;
+                    if (XOPS && a.round3) vv -= canon<3>(vv);      // encapsulation's Round
+                    op[k] = (std::remove_reference_t<decltype(*op)>)vv;
                 }
-            }
-#pragma unroll
-            for (int i = 0; i < FI; i++) {
-                const int k = tid + 128 * i;
-                if (k >= ostride_elems) break;
-                int v = k < P ? canon<M>(fa[i] + fb[i] + fc[i]) : 0;
-                if (XOPS && a.round3) v -= canon<3>(v);      // encapsulation's Round
-                if (a.out_bytes == 2) ((int16_t *)a.out)[orow * a.out_stride + k] = (int16_t)v;
-                else ((int8_t *)a.out)[orow * a.out_stride + k] = (int8_t)v;
-            }
+            };
+            uint8_t *orp = (uint8_t *)a.out + orow * a.out_stride * a.out_bytes;
+            if (a.out_bytes == 2) store(reinterpret_cast<int16_t *>(orp));
+            else store(reinterpret_cast<int8_t *>(orp));
         }
+        tc_fence_before();
     }
     tc_fence_before();
     __syncthreads();

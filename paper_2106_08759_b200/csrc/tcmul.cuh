@@ -15,18 +15,23 @@
 // reads element (r, k) of the descriptor's tile at byte 16*(r + k) + (k mod 16) of a "sliding
 // window" buffer whose 16-byte row rho holds hA[rho .. rho+15] (hA = a shifted by 127).  So the
 // whole 128 x K Hankel operand costs 16 B per row of a (16*(K+112) B) instead of 128*K B.
-// B is materialised (N rows of K bytes) from aligned 16-byte chunks of the reversed b.
+// B is materialised (N rows of K bytes) from aligned 16-byte chunks of the reversed b -- with the
+// reduction x^p = x + 1 folded into it (TcGeom below), so the GEMM produces the reduced product
+// directly: N = ceil(p/128) blocks (+ one fix row) and the epilogue stores straight to HBM.
 //
 // Coefficients of R/q do not fit int8: a big operand is split into limbs v = 64*hi + lo with
-// lo in [-32, 31] and hi in [-62, 62] (|v| <= (q-1)/2 <= 3939).  A-limbs are separate MMAs into
-// separate TMEM accumulators; B-limbs are stacked along N.  Small operands (R/3 elements, 3f,
-// g, the unit) are one limb.  Exactness: every accumulator is an exact int32 sum
-// (|sum| <= p * 62 * 62 < 2^23), combined mod q in the epilogue.
+// lo in [-32, 31] and hi in [-62, 62] (|v| <= (q-1)/2 <= 3939; the folded B holds sums of two
+// coefficients, |hi| <= 123).  A-limbs are separate MMAs into separate TMEM accumulators; B-limbs
+// are stacked along N.  Small operands (R/3 elements, 3f, g, the unit) are one limb.  Exactness:
+// every accumulator is an exact int32 sum (|sum| <= p * 62 * 123 < 2^24), combined mod q in the
+// epilogue.
 //
 // One CTA (4 warps) per product, persistent over the grid; thread r owns TMEM lane r (output
 // coefficient r of every block) in the epilogue.  Several CTAs per SM overlap one CTA's operand
 // build / epilogue with another's MMAs.
 #pragma once
+#include <type_traits>
+
 #include "common.cuh"
 #include "ringmul.cuh"
 
@@ -113,43 +118,67 @@ __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.
 // NPR products share one A operand per iteration (the down-sweep's two children share the
 // parent's inverse): their B rows are stacked along N, so the A tile read by every MMA -- the
 // dominant shared-memory traffic of a small-N GEMM -- is amortised over both products.
+//
+// Folded B operand.  The reduction x^p = x + 1 is folded into B: with the Laurent extension
+//   bt[m] = b[m] (m >= 1),  bt[0] = b[0] + b[p-1],  bt[m] = b[m+p] + b[m+p-1] (-p < m < 0),
+// the Toeplitz sum  sum_j a[j] bt[k - j]  equals the reduced product coefficient c[k] for every
+// 1 <= k < p (the wrapped terms raw[k+p] and raw[k+p-1] of section 3.3's reduction), and
+// c[0] + raw[p-1] for k = 0.  So the GEMM only needs the NT = ceil(p/MM) output blocks of the
+// reduced product (half the N of the full product, no fold pass), and c[0] is fixed with
+// c[0] = D(0) - D(p-1) + a[p-1] b[p-1] (raw[p-1] = c[p-1] - a[p-1] b[p-1]).  An extra B row
+// ("fix row") repeats output p-1 in accumulator row R0 = (p-1) mod 16, a lane of warp 0, so
+// thread 0 gets it with one shuffle.
+//   Z (per B limb) holds bt reversed: Z[ZMARG + E - m] = limb(bt[m]), E = MM*NT - 1; B row t
+//   (t < NT) is the window Z[ZMARG + MM(NT-1-t) + k], the fix row Z[ZMARG + MM NT + 1 - MM + R0 - p + k].
 template <class PS, int LA, int LB, int NPR, int MM = 128>
 struct TcGeom {
     static_assert(MM == 64 || MM == 128, "M is 64 or 128");
     static constexpr int P = PS::P;
     static constexpr int NKS = (P + MM - 1 + 31) / 32;       // K steps of 32
     static constexpr int K = 32 * NKS;
-    static constexpr int NBLK = (2 * P - 1 + MM - 1) / MM;   // output blocks of MM coefficients
-    static constexpr int NL = (NBLK + 7) / 8 * 8;            // B rows per limb
+    static constexpr int NT = (P + MM - 1) / MM;              // output blocks of MM coefficients
+    static constexpr int NL = (NT + 1 + 7) / 8 * 8;           // B rows per limb (+ the fix row)
     static constexpr int PCOL = (LB * NL + 15) / 16 * 16;    // B rows (= D columns) per product
     static constexpr int NB = NPR * PCOL;                    // N of the MMA
     static constexpr int AROWS = 32 * NKS + MM - 15;         // window rows 0..AROWS-1 (row 0 unused)
     static constexpr int A_BYTES = (AROWS + 7) / 8 * 128;    // 16 B per row, 128-aligned
     static constexpr int AROWS4 = (AROWS + 3) / 4;            // window rows are built 4 at a time
     static constexpr int HA_LEN = (4 * AROWS4 + 20 + 127) / 128 * 128;   // hA[MM + j] = limb(a_j)
-    static constexpr int ZR_LEN = (MM * NL + K + 127) / 128 * 128;  // zr[MM NL - 1 - j] = limb(b_j)
+    static constexpr int PD = P % 8;                          // s-groups start at 8c + PD
+    static constexpr int R0 = (P - 1) % 16;                   // accumulator row of the fix row
+    static constexpr int ZMARG = MM;
+    static constexpr int Z_LEN = (ZMARG + MM * NT + P + 32 + 127) / 128 * 128;
+    static constexpr int ZB_END = ZMARG + MM * NT;            // b part below, s part from here
     static constexpr int B_BYTES = 2 * NKS * NB * 16;
-    static constexpr int RAW_INTS = MM * NBLK;                // per product
     static constexpr int TCOLS_USED = LA * NB;
     static constexpr int TCOLS = TCOLS_USED <= 32 ? 32 : TCOLS_USED <= 64 ? 64 : TCOLS_USED <= 128 ? 128 : 256;
     static constexpr int NCHK = PS::P8 / 8;                   // 8-coefficient input chunks
-    static constexpr int CH = (NCHK + 127) / 128;             // chunks per thread
-    // smem carve-up (bytes, all 128-aligned); raw aliases the A windows (dead after the MMAs)
+    static constexpr int CH = (NCHK + 1 + 127) / 128;         // chunks per thread (+ the s-group -1)
+    // smem carve-up (bytes, all 128-aligned)
     static constexpr int OFF_A = 0;
     static constexpr int OFF_B = OFF_A + LA * A_BYTES;
     static constexpr int OFF_HA = OFF_B + B_BYTES;
     static constexpr int OFF_ZR = OFF_HA + LA * HA_LEN;
-    static constexpr int OFF_BAR = OFF_ZR + NPR * LB * ZR_LEN;
+    static constexpr int OFF_BAR = OFF_ZR + NPR * LB * Z_LEN;
     static constexpr int SMEM = OFF_BAR + 128;
-    static_assert(NPR * RAW_INTS * 4 <= LA * A_BYTES, "raw buffers must fit in the A region");
+    // resident CTAs the shared memory allows (up to 4): register budget for __launch_bounds__
+    static constexpr int MINB = (227 * 1024) / (SMEM + 1024) < 4 ? (227 * 1024) / (SMEM + 1024) : 4;
     static_assert(NB <= 256, "N too large");
     static_assert(MM + PS::P8 <= HA_LEN, "hA too short");
     static_assert(4 * AROWS4 * 16 <= A_BYTES, "A region too short");
-    // B build: (row, residue mod 8) work items; row = pp*PCOL + l*NL + t, K-chunks c = residue + 8i
-    static constexpr int BROWS = NPR * LB * NL;
+    static_assert(PD != 0 && NCHK * 8 > P, "p odd: the s-groups need the next chunk");
+    static_assert(ZMARG + MM * NT + 1 - MM + R0 - P >= 0 && (1 + R0 - P) % 16 == 0, "fix row window");
+    static_assert(ZMARG + MM * (NT - 1) + K <= Z_LEN, "Z too short");
+    // B build: (row, residue mod 8) work items; row = pp*PCOL + l*NL + t (t <= NT), K-chunks
+    // c = residue + 8i
+    static constexpr int BROWS = NPR * LB * (NT + 1);
     static constexpr int NCHB = 2 * NKS;                      // 16-byte K-chunks per B row
     static constexpr int BITEMS = BROWS * 8;
     static constexpr int BPER = (BITEMS + 127) / 128;
+    // start (bytes) of B row t's window in Z
+    static constexpr __host__ __device__ int zrow(int t) {
+        return t < NT ? ZMARG + MM * (NT - 1 - t) : ZMARG + MM * NT + 1 - MM + R0 - P;
+    }
 };
 
 // limb l (0 = hi, 1 = lo) of a centered coefficient when the operand has L limbs
@@ -160,12 +189,33 @@ __device__ __forceinline__ int limb_of(int v, int l) {
     return l == 0 ? (v - lo) >> 6 : lo;
 }
 
-// 16 raw bytes of chunk c (coefficients 8c .. 8c+7) of row `row` (int16: 16 B, int8: 8 B)
-__device__ __forceinline__ uint4 load_chunk(const RowDesc &d, long long row, int c) {
-    if (d.bytes == 2)
-        return __ldg(reinterpret_cast<const uint4 *>((const int16_t *)d.ptr + row * d.stride) + c);
-    const uint2 v = __ldg(reinterpret_cast<const uint2 *>((const int8_t *)d.ptr + row * d.stride) + c);
+// One operand row of a work item: its first byte, element size, load scale and mod-3 pre-op.
+struct Opnd {
+    const uint8_t *row;
+    int bytes, scale, mod3;
+};
+
+__device__ __forceinline__ Opnd opnd(const RowDesc &d, long long r) {
+    Opnd o;
+    o.row = (const uint8_t *)d.ptr + r * d.stride * d.bytes;
+    o.bytes = d.bytes; o.scale = d.scale; o.mod3 = d.mod3;
+    return o;
+}
+
+// 16 raw bytes of chunk c (coefficients 8c .. 8c+7) of an operand row (int16: 16 B, int8: 8 B)
+__device__ __forceinline__ uint4 load_chunk(const Opnd &d, int c) {
+    if (d.bytes == 2) return __ldg(reinterpret_cast<const uint4 *>(d.row) + c);
+    const uint2 v = __ldg(reinterpret_cast<const uint2 *>(d.row) + c);
     return make_uint4(v.x, v.y, 0, 0);
+}
+
+// coefficient k of an operand row (decoded: scale, optional mod-3 pre-op)
+template <bool XOPS>
+__device__ __forceinline__ int opnd_coef(const Opnd &d, bool unit, int k) {
+    if (unit) return k == 0 ? 1 : 0;
+    int v = d.bytes == 1 ? (int)((const int8_t *)d.row)[k] : (int)((const int16_t *)d.row)[k];
+    v *= d.scale;
+    return (XOPS && d.mod3) ? canon<3>(v) : v;
 }
 
 __device__ __forceinline__ void decode_chunk(const uint4 r, int bytes, int scale, bool unit, int c, int (&v)[8],
@@ -198,8 +248,8 @@ __device__ __forceinline__ uint32_t pack4(int a, int b, int c, int d) {
 // orow[pp] (orow < 0: no such product).
 template <int NPR>
 struct TcWork {
-    RowDesc du; long long ru; bool unit_u;
-    RowDesc dv[NPR]; long long rv[NPR]; bool unit_v[NPR];
+    Opnd du; bool unit_u;
+    Opnd dv[NPR]; bool unit_v[NPR];
     long long orow[NPR];
 };
 
@@ -207,15 +257,15 @@ template <int NPR>
 __device__ __forceinline__ void tc_work(const MulArgs &a, long long it, TcWork<NPR> &w) {
     w.unit_u = false;
 #pragma unroll
-    for (int pp = 0; pp < NPR; pp++) { w.unit_v[pp] = false; w.orow[pp] = -1; w.dv[pp] = a.X; w.rv[pp] = 0; }
+    for (int pp = 0; pp < NPR; pp++) { w.unit_v[pp] = false; w.orow[pp] = -1; w.dv[pp] = opnd(a.X, 0); }
     if constexpr (NPR == 2) {
         // MUL_DOWN2: parent it; out[2it] = Y[it] * X[2it+1] (unit if absent), out[2it+1] = Y[it] * X[2it]
         // MUL_DOWNH2: parent it; out[2it] = Y[it] * X[2it], out[2it+1] = Y[it] * X[2it+1] (if present)
         const bool noswap = a.mode == MUL_DOWNH2;
-        w.du = a.Y; w.ru = it;
-        w.dv[0] = a.X; w.rv[0] = noswap ? 2 * it : 2 * it + 1;
+        w.du = opnd(a.Y, it);
+        w.dv[0] = opnd(a.X, noswap ? 2 * it : 2 * it + 1);
         w.unit_v[0] = !noswap && 2 * it + 1 >= a.cnt_in; w.orow[0] = 2 * it;
-        w.dv[1] = a.X; w.rv[1] = noswap ? 2 * it + 1 : 2 * it;
+        w.dv[1] = opnd(a.X, noswap ? 2 * it + 1 : 2 * it);
         w.orow[1] = (2 * it + 1 < a.cnt_in) ? 2 * it + 1 : -1;
     } else {
         RowDesc du, dv; long long ru, rv; bool uv = false, uu = false;
@@ -238,8 +288,8 @@ __device__ __forceinline__ void tc_work(const MulArgs &a, long long it, TcWork<N
             const long long tr = ru; ru = rv; rv = tr;
             uu = uv; uv = false;
         }
-        w.du = du; w.ru = ru; w.unit_u = uu;
-        w.dv[0] = dv; w.rv[0] = rv; w.unit_v[0] = uv; w.orow[0] = it;
+        w.du = opnd(du, ru); w.unit_u = uu;
+        w.dv[0] = opnd(dv, rv); w.unit_v[0] = uv; w.orow[0] = it;
     }
 }
 
@@ -249,10 +299,11 @@ __device__ __forceinline__ void tc_work(const MulArgs &a, long long it, TcWork<N
 // XOPS: honour the operand pre-op (RowDesc.mod3) and the output post-op (MulArgs.round3) of the
 // KEM core; compiled out of the keygen instantiations.
 template <class PS, int M, int LA, int LB, int NPR, int MM = 128, bool XOPS = false>
-__global__ void __launch_bounds__(128) tc_mul_kernel(MulArgs a) {
+__global__ void __launch_bounds__(128, (TcGeom<PS, LA, LB, NPR, MM>::MINB)) tc_mul_kernel(MulArgs a) {
     using G = TcGeom<PS, LA, LB, NPR, MM>;
     constexpr int P = PS::P;
     constexpr int CH = G::CH;
+    constexpr int PD = G::PD;
     extern __shared__ __align__(1024) uint8_t sm[];
     uint8_t *sA = sm + G::OFF_A;
     uint8_t *sB = sm + G::OFF_B;
@@ -260,7 +311,6 @@ __global__ void __launch_bounds__(128) tc_mul_kernel(MulArgs a) {
     uint8_t *sZR = sm + G::OFF_ZR;
     uint64_t *bar = reinterpret_cast<uint64_t *>(sm + G::OFF_BAR);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sm + G::OFF_BAR + 64);
-    int *raw = reinterpret_cast<int *>(sm + G::OFF_A);
     const int tid = threadIdx.x, warp = tid >> 5;
 
     // ---- one-time setup: zero staging + B (pads stay zero forever), barrier, TMEM
@@ -290,41 +340,62 @@ __global__ void __launch_bounds__(128) tc_mul_kernel(MulArgs a) {
         const int w = tid + 128 * h;
         if (w < G::BITEMS) {
             const int row = w % G::BROWS, grp = w / G::BROWS;
-            const int pl = row / G::NL, t = row - pl * G::NL;       // pl = pp * LB + l
+            const int pl = row / (G::NT + 1), t = row - pl * (G::NT + 1);   // pl = pp * LB + l
             const int pp = pl / LB, l = pl - pp * LB;
             bres[h] = (grp + row) & 7;
-            bsrc[h] = pl * (G::ZR_LEN / 16) + (MM / 16) * (G::NL - 1 - t);
+            bsrc[h] = pl * (G::Z_LEN / 16) + G::zrow(t) / 16;
             bdst[h] = pp * G::PCOL + l * G::NL + t;
         } else {
             bsrc[h] = -1; bdst[h] = 0; bres[h] = 0;
         }
     }
 
-    // register prefetch of the next work item's rows (in flight during the MMAs / epilogue)
-    uint4 pu[CH], pv[NPR][CH];
+    // register prefetch of the next work item's rows (in flight during the MMAs / epilogue):
+    // chunk c of u and of every v, chunk c+1 of v (the s-groups straddle chunks), and for
+    // thread 0 the scalars u[p-1], v[p-1] (bt[0] and the c[0] fix)
+    uint4 pu[CH], pv[NPR][CH], pn[NPR][CH];
+    int pa1 = 0, pb1[NPR];
+#pragma unroll
+    for (int pp = 0; pp < NPR; pp++) pb1[pp] = 0;
+    // A-window rows 4m+s (s = (i + m) mod 4, stored rotated by m against bank conflicts): m = tid
+    // mod 128, so the byte selectors are per-thread constants
+    uint32_t wsel[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) wsel[i] = 0x3210u + (uint32_t)((i + tid) & 3) * 0x1111u;   // bytes s..s+3
+    TcWork<NPR> wn;                                       // work item of the prefetched rows
     auto prefetch = [&](long long it) {
         if (it >= a.n_out) return;
-        TcWork<NPR> w;
+        TcWork<NPR> &w = wn;
         tc_work<NPR>(a, it, w);
 #pragma unroll
         for (int h = 0; h < CH; h++) {
             const int c = tid + 128 * h;
-            if (c < G::NCHK) {
-                pu[h] = w.unit_u ? make_uint4(0, 0, 0, 0) : load_chunk(w.du, w.ru, c);
+            if (c < G::NCHK) pu[h] = w.unit_u ? make_uint4(0, 0, 0, 0) : load_chunk(w.du, c);
+            const int cs = c == G::NCHK ? -1 : c;                // thread NCHK: s-group -1
 #pragma unroll
-                for (int pp = 0; pp < NPR; pp++)
-                    pv[pp][h] = (w.unit_v[pp] || (pp > 0 && w.orow[pp] < 0)) ? make_uint4(0, 0, 0, 0)
-                                                                         : load_chunk(w.dv[pp], w.rv[pp], c);
+            for (int pp = 0; pp < NPR; pp++) {
+                const bool none = w.unit_v[pp] || (pp > 0 && w.orow[pp] < 0);
+                if (c < G::NCHK) pv[pp][h] = none ? make_uint4(0, 0, 0, 0) : load_chunk(w.dv[pp], c);
+                if (c <= G::NCHK && cs < G::NCHK - 1)
+                    pn[pp][h] = none ? make_uint4(0, 0, 0, 0) : load_chunk(w.dv[pp], cs + 1);
             }
+        }
+        if (tid == 0) {
+            pa1 = opnd_coef<XOPS>(w.du, w.unit_u, P - 1);
+#pragma unroll
+            for (int pp = 0; pp < NPR; pp++)
+                pb1[pp] = (pp > 0 && w.orow[pp] < 0) ? 0 : opnd_coef<XOPS>(w.dv[pp], w.unit_v[pp], P - 1);
         }
     };
     prefetch(blockIdx.x);
 
     for (long long it = blockIdx.x; it < a.n_out; it += gridDim.x) {
-        TcWork<NPR> w;
-        tc_work<NPR>(a, it, w);
-        // ---- stage limbs (8-byte aligned groups): hA_l[128 + j] = limb_l(u_j),
-        //      zr_{pp,l}[128 NL - 1 - j] = limb_l(v_pp,j) (reversed within the group)
+        const TcWork<NPR> w = wn;
+        int fixab[NPR];                                   // a[p-1] b[p-1] (thread 0)
+#pragma unroll
+        for (int pp = 0; pp < NPR; pp++) fixab[pp] = 0;
+        // ---- stage limbs (8-byte aligned groups): hA_l[MM + j] = limb_l(u_j);
+        //      Z_{pp,l}: b part (chunk c reversed) and s part (s-group c: bt at 8c+PD .. 8c+PD+7)
 #pragma unroll
         for (int h = 0; h < CH; h++) {
             const int c = tid + 128 * h;
@@ -339,17 +410,55 @@ __global__ void __launch_bounds__(128) tc_mul_kernel(MulArgs a) {
                     *reinterpret_cast<uint2 *>(sHA + l * G::HA_LEN + MM + 8 * c) =
                         make_uint2(pack4(x[0], x[1], x[2], x[3]), pack4(x[4], x[5], x[6], x[7]));
                 }
+            }
+            if (c <= G::NCHK) {
+                const int cs = c == G::NCHK ? -1 : c;               // s-group index
 #pragma unroll
                 for (int pp = 0; pp < NPR; pp++) {
-                    int vv8[8];
-                    decode_chunk(pv[pp][h], w.dv[pp].bytes, w.dv[pp].scale, w.unit_v[pp], c, vv8, XOPS ? w.dv[pp].mod3 : 0);
+                    int vv8[8], vn8[8];
+                    if (c < G::NCHK)
+                        decode_chunk(pv[pp][h], w.dv[pp].bytes, w.dv[pp].scale, w.unit_v[pp], c, vv8,
+                                     XOPS ? w.dv[pp].mod3 : 0);
+                    else
 #pragma unroll
-                    for (int l = 0; l < LB; l++) {
-                        int x[8];
+                        for (int i = 0; i < 8; i++) vv8[i] = 0;
+                    const bool has_s = cs < G::NCHK - 1;
+                    if (has_s)
+                        decode_chunk(pn[pp][h], w.dv[pp].bytes, w.dv[pp].scale, w.unit_v[pp], cs + 1, vn8,
+                                     XOPS ? w.dv[pp].mod3 : 0);
+                    uint8_t *zr = sZR + pp * LB * G::Z_LEN;
+                    if (has_s) {
+                        // s[i] = b[i] + b[i-1] for i = 8cs+PD+j, j = 0..7, at Z[ZB_END + p - 1 - i]
+                        int s8[8];
 #pragma unroll
-                        for (int i = 0; i < 8; i++) x[i] = limb_of<LB>(vv8[i], l);
-                        *reinterpret_cast<uint2 *>(sZR + (pp * LB + l) * G::ZR_LEN + MM * G::NL - 8 - 8 * c) =
-                            make_uint2(pack4(x[7], x[6], x[5], x[4]), pack4(x[3], x[2], x[1], x[0]));
+                        for (int j = 0; j < 8; j++) {
+                            const int i0 = PD + j, i1 = PD + j - 1;
+                            s8[j] = (i0 < 8 ? vv8[i0] : vn8[i0 - 8]) + (i1 < 8 ? vv8[i1] : vn8[i1 - 8]);
+                        }
+                        const int zo = G::ZB_END + (P - PD) - 8 - 8 * cs;
+#pragma unroll
+                        for (int l = 0; l < LB; l++) {
+                            int x[8];
+#pragma unroll
+                            for (int j = 0; j < 8; j++) x[j] = limb_of<LB>(s8[j], l);
+                            *reinterpret_cast<uint2 *>(zr + l * G::Z_LEN + zo) =
+                                make_uint2(pack4(x[7], x[6], x[5], x[4]), pack4(x[3], x[2], x[1], x[0]));
+                        }
+                    }
+                    if (c < G::NCHK) {
+                        if (c == 0) {
+                            vv8[0] += pb1[pp];                     // bt[0] = b[0] + b[p-1]
+                            fixab[pp] = pa1 * pb1[pp];
+                        }
+                        const int zo = G::ZB_END - 8 - 8 * c;      // b[8c+i] at ZB_END - 1 - 8c - i
+#pragma unroll
+                        for (int l = 0; l < LB; l++) {
+                            int x[8];
+#pragma unroll
+                            for (int i = 0; i < 8; i++) x[i] = limb_of<LB>(vv8[i], l);
+                            *reinterpret_cast<uint2 *>(zr + l * G::Z_LEN + zo) =
+                                make_uint2(pack4(x[7], x[6], x[5], x[4]), pack4(x[3], x[2], x[1], x[0]));
+                        }
                     }
                 }
             }
@@ -357,28 +466,30 @@ __global__ void __launch_bounds__(128) tc_mul_kernel(MulArgs a) {
         __syncthreads();
         // ---- A: sliding windows, row rho = hA[rho .. rho+15] (descriptor starts at row 1);
         //      each work item builds rows 4m .. 4m+3 from 5 words, stores rotated by m (banks)
-#pragma unroll 1
-        for (int wi = tid; wi < LA * G::AROWS4; wi += 128) {
-            const int l = wi / G::AROWS4, m = wi - l * G::AROWS4;
-            const uint32_t *src = reinterpret_cast<const uint32_t *>(sHA + l * G::HA_LEN) + m;
-            uint32_t wd[5];
 #pragma unroll
-            for (int i = 0; i < 5; i++) wd[i] = src[i];
-            uint4 *dst = reinterpret_cast<uint4 *>(sA + l * G::A_BYTES) + 4 * m;
+        for (int l = 0; l < LA; l++) {
 #pragma unroll
-            for (int i = 0; i < 4; i++) {
-                const int s_ = (i + m) & 3;
-                const uint32_t sel = 0x3210u + (uint32_t)s_ * 0x1111u;   // bytes s..s+3 of (hi:lo)
-                uint4 o;
-                o.x = __byte_perm(wd[0], wd[1], sel);
-                o.y = __byte_perm(wd[1], wd[2], sel);
-                o.z = __byte_perm(wd[2], wd[3], sel);
-                o.w = __byte_perm(wd[3], wd[4], sel);
-                dst[s_] = o;
+            for (int kw = 0; kw < (G::AROWS4 + 127) / 128; kw++) {
+                const int m = tid + 128 * kw;
+                if (m >= G::AROWS4) break;
+                const uint32_t *src = reinterpret_cast<const uint32_t *>(sHA + l * G::HA_LEN) + m;
+                uint32_t wd[5];
+#pragma unroll
+                for (int i = 0; i < 5; i++) wd[i] = src[i];
+                uint4 *dst = reinterpret_cast<uint4 *>(sA + l * G::A_BYTES) + 4 * m;
+#pragma unroll
+                for (int i = 0; i < 4; i++) {
+                    uint4 o;
+                    o.x = __byte_perm(wd[0], wd[1], wsel[i]);
+                    o.y = __byte_perm(wd[1], wd[2], wsel[i]);
+                    o.z = __byte_perm(wd[2], wd[3], wsel[i]);
+                    o.w = __byte_perm(wd[3], wd[4], wsel[i]);
+                    dst[(i + tid) & 3] = o;
+                }
             }
         }
-        // ---- B: row (pp*PCOL + l*NL + t), K-chunk c = zr_{pp,l} chunk 8(NL-1-t) + c.  Work item
-        //      (row, res): chunks c = res + 8i; res = (item/BROWS + row) mod 8 keeps 8
+        // ---- B: row (pp*PCOL + l*NL + t), K-chunk c = 16-byte unit c of the row's Z window.
+        //      Work item (row, res): chunks c = res + 8i; res = (item/BROWS + row) mod 8 keeps 8
         //      consecutive lanes on distinct banks for both the load and the store.
 #pragma unroll
         for (int h = 0; h < G::BPER; h++) {
@@ -412,13 +523,13 @@ __global__ void __launch_bounds__(128) tc_mul_kernel(MulArgs a) {
         phase ^= 1;
         __syncthreads();
         tc_fence_after();
-        // ---- epilogue: thread tid = TMEM lane = coefficient r of every block, product by product
+        // ---- epilogue: thread tid = TMEM lane = coefficient r of every block; outputs go
+        //      straight to HBM (lane-consecutive coefficients: coalesced)
         const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
         // accumulator row of this thread (MM = 64: lanes 16..31 of each warp hold nothing)
         const int lane = tid & 31;
         const int rrow = MM == 128 ? tid : 16 * warp + lane;
         const bool rowok = MM == 128 || lane < 16;
-        // (the MMAs have completed, so the A region is free: combined values go straight to raw)
 #pragma unroll
         for (int pp = 0; pp < NPR; pp++) {
             int v[LA][G::PCOL / 16][16];
@@ -428,53 +539,35 @@ __global__ void __launch_bounds__(128) tc_mul_kernel(MulArgs a) {
                 for (int c16 = 0; c16 < G::PCOL / 16; c16++)
                     tmem_ld16(lane_addr + l * G::NB + pp * G::PCOL + 16 * c16, v[l][c16]);
             tmem_ld_wait();
-            if (rowok) {
+            const long long orow = w.orow[pp];
+            auto comb = [&](int t) {     // limb recombination of D column t (exact in int32)
+                auto D = [&](int l, int lb) { const int col = lb * G::NL + t; return v[l][col >> 4][col & 15]; };
+                if (LA == 1 && LB == 1) return D(0, 0);
+                if (LA == 1) return (64 * D(0, 0) + D(0, 1)) % M;
+                if (LB == 1) return (64 * D(0, 0) + D(1, 0)) % M;
+                return (4096 * (D(0, 0) % M) + 64 * (D(0, 1) + D(1, 0)) + D(1, 1)) % M;
+            };
+            int fix = 0;
+            if (warp == 0) fix = __shfl_sync(FULL, comb(G::NT), G::R0);   // = D(p-1)
+            if (orow < 0 || !rowok) continue;
+            auto store = [&](auto *op) {
+                constexpr int OSTRIDE = sizeof(*op) == 2 ? PS::P8 : PS::P16;
 #pragma unroll
-                for (int t = 0; t < G::NBLK; t++) {
-                    // D[l][lb*NL + t]
-                    auto D = [&](int l, int lb) { const int col = lb * G::NL + t; return v[l][col >> 4][col & 15]; };
-                    int x;
-                    if (LA == 1 && LB == 1) x = D(0, 0);
-                    else if (LA == 1) x = (64 * D(0, 0) + D(0, 1)) % M;
-                    else if (LB == 1) x = (64 * D(0, 0) + D(1, 0)) % M;
-                    else x = (4096 * (D(0, 0) % M) + 64 * (D(0, 1) + D(1, 0)) + D(1, 1)) % M;
-                    raw[pp * G::RAW_INTS + MM * t + rrow] = x;
+                for (int t = 0; t < G::NT; t++) {
+                    const int k = MM * t + rrow;
+                    if (k >= OSTRIDE) break;
+                    int x = comb(t);
+                    if (k == 0) x = x - fix + fixab[pp] % M;
+                    int vv = k < P ? canon<M>(x) : 0;
+                    if (XOPS && a.round3) vv -= canon<3>(vv);      // encapsulation's Round
+                    op[k] = (std::remove_reference_t<decltype(*op)>)vv;
                 }
-            }
+            };
+            uint8_t *orp = (uint8_t *)a.out + orow * a.out_stride * a.out_bytes;
+            if (a.out_bytes == 2) store(reinterpret_cast<int16_t *>(orp));
+            else store(reinterpret_cast<int8_t *>(orp));
         }
         tc_fence_before();   // TMEM reads ordered before the next item's MMAs (issued after later barriers)
-        __syncthreads();
-        // ---- fold with x^p = x + 1, center, store (lane-consecutive coefficients: no bank conflicts)
-        // (all shared-memory reads of a product issued before its arithmetic: one latency)
-        const int ostride_elems = a.out_bytes == 2 ? PS::P8 : PS::P16;
-        constexpr int FI = (PS::P16 + 127) / 128;
-#pragma unroll
-        for (int pp = 0; pp < NPR; pp++) {
-            const long long orow = w.orow[pp];
-            if (orow < 0) continue;
-            const int *rw = raw + pp * G::RAW_INTS;
-            int fa[FI], fb[FI], fc[FI];
-#pragma unroll
-            for (int i = 0; i < FI; i++) {
-                const int k = tid + 128 * i;
-                fa[i] = fb[i] = fc[i] = 0;
-                if (k < P) {
-                    fa[i] = rw[k];
-                    fb[i] = rw[k + P];
-                    fc[i] = k >= 1 ? rw[k + P - 1] : 0;
-                }
-            }
-#pragma unroll
-            for (int i = 0; i < FI; i++) {
-                const int k = tid + 128 * i;
-                if (k >= ostride_elems) break;
-                int v = k < P ? canon<M>(fa[i] + fb[i] + fc[i]) : 0;
-                if (XOPS && a.round3) v -= canon<3>(v);      // encapsulation's Round
-                if (a.out_bytes == 2) ((int16_t *)a.out)[orow * a.out_stride + k] = (int16_t)v;
-                else ((int8_t *)a.out)[orow * a.out_stride + k] = (int8_t)v;
-            }
-        }
-        // the next iteration's first __syncthreads orders these raw reads before A rewrites
     }
     tc_fence_before();
     __syncthreads();
