@@ -50,7 +50,7 @@ def parse():
 
 
 DEFAULT_B = 512
-DEFAULT_CHUNK = 65536
+DEFAULT_CHUNK = 32768
 DEFAULT_RING_STREAMS = True   # R/3 and R/q chains on two streams (measured best; A/B in DESIGN.md)
 MUL_IMPL = "tc"          # ring products on the tensor cores (see --mul-impl)
 TRAFFIC = {}             # dram bytes per launch of the dominant kernel, from profiles/ (ncu)
@@ -493,6 +493,7 @@ def main():
         # A/B: the same step without the shared-A down-sweep, and on the int32 schoolbook
         ab = {}
         for name, impl in (("tc_int8_m64", S.MUL_TENSOR_CORE_M64),
+                           ("tc_int8_big_single", S.MUL_TENSOR_CORE_I8_SINGLE),
                            ("tc_fp4_all_small", S.MUL_TENSOR_CORE_FP4_ALL),
                            ("tc_int8_shared_a", S.MUL_TENSOR_CORE_INT8),
                            ("tc_int8_no_shared_a", S.MUL_TENSOR_CORE_NO_SHARED_A),

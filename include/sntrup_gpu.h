@@ -190,13 +190,14 @@ uint64_t sntrup_kernel_launch_count(void);
 
 /* Select the ring-product implementation used by every call (measurement / A-B evidence):
    0 = tensor cores (the default): tcgen05.mma kind::mxf4 (e2m1) for small x small products
-       (R/3, 3f x 3f), kind::i8 (int8 limbs) otherwise; in the R/3 down-sweep the two children
+       (R/3, 3f x 3f), kind::i8 (int8 limbs) otherwise; in the down-sweeps the two children
        of a parent share one A operand;
    1 = int32 schoolbook on the integer pipes (v1);
    2 = int8 tensor cores only, one product per work item (v2);
    3 = int8 tensor cores only, with the shared-A R/3 down-sweep;
    4 = as 0, plus big x small products on fp4 with balanced base-9 digits (A/B only);
-   5 = as 0, with the int8 products at MMA M = 64 instead of 128 (A/B only).
+   5 = as 0, with the int8 products at MMA M = 64 instead of 128 (A/B only);
+   6 = as 0, with one int8 big x big product per work item (A/B only).
    All are exact.  Returns SNTRUP_OK or SNTRUP_E_ARG. */
 int sntrup_set_mul_impl(int impl);
 

@@ -390,7 +390,8 @@ TreePlan make_plan(long long m, int B) {
 // operand is small + int8 (tcmul.cuh) otherwise, shared-A down-sweep; 1 = int32 schoolbook;
 // 2 = int8 tensor cores only, one product per work item; 3 = int8 tensor cores with shared A;
 // 4 = as 0 but big x small products also on fp4 (base-9 digits; slower, kept for A/B);
-// 5 = as 0 but int8 products with MMA M = 64 (A/B for the M = 128 choice)
+// 5 = as 0 but int8 products with MMA M = 64 (A/B for the M = 128 choice);
+// 6 = as 0 but one int8 big x big product per work item (A/B for the shared-A down-sweep)
 int g_mul_impl = 0;
 
 struct DevInfo { int sms = 0; };
@@ -503,10 +504,11 @@ int launch_mul(MulArgs a, cudaStream_t s, int la = 2, int lb = 2) {
         return SNTRUP_OK;
     }
     // down-sweep with both operands of one kind: the two children of a parent share the parent's
-    // inverse as the A operand (one work item per parent)
-    // (R/3 and small x small only: for int8 big x big the stacked-N variant needs 2 CTAs/SM of
-    // smem and measured no faster than one product per item)
-    const bool down2 = (a.mode == MUL_DOWN || a.mode == MUL_DOWNH) && (M == 3 || (la == 1 && lb == 1)) &&
+    // inverse as the A operand (one work item per parent), halving the A-operand fetch that
+    // bounds the tensor-core products.  int8 big x big at M = 128 too since the folded B operand
+    // halved N (3 CTAs/SM); impl 6 keeps one big x big product per item for A/B.
+    const bool big2 = la == 2 && lb == 2 && g_mul_impl != 5 && g_mul_impl != 6;
+    const bool down2 = (a.mode == MUL_DOWN || a.mode == MUL_DOWNH) && (M == 3 || (la == 1 && lb == 1) || big2) &&
                        g_mul_impl != 2;
     if (down2) {
         a.mode = a.mode == MUL_DOWN ? MUL_DOWN2 : MUL_DOWNH2;
@@ -536,6 +538,7 @@ int launch_mul(MulArgs a, cudaStream_t s, int la = 2, int lb = 2) {
             return m128 ? launch_tc<PS, M, 1, 2>(a, s) : launch_tc<PS, M, 1, 2, 1, 64>(a, s);
         }
         a.swap = 0;
+        if (down2) return launch_tc<PS, M, 2, 2, 2>(a, s);
         return m128 ? launch_tc<PS, M, 2, 2>(a, s) : launch_tc<PS, M, 2, 2, 1, 64>(a, s);
     }
 }
@@ -1404,7 +1407,7 @@ int sntrup_profile_read_kinds(int reset, double *ms, double *ops, uint64_t *laun
 }
 
 int sntrup_set_mul_impl(int impl) {
-    if (impl < 0 || impl > 5) return SNTRUP_E_ARG;
+    if (impl < 0 || impl > 6) return SNTRUP_E_ARG;
     std::lock_guard<std::mutex> lk(g_mu);
     g_mul_impl = impl;
     return SNTRUP_OK;
