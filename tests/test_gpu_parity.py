@@ -128,7 +128,8 @@ def test_cfg2_full_size_sampled(O):
     # compared on a sample the oracle computes one by one: first and last trees, every 97th key.
     n = 65536
     for B, chunk, fl in ((32, 0, 0), (128, 0, 0), (2048, 0, 0), (1024, 32768, 0),
-                         (512, 65536, S.OPT_RING_STREAMS)):                 # last: bench.py's config
+                         (512, 65536, S.OPT_RING_STREAMS),
+                         (512, 32768, S.OPT_RING_STREAMS)):                 # last: bench.py's config
         res = S.batch_keygen(761, n, 2, batch_size=B, chunk_keys=chunk, flags=fl)
         torch.cuda.synchronize()
         idx = np.unique(np.concatenate([np.arange(0, 128), np.arange(n - 128, n), np.arange(0, n, 97)]))
