@@ -93,7 +93,10 @@ struct Tc4Geom {
     static constexpr int OFF_ZR = OFF_HA + HA_BYTES;
     static constexpr int OFF_BAR = OFF_ZR + NPR * LB * ZR_BYTES;
     static constexpr int SMEM = OFF_BAR + 128;
-    static constexpr int BROWS = NPR * LB * (NT + 1);
+    // B build work items: per (pp, limb) group RPG row slots (NT + 1 rows, padded to a multiple
+    // of 8 so 8 consecutive lanes own 8 distinct rows = 8 distinct bank groups); 8 items per slot
+    static constexpr int RPG = (NT + 1 + 7) / 8 * 8;
+    static constexpr int BROWS = NPR * LB * RPG;
     static constexpr int BITEMS = BROWS * 8;
     static constexpr int BPER = (BITEMS + 127) / 128;
     static_assert(NB <= 256, "N too large");
@@ -192,12 +195,15 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
 #pragma unroll
     for (int h = 0; h < G::BPER; h++) {
         const int w = tid + 128 * h;
-        if (w < G::BITEMS) {
-            const int row = w % G::BROWS, grp = w / G::BROWS;
-            const int pl = row / (G::NT + 1), t = row - pl * (G::NT + 1);   // pl = pp * LB + l
+        const int slot = w % G::BROWS, grp = w / G::BROWS;
+        const int pl = slot / G::RPG, t = slot - pl * G::RPG;    // pl = pp * LB + l
+        if (w < G::BITEMS && t <= G::NT) {
             const int pp = pl / LB, l = pl - pp * LB;
-            bres[h] = (grp + row) & 7;
-            bsrc[h] = pl * (G::ZR_BYTES / 16) + G::zrow(t) / 32;
+            const int zs = G::zrow(t) / 32;                        // window start, 16-byte units
+            // chunks c = res + 8i; res makes the loads of 8 consecutive lanes hit 8 bank groups
+            // (stores: row t mod 8 already distinct)
+            bres[h] = (grp + slot - zs) & 7;
+            bsrc[h] = pl * (G::ZR_BYTES / 16) + zs;
             bdst[h] = pp * G::PCOL + l * G::NL + t;
         } else {
             bsrc[h] = -1; bdst[h] = 0; bres[h] = 0;
@@ -208,11 +214,11 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
     int pa1 = 0, pb1[NPR];
 #pragma unroll
     for (int pp = 0; pp < NPR; pp++) pb1[pp] = 0;
-    // window rows 4m+s, s = (i + m) mod 4 (rotated by m against bank conflicts), m = tid mod 128:
-    // nibble shifts are per-thread constants
+    // window rows 4m+s, s = (i + m/2) mod 4 (8 consecutive threads' 16-byte stores hit 8 distinct
+    // bank groups), m = tid mod 128: nibble shifts are per-thread constants
     uint32_t wsh[4];
 #pragma unroll
-    for (int i = 0; i < 4; i++) wsh[i] = 16u * (uint32_t)(tid & 1) + 4u * (uint32_t)((i + tid) & 3);
+    for (int i = 0; i < 4; i++) wsh[i] = 16u * (uint32_t)(tid & 1) + 4u * (uint32_t)((i + (tid >> 1)) & 3);
     TcWork<NPR> wn;                                       // work item of the prefetched rows
     auto prefetch = [&](long long it) {
         if (it >= a.n_out) return;
@@ -341,7 +347,7 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
                 o.y = __funnelshift_r(wd[1], wd[2], wsh[i]);
                 o.z = __funnelshift_r(wd[2], wd[3], wsh[i]);
                 o.w = __funnelshift_r(wd[3], wd[4], wsh[i]);
-                dst[(i + tid) & 3] = o;
+                dst[(i + (tid >> 1)) & 3] = o;
             }
         }
         // ---- B rows (aligned 16-byte chunks of the rows' Z windows)

@@ -171,7 +171,10 @@ struct TcGeom {
     static_assert(ZMARG + MM * (NT - 1) + K <= Z_LEN, "Z too short");
     // B build: (row, residue mod 8) work items; row = pp*PCOL + l*NL + t (t <= NT), K-chunks
     // c = residue + 8i
-    static constexpr int BROWS = NPR * LB * (NT + 1);
+    // B build work items: per (pp, limb) group RPG row slots (NT + 1 rows, padded to a multiple
+    // of 8 so 8 consecutive lanes own 8 distinct rows = 8 distinct bank groups); 8 items per slot
+    static constexpr int RPG = (NT + 1 + 7) / 8 * 8;
+    static constexpr int BROWS = NPR * LB * RPG;
     static constexpr int NCHB = 2 * NKS;                      // 16-byte K-chunks per B row
     static constexpr int BITEMS = BROWS * 8;
     static constexpr int BPER = (BITEMS + 127) / 128;
@@ -338,12 +341,15 @@ __global__ void __launch_bounds__(128, (TcGeom<PS, LA, LB, NPR, MM>::MINB)) tc_m
 #pragma unroll
     for (int h = 0; h < G::BPER; h++) {
         const int w = tid + 128 * h;
-        if (w < G::BITEMS) {
-            const int row = w % G::BROWS, grp = w / G::BROWS;
-            const int pl = row / (G::NT + 1), t = row - pl * (G::NT + 1);   // pl = pp * LB + l
+        const int slot = w % G::BROWS, grp = w / G::BROWS;
+        const int pl = slot / G::RPG, t = slot - pl * G::RPG;    // pl = pp * LB + l
+        if (w < G::BITEMS && t <= G::NT) {
             const int pp = pl / LB, l = pl - pp * LB;
-            bres[h] = (grp + row) & 7;
-            bsrc[h] = pl * (G::Z_LEN / 16) + G::zrow(t) / 16;
+            const int zs = G::zrow(t) / 16;                        // window start, 16-byte units
+            // chunks c = res + 8i; res makes the loads of 8 consecutive lanes hit 8 bank groups
+            // (stores: row t mod 8 already distinct)
+            bres[h] = (grp + slot - zs) & 7;
+            bsrc[h] = pl * (G::Z_LEN / 16) + zs;
             bdst[h] = pp * G::PCOL + l * G::NL + t;
         } else {
             bsrc[h] = -1; bdst[h] = 0; bres[h] = 0;
@@ -357,11 +363,12 @@ __global__ void __launch_bounds__(128, (TcGeom<PS, LA, LB, NPR, MM>::MINB)) tc_m
     int pa1 = 0, pb1[NPR];
 #pragma unroll
     for (int pp = 0; pp < NPR; pp++) pb1[pp] = 0;
-    // A-window rows 4m+s (s = (i + m) mod 4, stored rotated by m against bank conflicts): m = tid
-    // mod 128, so the byte selectors are per-thread constants
+    // A-window rows 4m+s, s = (i + m/2) mod 4: 8 consecutive threads' 16-byte stores then hit 8
+    // distinct bank groups (64m + 16s); m = tid mod 128, so the byte selectors are per-thread
+    // constants
     uint32_t wsel[4];
 #pragma unroll
-    for (int i = 0; i < 4; i++) wsel[i] = 0x3210u + (uint32_t)((i + tid) & 3) * 0x1111u;   // bytes s..s+3
+    for (int i = 0; i < 4; i++) wsel[i] = 0x3210u + (uint32_t)((i + (tid >> 1)) & 3) * 0x1111u;   // bytes s..s+3
     TcWork<NPR> wn;                                       // work item of the prefetched rows
     auto prefetch = [&](long long it) {
         if (it >= a.n_out) return;
@@ -484,7 +491,7 @@ __global__ void __launch_bounds__(128, (TcGeom<PS, LA, LB, NPR, MM>::MINB)) tc_m
                     o.y = __byte_perm(wd[1], wd[2], wsel[i]);
                     o.z = __byte_perm(wd[2], wd[3], wsel[i]);
                     o.w = __byte_perm(wd[3], wd[4], wsel[i]);
-                    dst[(i + tid) & 3] = o;
+                    dst[(i + (tid >> 1)) & 3] = o;
                 }
             }
         }
