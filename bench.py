@@ -44,14 +44,17 @@ def parse():
     ap.add_argument("--no-extras", action="store_true", help="skip B sweep / rq_mul / cpu baseline")
     ap.add_argument("--ring-streams", type=int, choices=[0, 1], default=-1,
                     help="R/3 and R/q tree chains on separate streams (default: tuned)")
+    ap.add_argument("--lanes", type=int, choices=[0, 2, 4], default=0,
+                    help="chunks pipelined concurrently (0 = tuned default)")
     ap.add_argument("--mul-impl", choices=["tc", "schoolbook"], default="tc",
                     help="ring products: tcgen05 int8 Hankel GEMM (default) or int32 schoolbook")
     return ap.parse_args()
 
 
-DEFAULT_B = 512
+DEFAULT_B = 1024
 DEFAULT_CHUNK = 32768
 DEFAULT_RING_STREAMS = True   # R/3 and R/q chains on two streams (measured best; A/B in DESIGN.md)
+DEFAULT_LANES = 2
 MUL_IMPL = "tc"          # ring products on the tensor cores (see --mul-impl)
 TRAFFIC = {}             # dram bytes per launch of the dominant kernel, from profiles/ (ncu)
 
@@ -339,7 +342,8 @@ def main():
     CHUNK = args.chunk_keys or DEFAULT_CHUNK
 
     RINGS = DEFAULT_RING_STREAMS if args.ring_streams < 0 else bool(args.ring_streams)
-    FLAGS = S.OPT_ASYNC | (S.OPT_RING_STREAMS if RINGS else 0)
+    LANES = args.lanes or DEFAULT_LANES
+    FLAGS = S.OPT_ASYNC | (S.OPT_RING_STREAMS if RINGS else 0) | (S.OPT_LANES4 if LANES == 4 else 0)
 
     def step(batch=B, chunk=None):
         S.batch_keygen(PARAM, n, SEED, first_key_index=first, batch_size=batch, pk_out=pk,
@@ -410,6 +414,15 @@ def main():
             e2e_by_chunk["%d%s" % (chunk, "+rings" if rings else "")] = world * n * e2e_steps / (ms_c / 1e3)
     best_chunk = max(e2e_by_chunk, key=e2e_by_chunk.get)
     e2e_value = e2e_by_chunk[best_chunk]
+    # the e2e ceiling set by the host link: one device->pinned-host copy of a step's pk+sk bytes
+    d2h_b = n * (P["pk_bytes"] + P["sk_bytes"])
+    dbuf = torch.empty(d2h_b, dtype=torch.uint8, device="cuda")
+    hbuf = torch.empty(d2h_b, dtype=torch.uint8).pin_memory()
+    hbuf.copy_(dbuf, non_blocking=True)
+    torch.cuda.synchronize()
+    d2h_ms = timed(lambda: hbuf.copy_(dbuf, non_blocking=True), 3) / 3
+    d2h_gbs = d2h_b / (d2h_ms / 1e3) / 1e9
+    del dbuf, hbuf
     clocks = clk.stop()
 
     result = {}
@@ -459,6 +472,7 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
             "config": {"workload": "configs[1]: sntrup761 batch keygen, 65,536 keys per GPU, seed 2",
                        "keys_per_gpu": n, "batch_size": B, "chunk_keys": CHUNK, "ring_streams": RINGS,
+                       "lanes": LANES,
                        "param_set": PARAM,
                        "l2": "flushed between timed steps (256 MiB write); working set > L2",
                        "parallelism": "key ranges per GPU (no collective)"},
@@ -468,6 +482,8 @@ def main():
                     "d2h_bytes_per_step": world * n * (P["pk_bytes"] + P["sk_bytes"]),
                     "chunk_keys": best_chunk,
                     "by_chunk_keys": e2e_by_chunk,
+                    "d2h_gbs_measured": d2h_gbs,
+                    "d2h_ceiling_keys_per_s": world * d2h_gbs * 1e9 / (P["pk_bytes"] + P["sk_bytes"]),
                     "note": "inputs are (param, n, seed, first key index): no H2D payload; "
                             "pk/sk copied D2H into pinned host buffers inside the timed region"},
             "roofline": roof,

@@ -80,6 +80,8 @@ int sntrup_batch_keygen(int param_set, uint64_t n_keys, uint64_t seed,
                                          B * P(small-factor rejection per draw) <= 1e-4,
                                          e.g. 761/857;
                                          outputs are identical either way) */
+#define SNTRUP_OPT_LANES4         32u /* pipeline up to 4 chunks concurrently (one stream set per
+                                         lane) instead of 2; outputs identical */
 
 typedef struct {
     uint64_t first_key_index; /* keys first .. first+n-1 (chunked / resumable / multi-GPU runs) */

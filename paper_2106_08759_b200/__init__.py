@@ -34,6 +34,7 @@ OPT_NO_SMALL_CHECK = 2
 OPT_ASYNC = 4
 OPT_FORCE_SMALL_CHECK = 8
 OPT_RING_STREAMS = 16
+OPT_LANES4 = 32
 
 PARAM_SETS = (653, 761, 857, 953, 1013, 1277)
 

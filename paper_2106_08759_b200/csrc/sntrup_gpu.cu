@@ -682,12 +682,12 @@ struct Lane {
     int *err = nullptr;
 };
 
-// internal second lane: a stream and its own aux stream (per device)
-int lane2_streams(cudaStream_t *s2, AuxStream **ax2) {
-    static std::map<int, std::pair<cudaStream_t, AuxStream>> m;
+// internal lane li >= 1: a stream and its own aux stream (per device)
+int lane_streams(int li, cudaStream_t *s2, AuxStream **ax2) {
+    static std::map<std::pair<int, int>, std::pair<cudaStream_t, AuxStream>> m;
     int dev = 0;
     CK(cudaGetDevice(&dev));
-    auto &e = m[dev];
+    auto &e = m[std::make_pair(dev, li)];
     if (!e.first) {
         CK(cudaStreamCreateWithFlags(&e.first, cudaStreamNonBlocking));
         CK(cudaStreamCreateWithFlags(&e.second.s, cudaStreamNonBlocking));
@@ -714,7 +714,8 @@ int ring_stream(int lane, AuxStream **out) {
     return SNTRUP_OK;
 }
 
-struct LaneJoin { cudaEvent_t start = nullptr, end = nullptr; };
+constexpr int MAX_LANES = 4;
+struct LaneJoin { cudaEvent_t start = nullptr, end[MAX_LANES] = {}; };
 int lane_join_events(LaneJoin **out) {
     static std::map<int, LaneJoin> m;
     int dev = 0;
@@ -722,7 +723,7 @@ int lane_join_events(LaneJoin **out) {
     LaneJoin &j = m[dev];
     if (!j.start) {
         CK(cudaEventCreateWithFlags(&j.start, cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&j.end, cudaEventDisableTiming));
+        for (int i = 0; i < MAX_LANES; i++) CK(cudaEventCreateWithFlags(&j.end[i], cudaEventDisableTiming));
     }
     *out = &j;
     return SNTRUP_OK;
@@ -745,7 +746,9 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
     if (chunk > n) chunk = (n + B - 1) / B * B;
     const size_t pkb = tb->enc.pk_bytes, skb = 2 * PS::SKH;
     const uint64_t nchunks = (n + chunk - 1) / chunk;
-    const int nl = nchunks >= 2 ? 2 : 1;
+    const int nlmax = (o.flags & SNTRUP_OPT_LANES4) ? 4 : 2;
+    const int nl = (int)(nchunks < (uint64_t)nlmax ? nchunks : nlmax);
+    const int nbuf = nl >= 2 ? nl : 2;          // host-output staging buffers (lane-owned if nl >= 2)
 
     // workspace: one chunk's buffers per lane (+ shared host-output staging)
     const TreePlan tpmax = make_plan((long long)chunk, B);
@@ -759,16 +762,16 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
     per_lane += 2 * align256(tpmax.cnt[tpmax.L]);                // root ok flags
     per_lane += 2 * 256;                                         // counters
     size_t need = nl * per_lane + 4096;
-    if (host_out) need += 2 * (align256(chunk * pkb) + align256(chunk * skb));
+    if (host_out) need += nbuf * (align256(chunk * pkb) + align256(chunk * skb));
     if ((rc = ws_reserve(need, s0))) return rc;
-    Lane lanes[2];
+    Lane lanes[MAX_LANES];
     for (int li = 0; li < nl; li++) {
         Lane &L = lanes[li];
         if (li == 0) {
             L.s = s0;
             if ((rc = aux_stream(&L.ax))) return rc;
         } else {
-            if ((rc = lane2_streams(&L.s, &L.ax))) return rc;
+            if ((rc = lane_streams(li, &L.s, &L.ax))) return rc;
         }
         L.G = ws_take<int8_t>(chunk * PS::P16);
         L.F = ws_take<int8_t>(chunk * PS::P16);
@@ -792,10 +795,10 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
         if (o.flags & SNTRUP_OPT_RING_STREAMS)
             if ((rc = ring_stream(li, &L.r3))) return rc;
     }
-    uint8_t *pk_stage[2] = {nullptr, nullptr}, *sk_stage[2] = {nullptr, nullptr};
-    CopyStream *csl[2] = {nullptr, nullptr};       // one copy stream per lane: copies follow readiness
+    uint8_t *pk_stage[MAX_LANES] = {}, *sk_stage[MAX_LANES] = {};
+    CopyStream *csl[MAX_LANES] = {};               // one copy stream per lane: copies follow readiness
     if (host_out) {
-        for (int i = 0; i < 2; i++) {
+        for (int i = 0; i < nbuf; i++) {
             pk_stage[i] = ws_take<uint8_t>(chunk * pkb);
             sk_stage[i] = ws_take<uint8_t>(chunk * skb);
         }
@@ -804,10 +807,10 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
         if (nl == 1) csl[1] = csl[0];
     }
     LaneJoin *lj = nullptr;
-    if (nl > 1) {                          // lane 1 starts after everything enqueued before the call
+    if (nl > 1) {                          // lanes >= 1 start after everything enqueued before the call
         if ((rc = lane_join_events(&lj))) return rc;
         CK(cudaEventRecord(lj->start, s0));
-        CK(cudaStreamWaitEvent(lanes[1].s, lj->start, 0));
+        for (int li = 1; li < nl; li++) CK(cudaStreamWaitEvent(lanes[li].s, lj->start, 0));
     }
     for (int li = 0; li < nl; li++) {
         CK(cudaMemsetAsync(lanes[li].repaired, 0, sizeof(unsigned long long), lanes[li].s));
@@ -822,18 +825,18 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
         const uint64_t ci = c0 / chunk;
         Lane &L = lanes[ci % nl];
         const cudaStream_t s = L.s;                          // this chunk's stream
-        // host outputs: staging buffer pair indexed by chunk parity (both lanes share the copy
-        // stream); a pair is reused two chunks later, after its copies
-        const int buf = (int)(ci & 1);
+        // host outputs: staging buffer ci mod nbuf (= the lane's own with >= 2 lanes, alternating
+        // with one lane), reused nbuf chunks later after its copies; events by buffer parity
+        const int sb = (int)(ci % nbuf), buf = sb & 1;
         int8_t *Gc = o.g_out ? o.g_out + c0 * PS::P16 : L.G;
         int8_t *Fc = o.f_out ? o.f_out + c0 * PS::P16 : L.F;
         int8_t *Ic = o.ginv_out ? o.ginv_out + c0 * PS::P16 : L.Ginv;
         uint8_t *Ac = o.attempts_out ? o.attempts_out + c0 : L.att;
         int16_t *Hc = o.h_out ? o.h_out + c0 * PS::P8 : L.H;
         CopyStream *cs = csl[ci % nl];
-        if (host_out && ci >= 2) CK(cudaStreamWaitEvent(s, cs->copy[buf], 0));   // staging free
-        uint8_t *pkc = host_out ? pk_stage[buf] : pk_out + c0 * pkb;
-        uint8_t *skc = host_out ? sk_stage[buf] : sk_out + c0 * skb;
+        if (host_out && ci >= (uint64_t)nbuf) CK(cudaStreamWaitEvent(s, cs->copy[buf], 0));   // staging free
+        uint8_t *pkc = host_out ? pk_stage[sb] : pk_out + c0 * pkb;
+        uint8_t *skc = host_out ? sk_stage[sb] : sk_out + c0 * skb;
 
         SampleArgs sa{};
         sa.seed = seed; sa.first = first; sa.n = m;
@@ -985,9 +988,9 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
         n_rq += m;
         if (host_out) CK(cudaEventRecord(cs->copy[buf], cs->s));
         }
-    if (nl > 1) {                          // join lane 1 into the caller's stream
-        CK(cudaEventRecord(lj->end, lanes[1].s));
-        CK(cudaStreamWaitEvent(s0, lj->end, 0));
+    for (int li = 1; li < nl; li++) {      // join the lanes into the caller's stream
+        CK(cudaEventRecord(lj->end[li], lanes[li].s));
+        CK(cudaStreamWaitEvent(s0, lj->end[li], 0));
     }
     if (host_out) {                        // join the copies into the caller's stream
         for (int li = 0; li < nl; li++)
@@ -995,19 +998,20 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
     }
     const bool sync = !(o.flags & SNTRUP_OPT_ASYNC) || host_out || o.stats_out;
     if (sync) {
-        int herr[2] = {0, 0};
-        unsigned long long hrep[2] = {0, 0};
+        int herr[MAX_LANES] = {};
+        unsigned long long hrep[MAX_LANES] = {};
         for (int li = 0; li < nl; li++) {
             CK(cudaMemcpyAsync(&herr[li], lanes[li].err, sizeof(int), cudaMemcpyDeviceToHost, s0));
             CK(cudaMemcpyAsync(&hrep[li], lanes[li].repaired, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s0));
         }
         CK(cudaStreamSynchronize(s0));
-        if (herr[0] || herr[1]) return SNTRUP_E_INTERNAL;
+        for (int li = 0; li < nl; li++)
+            if (herr[li]) return SNTRUP_E_INTERNAL;
         if (o.stats_out) {
             o.stats_out[0] = n_rq;
             o.stats_out[1] = n_r3;
             o.stats_out[2] = n_inv;
-            o.stats_out[3] = hrep[0] + hrep[1];
+            o.stats_out[3] = hrep[0] + hrep[1] + hrep[2] + hrep[3];
         }
     }
     return SNTRUP_OK;

@@ -113,12 +113,15 @@ def test_small_check_policies_761(O, flags):
     check_keys(O, 761, 17, res, np.arange(n))
 
 
-def test_host_output(O):
+@pytest.mark.parametrize("flags", [0, S.OPT_RING_STREAMS, S.OPT_LANES4, S.OPT_LANES4 | S.OPT_RING_STREAMS])
+def test_host_output(O, flags):
+    # host outputs through the staging buffers / copy streams, 1, 2 and 4 lanes (4 chunks of 32
+    # keys -> every lane reuses its staging buffer)
     P = S.params(761)
-    n = 100
+    n = 100 if not flags else 260
     pk = torch.empty((n, P["pk_bytes"]), dtype=torch.uint8).pin_memory()
     sk = torch.empty((n, P["sk_bytes"]), dtype=torch.uint8).pin_memory()
-    S.batch_keygen(761, n, 11, pk_out=pk, sk_out=sk, flags=S.OPT_HOST_OUTPUT, chunk_keys=32)
+    S.batch_keygen(761, n, 11, pk_out=pk, sk_out=sk, flags=S.OPT_HOST_OUTPUT | flags, chunk_keys=32)
     ref = oracle_keys(O, 761, 11, np.arange(n))
     assert np.array_equal(pk.numpy(), ref["pk"]) and np.array_equal(sk.numpy(), ref["sk"])
 
@@ -128,8 +131,9 @@ def test_cfg2_full_size_sampled(O):
     # compared on a sample the oracle computes one by one: first and last trees, every 97th key.
     n = 65536
     for B, chunk, fl in ((32, 0, 0), (128, 0, 0), (2048, 0, 0), (1024, 32768, 0),
-                         (512, 65536, S.OPT_RING_STREAMS),
-                         (512, 32768, S.OPT_RING_STREAMS)):                 # last: bench.py's config
+                         (512, 65536, S.OPT_RING_STREAMS), (512, 16384, S.OPT_LANES4),
+                         (1024, 16384, S.OPT_LANES4 | S.OPT_RING_STREAMS),
+                         (1024, 32768, S.OPT_RING_STREAMS)):                # last: bench.py's config
         res = S.batch_keygen(761, n, 2, batch_size=B, chunk_keys=chunk, flags=fl)
         torch.cuda.synchronize()
         idx = np.unique(np.concatenate([np.arange(0, 128), np.arange(n - 128, n), np.arange(0, n, 97)]))
