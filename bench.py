@@ -135,6 +135,27 @@ def int8_tc_peak_tops(peaks: dict):
     return 2.0 * 1400.0, "fallback 1.4 PF/s sustained bf16 (B200_PROFILING.md) x 2"
 
 
+def binding_resource(kind):
+    """What bounds the dominant ring-product kernels, from the committed ncu capture
+    (profiles/ncu_pipes.json): the largest launch of each kernel of that kind."""
+    pipes = load_ncu_pipes() or {}
+    tag = "tc_mul_kernel" if kind == "tc_int8" else "tc4_mul_kernel"
+    ev = {}
+    for name, e in pipes.get("kernels", {}).items():
+        if tag in name and e.get("largest_launch"):
+            L = e["largest_launch"]
+            ev[name.replace("void ", "")] = {
+                "tc_pipe_pct": L.get("tc_pipe_pct"), "tensor_math_pct": L.get("tensor_math_pct"),
+                "smem_tc_wavefronts_pct": L.get("smem_tc_wavefronts_pct"),
+                "smem_lsu_wavefronts_pct": L.get("smem_lsu_wavefronts_pct"),
+                "issue_active_pct": L.get("issue_active_pct"), "duration_us": L.get("duration_us")}
+    return {"resource": "shared-memory operand traffic: every MMA of a small-N GEMM re-reads its "
+                        "128 x 32-byte Hankel A tile (UMMA operand fetch, tc wavefronts) while the "
+                        "next item's operands are built (LSU wavefronts); tensor math stays low",
+            "evidence_largest_launch": ev,
+            "source": "profiles/ncu_pipes.json (ncu --clock-control none), DESIGN.md section 6.1"}
+
+
 def load_ncu_pipes():
     """Time-weighted pipe utilisation per kernel of the step from the committed ncu capture
     (profiles/ncu_pipes.json, written by scripts/ncu_pipes.py); {} if absent."""
@@ -453,11 +474,7 @@ def main():
                         "peak_source": src + ("" if kd == "tc_int8" else " x 2 (nominal fp4/int8 ratio 9/4.5 PF)"),
                         "share_of_step": share,
                         "by_kind_ms_per_step": {k: v["ms"] / args.steps for k, v in kinds.items()},
-                        "binding_resource": "the UMMA operand fetch from shared memory (every MMA of a "
-                                            "small-N GEMM re-reads its 128x32-byte A tile): ncu "
-                                            "sm__pipe_tc_cycles_active ~93% time-weighted over the "
-                                            "step's int8 launches vs tensor math ~33% "
-                                            "(profiles/ncu_pipes.json, DESIGN.md section 6.1)"}
+                        "binding_resource": binding_resource(kd)}
             else:
                 peak = 2 * int_peak_macs_per_s(sm_mhz) / 1e12
                 roof = {"bound": "alu", "kernel": "ring products, ring_mul_kernel (int32 schoolbook)",

@@ -22,6 +22,10 @@ M = {
     "duration_us": "gpu__time_duration.sum",
     "grid": "launch__grid_size",
     "registers": "launch__registers_per_thread",
+    "smem_lsu_wavefronts_pct": "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+    "smem_tc_wavefronts_pct": "l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+    "smem_bank_conflicts": "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+    "smem_lsu_wavefronts": "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
 }
 
 
@@ -53,7 +57,8 @@ def main():
             e = out["kernels"].setdefault(name, {"launches": 0, "time_weighted": {}, "largest_launch": None})
             e["launches"] += 1
             w = d.get("duration_us", 0)
-            for k in ("issue_active_pct", "alu_pipe_pct", "fma_pipe_pct", "tensor_math_pct", "tc_pipe_pct"):
+            for k in ("issue_active_pct", "alu_pipe_pct", "fma_pipe_pct", "tensor_math_pct", "tc_pipe_pct",
+                      "smem_lsu_wavefronts_pct", "smem_tc_wavefronts_pct"):
                 if k in d:
                     e["time_weighted"][k] = e["time_weighted"].get(k, 0) + w * d[k]
             e["_w"] = e.get("_w", 0) + w
