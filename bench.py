@@ -417,22 +417,26 @@ def main():
     pk_h = torch.empty((n, P["pk_bytes"]), dtype=torch.uint8).pin_memory()
     sk_h = torch.empty((n, P["sk_bytes"]), dtype=torch.uint8).pin_memory()
 
-    def step_host(chunk, rings):
+    def step_host(chunk, fl):
         S.batch_keygen(PARAM, n, SEED, first_key_index=first, batch_size=B, pk_out=pk_h,
-                       sk_out=sk_h, flags=S.OPT_HOST_OUTPUT | (S.OPT_RING_STREAMS if rings else 0),
-                       chunk_keys=chunk)
+                       sk_out=sk_h, flags=S.OPT_HOST_OUTPUT | fl, chunk_keys=chunk)
 
     # the chunk size trades D2H/compute overlap against per-chunk latency phases, and the ring
     # streams interact with the copy streams: measure the candidates and report the best (all are
     # in the line)
     e2e_steps = max(2, args.steps // 2)
+    # (lane priority: the first lane's chunk completes early, so its pk/sk copies overlap the
+    # other lanes' compute instead of queueing behind the end of the step)
     e2e_by_chunk = {}
-    for chunk in (16384, 32768, 65536):
-        for rings in (False, True):
-            step_host(chunk, rings)
-            barrier()
-            ms_c = timed(lambda: step_host(chunk, rings), e2e_steps)
-            e2e_by_chunk["%d%s" % (chunk, "+rings" if rings else "")] = world * n * e2e_steps / (ms_c / 1e3)
+    R, PR, L4 = S.OPT_RING_STREAMS, S.OPT_LANE_PRIORITY, S.OPT_LANES4
+    for chunk, fl, tag in ((65536, R, "+rings"), (32768, 0, ""), (32768, R, "+rings"),
+                           (16384, R, "+rings"), (32768, R | PR, "+rings+prio"),
+                           (16384, R | PR, "+rings+prio"), (16384, PR | L4, "+prio+lanes4"),
+                           (8192, R | PR, "+rings+prio")):
+        step_host(chunk, fl)
+        barrier()
+        ms_c = timed(lambda: step_host(chunk, fl), e2e_steps)
+        e2e_by_chunk["%d%s" % (chunk, tag)] = world * n * e2e_steps / (ms_c / 1e3)
     best_chunk = max(e2e_by_chunk, key=e2e_by_chunk.get)
     e2e_value = e2e_by_chunk[best_chunk]
     # the e2e ceiling set by the host link: one device->pinned-host copy of a step's pk+sk bytes

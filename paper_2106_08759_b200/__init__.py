@@ -35,6 +35,7 @@ OPT_ASYNC = 4
 OPT_FORCE_SMALL_CHECK = 8
 OPT_RING_STREAMS = 16
 OPT_LANES4 = 32
+OPT_LANE_PRIORITY = 64
 
 PARAM_SETS = (653, 761, 857, 953, 1013, 1277)
 

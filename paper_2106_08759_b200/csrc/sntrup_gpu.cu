@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <tuple>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -287,13 +288,30 @@ int build_tables(int dev, int ps, int WT, DevTables **out) {
 // Host-output keygen: chunk i's pk/sk are copied device->host on a copy stream while chunk i+1
 // computes (double-buffered device staging).  One per device (calls are serialised).
 struct CopyStream { cudaStream_t s = nullptr; cudaEvent_t comp[2] = {}, copy[2] = {}; };
-int copy_stream(CopyStream **out, int which = 0) {   // which: pipeline lane (0 or 1)
-    static std::map<std::pair<int, int>, CopyStream> m;
+// SNTRUP_OPT_LANE_PRIORITY: lane li's streams get priority rank li (lane 0 highest), so the
+// scheduler finishes lane 0's chunk first while the other lanes fill its latency gaps; -1 = the
+// default priority.
+int lane_priority(int prio_rank) {
+    if (prio_rank < 0) return 0;
+    int least = 0, greatest = 0;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    const int p = greatest + prio_rank;                  // greatest is numerically lowest
+    return p > least ? least : p;
+}
+
+int make_stream(cudaStream_t *s, int prio_rank) {
+    if (prio_rank < 0) CK(cudaStreamCreateWithFlags(s, cudaStreamNonBlocking));
+    else CK(cudaStreamCreateWithPriority(s, cudaStreamNonBlocking, lane_priority(prio_rank)));
+    return SNTRUP_OK;
+}
+
+int copy_stream(CopyStream **out, int which = 0, int prio_rank = -1) {   // which: pipeline lane
+    static std::map<std::tuple<int, int, int>, CopyStream> m;
     int dev = 0;
     CK(cudaGetDevice(&dev));
-    CopyStream &c = m[std::make_pair(dev, which)];
+    CopyStream &c = m[std::make_tuple(dev, which, prio_rank)];
     if (!c.s) {
-        CK(cudaStreamCreateWithFlags(&c.s, cudaStreamNonBlocking));
+        if (make_stream(&c.s, prio_rank)) return SNTRUP_E_CUDA;
         for (int i = 0; i < 2; i++) {
             CK(cudaEventCreateWithFlags(&c.comp[i], cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&c.copy[i], cudaEventDisableTiming));
@@ -369,6 +387,12 @@ T *ws_take(size_t count) {
 size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
 // ------------------------------------------------------------------------------ tree plan
+// rows r.. of a row descriptor
+inline RowDesc row_offset(RowDesc d, long long r) {
+    if (d.ptr) d.ptr = (const uint8_t *)d.ptr + r * d.stride * d.bytes;
+    return d;
+}
+
 struct TreePlan {
     int L;                          // levels = log2(B)
     std::vector<long long> cnt;     // cnt[0] = leaves, cnt[l] = ceil(cnt[l-1]/2)
@@ -617,15 +641,24 @@ struct TreeJob {
         return ia;
     }
     int down(cudaStream_t s, uint64_t *nprod, int stop = 1) const {
+        return down_group(s, nprod, tp.L, stop, 0, tp.cnt[tp.L]);
+    }
+    // Levels hi .. lo of the down-sweep restricted to the subtrees of roots [ra, rb): at level l
+    // they own rows [ra << (L-l), rb << (L-l)) (a contiguous range of every level).
+    int down_group(cudaStream_t s, uint64_t *nprod, int hi, int lo, long long ra, long long rb) const {
         int rc;
-        for (int l = tp.L; l >= stop; l--) {
+        for (int l = hi; l >= lo; l--) {
+            const long long r0 = ra << (tp.L - l + 1);
+            long long r1 = rb << (tp.L - l + 1);
+            if (r1 > tp.cnt[l - 1]) r1 = tp.cnt[l - 1];
+            if (r1 <= r0) continue;
             MulArgs a{};
             a.mode = MUL_DOWN;
-            a.n_out = tp.cnt[l - 1];
-            a.cnt_in = tp.cnt[l - 1];
-            a.X = desc(l - 1);
-            a.Y = idesc(l);
-            const RowDesc od = idesc(l - 1);
+            a.n_out = r1 - r0;
+            a.cnt_in = r1 - r0;
+            a.X = row_offset(desc(l - 1), r0);
+            a.Y = row_offset(idesc(l), r0 / 2);
+            const RowDesc od = row_offset(idesc(l - 1), r0);
             a.out = const_cast<void *>(od.ptr);
             a.out_stride = od.stride;
             a.out_bytes = out_bytes;
@@ -633,7 +666,7 @@ struct TreeJob {
             // operands: (inverse of the parent: big) x (sibling: small at level 1 over small leaves)
             const int lsib = (M == 3 || (l == 1 && leaves_small)) ? 1 : 2;
             if ((rc = launch_mul<PS, M>(a, s, M == 3 ? 1 : 2, lsib))) return rc;
-            *nprod += (tp.cnt[l - 1] / 2) * 2;
+            *nprod += ((r1 - r0) / 2) * 2;
         }
         return SNTRUP_OK;
     }
@@ -682,15 +715,14 @@ struct Lane {
     int *err = nullptr;
 };
 
-// internal lane li >= 1: a stream and its own aux stream (per device)
-int lane_streams(int li, cudaStream_t *s2, AuxStream **ax2) {
-    static std::map<std::pair<int, int>, std::pair<cudaStream_t, AuxStream>> m;
+// internal lane li: a stream and its own aux stream (per device, per priority mode)
+int lane_streams(int li, int prio_rank, cudaStream_t *s2, AuxStream **ax2) {
+    static std::map<std::tuple<int, int, int>, std::pair<cudaStream_t, AuxStream>> m;
     int dev = 0;
     CK(cudaGetDevice(&dev));
-    auto &e = m[std::make_pair(dev, li)];
+    auto &e = m[std::make_tuple(dev, li, prio_rank)];
     if (!e.first) {
-        CK(cudaStreamCreateWithFlags(&e.first, cudaStreamNonBlocking));
-        CK(cudaStreamCreateWithFlags(&e.second.s, cudaStreamNonBlocking));
+        if (make_stream(&e.first, prio_rank) || make_stream(&e.second.s, prio_rank)) return SNTRUP_E_CUDA;
         CK(cudaEventCreateWithFlags(&e.second.go, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&e.second.done, cudaEventDisableTiming));
     }
@@ -700,13 +732,13 @@ int lane_streams(int li, cudaStream_t *s2, AuxStream **ax2) {
 }
 
 // R/3-chain stream of a lane (SNTRUP_OPT_RING_STREAMS); go = sample done, done = R/3 chain done
-int ring_stream(int lane, AuxStream **out) {
-    static std::map<std::pair<int, int>, AuxStream> m;
+int ring_stream(int lane, int prio_rank, AuxStream **out) {
+    static std::map<std::tuple<int, int, int>, AuxStream> m;
     int dev = 0;
     CK(cudaGetDevice(&dev));
-    AuxStream &x = m[std::make_pair(dev, lane)];
+    AuxStream &x = m[std::make_tuple(dev, lane, prio_rank)];
     if (!x.s) {
-        CK(cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking));
+        if (make_stream(&x.s, prio_rank)) return SNTRUP_E_CUDA;
         CK(cudaEventCreateWithFlags(&x.go, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&x.done, cudaEventDisableTiming));
     }
@@ -765,13 +797,16 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
     if (host_out) need += nbuf * (align256(chunk * pkb) + align256(chunk * skb));
     if ((rc = ws_reserve(need, s0))) return rc;
     Lane lanes[MAX_LANES];
+    const bool prio = (o.flags & SNTRUP_OPT_LANE_PRIORITY) != 0;
+    const int l0 = prio ? 0 : 1;           // first lane on an internal stream (forked from s0)
     for (int li = 0; li < nl; li++) {
         Lane &L = lanes[li];
-        if (li == 0) {
+        const int pr = prio ? (nl > 1 ? li * 8 / (nl - 1) : 0) : -1;
+        if (li < l0) {
             L.s = s0;
             if ((rc = aux_stream(&L.ax))) return rc;
         } else {
-            if ((rc = lane_streams(li, &L.s, &L.ax))) return rc;
+            if ((rc = lane_streams(li, pr, &L.s, &L.ax))) return rc;
         }
         L.G = ws_take<int8_t>(chunk * PS::P16);
         L.F = ws_take<int8_t>(chunk * PS::P16);
@@ -793,7 +828,7 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
         L.repaired = ws_take<unsigned long long>(1);
         L.err = ws_take<int>(1);
         if (o.flags & SNTRUP_OPT_RING_STREAMS)
-            if ((rc = ring_stream(li, &L.r3))) return rc;
+            if ((rc = ring_stream(li, pr, &L.r3))) return rc;
     }
     uint8_t *pk_stage[MAX_LANES] = {}, *sk_stage[MAX_LANES] = {};
     CopyStream *csl[MAX_LANES] = {};               // one copy stream per lane: copies follow readiness
@@ -803,14 +838,14 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
             sk_stage[i] = ws_take<uint8_t>(chunk * skb);
         }
         for (int li = 0; li < nl; li++)
-            if ((rc = copy_stream(&csl[li], li))) return rc;
+            if ((rc = copy_stream(&csl[li], li, prio ? li : -1))) return rc;
         if (nl == 1) csl[1] = csl[0];
     }
     LaneJoin *lj = nullptr;
-    if (nl > 1) {                          // lanes >= 1 start after everything enqueued before the call
+    if (nl > l0) {                         // internal lanes start after everything enqueued before the call
         if ((rc = lane_join_events(&lj))) return rc;
         CK(cudaEventRecord(lj->start, s0));
-        for (int li = 1; li < nl; li++) CK(cudaStreamWaitEvent(lanes[li].s, lj->start, 0));
+        for (int li = l0; li < nl; li++) CK(cudaStreamWaitEvent(lanes[li].s, lj->start, 0));
     }
     for (int li = 0; li < nl; li++) {
         CK(cudaMemsetAsync(lanes[li].repaired, 0, sizeof(unsigned long long), lanes[li].s));
@@ -932,17 +967,30 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
             CK(cudaEventRecord(L.r3->done, s3));
             CK(cudaStreamWaitEvent(s, L.r3->done, 0));
         }
-        if ((rc = jq.down(s, &n_rq, utrick ? 2 : 1))) return rc;
+        // H and encode (KeyGen step 5).  With host outputs the tail runs in groups of subtrees:
+        // the bottom down-sweep levels (<= SG), h and the pk encode of group j complete before
+        // group j+1 starts, so group j's pk slice is copied D2H while the next groups compute
+        // (pk is 3/4 of the output bytes and only exists at the very end of its subtrees).
+        const int nsub = host_out ? 4 : 1;
+        const long long nroots = tp.cnt[tp.L];
+        const bool grouped = host_out && utrick && nroots >= nsub;
+        const int SG = tp.L < 5 ? tp.L : 5;
+        if ((rc = jq.down(s, &n_rq, grouped ? SG + 1 : (utrick ? 2 : 1)))) return rc;
         if (utrick) n_rq += m;                                     // the u products replace level 1
         n_inv += 2 * tp.cnt[tp.L];
-        // H and encode (KeyGen step 5).  With host outputs the tail runs in sub-batches (an even
-        // number of rows each, so parents are not split), each pk slice copied D2H while the next
-        // slice computes.
-        const int nsub = host_out ? 4 : 1;
         for (int j = 0; j < nsub; j++) {
-            const uint64_t r0 = (m * (uint64_t)j / nsub) & ~1ull;
-            const uint64_t r1 = (j + 1 == nsub) ? m : ((m * (uint64_t)(j + 1) / nsub) & ~1ull);
-            const uint64_t rows = r1 - r0;
+            uint64_t r0, r1;
+            if (grouped) {
+                const long long ra = nroots * j / nsub, rb = nroots * (j + 1) / nsub;
+                if ((rc = jq.down_group(s, &n_rq, SG, 2, ra, rb))) return rc;
+                r0 = (uint64_t)ra << tp.L;
+                r1 = (uint64_t)rb << tp.L;
+                if (r1 > m) r1 = m;
+            } else {
+                r0 = (m * (uint64_t)j / nsub) & ~1ull;
+                r1 = (j + 1 == nsub) ? m : ((m * (uint64_t)(j + 1) / nsub) & ~1ull);
+            }
+            const uint64_t rows = r1 > r0 ? r1 - r0 : 0;
             if (!rows) continue;
             {
                 MulArgs a{};
@@ -988,7 +1036,7 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
         n_rq += m;
         if (host_out) CK(cudaEventRecord(cs->copy[buf], cs->s));
         }
-    for (int li = 1; li < nl; li++) {      // join the lanes into the caller's stream
+    for (int li = l0; li < nl; li++) {     // join the lanes into the caller's stream
         CK(cudaEventRecord(lj->end[li], lanes[li].s));
         CK(cudaStreamWaitEvent(s0, lj->end[li], 0));
     }

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--n", type=int, default=65536)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--param", type=int, default=761)
+    ap.add_argument("--quick", action="store_true")
     args = ap.parse_args()
     P = S.params(args.param)
     n = args.n
@@ -28,10 +29,14 @@ def main():
     sk = torch.empty((n, P["sk_bytes"]), dtype=torch.uint8, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     st = torch.cuda.current_stream()
-    for B, chunk, lanes, rings in itertools.product((512, 1024), (65536, 32768, 16384, 8192), (2, 4), (0, 1)):
-        if lanes == 4 and chunk > 16384:
-            continue
-        fl = S.OPT_ASYNC | (S.OPT_RING_STREAMS if rings else 0) | (S.OPT_LANES4 if lanes == 4 else 0)
+    grid = [(B, c, l, r, 0) for B, c, l, r in itertools.product((512, 1024), (65536, 32768, 16384, 8192), (2, 4), (0, 1))
+            if not (l == 4 and c > 16384)]
+    if args.quick:
+        grid = [(1024, 32768, 2, 1, 0), (1024, 32768, 2, 1, 1), (1024, 16384, 4, 0, 0), (1024, 16384, 4, 0, 1),
+                (1024, 16384, 2, 1, 1), (512, 32768, 2, 0, 0), (1024, 32768, 2, 0, 1)]
+    for B, chunk, lanes, rings, prio in grid:
+        fl = S.OPT_ASYNC | (S.OPT_RING_STREAMS if rings else 0) | (S.OPT_LANES4 if lanes == 4 else 0) | \
+            (S.OPT_LANE_PRIORITY if prio else 0)
         f = lambda: S.batch_keygen(args.param, n, 2, batch_size=B, pk_out=pk, sk_out=sk, flags=fl, chunk_keys=chunk)
         for _ in range(3):
             f()
@@ -46,7 +51,7 @@ def main():
             torch.cuda.synchronize()
             tot += e0.elapsed_time(e1)
         ms = tot / args.steps
-        print("B=%5d chunk=%6d lanes=%d rings=%d  %7.3f ms  %6.2f M keys/s" % (B, chunk, lanes, rings, ms, n / ms / 1e3),
+        print("B=%5d chunk=%6d lanes=%d rings=%d prio=%d  %7.3f ms  %6.2f M keys/s" % (B, chunk, lanes, rings, prio, ms, n / ms / 1e3),
               flush=True)
 
 

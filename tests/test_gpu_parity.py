@@ -126,6 +126,29 @@ def test_host_output(O, flags):
     assert np.array_equal(pk.numpy(), ref["pk"]) and np.array_equal(sk.numpy(), ref["sk"])
 
 
+@pytest.mark.parametrize("B,chunk,flags", [(64, 2048, 0), (1024, 32768, S.OPT_RING_STREAMS),
+                                            (1024, 32768, S.OPT_RING_STREAMS | S.OPT_LANE_PRIORITY),
+                                            (512, 16384, S.OPT_LANES4 | S.OPT_LANE_PRIORITY)])
+def test_host_output_grouped_tail(O, B, chunk, flags):
+    # host outputs with enough trees per chunk for the grouped tail (bottom down-sweep levels, h and
+    # the pk encode per group of subtrees): byte-identical to the device-output call, and to the
+    # oracle on a sample (first/last keys of every chunk, every 61st key)
+    P = S.params(761)
+    n = 65536 if B >= 512 else 4096
+    pk = torch.empty((n, P["pk_bytes"]), dtype=torch.uint8).pin_memory()
+    sk = torch.empty((n, P["sk_bytes"]), dtype=torch.uint8).pin_memory()
+    S.batch_keygen(761, n, 23, batch_size=B, pk_out=pk, sk_out=sk, flags=S.OPT_HOST_OUTPUT | flags,
+                   chunk_keys=chunk)
+    ref = S.batch_keygen(761, n, 23, batch_size=B, chunk_keys=chunk)
+    torch.cuda.synchronize()
+    assert torch.equal(pk, ref["pk"].cpu()) and torch.equal(sk, ref["sk"].cpu())
+    idx = np.unique(np.concatenate([np.arange(0, n, 61)] +
+                                   [np.arange(c, min(c + 4, n)) for c in range(0, n, chunk)] +
+                                   [np.arange(max(c - 4, 0), c) for c in range(chunk, n + 1, chunk)]))
+    r = oracle_keys(O, 761, 23, idx)
+    assert np.array_equal(pk.numpy()[idx], r["pk"]) and np.array_equal(sk.numpy()[idx], r["sk"])
+
+
 def test_cfg2_full_size_sampled(O):
     # BASELINE configs[1]: 65,536 keys, seed 2, in the launch configuration bench.py times;
     # compared on a sample the oracle computes one by one: first and last trees, every 97th key.
