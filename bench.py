@@ -206,7 +206,8 @@ def oracle_keygen_rate(target_s: float = 10.0):
 def other_configs(S, torch, timed):
     """configs[0]: latency of one 32-key call (launch-bound; synchronous C-ABI call, host
     wall clock around it, and device time); configs[3]: keys/s per parameter set at 65,536 keys
-    (B = 512); configs[4]: sntrup1277, 2^20 keys, B = 1024, streamed in 65,536-key chunks."""
+    (the headline's B / chunking); configs[4]: sntrup1277, 2^20 keys, B = 1024, streamed in
+    65,536-key chunks."""
     out = {}
     # configs[0]: 761, 32 keys, seed 1, one tree of 32
     P = S.params(761)
@@ -232,22 +233,24 @@ def other_configs(S, torch, timed):
         n = 65536
         pk = torch.empty((n, P["pk_bytes"]), dtype=torch.uint8, device="cuda")
         sk = torch.empty((n, P["sk_bytes"]), dtype=torch.uint8, device="cuda")
-        f = lambda: S.batch_keygen(ps, n, 4, batch_size=512, pk_out=pk, sk_out=sk, flags=S.OPT_ASYNC)
+        f = lambda: S.batch_keygen(ps, n, 4, batch_size=DEFAULT_B, chunk_keys=DEFAULT_CHUNK, pk_out=pk,
+                                   sk_out=sk, flags=S.OPT_ASYNC | S.OPT_RING_STREAMS)
         f()
         ms = timed(f, 3) / 3
         sweep[str(ps)] = {"keys_per_s": n / (ms / 1e3), "ms": ms}
         del pk, sk
-    out["configs[3]"] = {"workload": "65,536 keys per set, seed 4, B = 512", "by_param_set": sweep}
+    out["configs[3]"] = {"workload": "65,536 keys per set, seed 4, B = %d, %d-key chunks on two lanes, "
+                                     "ring streams" % (DEFAULT_B, DEFAULT_CHUNK), "by_param_set": sweep}
     # configs[4]: 1277, 2^20 keys, B = 1024, 65,536-key chunks (two pipelined lanes)
     P = S.params(1277)
     n = 1 << 20
     pk = torch.empty((n, P["pk_bytes"]), dtype=torch.uint8, device="cuda")
     sk = torch.empty((n, P["sk_bytes"]), dtype=torch.uint8, device="cuda")
     f = lambda: S.batch_keygen(1277, n, 5, batch_size=1024, chunk_keys=65536, pk_out=pk, sk_out=sk,
-                               flags=S.OPT_ASYNC)
+                               flags=S.OPT_ASYNC | S.OPT_RING_STREAMS)
     f()
     ms = timed(f, 2) / 2
-    out["configs[4]"] = {"workload": "sntrup1277, 2^20 keys, seed 5, B = 1024, 65,536-key chunks",
+    out["configs[4]"] = {"workload": "sntrup1277, 2^20 keys, seed 5, B = 1024, 65,536-key chunks, ring streams",
                          "keys_per_s": n / (ms / 1e3), "ms": ms}
     del pk, sk
     # KEM core: 65,536 encapsulations (r from the encapsulation stream

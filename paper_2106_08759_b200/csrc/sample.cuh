@@ -21,8 +21,12 @@ namespace sntrup {
 template <int E>
 __device__ __forceinline__ void warp_bitonic_sort(uint32_t (&v)[E], int lane) {
     constexpr int N = 32 * E;
+    constexpr int LOGN = E == 16 ? 9 : E == 32 ? 10 : E == 64 ? 11 : E == 8 ? 8 : -1;
+    static_assert(LOGN > 0 && (1 << LOGN) == N, "E must be 8, 16, 32 or 64");
+    // (linear induction variables: the loops fully unroll and v stays in registers)
 #pragma unroll
-    for (int k = 2; k <= N; k <<= 1) {
+    for (int ls = 1; ls <= LOGN; ls++) {
+        const int k = 1 << ls;
         // mirror step
         if (k <= E) {
 #pragma unroll
@@ -45,7 +49,8 @@ __device__ __forceinline__ void warp_bitonic_sort(uint32_t (&v)[E], int lane) {
         }
         // half-cleaners
 #pragma unroll
-        for (int j = k >> 2; j > 0; j >>= 1) {
+        for (int lj = ls - 2; lj >= 0; lj--) {
+            const int j = 1 << lj;
             if (j >= E) {
                 const int lm = j / E;
                 const bool lower = (lane & lm) == 0;

@@ -531,7 +531,9 @@ int launch_mul(MulArgs a, cudaStream_t s, int la = 2, int lb = 2) {
     // inverse as the A operand (one work item per parent), halving the A-operand fetch that
     // bounds the tensor-core products.  int8 big x big at M = 128 too since the folded B operand
     // halved N (3 CTAs/SM); impl 6 keeps one big x big product per item for A/B.
-    const bool big2 = la == 2 && lb == 2 && g_mul_impl != 5 && g_mul_impl != 6;
+    // (only where two such CTAs still fit an SM: at p = 1277 the stacked B rows would leave one)
+    const bool big2 = la == 2 && lb == 2 && g_mul_impl != 5 && g_mul_impl != 6 &&
+                      TcGeom<PS, 2, 2, 2>::MINB >= 2;
     const bool down2 = (a.mode == MUL_DOWN || a.mode == MUL_DOWNH) && (M == 3 || (la == 1 && lb == 1) || big2) &&
                        g_mul_impl != 2;
     if (down2) {

@@ -137,7 +137,11 @@ struct TcGeom {
     static constexpr int NKS = (P + MM - 1 + 31) / 32;       // K steps of 32
     static constexpr int K = 32 * NKS;
     static constexpr int NT = (P + MM - 1) / MM;              // output blocks of MM coefficients
-    static constexpr int NL = (NT + 1 + 7) / 8 * 8;           // B rows per limb (+ the fix row)
+    // the fix row costs nothing when NT + 1 rows still fit the 8-row padding; otherwise (NT a
+    // multiple of 8: 953, 1013) c[p-1] goes from its own lane to thread 0 through shared memory
+    static constexpr bool FIXROW = (NT + 1 + 7) / 8 == (NT + 7) / 8;
+    static constexpr int NROWS = NT + (FIXROW ? 1 : 0);       // B rows built per limb
+    static constexpr int NL = (NROWS + 7) / 8 * 8;            // B rows per limb (padded)
     static constexpr int PCOL = (LB * NL + 15) / 16 * 16;    // B rows (= D columns) per product
     static constexpr int NB = NPR * PCOL;                    // N of the MMA
     static constexpr int AROWS = 32 * NKS + MM - 15;         // window rows 0..AROWS-1 (row 0 unused)
@@ -173,7 +177,7 @@ struct TcGeom {
     // c = residue + 8i
     // B build work items: per (pp, limb) group RPG row slots (NT + 1 rows, padded to a multiple
     // of 8 so 8 consecutive lanes own 8 distinct rows = 8 distinct bank groups); 8 items per slot
-    static constexpr int RPG = (NT + 1 + 7) / 8 * 8;
+    static constexpr int RPG = (NROWS + 7) / 8 * 8;
     static constexpr int BROWS = NPR * LB * RPG;
     static constexpr int NCHB = 2 * NKS;                      // 16-byte K-chunks per B row
     static constexpr int BITEMS = BROWS * 8;
@@ -314,6 +318,7 @@ __global__ void __launch_bounds__(128, (TcGeom<PS, LA, LB, NPR, MM>::MINB)) tc_m
     uint8_t *sZR = sm + G::OFF_ZR;
     uint64_t *bar = reinterpret_cast<uint64_t *>(sm + G::OFF_BAR);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sm + G::OFF_BAR + 64);
+    int *fixs = reinterpret_cast<int *>(sm + G::OFF_BAR + 72);     // c[p-1] hand-off (no fix row)
     const int tid = threadIdx.x, warp = tid >> 5;
 
     // ---- one-time setup: zero staging + B (pads stay zero forever), barrier, TMEM
@@ -343,7 +348,7 @@ __global__ void __launch_bounds__(128, (TcGeom<PS, LA, LB, NPR, MM>::MINB)) tc_m
         const int w = tid + 128 * h;
         const int slot = w % G::BROWS, grp = w / G::BROWS;
         const int pl = slot / G::RPG, t = slot - pl * G::RPG;    // pl = pp * LB + l
-        if (w < G::BITEMS && t <= G::NT) {
+        if (w < G::BITEMS && t < G::NROWS) {
             const int pp = pl / LB, l = pl - pp * LB;
             const int zs = G::zrow(t) / 16;                        // window start, 16-byte units
             // chunks c = res + 8i; res makes the loads of 8 consecutive lanes hit 8 bank groups
@@ -554,8 +559,19 @@ __global__ void __launch_bounds__(128, (TcGeom<PS, LA, LB, NPR, MM>::MINB)) tc_m
                 if (LB == 1) return (64 * D(0, 0) + D(1, 0)) % M;
                 return (4096 * (D(0, 0) % M) + 64 * (D(0, 1) + D(1, 0)) + D(1, 1)) % M;
             };
-            int fix = 0;
-            if (warp == 0) fix = __shfl_sync(FULL, comb(G::NT), G::R0);   // = D(p-1)
+            int fix = 0;                                   // = D(p-1), for thread 0
+            if constexpr (G::FIXROW) {
+                if (warp == 0) fix = __shfl_sync(FULL, comb(G::NT), G::R0);
+            } else {
+                // D(p-1) lives in accumulator row (p-1) mod MM of block (p-1)/MM
+                constexpr int RS = (P - 1) % MM, TS = (P - 1) / MM;
+                constexpr int WS = MM == 128 ? RS / 32 : RS / 16;
+                constexpr int LS = MM == 128 ? RS % 32 : RS % 16;
+                if (warp == WS && lane == LS) fixs[pp] = comb(TS);
+                if (WS == 0) __syncwarp();
+                else if (warp == 0 || warp == WS) asm volatile("bar.sync 1, 64;" ::: "memory");
+                if (tid == 0) fix = fixs[pp];
+            }
             if (orow < 0 || !rowok) continue;
             auto store = [&](auto *op) {
                 constexpr int OSTRIDE = sizeof(*op) == 2 ? PS::P8 : PS::P16;

@@ -185,7 +185,8 @@ def test_cfg4_full_size_sampled(O, param):
     # BASELINE configs[3]: 65,536 keys per set, seed 4.  Compared with the oracle on every key
     # that needed more than one g draw, the first and last trees, and every 97th key.
     n = 65536
-    res = S.batch_keygen(param, n, 4, batch_size=512, debug=True)
+    res = S.batch_keygen(param, n, 4, batch_size=1024, chunk_keys=32768, flags=S.OPT_RING_STREAMS,
+                         debug=True)                       # bench.py's configs[3] launch configuration
     torch.cuda.synchronize()
     att = res["attempts"].cpu().numpy()
     assert att.min() >= 1
@@ -200,7 +201,8 @@ def test_cfg5_full_size_sampled(O):
     # streamed in 65,536-key chunks.  Sampled: first/last chunk edges, every 509th key, every
     # 32nd key that needed more than one g draw; rejection total vs the per-draw probability.
     n = 1 << 20
-    res = S.batch_keygen(1277, n, 5, batch_size=1024, chunk_keys=65536, debug=True)
+    res = S.batch_keygen(1277, n, 5, batch_size=1024, chunk_keys=65536, flags=S.OPT_RING_STREAMS,
+                         debug=True)
     torch.cuda.synchronize()
     att = res["attempts"].cpu().numpy()
     assert att.min() >= 1
