@@ -31,7 +31,8 @@ PARAMS = {
 
 def build(force: bool = False) -> str:
     """Compile the oracle with plain gcc -O2 (no intrinsics)."""
-    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
+    deps = [SRC, os.path.join(HERE, "sha512_consts.h")]
+    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(d) for d in deps):
         tmp = LIB + ".tmp%d" % os.getpid()
         subprocess.check_call(["gcc", "-O2", "-fPIC", "-shared", "-pthread", "-o", tmp, SRC])
         os.replace(tmp, LIB)
@@ -57,6 +58,10 @@ def lib():
         L.or_poly_mul.argtypes = [i32, i64, vp, vp, vp]
         L.or_poly_inv.restype = i32
         L.or_poly_inv.argtypes = [i32, i64, vp, vp]
+        L.or_sha512.restype = None
+        L.or_sha512.argtypes = [vp, sz, vp]
+        L.or_full_sk.restype = sz
+        L.or_full_sk.argtypes = [i32, u64, u64, vp, sz, vp, sz, vp]
         L.or_rq_encode.restype = sz
         L.or_rq_encode.argtypes = [i32, i32, vp, vp]
         L.or_rq_decode.restype = i32
@@ -263,3 +268,26 @@ def keygen_many(param: int, seed: int, indices, threads: int = 0, want_polys: bo
     if want_polys:
         out.update(h=h, g=g, f=f, ginv=gi)
     return out
+
+
+def sha512(data: bytes) -> bytes:
+    """FIPS 180-4 SHA-512 (the oracle's own C implementation)."""
+    buf = ctypes.create_string_buffer(bytes(data), max(1, len(data)))
+    out = ctypes.create_string_buffer(64)
+    lib().or_sha512(buf, len(data), out)
+    return out.raw
+
+
+def full_sk_bytes(param: int) -> int:
+    """|sk_full| = 3 ceil(p/4) + |pk| + 32 (App. D pair storage minus pk; reading Z24)."""
+    p = PARAMS[param][0]
+    return sk_bytes(param) + pk_bytes(param) + (p + 3) // 4 + 32
+
+
+def full_sk(param: int, seed: int, k: int, pk: bytes, sk: bytes) -> bytes:
+    """sk_full = sk || pk || rho || SHA-512(4 || pk)[:32] for global key index k (reading Z24)."""
+    p = PARAMS[param][0]
+    out = ctypes.create_string_buffer(full_sk_bytes(param))
+    n = lib().or_full_sk(p, seed, k, bytes(pk), len(pk), bytes(sk), len(sk), out)
+    assert n == full_sk_bytes(param)
+    return out.raw

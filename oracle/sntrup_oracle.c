@@ -508,3 +508,83 @@ int or_decap_core(int p, int q, int w, const int8_t *f, const int8_t *ginv, cons
     free(F3); free(C); free(E); free(G); free(R);
     return weight == w;
 }
+
+/* ------------------------------------------------------------------------------------------ */
+/* Full-size secret key (reading Z24 in DESIGN.md): the paper stores key    */
+/* pairs of 2512 / 2921 / 3321 bytes (App. D) = pk + an sk of         */
+/* 3 ceil(p/4) + |pk| + 32 bytes, but names neither the extra secret rho nor the hash.  Ours:     */
+/*   sk_full = Small(f) || Small(1/g) || pk || rho || H(pk)                                     */
+/*   rho     = ceil(p/4) bytes of key k's stream domain OR_DOMAIN_RHO (C2), little-endian words  */
+/*   H(pk)   = SHA-512(0x04 || pk)[0..32)  (FIPS 180-4, written out below, one block at a time)  */
+/* ------------------------------------------------------------------------------------------ */
+#include "sha512_consts.h"
+
+#define OR_DOMAIN_RHO 0x8000000000000000ULL
+
+static uint64_t rotr64(uint64_t x, int n) { return (x >> n) | (x << (64 - n)); }
+
+/* FIPS 180-4 6.4.2: one 1024-bit block into the hash state */
+static void sha512_block(uint64_t H[8], const uint8_t blk[128])
+{
+    uint64_t W[80];
+    for (int t = 0; t < 16; t++) {
+        uint64_t w = 0;
+        for (int b = 0; b < 8; b++) w = (w << 8) | blk[8 * t + b];     /* big-endian words */
+        W[t] = w;
+    }
+    for (int t = 16; t < 80; t++) {
+        const uint64_t s0 = rotr64(W[t - 15], 1) ^ rotr64(W[t - 15], 8) ^ (W[t - 15] >> 7);
+        const uint64_t s1 = rotr64(W[t - 2], 19) ^ rotr64(W[t - 2], 61) ^ (W[t - 2] >> 6);
+        W[t] = s1 + W[t - 7] + s0 + W[t - 16];
+    }
+    uint64_t a = H[0], b = H[1], c = H[2], d = H[3], e = H[4], f = H[5], g = H[6], h = H[7];
+    for (int t = 0; t < 80; t++) {
+        const uint64_t S1 = rotr64(e, 14) ^ rotr64(e, 18) ^ rotr64(e, 41);
+        const uint64_t ch = (e & f) ^ (~e & g);
+        const uint64_t T1 = h + S1 + ch + OR_SHA512_K[t] + W[t];
+        const uint64_t S0 = rotr64(a, 28) ^ rotr64(a, 34) ^ rotr64(a, 39);
+        const uint64_t maj = (a & b) ^ (a & c) ^ (b & c);
+        const uint64_t T2 = S0 + maj;
+        h = g; g = f; f = e; e = d + T1; d = c; c = b; b = a; a = T1 + T2;
+    }
+    H[0] += a; H[1] += b; H[2] += c; H[3] += d; H[4] += e; H[5] += f; H[6] += g; H[7] += h;
+}
+
+/* SHA-512 of msg[0..len) (FIPS 180-4 5.1.2 padding: 0x80, zeros, 128-bit big-endian bit length) */
+void or_sha512(const uint8_t *msg, size_t len, uint8_t out[64])
+{
+    uint64_t H[8];
+    for (int i = 0; i < 8; i++) H[i] = OR_SHA512_H0[i];
+    const size_t total = ((len + 17 + 127) / 128) * 128;
+    uint8_t *buf = calloc(total, 1);
+    memcpy(buf, msg, len);
+    buf[len] = 0x80;
+    const uint64_t bits = (uint64_t)len * 8;
+    for (int b = 0; b < 8; b++) buf[total - 1 - b] = (uint8_t)(bits >> (8 * b));
+    for (size_t o = 0; o < total; o += 128) sha512_block(H, buf + o);
+    free(buf);
+    for (int i = 0; i < 8; i++)
+        for (int b = 0; b < 8; b++) out[8 * i + b] = (uint8_t)(H[i] >> (56 - 8 * b));
+}
+
+/* full sk of global key index k from its pk and sk bytes; returns the bytes written */
+size_t or_full_sk(int p, uint64_t seed, uint64_t k, const uint8_t *pk, size_t pkb,
+                  const uint8_t *sk, size_t skb, uint8_t *out)
+{
+    const size_t rb = (size_t)((p + 3) / 4);
+    size_t o = 0;
+    memcpy(out + o, sk, skb); o += skb;
+    memcpy(out + o, pk, pkb); o += pkb;
+    const uint64_t D = or_sm(or_sm(seed, k), OR_DOMAIN_RHO);
+    for (size_t j = 0; j < rb; j++) out[o + j] = (uint8_t)(or_sm(D, j / 8) >> (8 * (j % 8)));
+    o += rb;
+    uint8_t *m = malloc(pkb + 1);
+    m[0] = 4;
+    memcpy(m + 1, pk, pkb);
+    uint8_t hsh[64];
+    or_sha512(m, pkb + 1, hsh);
+    free(m);
+    memcpy(out + o, hsh, 32);
+    o += 32;
+    return o;
+}
