@@ -279,6 +279,14 @@ def other_configs(S, torch, timed):
                        "encaps_per_s": n / (enc_ms / 1e3), "decaps_per_s": n / (dec_ms / 1e3),
                        "paper_context_cycles": {"enc": 46914, "dec": 56241, "hardware": "Haswell, Table 1 P:864-876"}}
     del keys, r, c, r2, okb
+    # full-size secret keys (reading Z24): sk || pk || rho || SHA-512(4 || pk)[:32]
+    keys = S.batch_keygen(761, n, 2, batch_size=1024)
+    full = S.full_sk_batch(761, 2, keys["pk"], keys["sk"])
+    fsk_ms = timed(lambda: S.full_sk_batch(761, 2, keys["pk"], keys["sk"], out=full), 3) / 3
+    out["full_sk"] = {"workload": "sntrup761, 65,536 keys of configs[1]: full-size sk rows (%d B: sk || pk || "
+                                  "rho || SHA-512(4 || pk)[:32]) from device pk/sk" % full.shape[1],
+                      "keys_per_s": n / (fsk_ms / 1e3), "ms": fsk_ms}
+    del keys, full
     # key pool (the paper's engNTRU batch_lib provider: "first key 2.5 ms, then
     # 0 ms"): first take (lazy fill), then paced takes served from the pinned ring
     pool = S.KeyPool(761, seed=9, capacity=1 << 15, batch_keys=1 << 13, batch_size=512)
@@ -294,10 +302,22 @@ def other_configs(S, torch, timed):
     st = pool.stats()
     pool.close()
     lat.sort()
+    # the paper's series shape: wall time to obtain K keys from a fresh pool, unpaced
+    # (engNTRU batch_lib: (0.08 K + 2.5) ms on Haswell)
+    series = {}
+    for K in (1, 10, 100, 1000, 10000, 100000):
+        pool = S.KeyPool(761, seed=11, capacity=1 << 15, batch_keys=1 << 13, batch_size=512)
+        t0 = time.perf_counter()
+        for _ in range(K):
+            pool.take()
+        series[str(K)] = (time.perf_counter() - t0) * 1e3
+        pool.close()
     out["key_pool"] = {"workload": "sntrup761 pool: capacity 32768, refill batches of 8192 keys (B = 512), "
-                                   "2000 takes paced 0.2 ms apart",
+                                   "2000 takes paced 0.2 ms apart; series: K unpaced takes from a fresh pool",
                        "first_take_ms": first_ms, "take_us_median": lat[len(lat) // 2],
-                       "take_us_p99": lat[int(len(lat) * 0.99)], "waits_after_first": st["waits"] - 1}
+                       "take_us_p99": lat[int(len(lat) * 0.99)], "waits_after_first": st["waits"] - 1,
+                       "ms_for_K_keys": series,
+                       "paper_context": "engNTRU batch_lib on Haswell: (0.08 K + 2.5) ms for K keys (P:8616-8700)"}
     return out
 
 

@@ -124,6 +124,22 @@ int rq_mul_small_batch(int param_set, uint64_t n, const int16_t *a, const int8_t
 int r3_mul_batch(int param_set, uint64_t n, const int8_t *a, const int8_t *b, int8_t *c,
                  void *stream);
 
+/* ---- Full-size secret key (reading Z24).  The paper's
+   key-pair storage is 2512 / 2921 / 3321 bytes (App. D) = pk + an sk
+   of 3 ceil(p/4) + |pk| + 32 bytes; it names neither the extra secret nor the hash.  Ours:
+   sk_full = sk || pk || rho || SHA-512(0x04 || pk)[0..32), rho = ceil(p/4) bytes of stream
+   domain 2^63 of the key (C2). */
+
+/* Bytes of one full sk row (1763 for 761); 0 for an unknown parameter set. */
+size_t sntrup_full_sk_bytes(int param_set);
+
+/* sk_full[i] for global key indices first_key_index + i from that key's pk and sk rows.  All
+   pointers DEVICE: pk u8 [n][pk_bytes], sk u8 [n][sk_bytes] (as sntrup_batch_keygen writes
+   them), sk_full u8 [n][sntrup_full_sk_bytes].  Stream-ordered; SNTRUP_E_PARAM / SNTRUP_E_ARG
+   (n == 0 or a NULL pointer) / SNTRUP_E_CUDA. */
+int sntrup_full_sk_batch(int param_set, uint64_t n, uint64_t seed, uint64_t first_key_index,
+                         const uint8_t *pk, const uint8_t *sk, uint8_t *sk_full, void *stream);
+
 /* ---- Encapsulation / decapsulation core.  The paper benchmarks
    enc/dec (Table 1) for keys of shape (h, (f, 1/g)) but does not spell
    them out; the core follows Streamlined NTRU Prime as SPEC.md's encrypt_core/decrypt_core

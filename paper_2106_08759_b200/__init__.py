@@ -81,6 +81,9 @@ _lib.rq_mul_small_batch.argtypes = [_i32, _u64, _vp, _vp, _vp, _vp]
 _lib.sntrup_sample_short_batch.argtypes = [_i32, _u64, _u64, _u64, _u64, _vp, _vp]
 _lib.sntrup_encap_core_batch.argtypes = [_i32, _u64, _vp, _vp, _vp, _vp]
 _lib.sntrup_decap_core_batch.argtypes = [_i32, _u64, _vp, _vp, _vp, _vp, _vp, _vp]
+_lib.sntrup_full_sk_bytes.argtypes = [_i32]
+_lib.sntrup_full_sk_bytes.restype = ctypes.c_size_t
+_lib.sntrup_full_sk_batch.argtypes = [_i32, _u64, _u64, _u64, _vp, _vp, _vp, _vp]
 
 EXPORTED = ("sntrup_params", "sntrup_strerror", "sntrup_batch_keygen", "sntrup_batch_keygen_ex",
             "sntrup_keygen_workspace_bytes", "rq_mul_batch", "rq_mul_small_batch", "r3_mul_batch", "rq_recip_batch",
@@ -89,7 +92,7 @@ EXPORTED = ("sntrup_params", "sntrup_strerror", "sntrup_batch_keygen", "sntrup_b
             "sntrup_profile_enable", "sntrup_profile_read_kinds", "sntrup_pool_create",
             "sntrup_pool_take", "sntrup_pool_stats", "sntrup_pool_destroy",
             "sntrup_sample_short_batch", "sntrup_encap_core_batch", "sntrup_decap_core_batch",
-            "sntrup_profile_read")
+            "sntrup_profile_read", "sntrup_full_sk_bytes", "sntrup_full_sk_batch")
 
 PROFILE_CLASSES = ("sample", "r3_mul", "rq_mul", "root_inv", "rq_inv", "repair", "encode", "other")
 
@@ -191,6 +194,29 @@ def rq_mul_small_batch(param_set: int, a, b, c=None, stream=None):
 
 
 ENC_DOMAIN = 1 << 32      # C2: stream domains >= 2^32 are reserved for encapsulation draws
+
+
+def full_sk_bytes(param_set: int) -> int:
+    """Bytes of one full-size sk row: sk || pk || rho || SHA-512(4 || pk)[:32] (1763 for 761)."""
+    v = _lib.sntrup_full_sk_bytes(param_set)
+    if not v:
+        raise SntrupError(SNTRUP_E_PARAM, "sntrup_full_sk_bytes")
+    return v
+
+
+def full_sk_batch(param_set: int, seed: int, pk, sk, first_key_index: int = 0, out=None, stream=None):
+    """Full-size secret keys for keys first_key_index.. from their device pk / sk rows."""
+    P = params(param_set)
+    n = pk.shape[0]
+    _need(pk, torch.uint8, (n, P["pk_bytes"]), "pk")
+    _need(sk, torch.uint8, (n, P["sk_bytes"]), "sk")
+    fsb = full_sk_bytes(param_set)
+    if out is None:
+        out = torch.empty((n, fsb), dtype=torch.uint8, device=pk.device)
+    _need(out, torch.uint8, (n, fsb), "out")
+    _check(_lib.sntrup_full_sk_batch(param_set, n, seed, first_key_index, _ptr(pk), _ptr(sk), _ptr(out),
+                                     _stream(stream)), "sntrup_full_sk_batch")
+    return out
 
 
 def sample_short_batch(param_set: int, n: int, seed: int, first_key_index: int = 0,

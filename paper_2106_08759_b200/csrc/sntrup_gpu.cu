@@ -26,6 +26,7 @@
 #include "divstep.cuh"
 #include "encode.cuh"
 #include "factor_tables.h"
+#include "fullsk.cuh"
 #include "ringmul.cuh"
 #include "sample.cuh"
 #include "tcmul.cuh"
@@ -1288,6 +1289,31 @@ int rq_mul_small_batch(int param_set, uint64_t n, const int16_t *a, const int8_t
     m.out_bytes = 2;
     m.periodic = 0;
     SNTRUP_DISPATCH(param_set, return launch_mul<PS, PS::Q>(m, (cudaStream_t)stream, 2, 1));
+    return SNTRUP_E_PARAM;
+}
+
+size_t sntrup_full_sk_bytes(int param_set) {
+    size_t pkb = 0, skb = 0;
+    int p = 0;
+    if (sntrup_params(param_set, &p, nullptr, nullptr, nullptr, nullptr, &pkb, &skb)) return 0;
+    return skb + pkb + (size_t)((p + 3) / 4) + 32;
+}
+
+int sntrup_full_sk_batch(int param_set, uint64_t n, uint64_t seed, uint64_t first_key_index,
+                         const uint8_t *pk, const uint8_t *sk, uint8_t *sk_full, void *stream) {
+    size_t pkb = 0, skb = 0;
+    if (sntrup_params(param_set, nullptr, nullptr, nullptr, nullptr, nullptr, &pkb, &skb)) return SNTRUP_E_PARAM;
+    if (n == 0 || !pk || !sk || !sk_full) return SNTRUP_E_ARG;
+    FullSkArgs a{seed, first_key_index, n, pk, sk, sk_full};
+    const cudaStream_t s = (cudaStream_t)stream;
+    SNTRUP_DISPATCH(param_set, {
+        full_sk_copy_kernel<PS><<<(unsigned)((n + 3) / 4), 128, 0, s>>>(a, (int)pkb, (int)skb);
+        LAUNCHED();
+        sha512_pk_kernel<PS><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(a, (int)pkb, (int)skb);
+        LAUNCHED();
+        CK(cudaGetLastError());
+        return SNTRUP_OK;
+    });
     return SNTRUP_E_PARAM;
 }
 

@@ -75,6 +75,16 @@ def test_argument_errors_without_gpu(lib):
     S.set_mul_impl(S.MUL_TENSOR_CORE)
 
 
+def test_full_sk_sizes_host_query(lib):
+    import paper_2106_08759_b200 as S
+    # App. D key-pair storage: pk + full sk = 2512 / 2921 / 3321
+    for param, pair in ((653, 2512), (761, 2921), (857, 3321)):
+        assert S.params(param)["pk_bytes"] + S.full_sk_bytes(param) == pair
+    assert S._lib.sntrup_full_sk_bytes(700) == 0
+    assert S._lib.sntrup_full_sk_batch(761, 0, 1, 0, None, None, None, None) == S.SNTRUP_E_ARG
+    assert S._lib.sntrup_full_sk_batch(700, 5, 1, 0, None, None, None, None) == S.SNTRUP_E_PARAM
+
+
 def irreducible_gf3(f):
     """Rabin's test over GF(3): x^(3^d) = x mod f and gcd(x^(3^(d/r)) - x, f) = 1, r | d prime."""
     import numpy as np

@@ -424,6 +424,20 @@ def test_rq_encode(O, param):
         assert pk[i].tobytes() == O.rq_encode(p, q, h[i, :p])
 
 
+@pytest.mark.parametrize("param", [653, 761, 1277])
+def test_full_sk_matches_oracle(O, param):
+    # full-size secret keys (reading Z24) of a batch, byte-identical to the oracle's, every row;
+    # sizes = App. D pair storage minus pk
+    n = 300
+    res = S.batch_keygen(param, n, 31, first_key_index=1000, batch_size=64)
+    full = S.full_sk_batch(param, 31, res["pk"], res["sk"], first_key_index=1000)
+    torch.cuda.synchronize()
+    assert full.shape[1] == O.full_sk_bytes(param)
+    pk, sk, fu = res["pk"].cpu().numpy(), res["sk"].cpu().numpy(), full.cpu().numpy()
+    for i in range(n):
+        assert fu[i].tobytes() == O.full_sk(param, 31, 1000 + i, pk[i].tobytes(), sk[i].tobytes()), i
+
+
 def test_kernels_really_launch():
     before = S.kernel_launch_count()
     S.batch_keygen(761, 64, 1)
