@@ -14,6 +14,8 @@ import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_PKG, "libsntrup_gpu.so")
+if os.environ.get("SNTRUP_GPU_LIB"):            # e.g. the bounds-checked build (tests only)
+    _LIB_PATH = os.environ["SNTRUP_GPU_LIB"]
 
 if not os.path.exists(_LIB_PATH):
     raise ImportError("libsntrup_gpu.so is not built (run __graft_entry__.build() or "

@@ -4,6 +4,25 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// Bounds checks of shared-memory / global indexing, compiled in only for the checked build
+// (_build.build_checked(): -DSNTRUP_BOUNDS_CHECK, libsntrup_gpu_check.so; compute-sanitizer is
+// not available on the B200 pool).  A failed check prints and traps.
+#ifdef SNTRUP_BOUNDS_CHECK
+#include <cstdio>
+#define SNTRUP_CHECK(c)                                                                       \
+    do {                                                                                      \
+        if (!(c)) {                                                                           \
+            printf("SNTRUP_CHECK failed: %s (%s:%d) block %d thread %d\n", #c, __FILE__,       \
+                   __LINE__, (int)blockIdx.x, (int)threadIdx.x);                               \
+            __trap();                                                                         \
+        }                                                                                     \
+    } while (0)
+#else
+#define SNTRUP_CHECK(c) \
+    do {                \
+    } while (0)
+#endif
+
 namespace sntrup {
 
 // Parameter sets (p, q, w): 653/761/857 from P:1418-1430 (section 2.1); 953/1013/1277 from

@@ -265,6 +265,7 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
 #pragma unroll
                     for (int i = 0; i < 8; i++) word |= e2m1_code(uv8[i]) << (4 * i);
                 }
+                SNTRUP_CHECK(4 * (16 + c + 1) <= G::HA_BYTES);
                 sHA[16 + c] = word;                                  // nibbles 128 + 8c + i
             }
             if (c <= G::NCHK) {
@@ -275,6 +276,8 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
                     const bool fast = LB == 1 && w.dv[pp].bytes == 1 && !w.unit_v[pp] && !(XOPS && w.dv[pp].mod3);
                     const int zws = (G::ZB_END + (P - PD) - 8 - 8 * cs) / 8;    // s-group word
                     const int zwb = G::ZB_END / 8 - 1 - c;                      // b[8c+i]: nibble ZB_END-1-8c-i
+                    SNTRUP_CHECK(cs >= G::NCHK - 1 || (8 * zws >= G::ZB_END && 8 * zws + 8 <= G::Z_NIB));
+                    SNTRUP_CHECK(c >= G::NCHK || (zwb >= 0 && 8 * zwb + 8 <= G::ZB_END));
                     if (c == 0) fixab[pp] = pa1 * pb1[pp];
                     if (LB == 1 && fast) {
                         // SWAR: forward-packed chunks, s-group = pairwise sums of two shifted views
@@ -335,6 +338,7 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
         for (int kw = 0; kw < (G::AROWS / 4 + 127) / 128; kw++) {
             const int m = tid + 128 * kw;
             if (m >= G::AROWS / 4) break;
+            SNTRUP_CHECK(4 * ((m >> 1) + 5) <= G::HA_BYTES && 64 * (m + 1) <= G::A_BYTES);
             const uint32_t *src = sHA + (m >> 1);
             uint32_t wd[5];
 #pragma unroll
@@ -357,7 +361,11 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
             const uint4 *src = reinterpret_cast<const uint4 *>(sZR) + bsrc[h];
             uint4 *dst = reinterpret_cast<uint4 *>(sB) + bdst[h];
 #pragma unroll 4
-            for (int c = bres[h]; c < G::NCHB; c += 8) dst[c * G::NB] = src[c];
+            for (int c = bres[h]; c < G::NCHB; c += 8) {
+                SNTRUP_CHECK(bsrc[h] + c < NPR * LB * G::ZR_BYTES / 16 && bdst[h] + c * G::NB < G::B_BYTES / 16);
+                SNTRUP_CHECK((bsrc[h] % (G::ZR_BYTES / 16)) + c < G::ZR_BYTES / 16);
+                dst[c * G::NB] = src[c];
+            }
         }
         fence_async_smem();
         tc_fence_before();

@@ -419,6 +419,7 @@ __global__ void __launch_bounds__(128, (TcGeom<PS, LA, LB, NPR, MM>::MINB)) tc_m
                     int x[8];
 #pragma unroll
                     for (int i = 0; i < 8; i++) x[i] = limb_of<LA>(uv8[i], l);
+                    SNTRUP_CHECK(MM + 8 * c + 8 <= G::HA_LEN);
                     *reinterpret_cast<uint2 *>(sHA + l * G::HA_LEN + MM + 8 * c) =
                         make_uint2(pack4(x[0], x[1], x[2], x[3]), pack4(x[4], x[5], x[6], x[7]));
                 }
@@ -448,6 +449,7 @@ __global__ void __launch_bounds__(128, (TcGeom<PS, LA, LB, NPR, MM>::MINB)) tc_m
                             s8[j] = (i0 < 8 ? vv8[i0] : vn8[i0 - 8]) + (i1 < 8 ? vv8[i1] : vn8[i1 - 8]);
                         }
                         const int zo = G::ZB_END + (P - PD) - 8 - 8 * cs;
+                        SNTRUP_CHECK(zo >= G::ZB_END && zo + 8 <= G::Z_LEN && (zo & 7) == 0);
 #pragma unroll
                         for (int l = 0; l < LB; l++) {
                             int x[8];
@@ -463,6 +465,7 @@ __global__ void __launch_bounds__(128, (TcGeom<PS, LA, LB, NPR, MM>::MINB)) tc_m
                             fixab[pp] = pa1 * pb1[pp];
                         }
                         const int zo = G::ZB_END - 8 - 8 * c;      // b[8c+i] at ZB_END - 1 - 8c - i
+                        SNTRUP_CHECK(zo >= 0 && zo + 8 <= G::ZB_END);
 #pragma unroll
                         for (int l = 0; l < LB; l++) {
                             int x[8];
@@ -484,6 +487,7 @@ __global__ void __launch_bounds__(128, (TcGeom<PS, LA, LB, NPR, MM>::MINB)) tc_m
             for (int kw = 0; kw < (G::AROWS4 + 127) / 128; kw++) {
                 const int m = tid + 128 * kw;
                 if (m >= G::AROWS4) break;
+                SNTRUP_CHECK(4 * (m + 5) <= G::HA_LEN && 64 * (m + 1) <= G::A_BYTES);
                 const uint32_t *src = reinterpret_cast<const uint32_t *>(sHA + l * G::HA_LEN) + m;
                 uint32_t wd[5];
 #pragma unroll
@@ -509,7 +513,11 @@ __global__ void __launch_bounds__(128, (TcGeom<PS, LA, LB, NPR, MM>::MINB)) tc_m
             const uint4 *src = reinterpret_cast<const uint4 *>(sZR) + bsrc[h];
             uint4 *dst = reinterpret_cast<uint4 *>(sB) + bdst[h];
 #pragma unroll 4
-            for (int c = bres[h]; c < G::NCHB; c += 8) dst[c * G::NB] = src[c];
+            for (int c = bres[h]; c < G::NCHB; c += 8) {
+                SNTRUP_CHECK(bsrc[h] + c < NPR * LB * G::Z_LEN / 16 && bdst[h] + c * G::NB < G::B_BYTES / 16);
+                SNTRUP_CHECK((bsrc[h] % (G::Z_LEN / 16)) + c < G::Z_LEN / 16);
+                dst[c * G::NB] = src[c];
+            }
         }
         fence_async_smem();
         tc_fence_before();
