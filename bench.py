@@ -554,6 +554,7 @@ def main():
         ab = {}
         for name, impl in (("tc_int8_m64", S.MUL_TENSOR_CORE_M64),
                            ("tc_int8_big_single", S.MUL_TENSOR_CORE_I8_SINGLE),
+                           ("tc_u_fused_level1", S.MUL_TENSOR_CORE_U_FUSED),
                            ("tc_fp4_all_small", S.MUL_TENSOR_CORE_FP4_ALL),
                            ("tc_int8_shared_a", S.MUL_TENSOR_CORE_INT8),
                            ("tc_int8_no_shared_a", S.MUL_TENSOR_CORE_NO_SHARED_A),

@@ -218,7 +218,9 @@ uint64_t sntrup_kernel_launch_count(void);
    3 = int8 tensor cores only, with the shared-A R/3 down-sweep;
    4 = as 0, plus big x small products on fp4 with balanced base-9 digits (A/B only);
    5 = as 0, with the int8 products at MMA M = 64 instead of 128 (A/B only);
-   6 = as 0, with one int8 big x big product per work item (A/B only).
+   6 = as 0, with one int8 big x big product per work item (A/B only);
+   7 = as 0, with keygen's u_{2j} = g_{2j} * 3f_{2j+1} fused with the R/q tree's first level
+       3f_{2j} * 3f_{2j+1} (shared A operand) instead of running on their own stream (A/B only).
    All are exact.  Returns SNTRUP_OK or SNTRUP_E_ARG. */
 int sntrup_set_mul_impl(int impl);
 

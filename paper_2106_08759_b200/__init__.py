@@ -341,6 +341,7 @@ MUL_TENSOR_CORE_INT8 = 3          # int8 only, shared-A down-sweep
 MUL_TENSOR_CORE_FP4_ALL = 4       # fp4 also for big x small (base-9 digits)
 MUL_TENSOR_CORE_M64 = 5           # int8 products at MMA M = 64 (default: 128)
 MUL_TENSOR_CORE_I8_SINGLE = 6     # one int8 big x big product per work item (default: shared A)
+MUL_TENSOR_CORE_U_FUSED = 7       # keygen u products fused with the R/q level 1 (default: own stream)
 
 
 def set_mul_impl(impl: int):

@@ -20,7 +20,13 @@
 
 namespace sntrup {
 
-enum MulMode { MUL_ZIP = 0, MUL_PAIRS = 1, MUL_DOWN = 2, MUL_DOWN2 = 3, MUL_SIB = 4, MUL_DOWNH = 5, MUL_DOWNH2 = 6 };
+enum MulMode { MUL_ZIP = 0, MUL_PAIRS = 1, MUL_DOWN = 2, MUL_DOWN2 = 3, MUL_SIB = 4, MUL_DOWNH = 5, MUL_DOWNH2 = 6,
+               MUL_UP0 = 7, MUL_ODDSIB = 8 };
+// (tensor paths only)
+//   UP0   : item j, A = Y[2j+1] (unit if absent): out[2j] = X[2j] * A and out2[j] = Y[2j] * A
+//           (keygen: u_{2j} = g_{2j} * 3f_{2j+1} and the R/q tree's level 1, 3f_{2j} * 3f_{2j+1},
+//           share 3f_{2j+1})
+//   ODDSIB: out[2j+1] = X[2j+1] * Y[2j]   (the remaining u_{2j+1})
 
 struct MulArgs {
     int mode;
@@ -33,6 +39,8 @@ struct MulArgs {
     int periodic;           // both operands full-size -> lazy reductions inside the tile loop
     int swap;               // tensor-core path: the second operand takes the A (Hankel) role
     int round3;             // post-op: each output coefficient to the nearest multiple of 3
+    void *out2;             // MUL_UP0: second product's output rows (stride out2_stride)
+    long long out2_stride;
 };
 
 template <int NP>

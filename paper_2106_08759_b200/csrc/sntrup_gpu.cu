@@ -416,7 +416,8 @@ TreePlan make_plan(long long m, int B) {
 // 2 = int8 tensor cores only, one product per work item; 3 = int8 tensor cores with shared A;
 // 4 = as 0 but big x small products also on fp4 (base-9 digits; slower, kept for A/B);
 // 5 = as 0 but int8 products with MMA M = 64 (A/B for the M = 128 choice);
-// 6 = as 0 but one int8 big x big product per work item (A/B for the shared-A down-sweep)
+// 6 = as 0 but one int8 big x big product per work item (A/B for the shared-A down-sweep);
+// 7 = as 0 but the keygen's u products fused with the R/q tree's level 1 (shared A; A/B)
 int g_mul_impl = 0;
 
 struct DevInfo { int sms = 0; };
@@ -510,16 +511,17 @@ int launch_tc4(const MulArgs &a, cudaStream_t s) {
 template <class PS, int M>
 int launch_mul(MulArgs a, cudaStream_t s, int la = 2, int lb = 2) {
     if (a.n_out <= 0) return SNTRUP_OK;
+    const int impl = g_mul_impl == 7 ? 0 : g_mul_impl;     // 7 differs only in keygen's u products
     // algorithmic ops: tensor path = 2 p^2 int8 multiply-add ops per limb-pair product (the
     // limb-decomposed schoolbook contraction); schoolbook path = 2 p^2 int32 ops per product
     // (fp4 path: digit pairs = LB base-9 digits of the big operand x 1)
     const bool small_op = (M == 3) || la == 1 || lb == 1;
-    int limb_pairs = (g_mul_impl == 1 || M == 3) ? 1 : la * lb;
-    if ((g_mul_impl == 0 || g_mul_impl == 5) && small_op && M != 3) limb_pairs = (la == 1 && lb == 1) ? 1 : 2;
-    if (g_mul_impl == 4 && small_op && M != 3) limb_pairs = (la == 1 && lb == 1) ? 1 : digits9(M);
+    int limb_pairs = (impl == 1 || M == 3) ? 1 : la * lb;
+    if ((impl == 0 || impl == 5 || impl == 6) && small_op && M != 3) limb_pairs = (la == 1 && lb == 1) ? 1 : 2;
+    if (impl == 4 && small_op && M != 3) limb_pairs = (la == 1 && lb == 1) ? 1 : digits9(M);
     ProfScope ps_(M == 3 ? PC_MUL_R3 : PC_MUL_RQ, (double)a.n_out, s,
                   2.0 * PS::P * PS::P * limb_pairs * (double)a.n_out);
-    if (g_mul_impl == 1) {
+    if (impl == 1) {
         const int threads = (PS::P8 / 8 + 31) / 32 * 32;
         long long grid = a.n_out;
         if (grid > (1LL << 30)) grid = 1LL << 30;
@@ -533,15 +535,15 @@ int launch_mul(MulArgs a, cudaStream_t s, int la = 2, int lb = 2) {
     // bounds the tensor-core products.  int8 big x big at M = 128 too since the folded B operand
     // halved N (3 CTAs/SM); impl 6 keeps one big x big product per item for A/B.
     // (only where two such CTAs still fit an SM: at p = 1277 the stacked B rows would leave one)
-    const bool big2 = la == 2 && lb == 2 && g_mul_impl != 5 && g_mul_impl != 6 &&
+    const bool big2 = la == 2 && lb == 2 && impl != 5 && impl != 6 &&
                       TcGeom<PS, 2, 2, 2>::MINB >= 2;
     const bool down2 = (a.mode == MUL_DOWN || a.mode == MUL_DOWNH) && (M == 3 || (la == 1 && lb == 1) || big2) &&
-                       g_mul_impl != 2;
+                       impl != 2;
     if (down2) {
         a.mode = a.mode == MUL_DOWN ? MUL_DOWN2 : MUL_DOWNH2;
         a.n_out = (a.cnt_in + 1) / 2;
     }
-    const bool fp4 = g_mul_impl == 0 || g_mul_impl == 4 || g_mul_impl == 5;
+    const bool fp4 = impl == 0 || impl == 4 || impl == 5 || impl == 6;
     if constexpr (M == 3) {
         a.swap = 0;
         if (fp4) return down2 ? launch_tc4<PS, M, 1, 2>(a, s) : launch_tc4<PS, M, 1, 1>(a, s);
@@ -555,13 +557,13 @@ int launch_mul(MulArgs a, cudaStream_t s, int la = 2, int lb = 2) {
         }
         // int8 products at MMA M = 128; M = 64 (half the A bytes per MMA, twice the N) is kept
         // as an A/B mode (impl 5): measured slower
-        const bool m128 = g_mul_impl != 5;
+        const bool m128 = impl != 5;
         if (la == 1 || lb == 1) {
             // the small operand takes the A (Hankel) role.  int8 with two limbs for the big one:
             // measured faster than fp4 with D9 base-9 digits (larger N, digit staging), see
             // DESIGN.md section 6; the fp4 variant stays selectable for A/B (impl 4)
             a.swap = la == 1 ? 0 : 1;
-            if (g_mul_impl == 4) return launch_tc4<PS, M, D9, 1>(a, s);
+            if (impl == 4) return launch_tc4<PS, M, D9, 1>(a, s);
             return m128 ? launch_tc<PS, M, 1, 2>(a, s) : launch_tc<PS, M, 1, 2, 1, 64>(a, s);
         }
         a.swap = 0;
@@ -614,9 +616,9 @@ struct TreeJob {
         if (l == 0) return out_bytes == 2 ? rows16(out0, out_stride) : rows8(out0, out_stride);
         return out_bytes == 2 ? rows16(inv[l], stride()) : rows8(inv[l], stride());
     }
-    int up(cudaStream_t s, uint64_t *nprod) const {
+    int up(cudaStream_t s, uint64_t *nprod, int start = 1) const {
         int rc;
-        for (int l = 1; l <= tp.L; l++) {
+        for (int l = start; l <= tp.L; l++) {
             MulArgs a{};
             a.mode = MUL_PAIRS;
             a.n_out = tp.cnt[l];
@@ -913,8 +915,42 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
             CK(cudaStreamWaitEvent(s3, L.r3->go, 0));
         }
         if ((rc = j3.up(s3, &n_r3))) return rc;
-        if ((rc = jq.up(s, &n_rq))) return rc;
-        if (utrick) {
+        // fp4 small x small paths: u_{2j} = g_{2j} * 3f_{2j+1} and the R/q tree's level 1,
+        // 3f_{2j} * 3f_{2j+1}, share their A operand 3f_{2j+1} (one NPR = 2 work item), then the
+        // odd u_{2j+1} = g_{2j+1} * 3f_{2j}: 2 A-operand fetches per leaf pair instead of 3
+        // (A/B variant, impl 7: fewer A-operand fetches, but it moves the u products from the aux
+        // stream -- where they fill the SMs the latency-bound root inversion leaves idle -- onto
+        // the R/q chain's critical path; measured 2.5% slower than the default)
+        const bool fused_u = utrick && g_mul_impl == 7;
+        if (fused_u) {
+            MulArgs a{};
+            a.mode = MUL_UP0;
+            a.n_out = (long long)((m + 1) / 2);
+            a.cnt_in = (long long)m;
+            a.X = rows8(Gc, PS::P16);
+            a.Y = rows8(Fc, PS::P16, 3);
+            a.out = L.U;
+            a.out_stride = PS::P8;
+            a.out_bytes = 2;
+            a.out2 = L.lq[1];
+            a.out2_stride = PS::P8;
+            {
+                ProfScope ps_(PC_MUL_RQ, (double)(m + m / 2), s, 2.0 * PS::P * PS::P * (double)(m + m / 2));
+                if ((rc = launch_tc4<PS, PS::Q, 1, 2>(a, s))) return rc;
+            }
+            if (m >= 2) {
+                MulArgs b = a;
+                b.mode = MUL_ODDSIB;
+                b.n_out = (long long)(m / 2);
+                b.out2 = nullptr;
+                ProfScope ps_(PC_MUL_RQ, (double)(m / 2), s, 2.0 * PS::P * PS::P * (double)(m / 2));
+                if ((rc = launch_tc4<PS, PS::Q, 1, 1>(b, s))) return rc;
+            }
+            CK(cudaEventRecord(ax->done, s));                   // u final (repair waits on it)
+            n_rq += m / 2;                                       // level 1 (the u are counted below)
+        }
+        if ((rc = jq.up(s, &n_rq, fused_u ? 2 : 1))) return rc;
+        if (utrick && !fused_u) {
             CK(cudaEventRecord(ax->go, s));
             CK(cudaStreamWaitEvent(ax->s, ax->go, 0));
             MulArgs a{};
@@ -1487,7 +1523,7 @@ int sntrup_profile_read_kinds(int reset, double *ms, double *ops, uint64_t *laun
 }
 
 int sntrup_set_mul_impl(int impl) {
-    if (impl < 0 || impl > 6) return SNTRUP_E_ARG;
+    if (impl < 0 || impl > 7) return SNTRUP_E_ARG;
     std::lock_guard<std::mutex> lk(g_mu);
     g_mul_impl = impl;
     return SNTRUP_OK;

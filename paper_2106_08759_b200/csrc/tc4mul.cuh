@@ -423,7 +423,8 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
                     op[k] = (std::remove_reference_t<decltype(*op)>)vv;
                 }
             };
-            uint8_t *orp = (uint8_t *)a.out + orow * a.out_stride * a.out_bytes;
+            uint8_t *orp = (pp == 1 && a.out2) ? (uint8_t *)a.out2 + orow * a.out2_stride * a.out_bytes
+                                               : (uint8_t *)a.out + orow * a.out_stride * a.out_bytes;
             if (a.out_bytes == 2) store(reinterpret_cast<int16_t *>(orp));
             else store(reinterpret_cast<int8_t *>(orp));
         }

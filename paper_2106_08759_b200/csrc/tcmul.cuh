@@ -266,6 +266,14 @@ __device__ __forceinline__ void tc_work(const MulArgs &a, long long it, TcWork<N
 #pragma unroll
     for (int pp = 0; pp < NPR; pp++) { w.unit_v[pp] = false; w.orow[pp] = -1; w.dv[pp] = opnd(a.X, 0); }
     if constexpr (NPR == 2) {
+        if (a.mode == MUL_UP0) {
+            const long long i1 = 2 * it + 1;
+            w.unit_u = i1 >= a.cnt_in;
+            w.du = opnd(a.Y, w.unit_u ? 0 : i1);
+            w.dv[0] = opnd(a.X, 2 * it); w.orow[0] = 2 * it;
+            w.dv[1] = opnd(a.Y, 2 * it); w.orow[1] = it;          // into out2
+            return;
+        }
         // MUL_DOWN2: parent it; out[2it] = Y[it] * X[2it+1] (unit if absent), out[2it+1] = Y[it] * X[2it]
         // MUL_DOWNH2: parent it; out[2it] = Y[it] * X[2it], out[2it+1] = Y[it] * X[2it+1] (if present)
         const bool noswap = a.mode == MUL_DOWNH2;
@@ -284,6 +292,8 @@ __device__ __forceinline__ void tc_work(const MulArgs &a, long long it, TcWork<N
         } else if (a.mode == MUL_SIB) {
             du = a.X; ru = it; dv = a.Y; rv = it ^ 1;
             uv = rv >= a.cnt_in;
+        } else if (a.mode == MUL_ODDSIB) {
+            du = a.Y; ru = 2 * it; dv = a.X; rv = 2 * it + 1;
         } else if (a.mode == MUL_DOWNH) {
             du = a.Y; ru = it >> 1; dv = a.X; rv = it;
         } else {
@@ -296,7 +306,7 @@ __device__ __forceinline__ void tc_work(const MulArgs &a, long long it, TcWork<N
             uu = uv; uv = false;
         }
         w.du = opnd(du, ru); w.unit_u = uu;
-        w.dv[0] = opnd(dv, rv); w.unit_v[0] = uv; w.orow[0] = it;
+        w.dv[0] = opnd(dv, rv); w.unit_v[0] = uv; w.orow[0] = a.mode == MUL_ODDSIB ? 2 * it + 1 : it;
     }
 }
 
@@ -594,7 +604,8 @@ __global__ void __launch_bounds__(128, (TcGeom<PS, LA, LB, NPR, MM>::MINB)) tc_m
                     op[k] = (std::remove_reference_t<decltype(*op)>)vv;
                 }
             };
-            uint8_t *orp = (uint8_t *)a.out + orow * a.out_stride * a.out_bytes;
+            uint8_t *orp = (pp == 1 && a.out2) ? (uint8_t *)a.out2 + orow * a.out2_stride * a.out_bytes
+                                               : (uint8_t *)a.out + orow * a.out_stride * a.out_bytes;
             if (a.out_bytes == 2) store(reinterpret_cast<int16_t *>(orp));
             else store(reinterpret_cast<int8_t *>(orp));
         }
