@@ -1002,10 +1002,11 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
             CK(cudaStreamWaitEvent(cs->s, cs->comp[buf], 0));
             CK(cudaMemcpyAsync(sk_out + c0 * skb, skc, m * skb, cudaMemcpyDeviceToHost, cs->s));
         }
-        if (rings) {                               // join the R/3 chain (G, 1/g, u final)
-            CK(cudaEventRecord(L.r3->done, s3));
-            CK(cudaStreamWaitEvent(s, L.r3->done, 0));
-        }
+        // The R/q chain joins the R/3 chain (G, 1/g and u final after repair) only before its first
+        // h product: the R/q down-sweep needs nothing from R/3, so it overlaps the R/3 down-sweep,
+        // repair and sk encode.
+        bool joined = !rings;
+        if (rings) CK(cudaEventRecord(L.r3->done, s3));
         // H and encode (KeyGen step 5).  With host outputs the tail runs in groups of subtrees:
         // the bottom down-sweep levels (<= SG), h and the pk encode of group j complete before
         // group j+1 starts, so group j's pk slice is copied D2H while the next groups compute
@@ -1031,6 +1032,10 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
             }
             const uint64_t rows = r1 > r0 ? r1 - r0 : 0;
             if (!rows) continue;
+            if (!joined) {
+                CK(cudaStreamWaitEvent(s, L.r3->done, 0));
+                joined = true;
+            }
             {
                 MulArgs a{};
                 if (utrick) {
