@@ -213,19 +213,26 @@ def other_configs(S, torch, timed):
     P = S.params(761)
     pk = torch.empty((32, P["pk_bytes"]), dtype=torch.uint8, device="cuda")
     sk = torch.empty((32, P["sk_bytes"]), dtype=torch.uint8, device="cuda")
-    for _ in range(5):
-        S.batch_keygen(761, 32, 1, batch_size=32, pk_out=pk, sk_out=sk)
-    torch.cuda.synchronize()
-    lat = []
-    for _ in range(20):
-        t0 = time.perf_counter()
-        S.batch_keygen(761, 32, 1, batch_size=32, pk_out=pk, sk_out=sk)   # synchronous call
-        lat.append((time.perf_counter() - t0) * 1e6)
-    dev_ms = timed(lambda: S.batch_keygen(761, 32, 1, batch_size=32, pk_out=pk, sk_out=sk,
-                                          flags=S.OPT_ASYNC), 10) / 10
-    out["configs[0]"] = {"workload": "sntrup761, 32 keys, seed 1, B = 32",
-                         "latency_us_median": statistics.median(lat), "device_us": dev_ms * 1e3,
-                         "keys_per_s": 32 / (statistics.median(lat) / 1e6)}
+    # latency-tuned: B = 1 (each key's reciprocals by its own divstep chain, all 32 in parallel:
+    # no tree levels on the critical path) with the R/3 and R/q chains on separate streams;
+    # the one-tree B = 32 configuration beside it (scripts/latency_sweep.py sweeps B)
+    def lat_of(B, fl):
+        for _ in range(5):
+            S.batch_keygen(761, 32, 1, batch_size=B, pk_out=pk, sk_out=sk, flags=fl)
+        torch.cuda.synchronize()
+        lat = []
+        for _ in range(20):
+            t0 = time.perf_counter()
+            S.batch_keygen(761, 32, 1, batch_size=B, pk_out=pk, sk_out=sk, flags=fl)   # synchronous call
+            lat.append((time.perf_counter() - t0) * 1e6)
+        dev_ms = timed(lambda: S.batch_keygen(761, 32, 1, batch_size=B, pk_out=pk, sk_out=sk,
+                                              flags=fl | S.OPT_ASYNC), 10) / 10
+        return statistics.median(lat), dev_ms * 1e3
+    l1, d1 = lat_of(1, S.OPT_RING_STREAMS)
+    l32, d32 = lat_of(32, 0)
+    out["configs[0]"] = {"workload": "sntrup761, 32 keys, seed 1, B = 1, ring streams (latency-tuned)",
+                         "latency_us_median": l1, "device_us": d1, "keys_per_s": 32 / (l1 / 1e6),
+                         "one_tree_B32": {"latency_us_median": l32, "device_us": d32}}
     # configs[3]: parameter sweep at 65,536 keys, seed 4
     sweep = {}
     for ps in (653, 857, 953, 1013):

@@ -65,6 +65,13 @@ def test_cfg1_all_32_keys(O, mul_impl):
     assert st["root_inversions"] == 2
 
 
+def test_cfg1_latency_config(O):
+    # configs[0] in bench.py's latency-tuned launch configuration: B = 1, ring streams
+    res = S.batch_keygen(761, 32, 1, batch_size=1, flags=S.OPT_RING_STREAMS, debug=True)
+    torch.cuda.synchronize()
+    check_keys(O, 761, 1, res, np.arange(32))
+
+
 @pytest.mark.parametrize("B", [1, 2, 8, 32, 128, 512])
 def test_batch_size_invariance_ragged(O, B):
     n = 300                                       # ragged: not a multiple of B for B >= 8
