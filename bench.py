@@ -458,11 +458,11 @@ def main():
     # (lane priority: the first lane's chunk completes early, so its pk/sk copies overlap the
     # other lanes' compute instead of queueing behind the end of the step)
     e2e_by_chunk = {}
-    R, PR, L4 = S.OPT_RING_STREAMS, S.OPT_LANE_PRIORITY, S.OPT_LANES4
+    R, PR, L4, ST = S.OPT_RING_STREAMS, S.OPT_LANE_PRIORITY, S.OPT_LANES4, S.OPT_STAGGER
     for chunk, fl, tag in ((65536, R, "+rings"), (32768, 0, ""), (32768, R, "+rings"),
                            (16384, R, "+rings"), (32768, R | PR, "+rings+prio"),
-                           (16384, R | PR, "+rings+prio"), (16384, PR | L4, "+prio+lanes4"),
-                           (8192, R | PR, "+rings+prio")):
+                           (40960, R | ST | PR, "+rings+stagger+prio"), (32768, R | ST | PR, "+rings+stagger+prio"),
+                           (24576, R | ST | L4, "+rings+stagger+lanes4")):
         step_host(chunk, fl)
         barrier()
         ms_c = timed(lambda: step_host(chunk, fl), e2e_steps)

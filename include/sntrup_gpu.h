@@ -82,6 +82,9 @@ int sntrup_batch_keygen(int param_set, uint64_t n_keys, uint64_t seed,
                                          outputs are identical either way) */
 #define SNTRUP_OPT_LANES4         32u /* pipeline up to 4 chunks concurrently (one stream set per
                                          lane) instead of 2; outputs identical */
+#define SNTRUP_OPT_STAGGER       128u /* lane k of the first round starts when lane k-1 has finished
+                                         its R/q up-sweep (its throughput phases fill lane k-1's
+                                         latency-bound root inversion); outputs identical */
 #define SNTRUP_OPT_LANE_PRIORITY  64u /* lanes on internal streams of decreasing priority: the
                                          first lane's chunk completes first (its D2H copies overlap
                                          the other lanes' compute); outputs identical */

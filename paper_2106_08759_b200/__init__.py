@@ -38,6 +38,7 @@ OPT_FORCE_SMALL_CHECK = 8
 OPT_RING_STREAMS = 16
 OPT_LANES4 = 32
 OPT_LANE_PRIORITY = 64
+OPT_STAGGER = 128
 
 PARAM_SETS = (653, 761, 857, 953, 1013, 1277)
 

@@ -752,7 +752,7 @@ int ring_stream(int lane, int prio_rank, AuxStream **out) {
 }
 
 constexpr int MAX_LANES = 4;
-struct LaneJoin { cudaEvent_t start = nullptr, end[MAX_LANES] = {}; };
+struct LaneJoin { cudaEvent_t start = nullptr, end[MAX_LANES] = {}, upd[MAX_LANES] = {}; };
 int lane_join_events(LaneJoin **out) {
     static std::map<int, LaneJoin> m;
     int dev = 0;
@@ -760,7 +760,10 @@ int lane_join_events(LaneJoin **out) {
     LaneJoin &j = m[dev];
     if (!j.start) {
         CK(cudaEventCreateWithFlags(&j.start, cudaEventDisableTiming));
-        for (int i = 0; i < MAX_LANES; i++) CK(cudaEventCreateWithFlags(&j.end[i], cudaEventDisableTiming));
+        for (int i = 0; i < MAX_LANES; i++) {
+            CK(cudaEventCreateWithFlags(&j.end[i], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&j.upd[i], cudaEventDisableTiming));
+        }
     }
     *out = &j;
     return SNTRUP_OK;
@@ -878,6 +881,11 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
         uint8_t *pkc = host_out ? pk_stage[sb] : pk_out + c0 * pkb;
         uint8_t *skc = host_out ? sk_stage[sb] : sk_out + c0 * skb;
 
+        // SNTRUP_OPT_STAGGER: lane ci of the first round starts when lane ci-1 has finished its
+        // R/q up-sweep, i.e. its sampling and up-sweeps fill the SMs lane ci-1's root inversion
+        // leaves idle, and lane ci-1 (and its output) completes earlier
+        const bool stagger = (o.flags & SNTRUP_OPT_STAGGER) && nl > 1;
+        if (stagger && ci >= 1 && ci < (uint64_t)nl) CK(cudaStreamWaitEvent(s, lj->upd[ci - 1], 0));
         SampleArgs sa{};
         sa.seed = seed; sa.first = first; sa.n = m;
         sa.G = Gc; sa.F = Fc; sa.attempts = Ac;
@@ -950,6 +958,7 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
             n_rq += m / 2;                                       // level 1 (the u are counted below)
         }
         if ((rc = jq.up(s, &n_rq, fused_u ? 2 : 1))) return rc;
+        if (stagger && ci + 1 < (uint64_t)nl) CK(cudaEventRecord(lj->upd[ci], s));
         if (utrick && !fused_u) {
             CK(cudaEventRecord(ax->go, s));
             CK(cudaStreamWaitEvent(ax->s, ax->go, 0));

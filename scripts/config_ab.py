@@ -17,8 +17,9 @@ pk = torch.empty((n, P["pk_bytes"]), dtype=torch.uint8, device="cuda")
 sk = torch.empty((n, P["sk_bytes"]), dtype=torch.uint8, device="cuda")
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 R = S.OPT_RING_STREAMS
-cfgs = [(1024, 32768, R), (2048, 32768, R), (512, 32768, R), (2048, 65536, R), (1024, 16384, R | S.OPT_LANES4),
-        (2048, 16384, R | S.OPT_LANES4)]
+ST, L4 = S.OPT_STAGGER, S.OPT_LANES4
+cfgs = [(1024, 32768, R), (1024, 32768, R | ST), (1024, 16384, R | ST | L4), (1024, 16384, ST | L4),
+        (1024, 24576, R | ST), (1024, 16384, R | L4)]
 res = {c: [] for c in cfgs}
 for rnd in range(6):
     for c in cfgs:

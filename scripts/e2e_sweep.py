@@ -14,10 +14,11 @@ P = S.params(761)
 pk = torch.empty((n, P["pk_bytes"]), dtype=torch.uint8).pin_memory()
 sk = torch.empty((n, P["sk_bytes"]), dtype=torch.uint8).pin_memory()
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-R, PR, L4 = S.OPT_RING_STREAMS, S.OPT_LANE_PRIORITY, S.OPT_LANES4
-for B in (1024, 512):
-    for chunk in (65536, 49152, 40960, 32768, 24576, 20480, 16384):
-        for fl, tag in ((R, "rings"), (R | PR, "rings+prio"), (PR | L4, "prio+lanes4"), (R | PR | L4, "rings+prio+lanes4")):
+R, PR, L4, ST = S.OPT_RING_STREAMS, S.OPT_LANE_PRIORITY, S.OPT_LANES4, S.OPT_STAGGER
+for B in (1024,):
+    for chunk in (49152, 40960, 32768, 24576, 20480, 16384):
+        for fl, tag in ((R, "rings"), (R | ST, "rings+stagger"), (R | ST | PR, "rings+stagger+prio"),
+                        (ST | L4, "stagger+lanes4"), (R | ST | L4, "rings+stagger+lanes4")):
             if (fl & L4) and chunk > 24576:
                 continue
             f = lambda: S.batch_keygen(761, n, 2, batch_size=B, chunk_keys=chunk, pk_out=pk, sk_out=sk,

@@ -136,6 +136,8 @@ def test_host_output(O, flags):
 
 @pytest.mark.parametrize("B,chunk,flags", [(64, 2048, 0), (1024, 32768, S.OPT_RING_STREAMS),
                                             (1024, 32768, S.OPT_RING_STREAMS | S.OPT_LANE_PRIORITY),
+                                            (1024, 40960, S.OPT_RING_STREAMS | S.OPT_STAGGER | S.OPT_LANE_PRIORITY),
+                                            (1024, 24576, S.OPT_RING_STREAMS | S.OPT_STAGGER | S.OPT_LANES4),
                                             (512, 16384, S.OPT_LANES4 | S.OPT_LANE_PRIORITY)])
 def test_host_output_grouped_tail(O, B, chunk, flags):
     # host outputs with enough trees per chunk for the grouped tail (bottom down-sweep levels, h and
