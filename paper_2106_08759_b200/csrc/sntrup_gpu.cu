@@ -1320,6 +1320,7 @@ int rq_mul_batch(int param_set, uint64_t n, const int16_t *a, const int16_t *b, 
     m.out_stride = pi.p8;
     m.out_bytes = 2;
     m.periodic = 1;
+    std::lock_guard<std::mutex> lk(g_mu);             // launcher caches, profiler state
     SNTRUP_DISPATCH(param_set, return launch_mul<PS, PS::Q>(m, (cudaStream_t)stream));
     return SNTRUP_E_PARAM;
 }
@@ -1338,6 +1339,7 @@ int rq_mul_small_batch(int param_set, uint64_t n, const int16_t *a, const int8_t
     m.out_stride = pi.p8;
     m.out_bytes = 2;
     m.periodic = 0;
+    std::lock_guard<std::mutex> lk(g_mu);             // launcher caches, profiler state
     SNTRUP_DISPATCH(param_set, return launch_mul<PS, PS::Q>(m, (cudaStream_t)stream, 2, 1));
     return SNTRUP_E_PARAM;
 }
@@ -1450,6 +1452,7 @@ int r3_mul_batch(int param_set, uint64_t n, const int8_t *a, const int8_t *b, in
     m.out_stride = pi.p16;
     m.out_bytes = 1;
     m.periodic = 0;
+    std::lock_guard<std::mutex> lk(g_mu);             // launcher caches, profiler state
     SNTRUP_DISPATCH(param_set, return launch_mul<PS, 3>(m, (cudaStream_t)stream, 1, 1));
     return SNTRUP_E_PARAM;
 }

@@ -448,6 +448,50 @@ def test_full_sk_matches_oracle(O, param):
         assert fu[i].tobytes() == O.full_sk(param, 31, 1000 + i, pk[i].tobytes(), sk[i].tobytes()), i
 
 
+def test_concurrent_host_threads(O):
+    # calls from several host threads at once (keygen on one stream, ring products on others) are
+    # serialised where they share launcher state and stay exact
+    import threading
+    P = S.params(761)
+    rng = np.random.default_rng(5)
+    a = torch.from_numpy(rng.integers(-2295, 2296, (64, P["p8"]), dtype=np.int16)).cuda()
+    b = torch.from_numpy(rng.integers(-2295, 2296, (64, P["p8"]), dtype=np.int16)).cuda()
+    a[:, 761:] = 0
+    b[:, 761:] = 0
+    ref_c = O.mul_many(761, 4591, a.cpu().numpy(), b.cpu().numpy())
+    out, errs = {}, []
+
+    def keygen():
+        try:
+            st = torch.cuda.Stream()
+            out["k"] = S.batch_keygen(761, 200, 13, batch_size=32, stream=st)
+            st.synchronize()
+        except Exception as e:          # pragma: no cover
+            errs.append(e)
+
+    def mul(i):
+        try:
+            st = torch.cuda.Stream()
+            c = torch.empty_like(a)
+            for _ in range(20):
+                S.rq_mul_batch(761, a, b, c, stream=st)
+            st.synchronize()
+            out["c%d" % i] = c
+        except Exception as e:          # pragma: no cover
+            errs.append(e)
+
+    ts = [threading.Thread(target=keygen)] + [threading.Thread(target=mul, args=(i,)) for i in range(3)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    torch.cuda.synchronize()
+    assert not errs, errs
+    for i in range(3):
+        assert np.array_equal(out["c%d" % i].cpu().numpy(), ref_c)
+    check_keys(O, 761, 13, out["k"], np.arange(200))
+
+
 def test_kernels_really_launch():
     before = S.kernel_launch_count()
     S.batch_keygen(761, 64, 1)
