@@ -492,6 +492,18 @@ def test_concurrent_host_threads(O):
     check_keys(O, 761, 13, out["k"], np.arange(200))
 
 
+@pytest.mark.parametrize("n,B,chunk,flags", [(1, 1, 0, 0), (1, 4096, 0, 0), (2, 4096, 0, 0), (3, 2, 0, 0),
+                                            (31, 32, 0, 0), (33, 32, 0, 0), (33, 32, 16, 0),
+                                            (129, 64, 64, 0), (129, 64, 64, 2 | 16 | 32)])
+def test_edge_sizes(O, n, B, chunk, flags):
+    # single keys, B larger than n, ragged last trees and chunks (odd counts at every tree level),
+    # several lanes with the last lane partly empty
+    res = S.batch_keygen(761, n, 41, first_key_index=7, batch_size=B, chunk_keys=chunk, flags=flags,
+                         debug=True)
+    torch.cuda.synchronize()
+    check_keys(O, 761, 41, res, np.arange(7, 7 + n), offset=7)
+
+
 def test_kernels_really_launch():
     before = S.kernel_launch_count()
     S.batch_keygen(761, 64, 1)
