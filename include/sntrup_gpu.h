@@ -223,7 +223,9 @@ uint64_t sntrup_kernel_launch_count(void);
    5 = as 0, with the int8 products at MMA M = 64 instead of 128 (A/B only);
    6 = as 0, with one int8 big x big product per work item (A/B only);
    7 = as 0, with keygen's u_{2j} = g_{2j} * 3f_{2j+1} fused with the R/q tree's first level
-       3f_{2j} * 3f_{2j+1} (shared A operand) instead of running on their own stream (A/B only).
+       3f_{2j} * 3f_{2j+1} (shared A operand) instead of running on their own stream (A/B only);
+   8 = as 0, with the int8 big x big products software-pipelined inside one CTA of 8 warps
+       (two operand stages: item k+1 built and issued before item k's epilogue).
    All are exact.  Returns SNTRUP_OK or SNTRUP_E_ARG. */
 int sntrup_set_mul_impl(int impl);
 

@@ -343,6 +343,7 @@ MUL_TENSOR_CORE_FP4_ALL = 4       # fp4 also for big x small (base-9 digits)
 MUL_TENSOR_CORE_M64 = 5           # int8 products at MMA M = 64 (default: 128)
 MUL_TENSOR_CORE_I8_SINGLE = 6     # one int8 big x big product per work item (default: shared A)
 MUL_TENSOR_CORE_U_FUSED = 7       # keygen u products fused with the R/q level 1 (default: own stream)
+MUL_TENSOR_CORE_PIPELINED = 8     # int8 big x big products software-pipelined (2 stages, 8 warps)
 
 
 def set_mul_impl(impl: int):

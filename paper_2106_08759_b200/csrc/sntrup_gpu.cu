@@ -417,7 +417,8 @@ TreePlan make_plan(long long m, int B) {
 // 4 = as 0 but big x small products also on fp4 (base-9 digits; slower, kept for A/B);
 // 5 = as 0 but int8 products with MMA M = 64 (A/B for the M = 128 choice);
 // 6 = as 0 but one int8 big x big product per work item (A/B for the shared-A down-sweep);
-// 7 = as 0 but the keygen's u products fused with the R/q tree's level 1 (shared A; A/B)
+// 7 = as 0 but the keygen's u products fused with the R/q tree's level 1 (shared A; A/B);
+// 8 = as 0 but the int8 big x big products software-pipelined (two operand stages, 8 warps)
 int g_mul_impl = 0;
 
 struct DevInfo { int sms = 0; };
@@ -435,36 +436,37 @@ DevInfo &dev_info() {
 // persistent grid larger than what is resident runs a second partial wave after the first CTAs
 // finish their whole share, so this must not over-count.
 template <class F>
-int resident_ctas(F kern, int smem, int tcols) {
+int resident_ctas(F kern, int smem, int tcols, int threads = 128) {
     cudaFuncAttributes fa;
     if (cudaFuncGetAttributes(&fa, kern) != cudaSuccess) return 1;
     const int regs = (fa.numRegs + 7) / 8 * 8;                  // allocation granularity
-    const int by_regs = regs > 0 ? 65536 / (regs * 128) : 32;
+    const int by_regs = regs > 0 ? 65536 / (regs * threads) : 32;
     const int by_smem = (227 * 1024) / (smem + 1024);
     int nb = by_regs < by_smem ? by_regs : by_smem;
     if (nb * tcols > 512) nb = 512 / tcols;
     return nb < 1 ? 1 : nb;
 }
 
-template <class PS, int M, int LA, int LB, int NPR = 1, int MM = 128, bool XOPS = false>
+template <class PS, int M, int LA, int LB, int NPR = 1, int MM = 128, bool XOPS = false, int NT = 128, int ST = 1>
 int launch_tc_impl(const MulArgs &a, cudaStream_t s) {
     using G = TcGeom<PS, LA, LB, NPR, MM>;
-    auto kern = tc_mul_kernel<PS, M, LA, LB, NPR, MM, XOPS>;
+    constexpr int SMEM = tc_smem_bytes<G, LA, LB, NPR, ST>();
+    auto kern = tc_mul_kernel<PS, M, LA, LB, NPR, MM, XOPS, NT, ST>;
     static std::map<int, int> per_sm;                 // device -> resident CTAs per SM
     int dev = 0;
     CK(cudaGetDevice(&dev));
     auto it = per_sm.find(dev);
     if (it == per_sm.end()) {
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         int nb = 0;
-        nb = resident_ctas(kern, G::SMEM, G::TCOLS);
+        nb = resident_ctas(kern, SMEM, tc_tmem_cols<G, LA, ST>(), NT);
         it = per_sm.emplace(dev, nb).first;
     }
     long long grid = (long long)it->second * dev_info().sms;
     if (grid > a.n_out) grid = a.n_out;
     g_cur_kind = PK_I8;
-    kern<<<(unsigned)grid, 128, G::SMEM, s>>>(a);
+    kern<<<(unsigned)grid, NT, SMEM, s>>>(a);
     LAUNCHED();
     return SNTRUP_OK;
 }
@@ -476,6 +478,13 @@ template <class PS, int M, int LA, int LB, int NPR = 1, int MM = 128>
 int launch_tc(const MulArgs &a, cudaStream_t s) {
     return mul_xops(a) ? launch_tc_impl<PS, M, LA, LB, NPR, MM, true>(a, s)
                        : launch_tc_impl<PS, M, LA, LB, NPR, MM, false>(a, s);
+}
+
+// software-pipelined variant (two operand stages, 8 warps) of the int8 big x big products
+template <class PS, int M, int NPR>
+int launch_tc_pipe(const MulArgs &a, cudaStream_t s) {
+    return mul_xops(a) ? launch_tc_impl<PS, M, 2, 2, NPR, 128, true, 256, 2>(a, s)
+                       : launch_tc_impl<PS, M, 2, 2, NPR, 128, false, 256, 2>(a, s);
 }
 
 template <class PS, int M, int LB, int NPR = 1, bool XOPS = false>
@@ -511,7 +520,8 @@ int launch_tc4(const MulArgs &a, cudaStream_t s) {
 template <class PS, int M>
 int launch_mul(MulArgs a, cudaStream_t s, int la = 2, int lb = 2) {
     if (a.n_out <= 0) return SNTRUP_OK;
-    const int impl = g_mul_impl == 7 ? 0 : g_mul_impl;     // 7 differs only in keygen's u products
+    const int impl = (g_mul_impl == 7 || g_mul_impl == 8) ? 0 : g_mul_impl;   // 7, 8: as 0 except u / pipelining
+    const bool pipe = g_mul_impl == 8;
     // algorithmic ops: tensor path = 2 p^2 int8 multiply-add ops per limb-pair product (the
     // limb-decomposed schoolbook contraction); schoolbook path = 2 p^2 int32 ops per product
     // (fp4 path: digit pairs = LB base-9 digits of the big operand x 1)
@@ -567,7 +577,8 @@ int launch_mul(MulArgs a, cudaStream_t s, int la = 2, int lb = 2) {
             return m128 ? launch_tc<PS, M, 1, 2>(a, s) : launch_tc<PS, M, 1, 2, 1, 64>(a, s);
         }
         a.swap = 0;
-        if (down2) return launch_tc<PS, M, 2, 2, 2>(a, s);
+        if (down2) return pipe ? launch_tc_pipe<PS, M, 2>(a, s) : launch_tc<PS, M, 2, 2, 2>(a, s);
+        if (pipe) return launch_tc_pipe<PS, M, 1>(a, s);
         return m128 ? launch_tc<PS, M, 2, 2>(a, s) : launch_tc<PS, M, 2, 2, 1, 64>(a, s);
     }
 }
@@ -1540,7 +1551,7 @@ int sntrup_profile_read_kinds(int reset, double *ms, double *ops, uint64_t *laun
 }
 
 int sntrup_set_mul_impl(int impl) {
-    if (impl < 0 || impl > 7) return SNTRUP_E_ARG;
+    if (impl < 0 || impl > 8) return SNTRUP_E_ARG;
     std::lock_guard<std::mutex> lk(g_mu);
     g_mul_impl = impl;
     return SNTRUP_OK;

@@ -315,34 +315,49 @@ __device__ __forceinline__ void tc_work(const MulArgs &a, long long it, TcWork<N
 // the accumulator row r lives in TMEM lane 32(r/16) + r%16 (probed: scripts/probe/tmem_m64_probe.cu).
 // XOPS: honour the operand pre-op (RowDesc.mod3) and the output post-op (MulArgs.round3) of the
 // KEM core; compiled out of the keygen instantiations.
-template <class PS, int M, int LA, int LB, int NPR, int MM = 128, bool XOPS = false>
-__global__ void __launch_bounds__(128, (TcGeom<PS, LA, LB, NPR, MM>::MINB)) tc_mul_kernel(MulArgs a) {
+// NT threads per CTA and ST operand stages: ST = 1 (NT = 128) is the plain loop -- several CTAs
+// per SM overlap one CTA's operand build with another's MMAs; ST = 2 (NT = 256, one or two CTAs
+// per SM) software-pipelines inside the CTA: item k+1's operands are built in the second stage and
+// its MMAs issued before item k's epilogue, which then overlaps them.
+template <class PS, int M, int LA, int LB, int NPR, int MM = 128, bool XOPS = false, int NT = 128, int ST = 1>
+__global__ void __launch_bounds__(NT, (ST == 1 ? TcGeom<PS, LA, LB, NPR, MM>::MINB : 1)) tc_mul_kernel(MulArgs a) {
     using G = TcGeom<PS, LA, LB, NPR, MM>;
+    static_assert(ST == 1 || (ST == 2 && MM == 128 && NT == 256), "pipelined variant: M = 128, 8 warps");
+    static_assert(ST == 2 || NT == 128, "plain variant: 4 warps");
     constexpr int P = PS::P;
-    constexpr int CH = G::CH;
     constexpr int PD = G::PD;
+    constexpr int CH = (G::NCHK + 1 + NT - 1) / NT;           // staging chunks per thread (+ s-group -1)
+    constexpr int BPER = (G::BITEMS + NT - 1) / NT;
+    constexpr int ASTG = LA * G::A_BYTES;                     // one stage's A windows
+    constexpr int OFF_B = ST * ASTG;                          // B of stage b at OFF_B + b B_BYTES
+    constexpr int OFF_HA = OFF_B + ST * G::B_BYTES;
+    constexpr int OFF_ZR = OFF_HA + LA * G::HA_LEN;
+    constexpr int OFF_BAR = OFF_ZR + NPR * LB * G::Z_LEN;
+    constexpr int TCU = ST * LA * G::NB;                      // accumulators of every stage
+    constexpr int TCOLS = TCU <= 32 ? 32 : TCU <= 64 ? 64 : TCU <= 128 ? 128 : 256;
     extern __shared__ __align__(1024) uint8_t sm[];
-    uint8_t *sA = sm + G::OFF_A;
-    uint8_t *sB = sm + G::OFF_B;
-    uint8_t *sHA = sm + G::OFF_HA;
-    uint8_t *sZR = sm + G::OFF_ZR;
-    uint64_t *bar = reinterpret_cast<uint64_t *>(sm + G::OFF_BAR);
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sm + G::OFF_BAR + 64);
-    int *fixs = reinterpret_cast<int *>(sm + G::OFF_BAR + 72);     // c[p-1] hand-off (no fix row)
-    const int tid = threadIdx.x, warp = tid >> 5;
+    uint8_t *sHA = sm + OFF_HA;
+    uint8_t *sZR = sm + OFF_ZR;
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sm + OFF_BAR);          // bar[b], one per stage
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sm + OFF_BAR + 64);
+    int *fixs = reinterpret_cast<int *>(sm + OFF_BAR + 72);     // c[p-1] hand-off (no fix row), per product
+    int *fixab_s = reinterpret_cast<int *>(sm + OFF_BAR + 88);  // a[p-1] b[p-1] per stage and product
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    static_assert(88 + 4 * ST * NPR <= 128, "barrier area");
 
-    // ---- one-time setup: zero staging + B (pads stay zero forever), barrier, TMEM
-    for (int i = tid; i < (G::OFF_BAR - G::OFF_B) / 16; i += 128)
-        reinterpret_cast<uint4 *>(sB)[i] = make_uint4(0, 0, 0, 0);
+    // ---- one-time setup: zero staging + B (pads stay zero forever), barriers, TMEM
+    for (int i = tid; i < (OFF_BAR - OFF_B) / 16; i += NT)
+        reinterpret_cast<uint4 *>(sm + OFF_B)[i] = make_uint4(0, 0, 0, 0);
     __syncthreads();
     if (tid == 0) {
-        mbar_init(bar, 1);
+#pragma unroll
+        for (int b = 0; b < ST; b++) mbar_init(bar + b, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(tmem_slot)),
-                     "r"((uint32_t)G::TCOLS));
+                     "r"((uint32_t)TCOLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_fence_before();
@@ -350,12 +365,12 @@ __global__ void __launch_bounds__(128, (TcGeom<PS, LA, LB, NPR, MM>::MINB)) tc_m
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     constexpr uint32_t IDESC = umma_idesc_i8(G::NB, MM);
-    uint32_t phase = 0;
+    uint32_t phases = 0;                                    // mbarrier parity, bit b = stage b
     // fixed per-thread B-build items (product independent): 16-byte-unit offsets
-    int bsrc[G::BPER], bdst[G::BPER], bres[G::BPER];
+    int bsrc[BPER], bdst[BPER], bres[BPER];
 #pragma unroll
-    for (int h = 0; h < G::BPER; h++) {
-        const int w = tid + 128 * h;
+    for (int h = 0; h < BPER; h++) {
+        const int w = tid + NT * h;
         const int slot = w % G::BROWS, grp = w / G::BROWS;
         const int pl = slot / G::RPG, t = slot - pl * G::RPG;    // pl = pp * LB + l
         if (w < G::BITEMS && t < G::NROWS) {
@@ -379,7 +394,7 @@ __global__ void __launch_bounds__(128, (TcGeom<PS, LA, LB, NPR, MM>::MINB)) tc_m
 #pragma unroll
     for (int pp = 0; pp < NPR; pp++) pb1[pp] = 0;
     // A-window rows 4m+s, s = (i + m/2) mod 4: 8 consecutive threads' 16-byte stores then hit 8
-    // distinct bank groups (64m + 16s); m = tid mod 128, so the byte selectors are per-thread
+    // distinct bank groups (64m + 16s); m = tid mod NT, so the byte selectors are per-thread
     // constants
     uint32_t wsel[4];
 #pragma unroll
@@ -391,7 +406,7 @@ __global__ void __launch_bounds__(128, (TcGeom<PS, LA, LB, NPR, MM>::MINB)) tc_m
         tc_work<NPR>(a, it, w);
 #pragma unroll
         for (int h = 0; h < CH; h++) {
-            const int c = tid + 128 * h;
+            const int c = tid + NT * h;
             if (c < G::NCHK) pu[h] = w.unit_u ? make_uint4(0, 0, 0, 0) : load_chunk(w.du, c);
             const int cs = c == G::NCHK ? -1 : c;                // thread NCHK: s-group -1
 #pragma unroll
@@ -409,18 +424,15 @@ __global__ void __launch_bounds__(128, (TcGeom<PS, LA, LB, NPR, MM>::MINB)) tc_m
                 pb1[pp] = (pp > 0 && w.orow[pp] < 0) ? 0 : opnd_coef<XOPS>(w.dv[pp], w.unit_v[pp], P - 1);
         }
     };
-    prefetch(blockIdx.x);
 
-    for (long long it = blockIdx.x; it < a.n_out; it += gridDim.x) {
-        const TcWork<NPR> w = wn;
-        int fixab[NPR];                                   // a[p-1] b[p-1] (thread 0)
+    // ---- stage limbs of the prefetched item (8-byte aligned groups): hA_l[MM + j] = limb_l(u_j);
+    //      Z_{pp,l}: b part (chunk c reversed) and s part (s-group c: bt at 8c+PD .. 8c+PD+7)
+    auto stage = [&](const TcWork<NPR> &w, int (&fixab)[NPR], int b) {
 #pragma unroll
         for (int pp = 0; pp < NPR; pp++) fixab[pp] = 0;
-        // ---- stage limbs (8-byte aligned groups): hA_l[MM + j] = limb_l(u_j);
-        //      Z_{pp,l}: b part (chunk c reversed) and s part (s-group c: bt at 8c+PD .. 8c+PD+7)
 #pragma unroll
         for (int h = 0; h < CH; h++) {
-            const int c = tid + 128 * h;
+            const int c = tid + NT * h;
             if (c < G::NCHK) {
                 int uv8[8];
                 decode_chunk(pu[h], w.du.bytes, w.du.scale, w.unit_u, c, uv8, XOPS ? w.du.mod3 : 0);
@@ -473,6 +485,7 @@ __global__ void __launch_bounds__(128, (TcGeom<PS, LA, LB, NPR, MM>::MINB)) tc_m
                         if (c == 0) {
                             vv8[0] += pb1[pp];                     // bt[0] = b[0] + b[p-1]
                             fixab[pp] = pa1 * pb1[pp];
+                            if (NT == 256) fixab_s[b * NPR + pp] = fixab[pp];   // for the other warp group
                         }
                         const int zo = G::ZB_END - 8 - 8 * c;      // b[8c+i] at ZB_END - 1 - 8c - i
                         SNTRUP_CHECK(zo >= 0 && zo + 8 <= G::ZB_END);
@@ -488,14 +501,19 @@ __global__ void __launch_bounds__(128, (TcGeom<PS, LA, LB, NPR, MM>::MINB)) tc_m
                 }
             }
         }
-        __syncthreads();
-        // ---- A: sliding windows, row rho = hA[rho .. rho+15] (descriptor starts at row 1);
-        //      each work item builds rows 4m .. 4m+3 from 5 words, stores rotated by m (banks)
+    };
+
+    // ---- operands of stage b: A sliding windows (row rho = hA[rho .. rho+15], the descriptor
+    //      starts at row 1; each work item builds rows 4m .. 4m+3 from 5 words) and B rows
+    //      (row pp*PCOL + l*NL + t, K-chunk c = 16-byte unit c of the row's Z window)
+    auto build = [&](int b) {
+        uint8_t *sA = sm + b * ASTG;
+        uint8_t *sB = sm + OFF_B + b * G::B_BYTES;
 #pragma unroll
         for (int l = 0; l < LA; l++) {
 #pragma unroll
-            for (int kw = 0; kw < (G::AROWS4 + 127) / 128; kw++) {
-                const int m = tid + 128 * kw;
+            for (int kw = 0; kw < (G::AROWS4 + NT - 1) / NT; kw++) {
+                const int m = tid + NT * kw;
                 if (m >= G::AROWS4) break;
                 SNTRUP_CHECK(4 * (m + 5) <= G::HA_LEN && 64 * (m + 1) <= G::A_BYTES);
                 const uint32_t *src = reinterpret_cast<const uint32_t *>(sHA + l * G::HA_LEN) + m;
@@ -514,11 +532,10 @@ __global__ void __launch_bounds__(128, (TcGeom<PS, LA, LB, NPR, MM>::MINB)) tc_m
                 }
             }
         }
-        // ---- B: row (pp*PCOL + l*NL + t), K-chunk c = 16-byte unit c of the row's Z window.
-        //      Work item (row, res): chunks c = res + 8i; res = (item/BROWS + row) mod 8 keeps 8
-        //      consecutive lanes on distinct banks for both the load and the store.
+        // work item (row, res): chunks c = res + 8i; res keeps 8 consecutive lanes on distinct
+        // banks for both the load and the store
 #pragma unroll
-        for (int h = 0; h < G::BPER; h++) {
+        for (int h = 0; h < BPER; h++) {
             if (bsrc[h] < 0) continue;
             const uint4 *src = reinterpret_cast<const uint4 *>(sZR) + bsrc[h];
             uint4 *dst = reinterpret_cast<uint4 *>(sB) + bdst[h];
@@ -530,38 +547,41 @@ __global__ void __launch_bounds__(128, (TcGeom<PS, LA, LB, NPR, MM>::MINB)) tc_m
             }
         }
         fence_async_smem();
-        tc_fence_before();
-        __syncthreads();
-        // ---- MMAs (one thread).  Descriptors advance by adding to the start-address field.
-        if (tid == 0) {
-            tc_fence_after();
-            const uint64_t bd0 = umma_desc(smem_u32(sB), G::NB * 16, 128);
-            const uint64_t ad0 = umma_desc(smem_u32(sA) + 16, 256, 128);
-#pragma unroll
-            for (int ks = 0; ks < G::NKS; ks++) {
-                const uint64_t bd = bd0 + (uint64_t)((ks * 32 * G::NB) >> 4);
-#pragma unroll
-                for (int l = 0; l < LA; l++) {
-                    const uint64_t ad = ad0 + (uint64_t)((l * G::A_BYTES + ks * 512) >> 4);
-                    umma_i8(tmem + l * G::NB, ad, bd, IDESC, ks > 0 ? 1u : 0u);
-                }
-            }
-            umma_commit(bar);
-        }
-        prefetch(it + gridDim.x);
-        if (tid == 0) mbar_wait(bar, phase);
-        phase ^= 1;
-        __syncthreads();
+    };
+
+    // ---- MMAs of stage b (one thread) into accumulator set b; descriptors advance by adding to
+    //      the start-address field
+    auto issue = [&](int b) {
         tc_fence_after();
-        // ---- epilogue: thread tid = TMEM lane = coefficient r of every block; outputs go
-        //      straight to HBM (lane-consecutive coefficients: coalesced)
-        const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
+        const uint64_t bd0 = umma_desc(smem_u32(sm + OFF_B + b * G::B_BYTES), G::NB * 16, 128);
+        const uint64_t ad0 = umma_desc(smem_u32(sm + b * ASTG) + 16, 256, 128);
+        const uint32_t acc = tmem + (uint32_t)(b * LA * G::NB);
+#pragma unroll
+        for (int ks = 0; ks < G::NKS; ks++) {
+            const uint64_t bd = bd0 + (uint64_t)((ks * 32 * G::NB) >> 4);
+#pragma unroll
+            for (int l = 0; l < LA; l++) {
+                const uint64_t ad = ad0 + (uint64_t)((l * G::A_BYTES + ks * 512) >> 4);
+                umma_i8(acc + l * G::NB, ad, bd, IDESC, ks > 0 ? 1u : 0u);
+            }
+        }
+        umma_commit(bar + b);
+    };
+
+    // ---- epilogue of accumulator set b: thread = TMEM lane = coefficient r of every block;
+    //      outputs go straight to HBM (lane-consecutive coefficients: coalesced).  With 8 warps
+    //      the warp group g = warp / 4 takes product g (NPR = 2; NPR = 1: group 0 alone)
+    auto epilogue = [&](int b, const TcWork<NPR> &w, const int (&fixab)[NPR]) {
+        const int g = NT == 256 ? warp >> 2 : 0, wq = warp & 3;
+        if (NT == 256 && NPR == 1 && g == 1) return;
+        const uint32_t lane_addr = tmem + (uint32_t)(b * LA * G::NB) + ((uint32_t)(wq * 32) << 16);
         // accumulator row of this thread (MM = 64: lanes 16..31 of each warp hold nothing)
-        const int lane = tid & 31;
-        const int rrow = MM == 128 ? tid : 16 * warp + lane;
+        const int rrow = MM == 128 ? 32 * wq + lane : 16 * warp + lane;
         const bool rowok = MM == 128 || lane < 16;
+        const bool lead = (tid & 127) == 0;                // owns c[0] of its group's product
 #pragma unroll
         for (int pp = 0; pp < NPR; pp++) {
+            if (NT == 256 && NPR == 2 && pp != g) continue;
             int v[LA][G::PCOL / 16][16];
 #pragma unroll
             for (int l = 0; l < LA; l++)
@@ -577,18 +597,24 @@ __global__ void __launch_bounds__(128, (TcGeom<PS, LA, LB, NPR, MM>::MINB)) tc_m
                 if (LB == 1) return (64 * D(0, 0) + D(1, 0)) % M;
                 return (4096 * (D(0, 0) % M) + 64 * (D(0, 1) + D(1, 0)) + D(1, 1)) % M;
             };
-            int fix = 0;                                   // = D(p-1), for thread 0
-            if constexpr (G::FIXROW) {
-                if (warp == 0) fix = __shfl_sync(FULL, comb(G::NT), G::R0);
-            } else {
-                // D(p-1) lives in accumulator row (p-1) mod MM of block (p-1)/MM
-                constexpr int RS = (P - 1) % MM, TS = (P - 1) / MM;
-                constexpr int WS = MM == 128 ? RS / 32 : RS / 16;
-                constexpr int LS = MM == 128 ? RS % 32 : RS % 16;
-                if (warp == WS && lane == LS) fixs[pp] = comb(TS);
-                if (WS == 0) __syncwarp();
-                else if (warp == 0 || warp == WS) asm volatile("bar.sync 1, 64;" ::: "memory");
-                if (tid == 0) fix = fixs[pp];
+            int fix = 0;                                   // = D(p-1), for the c[0] owner
+            const int w0 = 4 * g;                          // first warp of this group
+            {
+                if constexpr (G::FIXROW) {
+                    if (warp == w0) fix = __shfl_sync(FULL, comb(G::NT), G::R0);
+                } else {
+                    // D(p-1) lives in accumulator row (p-1) mod MM of block (p-1)/MM
+                    constexpr int RS = (P - 1) % MM, TS = (P - 1) / MM;
+                    constexpr int WS = MM == 128 ? RS / 32 : RS / 16;
+                    constexpr int LS = MM == 128 ? RS % 32 : RS % 16;
+                    if (warp == w0 + WS && lane == LS) fixs[pp] = comb(TS);
+                    if (WS == 0) __syncwarp();
+                    else if (warp == w0 || warp == w0 + WS) {
+                        if (g == 0) asm volatile("bar.sync 1, 64;" ::: "memory");
+                        else asm volatile("bar.sync 2, 64;" ::: "memory");
+                    }
+                    if (lead) fix = fixs[pp];
+                }
             }
             if (orow < 0 || !rowok) continue;
             auto store = [&](auto *op) {
@@ -598,7 +624,7 @@ __global__ void __launch_bounds__(128, (TcGeom<PS, LA, LB, NPR, MM>::MINB)) tc_m
                     const int k = MM * t + rrow;
                     if (k >= OSTRIDE) break;
                     int x = comb(t);
-                    if (k == 0) x = x - fix + fixab[pp] % M;
+                    if (k == 0) x = x - fix + (NT == 256 ? fixab_s[b * NPR + pp] : fixab[pp]) % M;
                     int vv = k < P ? canon<M>(x) : 0;
                     if (XOPS && a.round3) vv -= canon<3>(vv);      // encapsulation's Round
                     op[k] = (std::remove_reference_t<decltype(*op)>)vv;
@@ -609,12 +635,87 @@ __global__ void __launch_bounds__(128, (TcGeom<PS, LA, LB, NPR, MM>::MINB)) tc_m
             if (a.out_bytes == 2) store(reinterpret_cast<int16_t *>(orp));
             else store(reinterpret_cast<int8_t *>(orp));
         }
-        tc_fence_before();   // TMEM reads ordered before the next item's MMAs (issued after later barriers)
+    };
+
+    if constexpr (ST == 1) {
+        prefetch(blockIdx.x);
+        for (long long it = blockIdx.x; it < a.n_out; it += gridDim.x) {
+            const TcWork<NPR> w = wn;
+            int fixab[NPR];                               // a[p-1] b[p-1] (thread 0)
+            stage(w, fixab, 0);
+            __syncthreads();
+            build(0);
+            tc_fence_before();
+            __syncthreads();
+            if (tid == 0) issue(0);
+            prefetch(it + gridDim.x);
+            if (tid == 0) mbar_wait(bar, phases & 1u);
+            phases ^= 1u;
+            __syncthreads();
+            tc_fence_after();
+            epilogue(0, w, fixab);
+            tc_fence_before();   // TMEM reads ordered before the next item's MMAs (issued after later barriers)
+        }
+    } else {
+        long long it = blockIdx.x;
+        if (it < a.n_out) {
+            prefetch(it);
+            TcWork<NPR> cur = wn;
+            int fcur[NPR];
+            stage(cur, fcur, 0);
+            __syncthreads();
+            build(0);
+            tc_fence_before();
+            __syncthreads();
+            if (tid == 0) issue(0);
+            prefetch(it + gridDim.x);
+            int b = 0;
+            for (; it < a.n_out; it += gridDim.x) {
+                const long long nx = it + gridDim.x;
+                TcWork<NPR> nxt = wn;
+                int fnx[NPR];
+#pragma unroll
+                for (int pp = 0; pp < NPR; pp++) fnx[pp] = 0;
+                if (nx < a.n_out) {
+                    // item nx into stage b^1 while item it's MMAs run (stage b^1's previous MMAs
+                    // completed one iteration ago; the staging area was last read by build before
+                    // the previous barrier)
+                    stage(nxt, fnx, b ^ 1);
+                    __syncthreads();
+                    build(b ^ 1);
+                    tc_fence_before();
+                    prefetch(nx + gridDim.x);
+                }
+                if (tid == 0) mbar_wait(bar + b, (phases >> b) & 1u);
+                phases ^= 1u << b;
+                __syncthreads();                          // also: stage b^1 complete
+                tc_fence_after();
+                // issue item nx's MMAs before this item's epilogue (thread 0 may block in the
+                // issue until the tensor pipe accepts them; the other warps go on)
+                if (tid == 0 && nx < a.n_out) issue(b ^ 1);
+                epilogue(b, cur, fcur);
+                tc_fence_before();
+                cur = nxt;
+#pragma unroll
+                for (int pp = 0; pp < NPR; pp++) fcur[pp] = fnx[pp];
+                b ^= 1;
+            }
+        }
     }
     tc_fence_before();
     __syncthreads();
     if (warp == 0)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)G::TCOLS));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)TCOLS));
+}
+
+// shared memory of a tc_mul_kernel instantiation (ST operand stages)
+template <class G, int LA, int LB, int NPR, int ST>
+constexpr int tc_smem_bytes() {
+    return ST * (LA * G::A_BYTES + G::B_BYTES) + LA * G::HA_LEN + NPR * LB * G::Z_LEN + 128;
+}
+template <class G, int LA, int ST>
+constexpr int tc_tmem_cols() {
+    return ST * LA * G::NB <= 32 ? 32 : ST * LA * G::NB <= 64 ? 64 : ST * LA * G::NB <= 128 ? 128 : 256;
 }
 
 }  // namespace sntrup
