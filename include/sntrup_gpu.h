@@ -102,7 +102,19 @@ typedef struct {
     uint8_t *attempts_out;    /* optional device [n]: number of g draws used (>= 1) */
     uint64_t *stats_out;      /* optional HOST uint64[4]: ring products R/q, ring products R/3,
                                  root inversions, keys repaired (trees whose R/3 root failed) */
+    void *done_event;         /* optional sntrup_event (sntrup_event_create): with
+                                 SNTRUP_OPT_HOST_OUTPUT | SNTRUP_OPT_ASYNC the call returns after
+                                 enqueueing, the outputs' D2H copies are NOT ordered into `stream`
+                                 (the next call's compute overlaps them), and this event completes
+                                 when every pk/sk byte is in host memory.  The host buffers must
+                                 stay untouched until then. */
 } sntrup_keygen_opts;
+
+/* Completion events for asynchronous host-output calls (opaque cudaEvent_t). */
+int sntrup_event_create(void **ev);
+int sntrup_event_synchronize(void *ev);       /* blocks until the event completed */
+int sntrup_event_query(void *ev);             /* SNTRUP_OK when complete, 1 when not yet */
+void sntrup_event_destroy(void *ev);
 
 /* Batch key generation with options (opt may be NULL = defaults). */
 int sntrup_batch_keygen_ex(int param_set, uint64_t n_keys, uint64_t seed,

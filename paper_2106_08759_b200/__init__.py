@@ -49,7 +49,7 @@ class KeygenOpts(ctypes.Structure):
                 ("stream", ctypes.c_void_p), ("h_out", ctypes.c_void_p),
                 ("g_out", ctypes.c_void_p), ("f_out", ctypes.c_void_p),
                 ("ginv_out", ctypes.c_void_p), ("attempts_out", ctypes.c_void_p),
-                ("stats_out", ctypes.c_void_p)]
+                ("stats_out", ctypes.c_void_p), ("done_event", ctypes.c_void_p)]
 
 
 _u64, _i32, _u32, _vp, _sz = ctypes.c_uint64, ctypes.c_int, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_size_t
@@ -87,6 +87,11 @@ _lib.sntrup_decap_core_batch.argtypes = [_i32, _u64, _vp, _vp, _vp, _vp, _vp, _v
 _lib.sntrup_full_sk_bytes.argtypes = [_i32]
 _lib.sntrup_full_sk_bytes.restype = ctypes.c_size_t
 _lib.sntrup_full_sk_batch.argtypes = [_i32, _u64, _u64, _u64, _vp, _vp, _vp, _vp]
+_lib.sntrup_event_create.argtypes = [ctypes.POINTER(_vp)]
+_lib.sntrup_event_synchronize.argtypes = [_vp]
+_lib.sntrup_event_query.argtypes = [_vp]
+_lib.sntrup_event_destroy.argtypes = [_vp]
+_lib.sntrup_event_destroy.restype = None
 
 EXPORTED = ("sntrup_params", "sntrup_strerror", "sntrup_batch_keygen", "sntrup_batch_keygen_ex",
             "sntrup_keygen_workspace_bytes", "rq_mul_batch", "rq_mul_small_batch", "r3_mul_batch", "rq_recip_batch",
@@ -95,7 +100,8 @@ EXPORTED = ("sntrup_params", "sntrup_strerror", "sntrup_batch_keygen", "sntrup_b
             "sntrup_profile_enable", "sntrup_profile_read_kinds", "sntrup_pool_create",
             "sntrup_pool_take", "sntrup_pool_stats", "sntrup_pool_destroy",
             "sntrup_sample_short_batch", "sntrup_encap_core_batch", "sntrup_decap_core_batch",
-            "sntrup_profile_read", "sntrup_full_sk_bytes", "sntrup_full_sk_batch")
+            "sntrup_profile_read", "sntrup_full_sk_bytes", "sntrup_full_sk_batch",
+            "sntrup_event_create", "sntrup_event_synchronize", "sntrup_event_query", "sntrup_event_destroy")
 
 PROFILE_CLASSES = ("sample", "r3_mul", "rq_mul", "root_inv", "rq_inv", "repair", "encode", "other")
 
@@ -135,9 +141,11 @@ def _need(t, dtype, shape, name):
 
 def batch_keygen(param_set: int, n_keys: int, seed: int, *, first_key_index: int = 0,
                  batch_size: int = 32, chunk_keys: int = 0, flags: int = 0, pk_out=None,
-                 sk_out=None, debug: bool = False, stream=None, stats: bool = False):
+                 sk_out=None, debug: bool = False, stream=None, stats: bool = False, done_event=None):
     """Generate n_keys key pairs (global indices first_key_index ..).  Returns dict with pk, sk
-    (uint8 CUDA tensors) and, with debug=True, h/g/f/ginv/attempts."""
+    (uint8 CUDA tensors) and, with debug=True, h/g/f/ginv/attempts.  With host outputs,
+    flags OPT_ASYNC and a done_event (Event), the call returns after enqueueing and the event
+    completes when every output byte is in host memory."""
     P = params(param_set)
     dev = torch.device("cuda", torch.cuda.current_device())
     if pk_out is None:
@@ -161,6 +169,8 @@ def batch_keygen(param_set: int, n_keys: int, seed: int, *, first_key_index: int
     st = (ctypes.c_uint64 * 4)()
     if stats:
         o.stats_out = ctypes.addressof(st)
+    if done_event is not None:
+        o.done_event = done_event.handle
     host = bool(flags & OPT_HOST_OUTPUT)
     pkp = pk_out.data_ptr() if not host else pk_out.data_ptr()
     _check(_lib.sntrup_batch_keygen_ex(param_set, n_keys, seed, ctypes.c_void_p(pkp),
@@ -170,6 +180,29 @@ def batch_keygen(param_set: int, n_keys: int, seed: int, *, first_key_index: int
         out["stats"] = dict(rq_products=st[0], r3_products=st[1], root_inversions=st[2],
                             keys_repaired=st[3])
     return out
+
+
+class Event:
+    """Completion event of an asynchronous host-output keygen call (sntrup_event_*)."""
+
+    def __init__(self):
+        h = ctypes.c_void_p()
+        _check(_lib.sntrup_event_create(ctypes.byref(h)), "sntrup_event_create")
+        self.handle = h.value
+
+    def synchronize(self):
+        _check(_lib.sntrup_event_synchronize(ctypes.c_void_p(self.handle)), "sntrup_event_synchronize")
+
+    def query(self) -> bool:
+        rc = _lib.sntrup_event_query(ctypes.c_void_p(self.handle))
+        if rc not in (0, 1):
+            _check(rc, "sntrup_event_query")
+        return rc == 0
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            _lib.sntrup_event_destroy(ctypes.c_void_p(self.handle))
+            self.handle = None
 
 
 def rq_mul_batch(param_set: int, a, b, c=None, stream=None):

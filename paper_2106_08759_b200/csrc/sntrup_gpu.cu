@@ -340,6 +340,22 @@ int aux_stream(AuxStream **out) {
     return SNTRUP_OK;
 }
 
+// side stream on which asynchronous host-output calls record their completion event, and an
+// event marking the end of the call's work on the caller's stream
+int done_stream(cudaStream_t *out, cudaEvent_t *s0_end) {
+    static std::map<int, std::pair<cudaStream_t, cudaEvent_t>> m;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    auto &x = m[dev];
+    if (!x.first) {
+        CK(cudaStreamCreateWithFlags(&x.first, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&x.second, cudaEventDisableTiming));
+    }
+    *out = x.first;
+    *s0_end = x.second;
+    return SNTRUP_OK;
+}
+
 // ------------------------------------------------------------------------------ workspace
 // One cached workspace per (device, caller stream): calls on different streams never share
 // scratch memory, so asynchronous calls on different streams are independent (the header's
@@ -888,7 +904,9 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
         uint8_t *Ac = o.attempts_out ? o.attempts_out + c0 : L.att;
         int16_t *Hc = o.h_out ? o.h_out + c0 * PS::P8 : L.H;
         CopyStream *cs = csl[ci % nl];
-        if (host_out && ci >= (uint64_t)nbuf) CK(cudaStreamWaitEvent(s, cs->copy[buf], 0));   // staging free
+        // (host outputs: the staging buffer is free once its previous copies -- this call's, or an
+        // earlier asynchronous call's -- are done; waited for right before its first write, so
+        // the chunk's compute overlaps those copies)
         uint8_t *pkc = host_out ? pk_stage[sb] : pk_out + c0 * pkb;
         uint8_t *skc = host_out ? sk_stage[sb] : sk_out + c0 * skb;
 
@@ -1011,6 +1029,7 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
         if (host_out) {
             // sk = Small(f) || Small(1/g) is final here (after repair): encode it and start its
             // D2H copy while the R/q tree runs
+            CK(cudaStreamWaitEvent(s3, cs->copy[buf], 0));          // staging free
             EncArgs ea{};
             ea.n = m; ea.h = nullptr; ea.f = Fc; ea.ginv = Ic; ea.pk = nullptr; ea.sk = skc; ea.t = tb->enc;
             {
@@ -1025,7 +1044,7 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
         // The R/q chain joins the R/3 chain (G, 1/g and u final after repair) only before its first
         // h product: the R/q down-sweep needs nothing from R/3, so it overlaps the R/3 down-sweep,
         // repair and sk encode.
-        bool joined = !rings;
+        bool joined = !rings, pk_staging_free = false;
         if (rings) CK(cudaEventRecord(L.r3->done, s3));
         // H and encode (KeyGen step 5).  With host outputs the tail runs in groups of subtrees:
         // the bottom down-sweep levels (<= SG), h and the pk encode of group j complete before
@@ -1053,8 +1072,12 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
             const uint64_t rows = r1 > r0 ? r1 - r0 : 0;
             if (!rows) continue;
             if (!joined) {
-                CK(cudaStreamWaitEvent(s, L.r3->done, 0));
+                CK(cudaStreamWaitEvent(s, L.r3->done, 0));   // (also orders the sk staging write)
                 joined = true;
+            }
+            if (host_out && !pk_staging_free) {
+                CK(cudaStreamWaitEvent(s, cs->copy[buf], 0));   // pk staging free
+                pk_staging_free = true;
             }
             {
                 MulArgs a{};
@@ -1104,11 +1127,24 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
         CK(cudaEventRecord(lj->end[li], lanes[li].s));
         CK(cudaStreamWaitEvent(s0, lj->end[li], 0));
     }
-    if (host_out) {                        // join the copies into the caller's stream
+    const bool async_host = host_out && (o.flags & SNTRUP_OPT_ASYNC) && o.done_event && !o.stats_out;
+    if (host_out && !async_host) {         // join the copies into the caller's stream
         for (int li = 0; li < nl; li++)
             for (int i = 0; i < 2; i++) CK(cudaStreamWaitEvent(s0, csl[li]->copy[i], 0));
     }
-    const bool sync = !(o.flags & SNTRUP_OPT_ASYNC) || host_out || o.stats_out;
+    if (async_host) {
+        // completion of every output byte, off the caller's stream: a side stream waits for
+        // the lanes' last work and every copy, then records the user's event
+        cudaStream_t ds = nullptr;
+        cudaEvent_t s0_end = nullptr;
+        if ((rc = done_stream(&ds, &s0_end))) return rc;
+        CK(cudaEventRecord(s0_end, s0));                 // the lanes are joined into s0 above
+        CK(cudaStreamWaitEvent(ds, s0_end, 0));
+        for (int li = 0; li < nl; li++)
+            for (int i = 0; i < 2; i++) CK(cudaStreamWaitEvent(ds, csl[li]->copy[i], 0));
+        CK(cudaEventRecord((cudaEvent_t)o.done_event, ds));
+    }
+    const bool sync = !(o.flags & SNTRUP_OPT_ASYNC) || (host_out && !async_host) || o.stats_out;
     if (sync) {
         int herr[MAX_LANES] = {};
         unsigned long long hrep[MAX_LANES] = {};
@@ -1378,6 +1414,32 @@ int sntrup_full_sk_batch(int param_set, uint64_t n, uint64_t seed, uint64_t firs
         return SNTRUP_OK;
     });
     return SNTRUP_E_PARAM;
+}
+
+int sntrup_event_create(void **ev) {
+    if (!ev) return SNTRUP_E_ARG;
+    cudaEvent_t e = nullptr;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    *ev = (void *)e;
+    return SNTRUP_OK;
+}
+
+int sntrup_event_synchronize(void *ev) {
+    if (!ev) return SNTRUP_E_ARG;
+    CK(cudaEventSynchronize((cudaEvent_t)ev));
+    return SNTRUP_OK;
+}
+
+int sntrup_event_query(void *ev) {
+    if (!ev) return SNTRUP_E_ARG;
+    const cudaError_t e = cudaEventQuery((cudaEvent_t)ev);
+    if (e == cudaErrorNotReady) return 1;
+    CK(e);
+    return SNTRUP_OK;
+}
+
+void sntrup_event_destroy(void *ev) {
+    if (ev) cudaEventDestroy((cudaEvent_t)ev);
 }
 
 int sntrup_sample_short_batch(int param_set, uint64_t n, uint64_t seed, uint64_t first_key_index,

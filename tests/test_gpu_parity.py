@@ -505,6 +505,36 @@ def test_edge_sizes(O, n, B, chunk, flags):
     check_keys(O, 761, 41, res, np.arange(7, 7 + n), offset=7)
 
 
+def test_async_host_output_pipeline(O):
+    # asynchronous host-output calls back to back (the next call's compute overlaps the previous
+    # call's copies; staging buffers are reused across calls): every call's bytes, read after its
+    # completion event, equal the synchronous device-output call's and the oracle's (sample)
+    P = S.params(761)
+    n = 8192
+    bufs = [(torch.empty((n, P["pk_bytes"]), dtype=torch.uint8).pin_memory(),
+             torch.empty((n, P["sk_bytes"]), dtype=torch.uint8).pin_memory()) for _ in range(2)]
+    evs = [S.Event(), S.Event()]
+    fl = S.OPT_HOST_OUTPUT | S.OPT_ASYNC | S.OPT_RING_STREAMS
+    seeds = [51, 52, 53, 54]
+    got = {}
+    for k, sd in enumerate(seeds):
+        pk, sk = bufs[k % 2]
+        S.batch_keygen(761, n, sd, batch_size=256, chunk_keys=2048, pk_out=pk, sk_out=sk, flags=fl,
+                       done_event=evs[k % 2])
+        if k >= 1:
+            evs[(k - 1) % 2].synchronize()
+            got[seeds[k - 1]] = (bufs[(k - 1) % 2][0].clone(), bufs[(k - 1) % 2][1].clone())
+    evs[(len(seeds) - 1) % 2].synchronize()
+    got[seeds[-1]] = (bufs[(len(seeds) - 1) % 2][0].clone(), bufs[(len(seeds) - 1) % 2][1].clone())
+    for sd in seeds:
+        ref = S.batch_keygen(761, n, sd, batch_size=256, chunk_keys=2048)
+        torch.cuda.synchronize()
+        assert torch.equal(got[sd][0], ref["pk"].cpu()) and torch.equal(got[sd][1], ref["sk"].cpu()), sd
+    idx = np.arange(0, n, 257)
+    r = oracle_keys(O, 761, seeds[0], idx)
+    assert np.array_equal(got[seeds[0]][0].numpy()[idx], r["pk"])
+
+
 def test_kernels_really_launch():
     before = S.kernel_launch_count()
     S.batch_keygen(761, 64, 1)
