@@ -66,8 +66,8 @@ struct Tc4Geom {
     static constexpr int K = 64 * NKS;
     static constexpr int NT = (P + 127) / 128;                // output blocks (folded B, tcmul.cuh)
     static constexpr int NL = (NT + 1 + 7) / 8 * 8;           // B rows per digit (+ the fix row)
-    static constexpr int PCOL = (LB * NL + 15) / 16 * 16;
-    static constexpr int NB = NPR * PCOL;
+    static constexpr int PCOL = LB * NL;                      // D columns per product (multiple of 8)
+    static constexpr int NB = (NPR * PCOL + 15) / 16 * 16;   // N of the MMA: the products' rows packed
     // window rows: the descriptor starts at row 1 and reads rows up to 127 + 32*(2*NKS-1) + 32
     static constexpr int AROWS = 64 * NKS + 128;             // multiple of 8
     static constexpr int A_BYTES = AROWS * 16;
@@ -389,17 +389,17 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
         tc_fence_after();
         // ---- epilogue: thread tid = TMEM lane = coefficient r of every block, straight to HBM
         const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
+        int v[G::NB / 16][16];                            // every product's columns, one load
+#pragma unroll
+        for (int c16 = 0; c16 < G::NB / 16; c16++) tmem_ld16(lane_addr + 16 * c16, v[c16]);
+        tmem_ld_wait();
 #pragma unroll
         for (int pp = 0; pp < NPR; pp++) {
-            int v[G::PCOL / 16][16];
-#pragma unroll
-            for (int c16 = 0; c16 < G::PCOL / 16; c16++) tmem_ld16(lane_addr + pp * G::PCOL + 16 * c16, v[c16]);
-            tmem_ld_wait();
             auto comb = [&](int t) {
                 int x = 0;
 #pragma unroll
                 for (int l = LB - 1; l >= 0; l--) {
-                    const int col = l * G::NL + t;
+                    const int col = pp * G::PCOL + l * G::NL + t;
                     x = 9 * x + __float2int_rn(__int_as_float(v[col >> 4][col & 15]));
                 }
                 return LB > 1 ? x % M : x;
@@ -416,7 +416,10 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
                     if (k >= OSTRIDE) break;
                     int vv;
                     if (k == 0) vv = canon<M>(comb(0) - fix + fixab[pp] % M);
-                    else if (M == 3 && LB == 1) vv = (int)fmodc<3>(__int_as_float(v[t >> 4][t & 15]));  // exact: |D| < 2^20
+                    else if (M == 3 && LB == 1) {
+                        const int col = pp * G::PCOL + t;
+                        vv = (int)fmodc<3>(__int_as_float(v[col >> 4][col & 15]));   // exact: |D| < 2^20
+                    }
                     else vv = canon<M>(comb(t));
                     if (k >= P) vv = 0;
                     if (XOPS && a.round3) vv -= canon<3>(vv);      // encapsulation's Round
