@@ -81,7 +81,10 @@ struct Tc4Geom {
     static constexpr int Z_NIB = (ZMARG + 128 * NT + P + 64 + 255) / 256 * 256;
     static constexpr int ZR_BYTES = Z_NIB / 2;
     static constexpr int NCHB = 2 * NKS;                      // 16-byte K-chunks per B row
-    static constexpr int B_BYTES = NCHB * NB * 16;
+    // B: K-chunk c of row r at 16-byte unit c (NB + 1) + r (one pad unit per chunk, so the B build's
+    // stores of consecutive chunks land on distinct bank groups)
+    static constexpr int BLD = NB + 1;                        // 16-byte units between K-chunks
+    static constexpr int B_BYTES = NCHB * BLD * 16;
     static constexpr int SFCOL = NB;                          // scale-factor columns after the accumulators
     static constexpr int TCOLS_USED = NB + 8;
     static constexpr int TCOLS = TCOLS_USED <= 32 ? 32 : TCOLS_USED <= 64 ? 64 : TCOLS_USED <= 128 ? 128 : 256;
@@ -93,12 +96,14 @@ struct Tc4Geom {
     static constexpr int OFF_ZR = OFF_HA + HA_BYTES;
     static constexpr int OFF_BAR = OFF_ZR + NPR * LB * ZR_BYTES;
     static constexpr int SMEM = OFF_BAR + 128;
-    // B build work items: per (pp, limb) group RPG row slots (NT + 1 rows, padded to a multiple
-    // of 8 so 8 consecutive lanes own 8 distinct rows = 8 distinct bank groups); 8 items per slot
-    static constexpr int RPG = (NT + 1 + 7) / 8 * 8;
-    static constexpr int BROWS = NPR * LB * RPG;
-    static constexpr int BITEMS = BROWS * 8;
-    static constexpr int BPER = (BITEMS + 127) / 128;
+    // B build: one work item per Z unit u of each (pp, limb) group: it feeds chunk c = u - zrow(t)/32 of
+    // every row t whose window covers it (each Z unit is read once, written to up to NT + 1 rows)
+    static constexpr int ZFIX = (ZMARG + 128 * NT + 1 - 128 + R0 - P) / 32;   // fix row's first unit
+    static constexpr int ZU0 = ZFIX < ZMARG / 32 ? ZFIX : ZMARG / 32;        // lowest unit read
+    static constexpr int ZU1 = (ZMARG + 128 * (NT - 1)) / 32 + NCHB;       // one past the highest
+    static constexpr int ZUN = ZU1 - ZU0;
+    static constexpr int UITEMS = NPR * LB * ZUN;
+    static constexpr int UPER = (UITEMS + 127) / 128;
     static_assert(NB <= 256, "N too large");
     static_assert(4 * (16 + NCHK) <= HA_BYTES, "hA too short (staging)");
     static_assert(4 * (AROWS / 8 + 5) <= HA_BYTES, "hA too short (windows)");
@@ -191,24 +196,8 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
     __syncthreads();
     constexpr uint32_t IDESC = umma_idesc_mxf4(G::NB);
     uint32_t phase = 0;
-    int bsrc[G::BPER], bdst[G::BPER], bres[G::BPER];
-#pragma unroll
-    for (int h = 0; h < G::BPER; h++) {
-        const int w = tid + 128 * h;
-        const int slot = w % G::BROWS, grp = w / G::BROWS;
-        const int pl = slot / G::RPG, t = slot - pl * G::RPG;    // pl = pp * LB + l
-        if (w < G::BITEMS && t <= G::NT) {
-            const int pp = pl / LB, l = pl - pp * LB;
-            const int zs = G::zrow(t) / 32;                        // window start, 16-byte units
-            // chunks c = res + 8i; res makes the loads of 8 consecutive lanes hit 8 bank groups
-            // (stores: row t mod 8 already distinct)
-            bres[h] = (grp + slot - zs) & 7;
-            bsrc[h] = pl * (G::ZR_BYTES / 16) + zs;
-            bdst[h] = pp * G::PCOL + l * G::NL + t;
-        } else {
-            bsrc[h] = -1; bdst[h] = 0; bres[h] = 0;
-        }
-    }
+    static_assert(G::zrow(G::NT) / 32 >= G::ZU0 && G::zrow(G::NT - 1) / 32 >= G::ZU0 &&
+                  G::zrow(0) / 32 + G::NCHB == G::ZU1 && G::ZU1 * 16 <= G::ZR_BYTES, "B build units");
 
     uint4 pu[CH], pv[NPR][CH], pn[NPR][CH];
     int pa1 = 0, pb1[NPR];
@@ -354,17 +343,23 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
                 dst[(i + (tid >> 1)) & 3] = o;
             }
         }
-        // ---- B rows (aligned 16-byte chunks of the rows' Z windows)
+        // ---- B rows: each Z unit read once and stored into every row window that covers it
 #pragma unroll
-        for (int h = 0; h < G::BPER; h++) {
-            if (bsrc[h] < 0) continue;
-            const uint4 *src = reinterpret_cast<const uint4 *>(sZR) + bsrc[h];
-            uint4 *dst = reinterpret_cast<uint4 *>(sB) + bdst[h];
-#pragma unroll 4
-            for (int c = bres[h]; c < G::NCHB; c += 8) {
-                SNTRUP_CHECK(bsrc[h] + c < NPR * LB * G::ZR_BYTES / 16 && bdst[h] + c * G::NB < G::B_BYTES / 16);
-                SNTRUP_CHECK((bsrc[h] % (G::ZR_BYTES / 16)) + c < G::ZR_BYTES / 16);
-                dst[c * G::NB] = src[c];
+        for (int h = 0; h < G::UPER; h++) {
+            const int w = tid + 128 * h;
+            if (w >= G::UITEMS) break;
+            const int pl = w / G::ZUN, u = G::ZU0 + (w - pl * G::ZUN);          // pl = pp * LB + l
+            const int pp = pl / LB, l = pl - pp * LB;
+            SNTRUP_CHECK(pl * (G::ZR_BYTES / 16) + u < NPR * LB * G::ZR_BYTES / 16);
+            const uint4 z = reinterpret_cast<const uint4 *>(sZR)[pl * (G::ZR_BYTES / 16) + u];
+            uint4 *dst = reinterpret_cast<uint4 *>(sB) + pp * G::PCOL + l * G::NL;
+#pragma unroll
+            for (int t = 0; t <= G::NT; t++) {
+                const int c = u - G::zrow(t) / 32;
+                if (c >= 0 && c < G::NCHB) {
+                    SNTRUP_CHECK(pp * G::PCOL + l * G::NL + t + c * G::BLD < G::B_BYTES / 16);
+                    dst[c * G::BLD + t] = z;
+                }
             }
         }
         fence_async_smem();
@@ -372,11 +367,11 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
         __syncthreads();
         if (tid == 0) {
             tc_fence_after();
-            const uint64_t bd0 = umma_desc(smem_u32(sB), G::NB * 16, 128);
+            const uint64_t bd0 = umma_desc(smem_u32(sB), G::BLD * 16, 128);
             const uint64_t ad0 = umma_desc(smem_u32(sA) + 16, 512, 128);
 #pragma unroll
             for (int ks = 0; ks < G::NKS; ks++) {
-                const uint64_t bd = bd0 + (uint64_t)((ks * 32 * G::NB) >> 4);
+                const uint64_t bd = bd0 + (uint64_t)((ks * 32 * G::BLD) >> 4);
                 const uint64_t ad = ad0 + (uint64_t)((ks * 1024) >> 4);
                 umma_mxf4(tmem, ad, bd, IDESC, ks > 0 ? 1u : 0u, tmem + G::SFCOL);
             }
