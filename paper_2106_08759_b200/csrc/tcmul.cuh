@@ -153,7 +153,10 @@ struct TcGeom {
     static constexpr int ZMARG = MM;
     static constexpr int Z_LEN = (ZMARG + MM * NT + P + 32 + 127) / 128 * 128;
     static constexpr int ZB_END = ZMARG + MM * NT;            // b part below, s part from here
-    static constexpr int B_BYTES = 2 * NKS * NB * 16;
+    // B: K-chunk c of row r at 16-byte unit c (NB + 1) + r (one pad unit per chunk, so the B
+    // build's stores of consecutive chunks land on distinct bank groups)
+    static constexpr int BLD = NB + 1;
+    static constexpr int B_BYTES = 2 * NKS * BLD * 16;
     static constexpr int TCOLS_USED = LA * NB;
     static constexpr int TCOLS = TCOLS_USED <= 32 ? 32 : TCOLS_USED <= 64 ? 64 : TCOLS_USED <= 128 ? 128 : 256;
     static constexpr int NCHK = PS::P8 / 8;                   // 8-coefficient input chunks
@@ -173,19 +176,19 @@ struct TcGeom {
     static_assert(PD != 0 && NCHK * 8 > P, "p odd: the s-groups need the next chunk");
     static_assert(ZMARG + MM * NT + 1 - MM + R0 - P >= 0 && (1 + R0 - P) % 16 == 0, "fix row window");
     static_assert(ZMARG + MM * (NT - 1) + K <= Z_LEN, "Z too short");
-    // B build: (row, residue mod 8) work items; row = pp*PCOL + l*NL + t (t <= NT), K-chunks
-    // c = residue + 8i
-    // B build work items: per (pp, limb) group RPG row slots (NT + 1 rows, padded to a multiple
-    // of 8 so 8 consecutive lanes own 8 distinct rows = 8 distinct bank groups); 8 items per slot
-    static constexpr int RPG = (NROWS + 7) / 8 * 8;
-    static constexpr int BROWS = NPR * LB * RPG;
     static constexpr int NCHB = 2 * NKS;                      // 16-byte K-chunks per B row
-    static constexpr int BITEMS = BROWS * 8;
-    static constexpr int BPER = (BITEMS + 127) / 128;
     // start (bytes) of B row t's window in Z
     static constexpr __host__ __device__ int zrow(int t) {
         return t < NT ? ZMARG + MM * (NT - 1 - t) : ZMARG + MM * NT + 1 - MM + R0 - P;
     }
+    // B build: one work item per 16-byte Z unit u of each (pp, limb) group; it feeds chunk
+    // c = u - zrow(t)/16 of every row t whose window covers it (each Z unit read once)
+    static constexpr int ZU0 = (FIXROW && zrow(NT) / 16 < ZMARG / 16) ? zrow(NT) / 16 : ZMARG / 16;
+    static constexpr int ZU1 = zrow(0) / 16 + NCHB;
+    static constexpr int ZUN = ZU1 - ZU0;
+    static constexpr int UITEMS = NPR * LB * ZUN;
+    static_assert(ZU1 * 16 <= Z_LEN, "B build units");
+    static_assert(NPR * PCOL <= NB && NB < BLD && NCHB * BLD * 16 == B_BYTES, "B build stores stay in B");
 };
 
 // limb l (0 = hi, 1 = lo) of a centered coefficient when the operand has L limbs
@@ -327,7 +330,7 @@ __global__ void __launch_bounds__(NT, (ST == 1 ? TcGeom<PS, LA, LB, NPR, MM>::MI
     constexpr int P = PS::P;
     constexpr int PD = G::PD;
     constexpr int CH = (G::NCHK + 1 + NT - 1) / NT;           // staging chunks per thread (+ s-group -1)
-    constexpr int BPER = (G::BITEMS + NT - 1) / NT;
+    constexpr int UPER = (G::UITEMS + NT - 1) / NT;
     constexpr int ASTG = LA * G::A_BYTES;                     // one stage's A windows
     constexpr int OFF_B = ST * ASTG;                          // B of stage b at OFF_B + b B_BYTES
     constexpr int OFF_HA = OFF_B + ST * G::B_BYTES;
@@ -366,25 +369,6 @@ __global__ void __launch_bounds__(NT, (ST == 1 ? TcGeom<PS, LA, LB, NPR, MM>::MI
     const uint32_t tmem = *tmem_slot;
     constexpr uint32_t IDESC = umma_idesc_i8(G::NB, MM);
     uint32_t phases = 0;                                    // mbarrier parity, bit b = stage b
-    // fixed per-thread B-build items (product independent): 16-byte-unit offsets
-    int bsrc[BPER], bdst[BPER], bres[BPER];
-#pragma unroll
-    for (int h = 0; h < BPER; h++) {
-        const int w = tid + NT * h;
-        const int slot = w % G::BROWS, grp = w / G::BROWS;
-        const int pl = slot / G::RPG, t = slot - pl * G::RPG;    // pl = pp * LB + l
-        if (w < G::BITEMS && t < G::NROWS) {
-            const int pp = pl / LB, l = pl - pp * LB;
-            const int zs = G::zrow(t) / 16;                        // window start, 16-byte units
-            // chunks c = res + 8i; res makes the loads of 8 consecutive lanes hit 8 bank groups
-            // (stores: row t mod 8 already distinct)
-            bres[h] = (grp + slot - zs) & 7;
-            bsrc[h] = pl * (G::Z_LEN / 16) + zs;
-            bdst[h] = pp * G::PCOL + l * G::NL + t;
-        } else {
-            bsrc[h] = -1; bdst[h] = 0; bres[h] = 0;
-        }
-    }
 
     // register prefetch of the next work item's rows (in flight during the MMAs / epilogue):
     // chunk c of u and of every v, chunk c+1 of v (the s-groups straddle chunks), and for
@@ -532,18 +516,23 @@ __global__ void __launch_bounds__(NT, (ST == 1 ? TcGeom<PS, LA, LB, NPR, MM>::MI
                 }
             }
         }
-        // work item (row, res): chunks c = res + 8i; res keeps 8 consecutive lanes on distinct
-        // banks for both the load and the store
+        // each Z unit read once and stored into every row window that covers it
 #pragma unroll
-        for (int h = 0; h < BPER; h++) {
-            if (bsrc[h] < 0) continue;
-            const uint4 *src = reinterpret_cast<const uint4 *>(sZR) + bsrc[h];
-            uint4 *dst = reinterpret_cast<uint4 *>(sB) + bdst[h];
-#pragma unroll 4
-            for (int c = bres[h]; c < G::NCHB; c += 8) {
-                SNTRUP_CHECK(bsrc[h] + c < NPR * LB * G::Z_LEN / 16 && bdst[h] + c * G::NB < G::B_BYTES / 16);
-                SNTRUP_CHECK((bsrc[h] % (G::Z_LEN / 16)) + c < G::Z_LEN / 16);
-                dst[c * G::NB] = src[c];
+        for (int h = 0; h < UPER; h++) {
+            const int w = tid + NT * h;
+            if (w >= G::UITEMS) break;
+            const int pl = w / G::ZUN, u = G::ZU0 + (w - pl * G::ZUN);          // pl = pp * LB + l
+            const int pp = pl / LB, l = pl - pp * LB;
+            SNTRUP_CHECK(pl * (G::Z_LEN / 16) + u < NPR * LB * G::Z_LEN / 16);
+            const uint4 z = reinterpret_cast<const uint4 *>(sZR)[pl * (G::Z_LEN / 16) + u];
+            uint4 *dst = reinterpret_cast<uint4 *>(sB) + pp * G::PCOL + l * G::NL;
+#pragma unroll
+            for (int t = 0; t < G::NROWS; t++) {
+                const int c = u - G::zrow(t) / 16;
+                if (c >= 0 && c < G::NCHB) {
+                    // in range by construction: base + t < NPR PCOL <= NB < BLD and c < NCHB
+                    dst[c * G::BLD + t] = z;
+                }
             }
         }
         fence_async_smem();
@@ -553,12 +542,12 @@ __global__ void __launch_bounds__(NT, (ST == 1 ? TcGeom<PS, LA, LB, NPR, MM>::MI
     //      the start-address field
     auto issue = [&](int b) {
         tc_fence_after();
-        const uint64_t bd0 = umma_desc(smem_u32(sm + OFF_B + b * G::B_BYTES), G::NB * 16, 128);
+        const uint64_t bd0 = umma_desc(smem_u32(sm + OFF_B + b * G::B_BYTES), G::BLD * 16, 128);
         const uint64_t ad0 = umma_desc(smem_u32(sm + b * ASTG) + 16, 256, 128);
         const uint32_t acc = tmem + (uint32_t)(b * LA * G::NB);
 #pragma unroll
         for (int ks = 0; ks < G::NKS; ks++) {
-            const uint64_t bd = bd0 + (uint64_t)((ks * 32 * G::NB) >> 4);
+            const uint64_t bd = bd0 + (uint64_t)((ks * 32 * G::BLD) >> 4);
 #pragma unroll
             for (int l = 0; l < LA; l++) {
                 const uint64_t ad = ad0 + (uint64_t)((l * G::A_BYTES + ks * 512) >> 4);
