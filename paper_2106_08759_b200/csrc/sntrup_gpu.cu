@@ -1050,7 +1050,9 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
         // the bottom down-sweep levels (<= SG), h and the pk encode of group j complete before
         // group j+1 starts, so group j's pk slice is copied D2H while the next groups compute
         // (pk is 3/4 of the output bytes and only exists at the very end of its subtrees).
-        const int nsub = host_out ? 4 : 1;
+        // (asynchronous host-output calls overlap their copies with the next call instead)
+        const bool async_req = host_out && (o.flags & SNTRUP_OPT_ASYNC) && o.done_event && !o.stats_out;
+        const int nsub = (host_out && !async_req) ? 4 : 1;
         const long long nroots = tp.cnt[tp.L];
         const bool grouped = host_out && utrick && nroots >= nsub;
         const int SG = tp.L < 5 ? tp.L : 5;
