@@ -15,62 +15,133 @@ namespace sntrup {
 // Warp-wide bitonic sort of 32*E uint32 keys held in registers, blocked layout: lane l holds
 // global elements l*E .. l*E+E-1 in v[0..E-1].  Ascending.  A fixed network (constant time).
 // Variant with every comparator ascending: each merge stage starts with the "mirror" step
-// (i <-> i ^ (k-1)) followed by half-cleaners (i <-> i ^ j), so no direction selects are needed;
-// across lanes a comparator is one SHFL plus one predicated min/max.
+// (i <-> i ^ (k-1)) followed by half-cleaners (i <-> i ^ j), so no direction selects are needed.
+// Comparators on the low log2(E) index bits are in-register (min + max).  For E >= 32 the merge
+// stages with k >= 4E transpose the warp's keys through shared memory into the striped layout
+// (lane L holds elements r*32 + L in v[r]), where every index bit >= 5 is a register bit: the
+// mirror is one SHFL per key and the half-cleaners with j >= 32 are in-register; the transpose
+// back then leaves j < 32 in registers again.  (The blocked-only network spends a SHFL and a
+// per-lane min/max select per key on each of its 15 cross-lane stages at E = 32.)
+// Shared memory: 4 warps per block (all callers launch 128 threads).
 // ---------------------------------------------------------------------------------------------
-template <int E>
-__device__ __forceinline__ void warp_bitonic_sort(uint32_t (&v)[E], int lane) {
-    constexpr int N = 32 * E;
-    constexpr int LOGN = E == 16 ? 9 : E == 32 ? 10 : E == 64 ? 11 : E == 8 ? 8 : -1;
-    static_assert(LOGN > 0 && (1 << LOGN) == N, "E must be 8, 16, 32 or 64");
-    // (linear induction variables: the loops fully unroll and v stays in registers)
+// Padded shared-memory index for the blocked <-> striped transposes: rows of 32 keys padded to
+// 36 words (16-byte aligned blocked accesses, conflict-free striped accesses).
+__device__ __forceinline__ int sort_pad(int i) { return i + 4 * (i >> 5); }
+
+// One merge stage (k = 2^LS) of warp_bitonic_sort, as a template so that every index is a
+// compile-time constant without relying on the unroller (E = 64 otherwise lands v in local memory).
+template <int E, int LS>
+__device__ __forceinline__ void bitonic_merge_stage(uint32_t (&v)[E], int lane, uint32_t *buf) {
+    constexpr int k = 1 << LS;
+    constexpr bool TRANSPOSE = E >= 32;
+    constexpr bool STRIPED = TRANSPOSE && k >= 4 * E;
+    constexpr int JTOP = STRIPED ? 16 : k >> 2;           // first half-cleaner in blocked layout
+    if constexpr (k <= E) {
+        // mirror step, in-register
 #pragma unroll
-    for (int ls = 1; ls <= LOGN; ls++) {
-        const int k = 1 << ls;
-        // mirror step
-        if (k <= E) {
+        for (int e = 0; e < E; e++) {
+            const int ex = e ^ (k - 1);
+            if ((e & (k >> 1)) == 0) {
+                const uint32_t a = v[e], b = v[ex];
+                v[e] = min(a, b);
+                v[ex] = max(a, b);
+            }
+        }
+    } else if constexpr (!STRIPED) {
+        // mirror step across lanes (blocked): partner lane = lane ^ lm, element E-1-e
+        constexpr int lm = k / E - 1;
+        const bool lower = (lane & ((k / E) >> 1)) == 0;
+        uint32_t o[E];
 #pragma unroll
-            for (int e = 0; e < E; e++) {
-                const int ex = e ^ (k - 1);
-                if ((e & (k >> 1)) == 0) {
-                    const uint32_t a = v[e], b = v[ex];
-                    v[e] = min(a, b);
-                    v[ex] = max(a, b);
+        for (int e = 0; e < E; e++) o[e] = __shfl_xor_sync(FULL, v[E - 1 - e], lm);
+#pragma unroll
+        for (int e = 0; e < E; e++) v[e] = lower ? min(v[e], o[e]) : max(v[e], o[e]);
+    } else {
+        // to striped: lane L holds elements 32 r + L in v[r]
+        __syncwarp();
+#pragma unroll
+        for (int e = 0; e < E; e += 4)
+            *reinterpret_cast<uint4 *>(&buf[sort_pad(lane * E + e)]) = make_uint4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < E; r++) v[r] = buf[sort_pad(32 * r + lane)];
+        // mirror: partner lane ^ 31, register r ^ rm; lower half (r & rh) == 0
+        constexpr int rm = (k - 1) >> 5, rh = k >> 6;
+#pragma unroll
+        for (int r = 0; r < E; r++) {
+            if ((r & rh) == 0) {
+                const uint32_t a = __shfl_xor_sync(FULL, v[r ^ rm], 31);
+                const uint32_t b = __shfl_xor_sync(FULL, v[r], 31);
+                v[r] = min(v[r], a);
+                v[r ^ rm] = max(v[r ^ rm], b);
+            }
+        }
+        // half-cleaners j = k/4 .. 32: register bit j/32
+#pragma unroll
+        for (int jr = k >> 7; jr >= 1; jr >>= 1) {
+#pragma unroll
+            for (int r = 0; r < E; r++) {
+                if ((r & jr) == 0) {
+                    const uint32_t a = v[r], b = v[r | jr];
+                    v[r] = min(a, b);
+                    v[r | jr] = max(a, b);
                 }
             }
-        } else {
-            const int lm = k / E - 1;                      // partner lane = lane ^ lm, element E-1-e
-            const bool lower = (lane & ((k / E) >> 1)) == 0;
-            uint32_t o[E];
-#pragma unroll
-            for (int e = 0; e < E; e++) o[e] = __shfl_xor_sync(FULL, v[E - 1 - e], lm);
-#pragma unroll
-            for (int e = 0; e < E; e++) v[e] = lower ? min(v[e], o[e]) : max(v[e], o[e]);
         }
-        // half-cleaners
+        // back to blocked
+        __syncwarp();
 #pragma unroll
-        for (int lj = ls - 2; lj >= 0; lj--) {
-            const int j = 1 << lj;
-            if (j >= E) {
-                const int lm = j / E;
-                const bool lower = (lane & lm) == 0;
+        for (int r = 0; r < E; r++) buf[sort_pad(32 * r + lane)] = v[r];
+        __syncwarp();
 #pragma unroll
-                for (int e = 0; e < E; e++) {
-                    const uint32_t o = __shfl_xor_sync(FULL, v[e], lm);
-                    v[e] = lower ? min(v[e], o) : max(v[e], o);
-                }
-            } else {
+        for (int e = 0; e < E; e += 4) {
+            const uint4 q = *reinterpret_cast<const uint4 *>(&buf[sort_pad(lane * E + e)]);
+            v[e] = q.x; v[e + 1] = q.y; v[e + 2] = q.z; v[e + 3] = q.w;
+        }
+    }
+    // half-cleaners j = JTOP .. 1 (blocked layout)
 #pragma unroll
-                for (int e = 0; e < E; e++) {
-                    if ((e & j) == 0) {
-                        const uint32_t a = v[e], b = v[e | j];
-                        v[e] = min(a, b);
-                        v[e | j] = max(a, b);
-                    }
+    for (int j = JTOP; j >= 1; j >>= 1) {
+        if (j >= E) {
+            const int lm = j / E;
+            const bool lower = (lane & lm) == 0;
+#pragma unroll
+            for (int e = 0; e < E; e++) {
+                const uint32_t o = __shfl_xor_sync(FULL, v[e], lm);
+                v[e] = lower ? min(v[e], o) : max(v[e], o);
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < E; e++) {
+                if ((e & j) == 0) {
+                    const uint32_t a = v[e], b = v[e | j];
+                    v[e] = min(a, b);
+                    v[e | j] = max(a, b);
                 }
             }
         }
     }
+}
+
+template <int E>
+__device__ __forceinline__ void warp_bitonic_sort(uint32_t (&v)[E], int lane) {
+    constexpr int N = 32 * E;
+    constexpr int LE = E == 8 ? 3 : E == 16 ? 4 : E == 32 ? 5 : E == 64 ? 6 : -1;
+    constexpr int LOGN = LE + 5;
+    static_assert(LE > 0, "E must be 8, 16, 32 or 64");
+    __shared__ __align__(16) uint32_t tb[4][E >= 32 ? N + N / 8 : 4];
+    uint32_t *buf = tb[(threadIdx.x >> 5) & 3];
+    bitonic_merge_stage<E, 1>(v, lane, buf);
+    bitonic_merge_stage<E, 2>(v, lane, buf);
+    bitonic_merge_stage<E, 3>(v, lane, buf);
+    bitonic_merge_stage<E, 4>(v, lane, buf);
+    bitonic_merge_stage<E, 5>(v, lane, buf);
+    bitonic_merge_stage<E, 6>(v, lane, buf);
+    bitonic_merge_stage<E, 7>(v, lane, buf);
+    bitonic_merge_stage<E, 8>(v, lane, buf);
+    if constexpr (LOGN >= 9) bitonic_merge_stage<E, 9>(v, lane, buf);
+    if constexpr (LOGN >= 10) bitonic_merge_stage<E, 10>(v, lane, buf);
+    if constexpr (LOGN >= 11) bitonic_merge_stage<E, 11>(v, lane, buf);
 }
 
 // C4: Short f for key root K (domain d = 0).  Writes the int8 row f[0..P16).
@@ -104,10 +175,10 @@ __device__ __forceinline__ void sample_short_warp(uint64_t K, int8_t *frow, int 
             for (int b = 0; b < 4; b++) {
                 const int e = 16 * w4 + 4 * q + b;
                 const int i = lane * E + e;
-                const int fv = i < PS::P ? (int)(v[e] & 3u) - 1 : 0;
-                word |= ((uint32_t)(fv & 0xff)) << (8 * b);
+                word |= (i < PS::P ? (v[e] & 3u) : 1u) << (8 * b);   // f + 1 in {0,1,2}
             }
-            wd[q] = word;
+            // byte-wise (f + 1) - 1 without borrows: bytes are < 0x80.
+            wd[q] = ((word | 0x80808080u) - 0x01010101u) ^ 0x80808080u;
         }
         *reinterpret_cast<uint4 *>(frow + base) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
     }
@@ -125,13 +196,14 @@ __device__ __forceinline__ void small_block(uint64_t D, int b, uint32_t &pl, uin
         if (i >= PS::P) break;
         const uint64_t z = sm_at(D, (uint64_t)(i / 2));
         const uint32_t u0 = (uint32_t)z & 0x3FFFFFFFu, u1 = (uint32_t)(z >> 32) & 0x3FFFFFFFu;
-        const int c0 = (int)((3ull * u0) >> 30);           // 0,1,2 -> g = c - 1
-        const int c1 = (int)((3ull * u1) >> 30);
-        pl |= (uint32_t)(c0 == 2) << (2 * t);
-        mi |= (uint32_t)(c0 == 0) << (2 * t);
+        // c = (3 u) >> 30 in {0,1,2} -> g = c - 1 (3 u < 2^32): plus iff bit 31 is set, minus iff
+        // c - 1 is negative.
+        const uint32_t t0 = 3u * u0, t1 = 3u * u1;
+        pl |= (t0 >> 31) << (2 * t);
+        mi |= (((t0 >> 30) - 1u) >> 31) << (2 * t);
         if (i + 1 < PS::P) {
-            pl |= (uint32_t)(c1 == 2) << (2 * t + 1);
-            mi |= (uint32_t)(c1 == 0) << (2 * t + 1);
+            pl |= (t1 >> 31) << (2 * t + 1);
+            mi |= (((t1 >> 30) - 1u) >> 31) << (2 * t + 1);
         }
     }
 }
@@ -146,14 +218,12 @@ __device__ __forceinline__ void store_block_int8(int8_t *row, int b, uint32_t pl
         uint32_t wd[4];
 #pragma unroll
         for (int q = 0; q < 4; q++) {
-            uint32_t word = 0;
-#pragma unroll
-            for (int c = 0; c < 4; c++) {
-                const int bit = 16 * h + 4 * q + c;
-                const int val = (int)((pl >> bit) & 1u) - (int)((mi >> bit) & 1u);
-                word |= ((uint32_t)(val & 0xff)) << (8 * c);
-            }
-            wd[q] = word;
+            // SWAR: spread 4 plane bits to the 4 bytes (copies at shifts 0, 7, 14, 21 are disjoint),
+            // then byte = +1 (pl) or 0xFF (mi); the planes are disjoint so no byte sees both.
+            const int sh = 16 * h + 4 * q;
+            const uint32_t P = (((pl >> sh) & 15u) * 0x00204081u) & 0x01010101u;
+            const uint32_t M = (((mi >> sh) & 15u) * 0x00204081u) & 0x01010101u;
+            wd[q] = P | (M * 0xFFu);
         }
         *reinterpret_cast<uint4 *>(row + base) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
     }
