@@ -237,7 +237,10 @@ uint64_t sntrup_kernel_launch_count(void);
    7 = as 0, with keygen's u_{2j} = g_{2j} * 3f_{2j+1} fused with the R/q tree's first level
        3f_{2j} * 3f_{2j+1} (shared A operand) instead of running on their own stream (A/B only);
    8 = as 0, with the int8 big x big products software-pipelined inside one CTA of 8 warps
-       (two operand stages: item k+1 built and issued before item k's epilogue).
+       (two operand stages: item k+1 built and issued before item k's epilogue);
+   9 = as 0, with the first K steps of the fp4 products' Hankel A operand written to TMEM
+       (tcgen05.st) and read by the MMAs from there instead of from shared memory (128-column
+       TMEM allocation per CTA); 10 = as 9 with 64 columns (fewer K steps in TMEM, more CTAs).
    All are exact.  Returns SNTRUP_OK or SNTRUP_E_ARG. */
 int sntrup_set_mul_impl(int impl);
 

@@ -377,6 +377,8 @@ MUL_TENSOR_CORE_M64 = 5           # int8 products at MMA M = 64 (default: 128)
 MUL_TENSOR_CORE_I8_SINGLE = 6     # one int8 big x big product per work item (default: shared A)
 MUL_TENSOR_CORE_U_FUSED = 7       # keygen u products fused with the R/q level 1 (default: own stream)
 MUL_TENSOR_CORE_PIPELINED = 8     # int8 big x big products software-pipelined (2 stages, 8 warps)
+MUL_TENSOR_CORE_TMEM_A = 9        # fp4 products: first K steps of the Hankel A operand in TMEM (128 cols)
+MUL_TENSOR_CORE_TMEM_A64 = 10     # as 9 with a 64-column TMEM allocation
 
 
 def set_mul_impl(impl: int):

@@ -503,10 +503,10 @@ int launch_tc_pipe(const MulArgs &a, cudaStream_t s) {
                        : launch_tc_impl<PS, M, 2, 2, NPR, 128, false, 256, 2>(a, s);
 }
 
-template <class PS, int M, int LB, int NPR = 1, bool XOPS = false>
+template <class PS, int M, int LB, int NPR = 1, bool XOPS = false, int TA = 0>
 int launch_tc4_impl(const MulArgs &a, cudaStream_t s) {
-    using G = Tc4Geom<PS, LB, NPR>;
-    auto kern = tc4_mul_kernel<PS, M, LB, NPR, XOPS>;
+    using G = Tc4Geom<PS, LB, NPR, TA>;
+    auto kern = tc4_mul_kernel<PS, M, LB, NPR, XOPS, TA>;
     static std::map<int, int> per_sm;
     int dev = 0;
     CK(cudaGetDevice(&dev));
@@ -528,6 +528,14 @@ int launch_tc4_impl(const MulArgs &a, cudaStream_t s) {
 
 template <class PS, int M, int LB, int NPR = 1>
 int launch_tc4(const MulArgs &a, cudaStream_t s) {
+    if constexpr (LB == 1) {
+        if (g_mul_impl == 9)                              // A operand in TMEM (128-column allocation)
+            return mul_xops(a) ? launch_tc4_impl<PS, M, LB, NPR, true, 128>(a, s)
+                               : launch_tc4_impl<PS, M, LB, NPR, false, 128>(a, s);
+        if (g_mul_impl == 10)                             // A operand in TMEM (64-column allocation)
+            return mul_xops(a) ? launch_tc4_impl<PS, M, LB, NPR, true, 64>(a, s)
+                               : launch_tc4_impl<PS, M, LB, NPR, false, 64>(a, s);
+    }
     return mul_xops(a) ? launch_tc4_impl<PS, M, LB, NPR, true>(a, s)
                        : launch_tc4_impl<PS, M, LB, NPR, false>(a, s);
 }
@@ -536,7 +544,7 @@ int launch_tc4(const MulArgs &a, cudaStream_t s) {
 template <class PS, int M>
 int launch_mul(MulArgs a, cudaStream_t s, int la = 2, int lb = 2) {
     if (a.n_out <= 0) return SNTRUP_OK;
-    const int impl = (g_mul_impl == 7 || g_mul_impl == 8) ? 0 : g_mul_impl;   // 7, 8: as 0 except u / pipelining
+    const int impl = (g_mul_impl >= 7) ? 0 : g_mul_impl;   // 7, 8, 9: as 0 except u / pipelining / TMEM A
     const bool pipe = g_mul_impl == 8;
     // algorithmic ops: tensor path = 2 p^2 int8 multiply-add ops per limb-pair product (the
     // limb-decomposed schoolbook contraction); schoolbook path = 2 p^2 int32 ops per product
@@ -1615,7 +1623,7 @@ int sntrup_profile_read_kinds(int reset, double *ms, double *ops, uint64_t *laun
 }
 
 int sntrup_set_mul_impl(int impl) {
-    if (impl < 0 || impl > 8) return SNTRUP_E_ARG;
+    if (impl < 0 || impl > 10) return SNTRUP_E_ARG;
     std::lock_guard<std::mutex> lk(g_mu);
     g_mul_impl = impl;
     return SNTRUP_OK;

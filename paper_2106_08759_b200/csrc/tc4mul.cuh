@@ -59,7 +59,12 @@ __device__ __forceinline__ uint32_t nibble_reverse(uint32_t x) {
     return ((y >> 4) & 0x0F0F0F0Fu) | ((y << 4) & 0xF0F0F0F0u);
 }
 
-template <class PS, int LB, int NPR>
+// TA > 0: the first NTA K steps of the Hankel A operand live in TMEM ([a-tmem] MMA form) instead
+// of shared memory, within a TA-column allocation: every thread writes its own window row (TMEM
+// lane r = output residue r) from registers with tcgen05.st, so those MMAs read only B from shared
+// memory (scripts/probe/tmem_a_probe.cu: exact; 12.5 vs 39 cycles per M128 N16 K64 MMA per SM at 4
+// CTAs).  The remaining K steps read shared-memory windows as before.
+template <class PS, int LB, int NPR, int TA = 0>
 struct Tc4Geom {
     static constexpr int P = PS::P;
     static constexpr int NKS = (P + 127 + 63) / 64;          // K steps of 64
@@ -73,6 +78,11 @@ struct Tc4Geom {
     static constexpr int A_BYTES = AROWS * 16;
     static constexpr int HA_WORDS = AROWS / 8 + 8;           // 8 nibbles per word; nibble 128 + j = digit(a_j)
     static constexpr int HA_BYTES = (HA_WORDS * 4 + 127) / 128 * 128;
+    // TA: 5 copies of hA, copy g shifted by g words (copy_g[x] = hA[x + g]) so that every lane's
+    // window words start 16-byte aligned; copies 16 B apart modulo 128 (distinct bank groups)
+    static constexpr int HA_COPIES = TA ? 5 : 1;
+    static constexpr int HA_CSTRIDE = TA ? HA_BYTES + 16 : HA_BYTES;     // bytes between copies
+    static constexpr int HA_TOTAL = (HA_COPIES * HA_CSTRIDE + 127) / 128 * 128;
     // Z (nibbles): bt reversed, Z[ZMARG + E - m] = digit(bt[m]), E = 128 NT - 1 (tcmul.cuh)
     static constexpr int PD = P % 8;
     static constexpr int R0 = (P - 1) % 32;                   // accumulator row of the fix row
@@ -86,14 +96,16 @@ struct Tc4Geom {
     static constexpr int BLD = NB + 1;                        // 16-byte units between K-chunks
     static constexpr int B_BYTES = NCHB * BLD * 16;
     static constexpr int SFCOL = NB;                          // scale-factor columns after the accumulators
-    static constexpr int TCOLS_USED = NB + 8;
-    static constexpr int TCOLS = TCOLS_USED <= 32 ? 32 : TCOLS_USED <= 64 ? 64 : TCOLS_USED <= 128 ? 128 : 256;
+    static constexpr int ACOL = NB + 8;                       // TA: A operand, 8 columns per K step
+    static constexpr int NTA = TA ? ((TA - ACOL) / 8 < NKS ? (TA - ACOL) / 8 : NKS) : 0;
+    static constexpr int TCOLS_USED = ACOL + 8 * NTA;
+    static constexpr int TCOLS = TCOLS_USED <= 32 ? 32 : TCOLS_USED <= 64 ? 64 : TCOLS_USED <= 128 ? 128 : TCOLS_USED <= 256 ? 256 : 512;
     static constexpr int NCHK = PS::P8 / 8;
     static constexpr int CH = (NCHK + 1 + 127) / 128;
     static constexpr int OFF_A = 0;
     static constexpr int OFF_B = OFF_A + A_BYTES;
     static constexpr int OFF_HA = OFF_B + B_BYTES;
-    static constexpr int OFF_ZR = OFF_HA + HA_BYTES;
+    static constexpr int OFF_ZR = OFF_HA + HA_TOTAL;
     static constexpr int OFF_BAR = OFF_ZR + NPR * LB * ZR_BYTES;
     static constexpr int SMEM = OFF_BAR + 128;
     // B build: one work item per Z unit u of each (pp, limb) group: it feeds chunk c = u - zrow(t)/32 of
@@ -105,7 +117,8 @@ struct Tc4Geom {
     static constexpr int UITEMS = NPR * LB * ZUN;
     static constexpr int UPER = (UITEMS + 127) / 128;
     static_assert(NPR * PCOL <= NB && NB < BLD, "B build stores stay in B");
-    static_assert(NB <= 256, "N too large");
+    static_assert(NB <= 256 && TCOLS_USED <= 512, "N too large");
+    static_assert(!TA || (NTA >= 1 && 4 * (8 * NTA + 16) <= HA_BYTES), "TMEM A windows");
     static_assert(4 * (16 + NCHK) <= HA_BYTES, "hA too short (staging)");
     static_assert(4 * (AROWS / 8 + 5) <= HA_BYTES, "hA too short (windows)");
     static_assert(PD != 0 && NCHK * 8 > P, "p odd: the s-groups need the next chunk");
@@ -128,6 +141,16 @@ __device__ __forceinline__ void umma_mxf4(uint32_t tmem_d, uint64_t adesc, uint6
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}\n" ::"r"(tmem_d),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(tsf), "r"(tsf));
+}
+
+// A operand in TMEM ([a-tmem] form; scripts/probe/tmem_a_probe.cu)
+__device__ __forceinline__ void umma_mxf4_ta(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate, uint32_t tsf) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], [%1], %2, %3, [%5], [%6], p;\n\t}\n" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(tsf), "r"(tsf));
 }
 
 // 8 B digits (reversed into one word: value i -> nibble 7 - i), digit l of each value
@@ -154,9 +177,9 @@ __device__ __forceinline__ void digits_rev8(const int (&vals)[8], uint32_t (&dw)
 // M = modulus; A = one digit (the small operand); LB digits for the B operand; NPR products per A.
 // The B operand is folded (bt of tcmul.cuh): LB = 1 sums stay in {0, +-s, +-2s} (s = 1 or 3:
 // e2m1-exact up to 6); LB > 1 sums are reduced mod M before their base-9 digits.
-template <class PS, int M, int LB, int NPR, bool XOPS = false>
+template <class PS, int M, int LB, int NPR, bool XOPS = false, int TA = 0>
 __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
-    using G = Tc4Geom<PS, LB, NPR>;
+    using G = Tc4Geom<PS, LB, NPR, TA>;
     constexpr int P = PS::P;
     constexpr int CH = G::CH;
     constexpr int PD = G::PD;
@@ -257,6 +280,10 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
                 }
                 SNTRUP_CHECK(4 * (16 + c + 1) <= G::HA_BYTES);
                 sHA[16 + c] = word;                                  // nibbles 128 + 8c + i
+                if constexpr (TA) {
+#pragma unroll
+                    for (int g = 1; g < G::HA_COPIES; g++) sHA[g * (G::HA_CSTRIDE / 4) + 16 + c - g] = word;
+                }
             }
             if (c <= G::NCHK) {
                 const int cs = c == G::NCHK ? -1 : c;
@@ -323,10 +350,33 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
             }
         }
         __syncthreads();
+        if constexpr (TA) {
+            // ---- A rows into TMEM: lane r, K step ks = nibbles [1 + r + 64 ks, +64) of hA (the row the
+            // shared-memory descriptor below starts at), 8 columns of 8 nibbles
+            tc_fence_after();
+            const int r1 = tid + 1, g = (r1 >> 3) - 4 * warp;             // 0..4
+            const uint32_t sh = 4u * (uint32_t)(r1 & 7);
+            const uint4 *src = reinterpret_cast<const uint4 *>(reinterpret_cast<const uint8_t *>(sHA) +
+                                                               g * G::HA_CSTRIDE) + warp;
+            const uint32_t la = tmem + ((uint32_t)(warp * 32) << 16) + G::ACOL;
+            uint4 q0 = src[0];
+#pragma unroll
+            for (int ks = 0; ks < G::NTA; ks++) {
+                const uint4 q1 = src[2 * ks + 1], q2 = src[2 * ks + 2];
+                const uint32_t x[9] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x};
+                uint32_t o[8];
+#pragma unroll
+                for (int i = 0; i < 8; i++) o[i] = __funnelshift_r(x[i], x[i + 1], sh);
+                asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(la + 8 * ks),
+                             "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3]), "r"(o[4]), "r"(o[5]), "r"(o[6]), "r"(o[7]));
+                q0 = q2;
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
         // ---- A windows: row rho = nibbles [rho, rho+32); rows 4m..4m+3 share word base m/2
 #pragma unroll
-        for (int kw = 0; kw < (G::AROWS / 4 + 127) / 128; kw++) {
-            const int m = tid + 128 * kw;
+        for (int kw = 0; kw < (G::AROWS / 4 - 16 * G::NTA + 127) / 128; kw++) {
+            const int m = 16 * G::NTA + tid + 128 * kw;          // rows >= 64 NTA: the K steps >= NTA
             if (m >= G::AROWS / 4) break;
             SNTRUP_CHECK(4 * ((m >> 1) + 5) <= G::HA_BYTES && 64 * (m + 1) <= G::A_BYTES);
             const uint32_t *src = sHA + (m >> 1);
@@ -374,7 +424,8 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
             for (int ks = 0; ks < G::NKS; ks++) {
                 const uint64_t bd = bd0 + (uint64_t)((ks * 32 * G::BLD) >> 4);
                 const uint64_t ad = ad0 + (uint64_t)((ks * 1024) >> 4);
-                umma_mxf4(tmem, ad, bd, IDESC, ks > 0 ? 1u : 0u, tmem + G::SFCOL);
+                if (ks < G::NTA) umma_mxf4_ta(tmem, tmem + G::ACOL + 8 * ks, bd, IDESC, ks > 0 ? 1u : 0u, tmem + G::SFCOL);
+                else umma_mxf4(tmem, ad, bd, IDESC, ks > 0 ? 1u : 0u, tmem + G::SFCOL);
             }
             umma_commit(bar);
         }

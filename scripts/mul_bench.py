@@ -48,9 +48,11 @@ def main():
     c3 = torch.empty_like(g)
     impls = {"tc": [S.MUL_TENSOR_CORE], "school": [S.MUL_SCHOOLBOOK]}.get(
         args.impl, [S.MUL_TENSOR_CORE, S.MUL_SCHOOLBOOK])
+    if args.impl.isdigit():
+        impls = [int(args.impl)]
     for impl in impls:
         S.set_mul_impl(impl)
-        name = "tc" if impl == S.MUL_TENSOR_CORE else "schoolbook"
+        name = {S.MUL_TENSOR_CORE: "tc", S.MUL_SCHOOLBOOK: "schoolbook"}.get(impl, "impl%d" % impl)
         w = args.which.split(",")
         if "rq" in w:
             ms = timeit(lambda: S.rq_mul_batch(args.param, a, b, c), args.iters)
