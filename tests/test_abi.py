@@ -4,6 +4,7 @@ import ctypes
 import os
 import re
 import subprocess
+import sys
 
 import pytest
 
@@ -137,3 +138,35 @@ def test_factor_tables_are_factors():
             assert irreducible_gf3(f)
     # 761: f1 digits match SURVEY C16's golden table check
     assert '"22022212120211112011"' in src
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    # no CPU fallback: without the CUDA library the package refuses to import
+    env = dict(os.environ, SNTRUP_GPU_LIB=str(tmp_path / "absent.so"))
+    r = subprocess.run([sys.executable, "-c", "import paper_2106_08759_b200"], cwd=ROOT, env=env,
+                       capture_output=True, text=True)
+    assert r.returncode != 0 and "no CPU fallback" in r.stderr
+
+
+def test_product_code_never_touches_the_oracle():
+    # the oracle is test infrastructure: nothing in the package (Python or CUDA/C) names it
+    pkg = os.path.join(ROOT, "paper_2106_08759_b200")
+    offenders = []
+    for d, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp", ".c")):
+                src = open(os.path.join(d, f), encoding="utf-8", errors="replace").read()
+                for pat in (r"^\s*(import|from)\s+oracle\b", r"#include\s+[\"<][^\">]*oracle",
+                            r"sntrup_oracle|liboracle|oracle\.so|oracle\.py", r"\bor_keygen\b"):
+                    if re.search(pat, src, re.M):
+                        offenders.append((f, pat))
+    assert not offenders, offenders
+
+
+def test_compute_calls_reject_host_tensors(lib):
+    # the Python binding only marshals device tensors; host tensors are an error, not a fallback
+    import torch
+    import paper_2106_08759_b200 as S
+    a = torch.zeros((4, 768), dtype=torch.int16)
+    with pytest.raises((ValueError, RuntimeError, AssertionError)):
+        S.rq_mul_batch(761, a, a.clone())
