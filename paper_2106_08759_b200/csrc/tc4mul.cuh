@@ -257,97 +257,113 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
                 pb1[pp] = (pp > 0 && w.orow[pp] < 0) ? 0 : opnd_coef<XOPS>(w.dv[pp], w.unit_v[pp], P - 1);
         }
     };
-    prefetch(blockIdx.x);
-
-    for (long long it = blockIdx.x; it < a.n_out; it += gridDim.x) {
-        const TcWork<NPR> w = wn;
-        int fixab[NPR];
+    // ---- stage digits of work item w (registers -> hA / Z staging, which the MMAs do not read)
+    auto stage = [&](const TcWork<NPR> &w, int (&fixab)[NPR]) {
 #pragma unroll
         for (int pp = 0; pp < NPR; pp++) fixab[pp] = 0;
-        // ---- stage digits: one 32-bit word (8 nibbles) per 8 coefficients
+            // ---- stage digits: one 32-bit word (8 nibbles) per 8 coefficients
 #pragma unroll
-        for (int h = 0; h < CH; h++) {
-            const int c = tid + 128 * h;
-            if (c < G::NCHK) {
-                uint32_t word = 0;
-                if (w.du.bytes == 1 && !w.unit_u && !(XOPS && w.du.mod3)) {
-                    word = e2m1_pack8_int8(pu[h].x, pu[h].y, w.du.scale);
-                } else {
-                    int uv8[8];
-                    decode_chunk(pu[h], w.du.bytes, w.du.scale, w.unit_u, c, uv8, XOPS ? w.du.mod3 : 0);
+            for (int h = 0; h < CH; h++) {
+                const int c = tid + 128 * h;
+                if (c < G::NCHK) {
+                    uint32_t word = 0;
+                    if (w.du.bytes == 1 && !w.unit_u && !(XOPS && w.du.mod3)) {
+                        word = e2m1_pack8_int8(pu[h].x, pu[h].y, w.du.scale);
+                    } else {
+                        int uv8[8];
+                        decode_chunk(pu[h], w.du.bytes, w.du.scale, w.unit_u, c, uv8, XOPS ? w.du.mod3 : 0);
 #pragma unroll
-                    for (int i = 0; i < 8; i++) word |= e2m1_code(uv8[i]) << (4 * i);
+                        for (int i = 0; i < 8; i++) word |= e2m1_code(uv8[i]) << (4 * i);
+                    }
+                    SNTRUP_CHECK(4 * (16 + c + 1) <= G::HA_BYTES);
+                    sHA[16 + c] = word;                                  // nibbles 128 + 8c + i
+                    if constexpr (TA) {
+#pragma unroll
+                        for (int g = 1; g < G::HA_COPIES; g++) sHA[g * (G::HA_CSTRIDE / 4) + 16 + c - g] = word;
+                    }
                 }
-                SNTRUP_CHECK(4 * (16 + c + 1) <= G::HA_BYTES);
-                sHA[16 + c] = word;                                  // nibbles 128 + 8c + i
-                if constexpr (TA) {
+                if (c <= G::NCHK) {
+                    const int cs = c == G::NCHK ? -1 : c;
 #pragma unroll
-                    for (int g = 1; g < G::HA_COPIES; g++) sHA[g * (G::HA_CSTRIDE / 4) + 16 + c - g] = word;
-                }
-            }
-            if (c <= G::NCHK) {
-                const int cs = c == G::NCHK ? -1 : c;
+                    for (int pp = 0; pp < NPR; pp++) {
+                        uint32_t *zr = reinterpret_cast<uint32_t *>(sZR + pp * LB * G::ZR_BYTES);
+                        const bool fast = LB == 1 && w.dv[pp].bytes == 1 && !w.unit_v[pp] && !(XOPS && w.dv[pp].mod3);
+                        const int zws = (G::ZB_END + (P - PD) - 8 - 8 * cs) / 8;    // s-group word
+                        const int zwb = G::ZB_END / 8 - 1 - c;                      // b[8c+i]: nibble ZB_END-1-8c-i
+                        SNTRUP_CHECK(cs >= G::NCHK - 1 || (8 * zws >= G::ZB_END && 8 * zws + 8 <= G::Z_NIB));
+                        SNTRUP_CHECK(c >= G::NCHK || (zwb >= 0 && 8 * zwb + 8 <= G::ZB_END));
+                        if (c == 0) fixab[pp] = pa1 * pb1[pp];
+                        if (LB == 1 && fast) {
+                            // SWAR: forward-packed chunks, s-group = pairwise sums of two shifted views
+                            const int sc = w.dv[pp].scale;
+                            const uint32_t W0 = c < G::NCHK ? e2m1_pack8_int8(pv[pp][h].x, pv[pp][h].y, sc) : 0u;
+                            if (cs < G::NCHK - 1) {
+                                const uint32_t W1 = e2m1_pack8_int8(pn[pp][h].x, pn[pp][h].y, sc);
+                                zr[zws] = nibble_reverse(e2m1_pair_sum(__funnelshift_r(W0, W1, 4 * PD),
+                                                                       __funnelshift_r(W0, W1, 4 * (PD - 1)), sc));
+                            }
+                            if (c < G::NCHK) {
+                                uint32_t fw = W0;
+                                if (c == 0)                                  // bt[0] = b[0] + b[p-1]
+                                    fw = (W0 & ~0xFu) | e2m1_code(sc * (int)(int8_t)(pv[pp][h].x & 0xFFu) + pb1[pp]);
+                                zr[zwb] = nibble_reverse(fw);
+                            }
+                            continue;
+                        }
+                        int vv8[8], vn8[8];
+                        if (c < G::NCHK)
+                            decode_chunk(pv[pp][h], w.dv[pp].bytes, w.dv[pp].scale, w.unit_v[pp], c, vv8,
+                                         XOPS ? w.dv[pp].mod3 : 0);
+                        else
 #pragma unroll
-                for (int pp = 0; pp < NPR; pp++) {
-                    uint32_t *zr = reinterpret_cast<uint32_t *>(sZR + pp * LB * G::ZR_BYTES);
-                    const bool fast = LB == 1 && w.dv[pp].bytes == 1 && !w.unit_v[pp] && !(XOPS && w.dv[pp].mod3);
-                    const int zws = (G::ZB_END + (P - PD) - 8 - 8 * cs) / 8;    // s-group word
-                    const int zwb = G::ZB_END / 8 - 1 - c;                      // b[8c+i]: nibble ZB_END-1-8c-i
-                    SNTRUP_CHECK(cs >= G::NCHK - 1 || (8 * zws >= G::ZB_END && 8 * zws + 8 <= G::Z_NIB));
-                    SNTRUP_CHECK(c >= G::NCHK || (zwb >= 0 && 8 * zwb + 8 <= G::ZB_END));
-                    if (c == 0) fixab[pp] = pa1 * pb1[pp];
-                    if (LB == 1 && fast) {
-                        // SWAR: forward-packed chunks, s-group = pairwise sums of two shifted views
-                        const int sc = w.dv[pp].scale;
-                        const uint32_t W0 = c < G::NCHK ? e2m1_pack8_int8(pv[pp][h].x, pv[pp][h].y, sc) : 0u;
+                            for (int i = 0; i < 8; i++) vv8[i] = 0;
                         if (cs < G::NCHK - 1) {
-                            const uint32_t W1 = e2m1_pack8_int8(pn[pp][h].x, pn[pp][h].y, sc);
-                            zr[zws] = nibble_reverse(e2m1_pair_sum(__funnelshift_r(W0, W1, 4 * PD),
-                                                                   __funnelshift_r(W0, W1, 4 * (PD - 1)), sc));
+                            // s-group: s[i] = b[i] + b[i-1], i = 8cs+PD+j, at nibble ZB_END + p - 1 - i
+                            decode_chunk(pn[pp][h], w.dv[pp].bytes, w.dv[pp].scale, w.unit_v[pp], cs + 1, vn8,
+                                         XOPS ? w.dv[pp].mod3 : 0);
+                            int s8[8];
+#pragma unroll
+                            for (int j = 0; j < 8; j++) {
+                                const int i0 = PD + j, i1 = PD + j - 1;
+                                s8[j] = (i0 < 8 ? vv8[i0] : vn8[i0 - 8]) + (i1 < 8 ? vv8[i1] : vn8[i1 - 8]);
+                                if (LB > 1) s8[j] = canon<M>(s8[j]);
+                            }
+                            uint32_t dw[LB];
+                            digits_rev8<LB>(s8, dw);
+#pragma unroll
+                            for (int l = 0; l < LB; l++) zr[l * (G::ZR_BYTES / 4) + zws] = dw[l];
                         }
                         if (c < G::NCHK) {
-                            uint32_t fw = W0;
-                            if (c == 0)                                  // bt[0] = b[0] + b[p-1]
-                                fw = (W0 & ~0xFu) | e2m1_code(sc * (int)(int8_t)(pv[pp][h].x & 0xFFu) + pb1[pp]);
-                            zr[zwb] = nibble_reverse(fw);
+                            uint32_t dw[LB];
+                            if (c == 0) {
+                                vv8[0] += pb1[pp];                       // bt[0] = b[0] + b[p-1]
+                                if (LB > 1) vv8[0] = canon<M>(vv8[0]);
+                            }
+                            digits_rev8<LB>(vv8, dw);
+#pragma unroll
+                            for (int l = 0; l < LB; l++) zr[l * (G::ZR_BYTES / 4) + zwb] = dw[l];
                         }
-                        continue;
-                    }
-                    int vv8[8], vn8[8];
-                    if (c < G::NCHK)
-                        decode_chunk(pv[pp][h], w.dv[pp].bytes, w.dv[pp].scale, w.unit_v[pp], c, vv8,
-                                     XOPS ? w.dv[pp].mod3 : 0);
-                    else
-#pragma unroll
-                        for (int i = 0; i < 8; i++) vv8[i] = 0;
-                    if (cs < G::NCHK - 1) {
-                        // s-group: s[i] = b[i] + b[i-1], i = 8cs+PD+j, at nibble ZB_END + p - 1 - i
-                        decode_chunk(pn[pp][h], w.dv[pp].bytes, w.dv[pp].scale, w.unit_v[pp], cs + 1, vn8,
-                                     XOPS ? w.dv[pp].mod3 : 0);
-                        int s8[8];
-#pragma unroll
-                        for (int j = 0; j < 8; j++) {
-                            const int i0 = PD + j, i1 = PD + j - 1;
-                            s8[j] = (i0 < 8 ? vv8[i0] : vn8[i0 - 8]) + (i1 < 8 ? vv8[i1] : vn8[i1 - 8]);
-                            if (LB > 1) s8[j] = canon<M>(s8[j]);
-                        }
-                        uint32_t dw[LB];
-                        digits_rev8<LB>(s8, dw);
-#pragma unroll
-                        for (int l = 0; l < LB; l++) zr[l * (G::ZR_BYTES / 4) + zws] = dw[l];
-                    }
-                    if (c < G::NCHK) {
-                        uint32_t dw[LB];
-                        if (c == 0) {
-                            vv8[0] += pb1[pp];                       // bt[0] = b[0] + b[p-1]
-                            if (LB > 1) vv8[0] = canon<M>(vv8[0]);
-                        }
-                        digits_rev8<LB>(vv8, dw);
-#pragma unroll
-                        for (int l = 0; l < LB; l++) zr[l * (G::ZR_BYTES / 4) + zwb] = dw[l];
                     }
                 }
             }
+    };
+
+    // ES: the next item is staged while this item's MMAs run (its rows prefetched one iteration
+    // earlier).  Not with two products per item: the second item's live state costs registers
+    // (72 -> 86: 7 -> 5 CTAs per SM), measured slower in keygen.
+    constexpr bool ES = NPR == 1;
+    prefetch(blockIdx.x);
+    TcWork<NPR> w = wn;
+    int fixab[NPR];
+    if (ES && blockIdx.x < a.n_out) {
+        stage(w, fixab);
+        prefetch(blockIdx.x + gridDim.x);
+    }
+    for (long long it = blockIdx.x; it < a.n_out; it += gridDim.x) {
+        const long long nx = it + gridDim.x;
+        if constexpr (!ES) {
+            w = wn;
+            stage(w, fixab);
         }
         __syncthreads();
         if constexpr (TA) {
@@ -429,7 +445,18 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
             }
             umma_commit(bar);
         }
-        prefetch(it + gridDim.x);
+        const TcWork<NPR> nxt = wn;
+        int fnx[NPR];
+#pragma unroll
+        for (int pp = 0; pp < NPR; pp++) fnx[pp] = 0;
+        if constexpr (ES) {
+            if (nx < a.n_out) {
+                stage(nxt, fnx);
+                prefetch(nx + gridDim.x);
+            }
+        } else {
+            prefetch(nx);
+        }
         if (tid == 0) mbar_wait(bar, phase);
         phase ^= 1;
         __syncthreads();
@@ -479,6 +506,11 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
             else store(reinterpret_cast<int8_t *>(orp));
         }
         tc_fence_before();
+        if constexpr (ES) {
+            w = nxt;
+#pragma unroll
+            for (int pp = 0; pp < NPR; pp++) fixab[pp] = fnx[pp];
+        }
     }
     tc_fence_before();
     __syncthreads();

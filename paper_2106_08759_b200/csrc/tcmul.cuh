@@ -626,7 +626,12 @@ __global__ void __launch_bounds__(NT, (ST == 1 ? TcGeom<PS, LA, LB, NPR, MM>::MI
         }
     };
 
-    if constexpr (ST == 1) {
+    // ES (big x big only): the next item is staged (registers -> hA / Z staging, which the MMAs
+    // do not read) while this item's MMAs run; its rows were prefetched one iteration earlier.
+    // Elsewhere the second item's live state costs registers and CTAs per SM (80 -> 87 for
+    // big x small: 6 -> 5).
+    constexpr bool ES = LA == 2 && LB == 2;
+    if constexpr (ST == 1 && !ES) {
         prefetch(blockIdx.x);
         for (long long it = blockIdx.x; it < a.n_out; it += gridDim.x) {
             const TcWork<NPR> w = wn;
@@ -644,6 +649,40 @@ __global__ void __launch_bounds__(NT, (ST == 1 ? TcGeom<PS, LA, LB, NPR, MM>::MI
             tc_fence_after();
             epilogue(0, w, fixab);
             tc_fence_before();   // TMEM reads ordered before the next item's MMAs (issued after later barriers)
+        }
+    } else if constexpr (ST == 1) {
+        long long it = blockIdx.x;
+        if (it < a.n_out) {
+            prefetch(it);
+            TcWork<NPR> cur = wn;
+            int fcur[NPR];                                // a[p-1] b[p-1] (thread 0)
+            stage(cur, fcur, 0);
+            prefetch(it + gridDim.x);
+            for (; it < a.n_out; it += gridDim.x) {
+                const long long nx = it + gridDim.x;
+                __syncthreads();                          // staging of item it complete
+                build(0);
+                tc_fence_before();
+                __syncthreads();                          // operands built; staging area free
+                if (tid == 0) issue(0);
+                const TcWork<NPR> nxt = wn;
+                int fnx[NPR];
+#pragma unroll
+                for (int pp = 0; pp < NPR; pp++) fnx[pp] = 0;
+                if (nx < a.n_out) {
+                    stage(nxt, fnx, 0);
+                    prefetch(nx + gridDim.x);
+                }
+                if (tid == 0) mbar_wait(bar, phases & 1u);
+                phases ^= 1u;
+                __syncthreads();
+                tc_fence_after();
+                epilogue(0, cur, fcur);
+                tc_fence_before();   // TMEM reads ordered before the next item's MMAs (issued after later barriers)
+                cur = nxt;
+#pragma unroll
+                for (int pp = 0; pp < NPR; pp++) fcur[pp] = fnx[pp];
+            }
         }
     } else {
         long long it = blockIdx.x;
