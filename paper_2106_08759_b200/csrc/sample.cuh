@@ -30,9 +30,14 @@ __device__ __forceinline__ int sort_pad(int i) { return i + 4 * (i >> 5); }
 
 // One merge stage (k = 2^LS) of warp_bitonic_sort, as a template so that every index is a
 // compile-time constant without relying on the unroller (E = 64 otherwise lands v in local memory).
-template <int E, int LS>
+// NR: keys at positions >= NR are pads (0xFFFFFFFF, above every real key); since every comparator
+// puts the minimum at the lower position, pads never move and a comparator whose upper position
+// is a pad is a no-op -- in the striped layout, registers r >= RP hold only pads and such
+// comparators (and their transposes) are skipped at compile time.
+template <int E, int LS, int NR>
 __device__ __forceinline__ void bitonic_merge_stage(uint32_t (&v)[E], int lane, uint32_t *buf) {
     constexpr int k = 1 << LS;
+    constexpr int RP = (NR + 31) / 32;                    // striped registers holding a real key
     constexpr bool TRANSPOSE = E >= 32;
     constexpr bool STRIPED = TRANSPOSE && k >= 4 * E;
     constexpr int JTOP = STRIPED ? 16 : k >> 2;           // first half-cleaner in blocked layout
@@ -64,12 +69,12 @@ __device__ __forceinline__ void bitonic_merge_stage(uint32_t (&v)[E], int lane, 
             *reinterpret_cast<uint4 *>(&buf[sort_pad(lane * E + e)]) = make_uint4(v[e], v[e + 1], v[e + 2], v[e + 3]);
         __syncwarp();
 #pragma unroll
-        for (int r = 0; r < E; r++) v[r] = buf[sort_pad(32 * r + lane)];
+        for (int r = 0; r < E; r++) v[r] = r < RP ? buf[sort_pad(32 * r + lane)] : 0xFFFFFFFFu;
         // mirror: partner lane ^ 31, register r ^ rm; lower half (r & rh) == 0
         constexpr int rm = (k - 1) >> 5, rh = k >> 6;
 #pragma unroll
         for (int r = 0; r < E; r++) {
-            if ((r & rh) == 0) {
+            if ((r & rh) == 0 && (r ^ rm) < RP) {
                 const uint32_t a = __shfl_xor_sync(FULL, v[r ^ rm], 31);
                 const uint32_t b = __shfl_xor_sync(FULL, v[r], 31);
                 v[r] = min(v[r], a);
@@ -81,7 +86,7 @@ __device__ __forceinline__ void bitonic_merge_stage(uint32_t (&v)[E], int lane, 
         for (int jr = k >> 7; jr >= 1; jr >>= 1) {
 #pragma unroll
             for (int r = 0; r < E; r++) {
-                if ((r & jr) == 0) {
+                if ((r & jr) == 0 && (r | jr) < RP) {
                     const uint32_t a = v[r], b = v[r | jr];
                     v[r] = min(a, b);
                     v[r | jr] = max(a, b);
@@ -91,7 +96,7 @@ __device__ __forceinline__ void bitonic_merge_stage(uint32_t (&v)[E], int lane, 
         // back to blocked
         __syncwarp();
 #pragma unroll
-        for (int r = 0; r < E; r++) buf[sort_pad(32 * r + lane)] = v[r];
+        for (int r = 0; r < RP && r < E; r++) buf[sort_pad(32 * r + lane)] = v[r];   // pads stay in buf
         __syncwarp();
 #pragma unroll
         for (int e = 0; e < E; e += 4) {
@@ -123,7 +128,7 @@ __device__ __forceinline__ void bitonic_merge_stage(uint32_t (&v)[E], int lane, 
     }
 }
 
-template <int E>
+template <int E, int NR = 32 * E>
 __device__ __forceinline__ void warp_bitonic_sort(uint32_t (&v)[E], int lane) {
     constexpr int N = 32 * E;
     constexpr int LE = E == 8 ? 3 : E == 16 ? 4 : E == 32 ? 5 : E == 64 ? 6 : -1;
@@ -131,17 +136,17 @@ __device__ __forceinline__ void warp_bitonic_sort(uint32_t (&v)[E], int lane) {
     static_assert(LE > 0, "E must be 8, 16, 32 or 64");
     __shared__ __align__(16) uint32_t tb[4][E >= 32 ? N + N / 8 : 4];
     uint32_t *buf = tb[(threadIdx.x >> 5) & 3];
-    bitonic_merge_stage<E, 1>(v, lane, buf);
-    bitonic_merge_stage<E, 2>(v, lane, buf);
-    bitonic_merge_stage<E, 3>(v, lane, buf);
-    bitonic_merge_stage<E, 4>(v, lane, buf);
-    bitonic_merge_stage<E, 5>(v, lane, buf);
-    bitonic_merge_stage<E, 6>(v, lane, buf);
-    bitonic_merge_stage<E, 7>(v, lane, buf);
-    bitonic_merge_stage<E, 8>(v, lane, buf);
-    if constexpr (LOGN >= 9) bitonic_merge_stage<E, 9>(v, lane, buf);
-    if constexpr (LOGN >= 10) bitonic_merge_stage<E, 10>(v, lane, buf);
-    if constexpr (LOGN >= 11) bitonic_merge_stage<E, 11>(v, lane, buf);
+    bitonic_merge_stage<E, 1, NR>(v, lane, buf);
+    bitonic_merge_stage<E, 2, NR>(v, lane, buf);
+    bitonic_merge_stage<E, 3, NR>(v, lane, buf);
+    bitonic_merge_stage<E, 4, NR>(v, lane, buf);
+    bitonic_merge_stage<E, 5, NR>(v, lane, buf);
+    bitonic_merge_stage<E, 6, NR>(v, lane, buf);
+    bitonic_merge_stage<E, 7, NR>(v, lane, buf);
+    bitonic_merge_stage<E, 8, NR>(v, lane, buf);
+    if constexpr (LOGN >= 9) bitonic_merge_stage<E, 9, NR>(v, lane, buf);
+    if constexpr (LOGN >= 10) bitonic_merge_stage<E, 10, NR>(v, lane, buf);
+    if constexpr (LOGN >= 11) bitonic_merge_stage<E, 11, NR>(v, lane, buf);
 }
 
 // C4: Short f for key root K (domain d = 0).  Writes the int8 row f[0..P16).
@@ -161,7 +166,7 @@ __device__ __forceinline__ void sample_short_warp(uint64_t K, int8_t *frow, int 
                                                       : ((hi & 0xFFFFFFFCu) | 1u))
                                      : 0xFFFFFFFFu;
     }
-    warp_bitonic_sort<E>(v, lane);
+    warp_bitonic_sort<E, PS::P>(v, lane);
     // f_i = (L_(i) & 3) - 1 for i < P, 0 in the pad; pack 4 per word, 16-byte stores.
 #pragma unroll
     for (int w4 = 0; w4 < E / 16; w4++) {

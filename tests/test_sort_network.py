@@ -16,8 +16,10 @@ def _cmp(X, lo, hi):
     X[..., hi] = np.maximum(a, b)
 
 
-def model_sort(x, E):
+def model_sort(x, E, NR=None):
     N = 32 * E
+    NR = N if NR is None else NR
+    RP = (NR + 31) // 32                          # striped registers holding a real key
     LE = {8: 3, 16: 4, 32: 5, 64: 6}[E]
     LOGN = LE + 5
     V = x.reshape(32, E).copy()                   # blocked: V[lane, e] = x[lane*E + e]
@@ -37,9 +39,10 @@ def model_sort(x, E):
             V = np.where(lower[:, None], np.minimum(V, o), np.maximum(V, o))
         else:
             S = V.reshape(-1).reshape(E, 32).T.copy()  # striped: S[lane, r] = x[32 r + lane]
+            S[:, RP:] = 0xFFFFFFFF                     # pad registers are not loaded
             rm, rh = (k - 1) >> 5, k >> 6
             for r in range(E):
-                if r & rh == 0:
+                if r & rh == 0 and (r ^ rm) < RP:
                     a = S[lanes ^ 31, r ^ rm].copy()
                     b = S[lanes ^ 31, r].copy()
                     S[:, r] = np.minimum(S[:, r], a)
@@ -47,10 +50,12 @@ def model_sort(x, E):
             jr = k >> 7
             while jr >= 1:
                 for r in range(E):
-                    if r & jr == 0:
+                    if r & jr == 0 and (r | jr) < RP:
                         _cmp(S, r, r | jr)
                 jr >>= 1
-            V = S.T.reshape(-1).reshape(32, E).copy()
+            flat = V.reshape(-1).copy()                # pad registers are not stored back
+            flat.reshape(E, 32).T[:, :RP] = S[:, :RP]
+            V = flat.reshape(32, E)
         j = jtop
         while j >= 1:
             if j >= E:
@@ -84,6 +89,17 @@ def test_pads_stay_on_top():
     p, E = 761, 32
     x = np.full(32 * E, 0xFFFFFFFF, dtype=np.uint32)
     x[:p] = rng.integers(0, 2 ** 32 - 1, p, dtype=np.uint64).astype(np.uint32) & 0xFFFFFFFE
-    out = model_sort(x, E)
+    out = model_sort(x, E, NR=p)                  # the sampler's schedule skips pad comparators
     assert np.array_equal(out[:p], np.sort(x[:p]))
     assert (out[p:] == 0xFFFFFFFF).all()
+
+
+@pytest.mark.parametrize("p,E", [(653, 32), (761, 32), (857, 32), (953, 32), (1013, 32), (1277, 64)])
+def test_pad_skipping_schedule(p, E):
+    rng = np.random.default_rng(p)
+    for t in range(3):
+        x = np.full(32 * E, 0xFFFFFFFF, dtype=np.uint32)
+        hi = 4 if t == 1 else 2 ** 32 - 2
+        x[:p] = rng.integers(0, hi, p, dtype=np.uint64).astype(np.uint32)
+        out = model_sort(x, E, NR=p)
+        assert np.array_equal(out[:p], np.sort(x[:p]))
