@@ -39,6 +39,84 @@ struct EncArgs {
     EncTables t;
 };
 
+// The same level plan as the host table (C10), evaluated at compile time per parameter set so that
+// the kernel's byte-emission loops have constant trip counts (the host checks the two agree).
+struct EncPlan {
+    int nlev = 0;
+    int lev_n[ENC_MAXLEV] = {}, lev_e[ENC_MAXLEV] = {}, lev_elast[ENC_MAXLEV] = {}, lev_off[ENC_MAXLEV] = {};
+    uint32_t lev_M[ENC_MAXLEV] = {};
+    int top_emit = 0, top_off = 0, pk_bytes = 0;
+};
+
+template <int P, int Q>
+__host__ __device__ constexpr EncPlan enc_plan() {
+    EncPlan t{};
+    uint32_t M[P] = {};
+    for (int i = 0; i < P; i++) M[i] = (uint32_t)Q;
+    int n = P, lev = 0, pos = 0;
+    while (n > 1 && lev < ENC_MAXLEV) {
+        t.lev_n[lev] = n;
+        t.lev_off[lev] = pos;
+        t.lev_M[lev] = M[0];
+        for (int i = 0; i + 1 < n; i += 2) {
+            uint32_t m = M[i] * M[i + 1];
+            int e = 0;
+            while (m >= 16384u) { e++; m = (m + 255u) >> 8; }
+            if (i == 0) t.lev_e[lev] = e;
+            t.lev_elast[lev] = e;
+            pos += e;
+            M[i / 2] = m;                                   // i / 2 <= i: in-place is safe
+        }
+        if (n & 1) M[n / 2] = M[n - 1];
+        n = (n + 1) / 2;
+        lev++;
+    }
+    t.nlev = lev;
+    uint32_t m = M[0];
+    int e = 0;
+    while (m > 1) { e++; m = (m + 255u) >> 8; }
+    t.top_emit = e;
+    t.top_off = pos;
+    t.pk_bytes = pos + e;
+    return t;
+}
+
+template <class PS>
+struct EncPlanOf {
+    static constexpr EncPlan v = enc_plan<PS::P, PS::Q>();
+};
+
+// level L >= 1 of the radix merge (R -> R2), constant moduli and byte counts
+template <class PS, int L>
+__device__ __forceinline__ void enc_levels(uint16_t *R, uint16_t *R2, uint8_t *dst, int lane) {
+    constexpr EncPlan t = EncPlanOf<PS>::v;
+    if constexpr (L < t.nlev) {
+        constexpr int n = t.lev_n[L], npairs = n / 2, e = t.lev_e[L], el = t.lev_elast[L], ob = t.lev_off[L];
+        constexpr uint32_t m0 = t.lev_M[L];
+        for (int i = lane; i < npairs; i += 32) {
+            uint32_t r = (uint32_t)R[2 * i] + m0 * (uint32_t)R[2 * i + 1];
+            const int o = ob + e * i;
+            if (el != e && i == npairs - 1) {
+#pragma unroll
+                for (int b = 0; b < el; b++) { dst[o + b] = (uint8_t)(r & 255u); r >>= 8; }
+            } else {
+#pragma unroll
+                for (int b = 0; b < e; b++) { dst[o + b] = (uint8_t)(r & 255u); r >>= 8; }
+            }
+            R2[i] = (uint16_t)r;
+        }
+        if ((n & 1) && lane == 0) R2[n / 2] = R[n - 1];
+        __syncwarp();
+        enc_levels<PS, L + 1>(R2, R, dst, lane);
+    } else {
+        if (lane == 0) {
+            uint32_t r = R[0];
+#pragma unroll
+            for (int b = 0; b < t.top_emit; b++) { dst[t.top_off + b] = (uint8_t)(r & 255u); r >>= 8; }
+        }
+    }
+}
+
 template <class PS>
 __device__ __forceinline__ uint8_t small_byte(const int8_t *row, int j) {
     int v = 0;
@@ -70,12 +148,15 @@ __global__ void __launch_bounds__(128) encode_kernel(EncArgs a) {
         uint8_t *dst = a.pk + key * (uint64_t)a.t.pk_bytes;
         const int16_t *hrow = a.h + key * PS::P8;
         // level 0 straight from HBM: 8 coefficients (4 pairs) per lane and 16-byte load; every
-        // level-0 pair has M = q*q and emits the same number of bytes e0 at offset e0*i.
+        // level-0 pair has M = q*q and emits the same number of bytes e0 at offset e0*i.  Level
+        // constants come from the compile-time plan (EncPlanOf, checked against the host table).
         // Emitted bytes go straight to the pk row (consecutive lanes, consecutive bytes).
         {
-            const uint32_t m0 = a.t.lev_M[0];
-            const int e0 = a.t.lev_e[0];
-            const int npairs = a.t.lev_n[0] / 2;
+            constexpr EncPlan pl = EncPlanOf<PS>::v;
+            constexpr uint32_t m0 = pl.lev_M[0];
+            constexpr int e0 = pl.lev_e[0];
+            constexpr int npairs = pl.lev_n[0] / 2;
+            static_assert(pl.lev_elast[0] == e0 && pl.nlev >= 2, "level 0: uniform pairs");
             for (int c = lane; c < PS::P8 / 8; c += 32) {
                 const uint4 q4 = __ldg(reinterpret_cast<const uint4 *>(hrow) + c);
                 const uint32_t w[4] = {q4.x, q4.y, q4.z, q4.w};
@@ -86,6 +167,7 @@ __global__ void __launch_bounds__(128) encode_kernel(EncArgs a) {
                     const uint32_t r1 = (uint32_t)((int)(int16_t)(w[t] >> 16) + PS::QH);
                     if (i < npairs) {
                         uint32_t r = r0 + m0 * r1;
+#pragma unroll
                         for (int b = 0; b < e0; b++) { dst[e0 * i + b] = (uint8_t)(r & 255u); r >>= 8; }
                         R2[i] = (uint16_t)r;
                     } else if (2 * i < PS::P) {
@@ -95,29 +177,7 @@ __global__ void __launch_bounds__(128) encode_kernel(EncArgs a) {
             }
         }
         __syncwarp();
-        {
-            uint16_t *tmp = R; R = R2; R2 = tmp;
-        }
-        for (int lev = 1; lev < a.t.nlev; lev++) {
-            const int n = a.t.lev_n[lev];
-            const uint32_t m0 = a.t.lev_M[lev];
-            const int e = a.t.lev_e[lev], el = a.t.lev_elast[lev], ob = a.t.lev_off[lev];
-            const int npairs = n / 2;
-            for (int i = lane; i < npairs; i += 32) {
-                uint32_t r = (uint32_t)R[2 * i] + m0 * (uint32_t)R[2 * i + 1];
-                const int ee = (i == npairs - 1) ? el : e;
-                const int o = ob + e * i;
-                for (int t = 0; t < ee; t++) { dst[o + t] = (uint8_t)(r & 255u); r >>= 8; }
-                R2[i] = (uint16_t)r;
-            }
-            if ((n & 1) && lane == 0) R2[n / 2] = R[n - 1];
-            __syncwarp();
-            uint16_t *tmp = R; R = R2; R2 = tmp;
-        }
-        if (lane == 0) {
-            uint32_t r = R[0];
-            for (int t = 0; t < a.t.top_emit; t++) { dst[a.t.top_off + t] = (uint8_t)(r & 255u); r >>= 8; }
-        }
+        enc_levels<PS, 1>(R2, R, dst, lane);
     }
     if (a.f) {
         // 16 trits per 16-byte load -> 4 sk bytes; trits >= P are 0 (pad) and contribute (0+1)

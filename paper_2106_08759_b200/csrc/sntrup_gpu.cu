@@ -265,6 +265,19 @@ int build_tables(int dev, int ps, int WT, DevTables **out) {
         enc.top_off = (int)pos;
         enc.pk_bytes = (int)(pos + e);
         if ((size_t)enc.pk_bytes != pi.pk) return SNTRUP_E_INTERNAL;
+        // the kernel's compile-time plan must be this table
+        bool same = false;
+        auto cmp = [&](const EncPlan &c) {
+            same = c.nlev == enc.nlev && c.top_emit == enc.top_emit && c.top_off == enc.top_off &&
+                   c.pk_bytes == enc.pk_bytes;
+            for (int l = 0; same && l < enc.nlev; l++)
+                same = c.lev_n[l] == enc.lev_n[l] && c.lev_e[l] == enc.lev_e[l] &&
+                       c.lev_elast[l] == enc.lev_elast[l] && c.lev_off[l] == enc.lev_off[l] &&
+                       c.lev_M[l] == enc.lev_M[l];
+            return 0;
+        };
+        SNTRUP_DISPATCH(p, cmp(EncPlanOf<PS>::v));
+        if (!same) return SNTRUP_E_INTERNAL;
     }
     CK(cudaMalloc(&t.T, T.size() * sizeof(uint2)));
     CK(cudaMemcpy(t.T, T.data(), T.size() * sizeof(uint2), cudaMemcpyHostToDevice));
