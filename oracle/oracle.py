@@ -83,6 +83,8 @@ def lib():
         L.or_encap_core.argtypes = [i32, i32, vp, vp, vp]
         L.or_decap_core.restype = i32
         L.or_decap_core.argtypes = [i32, i32, i32, vp, vp, vp, vp]
+        L.or_uniform_from_words.restype = None
+        L.or_uniform_from_words.argtypes = [i32, i32, vp, vp]
         L.or_mul_many.restype = None
         L.or_mul_many.argtypes = [i32, i64, u64, vp, vp, vp, sz, i32]
         _lib = L
@@ -116,6 +118,23 @@ def short_from_words(p: int, w: int, u: np.ndarray) -> np.ndarray:
     f = np.zeros(p, dtype=np.int8)
     lib().or_short_from_words(p, w, _p(u), _p(f))
     return f
+
+
+def uniform_from_words(p: int, q: int, u: np.ndarray) -> np.ndarray:
+    """C12: a_j = floor(u_j q / 2^32) - (q-1)/2 (the R/q microbenchmark's uniform operand)."""
+    u = np.ascontiguousarray(u, dtype=np.uint32)
+    a = np.zeros(p, dtype=np.int16)
+    lib().or_uniform_from_words(p, q, _p(u), _p(a))
+    return a
+
+
+def c12_pair(param: int, seed: int, i: int):
+    """Pair i of the R/q microbenchmark (BASELINE configs[2]): with key root
+    K_i = SM(seed, i), a from domain 0 (uniform, C12) and b from domain 1 (Short, C4)."""
+    p, q, w = PARAMS[param]
+    a = uniform_from_words(p, q, stream_words(seed, i, 0, p))
+    b = short_from_words(p, w, stream_words(seed, i, 1, p))
+    return a, b
 
 
 # ----------------------------------------------------------------------------- ring (C5-C7)

@@ -80,6 +80,16 @@ void or_short_from_words(int p, int w, const uint32_t *u, int8_t *f)
     free(L);
 }
 
+/* C12: uniform R/q element of the R/q microbenchmark (BASELINE configs[2]):
+   a_j = floor(u_j * q / 2^32) - (q-1)/2, j = 0..p-1, from the words of its stream domain. */
+void or_uniform_from_words(int p, int q, const uint32_t *u, int16_t *a)
+{
+    for (int j = 0; j < p; j++) {
+        uint64_t t = ((uint64_t)u[j] * (uint64_t)q) >> 32;
+        a[j] = (int16_t)((int64_t)t - (q - 1) / 2);
+    }
+}
+
 /* ------------------------------------------------------------------------------------------ */
 /* Arithmetic in Z/m and (Z/m)[x]                                                               */
 /* ------------------------------------------------------------------------------------------ */

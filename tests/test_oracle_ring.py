@@ -140,3 +140,18 @@ def test_toy_ring_unit_counts(O, p, m):
             cnt += 1
             assert np.array_equal(PT.ring_mul(e, inv, p, m), one)
     assert cnt == expected
+
+
+@pytest.mark.parametrize("p,m,threads", [(761, 4591, 1), (761, 4591, 3), (653, 3, 2), (1277, 7879, 4)])
+def test_mul_many_equals_rowwise_long_division(O, p, m, threads):
+    # or_mul_many (the threaded batch wrapper the R/q parity tests and cpu_baseline use) against
+    # the independent long-division product (tests/polytools.py) row by row, ragged row stride.
+    rng = np.random.default_rng(p + m + threads)
+    n, row = 7, p + 5
+    a = np.zeros((n, row), np.int16); b = np.zeros((n, row), np.int16)
+    a[:, :p] = rng.integers(-(m - 1) // 2, (m - 1) // 2 + 1, size=(n, p))
+    b[:, :p] = rng.integers(-(m - 1) // 2, (m - 1) // 2 + 1, size=(n, p))
+    c = O.mul_many(p, m, a, b, threads=threads)
+    for i in range(n):
+        assert np.array_equal(c[i, :p], PT.ring_mul(a[i, :p].astype(np.int64), b[i, :p].astype(np.int64), p, m))
+        assert not c[i, p:].any()

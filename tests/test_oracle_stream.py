@@ -108,3 +108,36 @@ def test_short_position_and_sign_balance(O):
     plus = (F == 1).sum()
     total = nz.sum()
     assert abs(plus - total / 2) < 5 * np.sqrt(total / 4)
+
+
+def test_c12_uniform_mapping_boundaries(O):
+    # C12: a_j = floor(u_j q / 2^32) - (q-1)/2 maps [0, 2^32) onto [-(q-1)/2, (q-1)/2]; the
+    # boundaries of the first and last class are ceil(2^32/q) and floor((q-1) 2^32/q) (q = 4591).
+    q = 4591
+    b1 = -(-(1 << 32) // q)            # smallest u with floor(u q / 2^32) = 1
+    blast = -(-((q - 1) << 32) // q)   # smallest u with floor(u q / 2^32) = q - 1
+    u = np.array([0, b1 - 1, b1, blast - 1, blast, (1 << 32) - 1], dtype=np.uint32)
+    a = O.uniform_from_words(len(u), q, u)
+    assert list(a) == [-2295, -2295, -2294, 2294, 2295, 2295]
+
+
+def test_c12_uniform_frequencies(O):
+    rng = np.random.default_rng(11)
+    u = rng.integers(0, 1 << 32, size=400_000, dtype=np.uint64).astype(np.uint32)
+    a = O.uniform_from_words(len(u), 4591, u).astype(np.int64)
+    assert a.min() == -2295 and a.max() == 2295
+    # mean 0, variance (q^2 - 1)/12 of the discrete uniform law, within 5 sigma
+    n, var = len(a), (4591 ** 2 - 1) / 12
+    assert abs(a.mean()) < 5 * np.sqrt(var / n)
+    assert abs(a.var() / var - 1) < 5 * np.sqrt(0.8 / n)
+
+
+def test_c12_pair0_golden(O):
+    # SURVEY.md C14 "Config 3, pair 0 (seed = 3)": a third implementation's values for C12 + C7.
+    g = json.load(open(os.path.join(GOLD, "survey_c14.json")))["config3_pair0_seed3"]
+    a, b = O.c12_pair(761, 3, 0)
+    assert list(map(int, a[:6])) == g["a0_5"]
+    assert list(map(int, np.nonzero(b)[0][:4])) == g["b_first_nonzero"]
+    assert int(np.count_nonzero(b)) == 286 and set(map(int, np.unique(b))) <= {-1, 0, 1}
+    c = O.poly_mul(761, 4591, a, b)
+    assert list(map(int, c[:6])) == g["c0_5"]
