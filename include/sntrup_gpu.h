@@ -85,6 +85,10 @@ int sntrup_batch_keygen(int param_set, uint64_t n_keys, uint64_t seed,
 #define SNTRUP_OPT_STAGGER       128u /* lane k of the first round starts when lane k-1 has finished
                                          its R/q up-sweep (its throughput phases fill lane k-1's
                                          latency-bound root inversion); outputs identical */
+#define SNTRUP_OPT_SERIAL        256u /* measurement: every kernel of the call on the caller's
+                                         stream, one at a time (one lane, no ring / aux streams),
+                                         so per-launch CUDA-event times are each kernel's own;
+                                         outputs identical */
 #define SNTRUP_OPT_LANE_PRIORITY  64u /* lanes on internal streams of decreasing priority: the
                                          first lane's chunk completes first (its D2H copies overlap
                                          the other lanes' compute); outputs identical */
@@ -108,6 +112,13 @@ typedef struct {
                                  (the next call's compute overlaps them), and this event completes
                                  when every pk/sk byte is in host memory.  The host buffers must
                                  stay untouched until then. */
+    void *workspace;          /* optional caller-owned DEVICE scratch (256-byte aligned) of
+                                 workspace_bytes >= sntrup_keygen_workspace_bytes_ex(...) for this
+                                 call's shape (else SNTRUP_E_WORKSPACE; misaligned -> SNTRUP_E_ARG);
+                                 NULL -> the library's cached workspace of `stream`.  The caller
+                                 keeps it alive and unused until the call's work has completed
+                                 (host-output staging is separate and library-owned). */
+    size_t workspace_bytes;
 } sntrup_keygen_opts;
 
 /* Completion events for asynchronous host-output calls (opaque cudaEvent_t). */
@@ -120,8 +131,17 @@ void sntrup_event_destroy(void *ev);
 int sntrup_batch_keygen_ex(int param_set, uint64_t n_keys, uint64_t seed,
                            uint8_t *pk_out, uint8_t *sk_out, const sntrup_keygen_opts *opt);
 
-/* Device bytes the library will allocate internally for a keygen call of this shape. */
+/* Exact device workspace bytes a keygen call of this shape takes (what it carves from the
+   caller's workspace, or the minimum the cached per-stream workspace is grown to; the cache
+   allocates this + 1/8 + 1 MiB of slack).  Host-output calls additionally hold a library-owned
+   staging allocation.  0 for an unknown parameter set, n_keys == 0 or a bad batch size.
+   The plain form assumes default options (flags 0, default chunking). */
 size_t sntrup_keygen_workspace_bytes(int param_set, uint64_t n_keys, uint32_t batch_size);
+size_t sntrup_keygen_workspace_bytes_ex(int param_set, uint64_t n_keys, uint32_t batch_size,
+                                        uint32_t flags, uint64_t chunk_keys);
+/* Introspection (tests): bytes currently allocated for `stream` on the current device --
+   which = 0: the cached workspace, 1: the host-output staging; 0 if none. */
+size_t sntrup_workspace_reserved_bytes(void *stream, int which);
 
 /* c[i] = a[i] * b[i] in R/q for i < n (the ring product of P:5339-5442: full product, then
    reduction by x^p - x - 1, coefficients centered).  a, b, c: int16 [n][p8], no aliasing of c
@@ -165,6 +185,13 @@ int sntrup_full_sk_batch(int param_set, uint64_t n, uint64_t seed, uint64_t firs
    int8 [n][p16].  Stream-ordered. */
 int sntrup_sample_short_batch(int param_set, uint64_t n, uint64_t seed, uint64_t first_key_index,
                               uint64_t domain, int8_t *r_out, void *stream);
+
+/* a_out[i] = uniform R/q element of SURVEY.md 8(c) C12 (the R/q microbenchmark's operand,
+   BASELINE configs[2]) from stream domain `domain` of global key index first_key_index + i:
+   a_j = floor(u_j q / 2^32) - (q-1)/2 with u the domain's 32-bit words (C2).
+   int16 [n][p8] device, pad 0.  Stream-ordered; SNTRUP_E_PARAM / SNTRUP_E_ARG (n == 0, NULL). */
+int sntrup_sample_uniform_rq_batch(int param_set, uint64_t n, uint64_t seed, uint64_t first_key_index,
+                                   uint64_t domain, int16_t *a_out, void *stream);
 
 /* c[i] = Round(h[i] * r[i]) in R/q: each centered coefficient to the nearest multiple of 3.
    h, c int16 [n][p8] centered; r int8 [n][p16] (weight w).  Stream-ordered. */
@@ -218,8 +245,18 @@ int sntrup_pool_stats(sntrup_pool *pool, uint64_t *taken, uint64_t *generated, u
                       uint64_t *ready);
 void sntrup_pool_destroy(sntrup_pool *pool);
 
-/* Release the cached device workspaces (all streams). */
+/* Release the cached device workspaces and host-output staging (all streams). */
 void sntrup_release_workspace(void);
+/* Synchronise `stream`, erase (zero) and free its cached workspace and staging (they hold secret
+   f, 1/g and tree rows).  SNTRUP_OK or SNTRUP_E_CUDA. */
+int sntrup_release_stream_workspace(void *stream);
+
+/* Integer-pipe peak (measurement for bench.py's roofline; BASELINE metric "int-pipe % of peak"):
+   op 0 = IMAD (FMA pipe), 1 = IADD3, 2 = LOP3, 3 = SHF (ALU pipe).  A full-occupancy kernel of 8
+   independent chains per thread of that one instruction; *lane_ops_per_clk_sm = lane-ops per SM
+   clock per SM (from in-kernel clock64 spans per SM, clock-independent), *lane_ops_per_s = the
+   whole GPU's lane-ops/s at the clock of this run (CUDA events).  Synchronous; device 0-stream. */
+int sntrup_measure_int_peak(int op, double *lane_ops_per_clk_sm, double *lane_ops_per_s);
 
 /* Number of kernels this library launched since load (device work only; for bench accounting). */
 uint64_t sntrup_kernel_launch_count(void);
@@ -247,17 +284,22 @@ int sntrup_set_mul_impl(int impl);
 /* Measurement hooks (bench.py).  When enabled, every kernel launch is bracketed by CUDA events
    recorded on its launching stream.  sntrup_profile_read() waits for the recorded events and
    returns, per kernel class, the summed device milliseconds, the summed work units, the summed
-   algorithmic integer ops (ring products: 2 p^2 per limb-pair product on the tensor path, 2 p^2
-   per product on the schoolbook path; 0 for other classes) and the launch count (classes:
+   algorithmic integer ops (ring products: 2 p^2 per product, the method's multiply-adds; 0 for
+   other classes) and the launch count (classes:
    0 sample [keys], 1 R/3 product [products], 2 R/q product [products], 3 root inversions
    [inversions: R/3 roots, and in keygen both rings' roots in one launch], 4 R/q root inversion
    [inversions, rq_recip_batch], 5 repair [keys], 6 encode [keys], 7 other).
    Any output pointer may be NULL.  Returns the number of classes. */
 void sntrup_profile_enable(int on);
 /* Ring-product launches by arithmetic kind (0 = int8 tensor, 1 = fp4 tensor, 2 = int32
-   schoolbook): summed device ms, algorithmic ops (2 p^2 per limb/digit-pair product) and launch
-   counts since the last reset.  Returns the number of kinds (3). */
+   schoolbook): summed device ms, algorithmic ops (2 p^2 per product) and launch counts since the
+   last reset.  Returns the number of kinds (3). */
 int sntrup_profile_read_kinds(int reset, double *ms, double *ops, uint64_t *launches);
+/* As above, plus per kind the ring products computed and the bytes the tensor cores' MMAs fetched
+   from shared memory (A and B tiles: work items x MMAs per item x tile bytes, from the kernels'
+   geometry).  Algorithmic ops are 2 p^2 per ring product (the method's work), never per limb. */
+int sntrup_profile_read_kinds_ex(int reset, double *ms, double *ops, uint64_t *launches, double *products,
+                                 double *smem_bytes);
 int sntrup_profile_read(int reset, double *ms, double *units, double *ops, uint64_t *launches,
                         int max_classes);
 

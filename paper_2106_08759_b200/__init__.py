@@ -39,6 +39,7 @@ OPT_RING_STREAMS = 16
 OPT_LANES4 = 32
 OPT_LANE_PRIORITY = 64
 OPT_STAGGER = 128
+OPT_SERIAL = 256
 
 PARAM_SETS = (653, 761, 857, 953, 1013, 1277)
 
@@ -49,7 +50,8 @@ class KeygenOpts(ctypes.Structure):
                 ("stream", ctypes.c_void_p), ("h_out", ctypes.c_void_p),
                 ("g_out", ctypes.c_void_p), ("f_out", ctypes.c_void_p),
                 ("ginv_out", ctypes.c_void_p), ("attempts_out", ctypes.c_void_p),
-                ("stats_out", ctypes.c_void_p), ("done_event", ctypes.c_void_p)]
+                ("stats_out", ctypes.c_void_p), ("done_event", ctypes.c_void_p),
+                ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t)]
 
 
 _u64, _i32, _u32, _vp, _sz = ctypes.c_uint64, ctypes.c_int, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_size_t
@@ -60,6 +62,10 @@ _lib.sntrup_batch_keygen.argtypes = [_i32, _u64, _u64, _vp, _vp]
 _lib.sntrup_batch_keygen_ex.argtypes = [_i32, _u64, _u64, _vp, _vp, ctypes.POINTER(KeygenOpts)]
 _lib.sntrup_keygen_workspace_bytes.restype = _sz
 _lib.sntrup_keygen_workspace_bytes.argtypes = [_i32, _u64, _u32]
+_lib.sntrup_keygen_workspace_bytes_ex.restype = _sz
+_lib.sntrup_keygen_workspace_bytes_ex.argtypes = [_i32, _u64, _u32, _u32, _u64]
+_lib.sntrup_workspace_reserved_bytes.restype = _sz
+_lib.sntrup_workspace_reserved_bytes.argtypes = [_vp, _i32]
 _lib.rq_mul_batch.argtypes = [_i32, _u64, _vp, _vp, _vp, _vp]
 _lib.r3_mul_batch.argtypes = [_i32, _u64, _vp, _vp, _vp, _vp]
 _lib.rq_recip_batch.argtypes = [_i32, _u64, _vp, _vp, _u32, ctypes.POINTER(ctypes.c_uint64), _vp]
@@ -67,6 +73,7 @@ _lib.r3_recip_batch.argtypes = [_i32, _u64, _vp, _vp, _vp, _u32, _vp]
 _lib.r3_is_invertible_batch.argtypes = [_i32, _u64, _vp, _vp, _vp]
 _lib.rq_encode_batch.argtypes = [_i32, _u64, _vp, _vp, _vp]
 _lib.sntrup_release_workspace.restype = None
+_lib.sntrup_release_stream_workspace.argtypes = [_vp]
 _lib.sntrup_kernel_launch_count.restype = _u64
 _lib.sntrup_set_mul_impl.argtypes = [_i32]
 _lib.sntrup_profile_enable.restype = None
@@ -75,6 +82,9 @@ _lib.sntrup_profile_read.restype = _i32
 _lib.sntrup_profile_read.argtypes = [_i32, _vp, _vp, _vp, _vp, _i32]
 _lib.sntrup_profile_read_kinds.restype = _i32
 _lib.sntrup_profile_read_kinds.argtypes = [_i32, _vp, _vp, _vp]
+_lib.sntrup_profile_read_kinds_ex.restype = _i32
+_lib.sntrup_profile_read_kinds_ex.argtypes = [_i32, _vp, _vp, _vp, _vp, _vp]
+_lib.sntrup_measure_int_peak.argtypes = [_i32, _vp, _vp]
 _lib.sntrup_pool_create.argtypes = [_i32, _u64, _u64, _u64, _u64, _u32, ctypes.POINTER(_vp)]
 _lib.sntrup_pool_take.argtypes = [_vp, _vp, _vp, ctypes.POINTER(ctypes.c_uint64)]
 _lib.sntrup_pool_stats.argtypes = [_vp] + [ctypes.POINTER(ctypes.c_uint64)] * 4
@@ -82,6 +92,7 @@ _lib.sntrup_pool_destroy.argtypes = [_vp]
 _lib.sntrup_pool_destroy.restype = None
 _lib.rq_mul_small_batch.argtypes = [_i32, _u64, _vp, _vp, _vp, _vp]
 _lib.sntrup_sample_short_batch.argtypes = [_i32, _u64, _u64, _u64, _u64, _vp, _vp]
+_lib.sntrup_sample_uniform_rq_batch.argtypes = [_i32, _u64, _u64, _u64, _u64, _vp, _vp]
 _lib.sntrup_encap_core_batch.argtypes = [_i32, _u64, _vp, _vp, _vp, _vp]
 _lib.sntrup_decap_core_batch.argtypes = [_i32, _u64, _vp, _vp, _vp, _vp, _vp, _vp]
 _lib.sntrup_full_sk_bytes.argtypes = [_i32]
@@ -94,12 +105,14 @@ _lib.sntrup_event_destroy.argtypes = [_vp]
 _lib.sntrup_event_destroy.restype = None
 
 EXPORTED = ("sntrup_params", "sntrup_strerror", "sntrup_batch_keygen", "sntrup_batch_keygen_ex",
-            "sntrup_keygen_workspace_bytes", "rq_mul_batch", "rq_mul_small_batch", "r3_mul_batch", "rq_recip_batch",
+            "sntrup_keygen_workspace_bytes", "sntrup_keygen_workspace_bytes_ex",
+            "sntrup_workspace_reserved_bytes", "rq_mul_batch", "rq_mul_small_batch", "r3_mul_batch", "rq_recip_batch",
             "r3_recip_batch", "r3_is_invertible_batch", "rq_encode_batch",
-            "sntrup_release_workspace", "sntrup_kernel_launch_count", "sntrup_set_mul_impl",
-            "sntrup_profile_enable", "sntrup_profile_read_kinds", "sntrup_pool_create",
+            "sntrup_release_workspace", "sntrup_release_stream_workspace", "sntrup_kernel_launch_count", "sntrup_set_mul_impl",
+            "sntrup_profile_enable", "sntrup_profile_read_kinds", "sntrup_profile_read_kinds_ex",
+            "sntrup_measure_int_peak", "sntrup_pool_create",
             "sntrup_pool_take", "sntrup_pool_stats", "sntrup_pool_destroy",
-            "sntrup_sample_short_batch", "sntrup_encap_core_batch", "sntrup_decap_core_batch",
+            "sntrup_sample_short_batch", "sntrup_sample_uniform_rq_batch", "sntrup_encap_core_batch", "sntrup_decap_core_batch",
             "sntrup_profile_read", "sntrup_full_sk_bytes", "sntrup_full_sk_batch",
             "sntrup_event_create", "sntrup_event_synchronize", "sntrup_event_query", "sntrup_event_destroy")
 
@@ -134,24 +147,33 @@ def _stream(stream):
     return ctypes.c_void_p(stream.cuda_stream)
 
 
-def _need(t, dtype, shape, name):
-    if t.dtype != dtype or tuple(t.shape) != tuple(shape) or not t.is_contiguous() or not t.is_cuda:
-        raise ValueError("%s must be a contiguous CUDA %s tensor of shape %s" % (name, dtype, shape))
+def _need(t, dtype, shape, name, host: bool = False):
+    """Inputs and caller-supplied outputs: exact dtype and shape, contiguous, on the device (or, for
+    host-output keygen, in host memory) -- a short or mistyped buffer would be written past."""
+    if (not isinstance(t, torch.Tensor) or t.dtype != dtype or tuple(t.shape) != tuple(shape)
+            or not t.is_contiguous() or t.is_cuda == host):
+        raise ValueError("%s must be a contiguous %s %s tensor of shape %s"
+                         % (name, "host" if host else "CUDA", dtype, tuple(shape)))
 
 
 def batch_keygen(param_set: int, n_keys: int, seed: int, *, first_key_index: int = 0,
                  batch_size: int = 32, chunk_keys: int = 0, flags: int = 0, pk_out=None,
-                 sk_out=None, debug: bool = False, stream=None, stats: bool = False, done_event=None):
+                 sk_out=None, debug: bool = False, stream=None, stats: bool = False, done_event=None,
+                 workspace=None):
     """Generate n_keys key pairs (global indices first_key_index ..).  Returns dict with pk, sk
     (uint8 CUDA tensors) and, with debug=True, h/g/f/ginv/attempts.  With host outputs,
     flags OPT_ASYNC and a done_event (Event), the call returns after enqueueing and the event
     completes when every output byte is in host memory."""
     P = params(param_set)
-    dev = torch.device("cuda", torch.cuda.current_device())
+    host = bool(flags & OPT_HOST_OUTPUT)
+    # host outputs default to pinned host memory (the library copies each chunk back into them)
+    where = dict(device="cpu", pin_memory=True) if host else dict(device="cuda")
     if pk_out is None:
-        pk_out = torch.empty((n_keys, P["pk_bytes"]), dtype=torch.uint8, device=dev)
+        pk_out = torch.empty((n_keys, P["pk_bytes"]), dtype=torch.uint8, **where)
     if sk_out is None:
-        sk_out = torch.empty((n_keys, P["sk_bytes"]), dtype=torch.uint8, device=dev)
+        sk_out = torch.empty((n_keys, P["sk_bytes"]), dtype=torch.uint8, **where)
+    _need(pk_out, torch.uint8, (n_keys, P["pk_bytes"]), "pk_out", host=host)
+    _need(sk_out, torch.uint8, (n_keys, P["sk_bytes"]), "sk_out", host=host)
     o = KeygenOpts()
     o.first_key_index = first_key_index
     o.batch_size = batch_size
@@ -159,6 +181,7 @@ def batch_keygen(param_set: int, n_keys: int, seed: int, *, first_key_index: int
     o.chunk_keys = chunk_keys
     o.stream = _stream(stream)
     out = dict(pk=pk_out, sk=sk_out)
+    dev = torch.device("cuda", torch.cuda.current_device())
     if debug:
         out["h"] = torch.zeros((n_keys, P["p8"]), dtype=torch.int16, device=dev)
         for k in ("g", "f", "ginv"):
@@ -171,9 +194,12 @@ def batch_keygen(param_set: int, n_keys: int, seed: int, *, first_key_index: int
         o.stats_out = ctypes.addressof(st)
     if done_event is not None:
         o.done_event = done_event.handle
-    host = bool(flags & OPT_HOST_OUTPUT)
-    pkp = pk_out.data_ptr() if not host else pk_out.data_ptr()
-    _check(_lib.sntrup_batch_keygen_ex(param_set, n_keys, seed, ctypes.c_void_p(pkp),
+    if workspace is not None:               # caller-owned device scratch (uint8 CUDA tensor)
+        if not (isinstance(workspace, torch.Tensor) and workspace.is_cuda and workspace.is_contiguous()):
+            raise ValueError("workspace must be a contiguous CUDA tensor")
+        o.workspace = workspace.data_ptr()
+        o.workspace_bytes = workspace.numel() * workspace.element_size()
+    _check(_lib.sntrup_batch_keygen_ex(param_set, n_keys, seed, ctypes.c_void_p(pk_out.data_ptr()),
                                        ctypes.c_void_p(sk_out.data_ptr()), ctypes.byref(o)),
            "sntrup_batch_keygen_ex")
     if stats:
@@ -212,6 +238,7 @@ def rq_mul_batch(param_set: int, a, b, c=None, stream=None):
     _need(b, torch.int16, (n, P["p8"]), "b")
     if c is None:
         c = torch.empty_like(a)
+    _need(c, torch.int16, (n, P["p8"]), "c")
     _check(_lib.rq_mul_batch(param_set, n, _ptr(a), _ptr(b), _ptr(c), _stream(stream)), "rq_mul_batch")
     return c
 
@@ -224,6 +251,7 @@ def rq_mul_small_batch(param_set: int, a, b, c=None, stream=None):
     _need(b, torch.int8, (n, P["p16"]), "b")
     if c is None:
         c = torch.empty_like(a)
+    _need(c, torch.int16, (n, P["p8"]), "c")
     _check(_lib.rq_mul_small_batch(param_set, n, _ptr(a), _ptr(b), _ptr(c), _stream(stream)),
            "rq_mul_small_batch")
     return c
@@ -267,6 +295,19 @@ def sample_short_batch(param_set: int, n: int, seed: int, first_key_index: int =
     return out
 
 
+def sample_uniform_rq_batch(param_set: int, n: int, seed: int, first_key_index: int = 0,
+                            domain: int = 0, out=None, stream=None):
+    """Uniform R/q elements (the R/q microbenchmark's operand) of one stream domain
+    for global key indices first.. (int16 rows of p8)."""
+    P = params(param_set)
+    if out is None:
+        out = torch.empty((n, P["p8"]), dtype=torch.int16, device="cuda")
+    _need(out, torch.int16, (n, P["p8"]), "out")
+    _check(_lib.sntrup_sample_uniform_rq_batch(param_set, n, seed, first_key_index, domain, _ptr(out),
+                                               _stream(stream)), "sntrup_sample_uniform_rq_batch")
+    return out
+
+
 def encap_core_batch(param_set: int, h, r, c=None, stream=None):
     """c = Round(h * r) in R/q (each coefficient to the nearest multiple of 3)."""
     P = params(param_set)
@@ -275,6 +316,7 @@ def encap_core_batch(param_set: int, h, r, c=None, stream=None):
     _need(r, torch.int8, (n, P["p16"]), "r")
     if c is None:
         c = torch.empty_like(h)
+    _need(c, torch.int16, (n, P["p8"]), "c")
     _check(_lib.sntrup_encap_core_batch(param_set, n, _ptr(h), _ptr(r), _ptr(c), _stream(stream)),
            "sntrup_encap_core_batch")
     return c
@@ -291,6 +333,8 @@ def decap_core_batch(param_set: int, f, ginv, c, r_out=None, ok=None, stream=Non
         r_out = torch.empty_like(f)
     if ok is None:
         ok = torch.empty(n, dtype=torch.uint8, device=c.device)
+    _need(r_out, torch.int8, (n, P["p16"]), "r_out")
+    _need(ok, torch.uint8, (n,), "ok")
     _check(_lib.sntrup_decap_core_batch(param_set, n, _ptr(f), _ptr(ginv), _ptr(c), _ptr(r_out), _ptr(ok),
                                         _stream(stream)), "sntrup_decap_core_batch")
     return r_out, ok
@@ -303,6 +347,7 @@ def r3_mul_batch(param_set: int, a, b, c=None, stream=None):
     _need(b, torch.int8, (n, P["p16"]), "b")
     if c is None:
         c = torch.empty_like(a)
+    _need(c, torch.int8, (n, P["p16"]), "c")
     _check(_lib.r3_mul_batch(param_set, n, _ptr(a), _ptr(b), _ptr(c), _stream(stream)), "r3_mul_batch")
     return c
 
@@ -314,6 +359,7 @@ def rq_recip_batch(param_set: int, a, out=None, batch_size: int = 32, stream=Non
     _need(a, torch.int16, (n, P["p8"]), "a")
     if out is None:
         out = torch.empty_like(a)
+    _need(out, torch.int16, (n, P["p8"]), "out")
     bad = ctypes.c_uint64(0)
     rc = _lib.rq_recip_batch(param_set, n, _ptr(a), _ptr(out), batch_size, ctypes.byref(bad), _stream(stream))
     if rc != SNTRUP_OK:
@@ -331,6 +377,8 @@ def r3_recip_batch(param_set: int, g, out=None, ok=None, batch_size: int = 32, s
         out = torch.empty_like(g)
     if ok is None:
         ok = torch.empty(n, dtype=torch.uint8, device=g.device)
+    _need(out, torch.int8, (n, P["p16"]), "out")
+    _need(ok, torch.uint8, (n,), "ok")
     _check(_lib.r3_recip_batch(param_set, n, _ptr(g), _ptr(out), _ptr(ok), batch_size, _stream(stream)),
            "r3_recip_batch")
     return out, ok
@@ -352,16 +400,27 @@ def rq_encode_batch(param_set: int, h, pk=None, stream=None):
     _need(h, torch.int16, (n, P["p8"]), "h")
     if pk is None:
         pk = torch.empty((n, P["pk_bytes"]), dtype=torch.uint8, device=h.device)
+    _need(pk, torch.uint8, (n, P["pk_bytes"]), "pk")
     _check(_lib.rq_encode_batch(param_set, n, _ptr(h), _ptr(pk), _stream(stream)), "rq_encode_batch")
     return pk
 
 
-def keygen_workspace_bytes(param_set: int, n_keys: int, batch_size: int = 32) -> int:
-    return int(_lib.sntrup_keygen_workspace_bytes(param_set, n_keys, batch_size))
+def keygen_workspace_bytes(param_set: int, n_keys: int, batch_size: int = 32, flags: int = 0,
+                           chunk_keys: int = 0) -> int:
+    return int(_lib.sntrup_keygen_workspace_bytes_ex(param_set, n_keys, batch_size, flags, chunk_keys))
+
+
+def workspace_reserved_bytes(stream=None, staging: bool = False) -> int:
+    """Bytes the library holds for `stream` (the cached workspace, or the host-output staging)."""
+    return int(_lib.sntrup_workspace_reserved_bytes(_stream(stream), 1 if staging else 0))
 
 
 def release_workspace():
     _lib.sntrup_release_workspace()
+
+
+def release_stream_workspace(stream=None):
+    _check(_lib.sntrup_release_stream_workspace(_stream(stream)), "sntrup_release_stream_workspace")
 
 
 def kernel_launch_count() -> int:
@@ -429,12 +488,28 @@ MUL_KINDS = ("tc_int8", "tc_fp4", "int32")
 
 
 def profile_read_kinds(reset: bool = True) -> dict:
-    """Ring-product launches by arithmetic kind: device ms, algorithmic ops, launches."""
+    """Ring-product launches by arithmetic kind: device ms, algorithmic ops (2 p^2 per product),
+    launches, products, and the operand bytes the MMAs fetched from shared memory."""
     ms = (ctypes.c_double * 3)()
     op = (ctypes.c_double * 3)()
     la = (ctypes.c_uint64 * 3)()
-    _lib.sntrup_profile_read_kinds(1 if reset else 0, ms, op, la)
-    return {MUL_KINDS[i]: dict(ms=ms[i], ops=op[i], launches=la[i]) for i in range(3)}
+    pr = (ctypes.c_double * 3)()
+    sm = (ctypes.c_double * 3)()
+    _lib.sntrup_profile_read_kinds_ex(1 if reset else 0, ms, op, la, pr, sm)
+    return {MUL_KINDS[i]: dict(ms=ms[i], ops=op[i], launches=la[i], products=pr[i], smem_bytes=sm[i])
+            for i in range(3)}
+
+
+INT_OPS = ("IMAD", "IADD3", "LOP3", "SHF")
+
+
+def measure_int_peak(op: str) -> dict:
+    """Integer-pipe peak of one SASS op (full-occupancy microkernel): lane-ops per SM clock per SM,
+    and lane-ops/s of the whole GPU at this run's clock."""
+    a, b = ctypes.c_double(), ctypes.c_double()
+    _check(_lib.sntrup_measure_int_peak(INT_OPS.index(op), ctypes.byref(a), ctypes.byref(b)),
+           "sntrup_measure_int_peak")
+    return dict(lanes_per_clk_sm=a.value, lane_ops_per_s=b.value)
 
 
 def profile_read(reset: bool = True) -> dict:

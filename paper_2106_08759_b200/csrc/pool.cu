@@ -180,7 +180,10 @@ void sntrup_pool_destroy(sntrup_pool *p) {
     int dev_save = 0;
     cudaGetDevice(&dev_save);
     cudaSetDevice(p->dev);
-    if (p->st) cudaStreamSynchronize(p->st);
+    if (p->st) {
+        cudaStreamSynchronize(p->st);
+        sntrup_release_stream_workspace(p->st);   // erase + free the keygen workspace of the pool's stream
+    }
     if (p->h_sk) { memset(p->h_sk, 0, (size_t)p->nslots * p->batch * p->skb); cudaFreeHost(p->h_sk); }
     if (p->h_pk) cudaFreeHost(p->h_pk);
     if (p->d_pk) cudaFree(p->d_pk);

@@ -367,6 +367,26 @@ __global__ void __launch_bounds__(128) short_kernel(uint64_t seed, uint64_t firs
     sample_short_warp<PS>(sm_at(seed, first + row), out + row * PS::P16, lane, domain);
 }
 
+// SURVEY.md 8(c) C12 (BASELINE configs[2] inputs): uniform R/q element from stream domain
+// `domain` of key root SM(seed, first + row): a_j = floor(u_j q / 2^32) - (q-1)/2, int16 rows of
+// P8 (pad 0).  One thread per output word pair: thread t of the row computes SM(D, t) and writes
+// coefficients 2t, 2t+1 (low word first, C2).
+template <class PS>
+__global__ void __launch_bounds__(128) uniform_rq_kernel(uint64_t seed, uint64_t first, uint64_t n,
+                                                         uint64_t domain, int16_t *out) {
+    constexpr int PAIRS = PS::P8 / 2;
+    const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t row = gid / PAIRS;
+    const int t = (int)(gid - row * PAIRS);
+    if (row >= n) return;
+    const uint64_t D = sm_at(sm_at(seed, first + row), domain);
+    const uint64_t z = sm_at(D, (uint64_t)t);
+    const uint32_t u0 = (uint32_t)z, u1 = (uint32_t)(z >> 32);
+    const int a0 = 2 * t < PS::P ? (int)(((uint64_t)u0 * PS::Q) >> 32) - PS::QH : 0;
+    const int a1 = 2 * t + 1 < PS::P ? (int)(((uint64_t)u1 * PS::Q) >> 32) - PS::QH : 0;
+    reinterpret_cast<uint32_t *>(out + row * PS::P8)[t] = (uint32_t)(uint16_t)a0 | ((uint32_t)(uint16_t)a1 << 16);
+}
+
 // ok[row] = (number of nonzero coefficients of row == W) (decapsulation's weight check)
 template <class PS>
 __global__ void __launch_bounds__(128) weight_check_kernel(const int8_t *r, uint64_t n, uint8_t *ok) {

@@ -27,6 +27,7 @@
 #include "encode.cuh"
 #include "factor_tables.h"
 #include "fullsk.cuh"
+#include "intpeak.cuh"
 #include "ringmul.cuh"
 #include "sample.cuh"
 #include "tcmul.cuh"
@@ -45,17 +46,18 @@ std::mutex g_mu;                                   // serialises calls (shared w
 // inversions).  Read back with sntrup_profile_read().
 enum ProfClass { PC_SAMPLE = 0, PC_MUL_R3, PC_MUL_RQ, PC_INV_R3, PC_INV_RQ, PC_REPAIR, PC_ENCODE,
                  PC_MISC, PC_N };
-struct ProfRec { int cls; cudaEvent_t a, b; double units, ops; int kind; };
+struct ProfRec { int cls; cudaEvent_t a, b; double units, ops; int kind; double smem; };
 bool g_prof_on = false;
 std::vector<ProfRec> g_prof;
 std::vector<cudaEvent_t> g_evpool;
-struct ProfAgg { double ms = 0, units = 0, ops = 0; uint64_t launches = 0; };
+struct ProfAgg { double ms = 0, units = 0, ops = 0, smem = 0; uint64_t launches = 0; };
 ProfAgg g_agg[PC_N];
 // ring-product launches by arithmetic kind: 0 = int8 tensor (kind::i8), 1 = fp4 tensor
 // (kind::mxf4), 2 = int32 schoolbook
 enum { PK_I8 = 0, PK_F4 = 1, PK_I32 = 2, PK_N = 3 };
 ProfAgg g_kagg[PK_N];
 int g_cur_kind = -1;                 // set by the launcher inside a ProfScope
+double g_cur_smem = 0;               // tensor-core operand bytes the launch's MMAs fetch from smem
 
 cudaEvent_t ev_get() {
     if (!g_evpool.empty()) { cudaEvent_t e = g_evpool.back(); g_evpool.pop_back(); return e; }
@@ -71,8 +73,9 @@ struct ProfScope {
         if (g_prof_on) { a = ev_get(); cudaEventRecord(a, s); }
     }
     ~ProfScope() {
-        if (a) { cudaEvent_t b = ev_get(); cudaEventRecord(b, s); g_prof.push_back(ProfRec{cls, a, b, units, ops, g_cur_kind}); }
+        if (a) { cudaEvent_t b = ev_get(); cudaEventRecord(b, s); g_prof.push_back(ProfRec{cls, a, b, units, ops, g_cur_kind, g_cur_smem}); }
         g_cur_kind = -1;
+        g_cur_smem = 0;
     }
 };
 
@@ -88,6 +91,7 @@ void prof_drain() {
             g_kagg[r.kind].ms += ms;
             g_kagg[r.kind].ops += r.ops;
             g_kagg[r.kind].units += r.units;
+            g_kagg[r.kind].smem += r.smem;
             g_kagg[r.kind].launches += 1;
         }
         g_agg[r.cls].launches += 1;
@@ -302,6 +306,7 @@ int build_tables(int dev, int ps, int WT, DevTables **out) {
 // Host-output keygen: chunk i's pk/sk are copied device->host on a copy stream while chunk i+1
 // computes (double-buffered device staging).  One per device (calls are serialised).
 struct CopyStream { cudaStream_t s = nullptr; cudaEvent_t comp[2] = {}, copy[2] = {}; };
+std::vector<cudaStream_t> g_copy_streams;     // every copy stream created (staging layout changes)
 // SNTRUP_OPT_LANE_PRIORITY: lane li's streams get priority rank li (lane 0 highest), so the
 // scheduler finishes lane 0's chunk first while the other lanes fill its latency gaps; -1 = the
 // default priority.
@@ -326,6 +331,7 @@ int copy_stream(CopyStream **out, int which = 0, int prio_rank = -1) {   // whic
     CopyStream &c = m[std::make_tuple(dev, which, prio_rank)];
     if (!c.s) {
         if (make_stream(&c.s, prio_rank)) return SNTRUP_E_CUDA;
+        g_copy_streams.push_back(c.s);
         for (int i = 0; i < 2; i++) {
             CK(cudaEventCreateWithFlags(&c.comp[i], cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&c.copy[i], cudaEventDisableTiming));
@@ -380,10 +386,25 @@ struct Workspace {
 };
 std::map<std::pair<int, uintptr_t>, Workspace> g_wsmap;
 Workspace *g_ws = nullptr;
+Workspace g_user_ws;                          // a caller-supplied workspace (opts.workspace)
 
-int ws_reserve(size_t bytes, cudaStream_t stream) {
+// bytes ws_reserve allocates for a request of `bytes` (slack so that slightly larger later
+// calls on the same stream reuse the allocation)
+size_t ws_alloc_bytes(size_t bytes) { return bytes + (bytes >> 3) + (1 << 20); }
+
+int ws_reserve(size_t bytes, cudaStream_t stream, void *user = nullptr, size_t user_bytes = 0) {
     int dev;
     CK(cudaGetDevice(&dev));
+    if (user) {                               // caller-owned memory: no caching, no allocation
+        if (user_bytes < bytes) return SNTRUP_E_WORKSPACE;
+        if ((uintptr_t)user & 255) return SNTRUP_E_ARG;
+        g_user_ws.base = (char *)user;
+        g_user_ws.cap = user_bytes;
+        g_user_ws.used = 0;
+        g_user_ws.dev = dev;
+        g_ws = &g_user_ws;
+        return SNTRUP_OK;
+    }
     Workspace &w = g_wsmap[std::make_pair(dev, (uintptr_t)stream)];
     g_ws = &w;
     if (w.base && w.cap >= bytes) { w.used = 0; return SNTRUP_OK; }
@@ -393,7 +414,7 @@ int ws_reserve(size_t bytes, cudaStream_t stream) {
         w.base = nullptr;
         w.cap = 0;
     }
-    size_t cap = bytes + (bytes >> 3) + (1 << 20);
+    size_t cap = ws_alloc_bytes(bytes);
     if (cudaMalloc(&w.base, cap) != cudaSuccess) {
         cudaGetLastError();
         w.base = nullptr;
@@ -406,6 +427,42 @@ int ws_reserve(size_t bytes, cudaStream_t stream) {
     return SNTRUP_OK;
 }
 
+// Host-output staging (device buffers the D2H copies read from) lives in its own allocation per
+// (device, caller stream), NOT in the workspace: asynchronous host-output calls leave their copies
+// running after return, and the next call on the stream reuses the workspace at once.  Within a
+// fixed layout each staging buffer is waited for (its copy-done event) right before its first
+// write; a layout change (chunk, lanes, sizes) or growth first waits for every copy in flight.
+struct Staging {
+    char *base = nullptr;
+    size_t cap = 0;
+    uint64_t layout = 0;
+};
+std::map<std::pair<int, uintptr_t>, Staging> g_stmap;
+
+int staging_reserve(size_t bytes, uint64_t layout, cudaStream_t stream, char **out) {
+    int dev;
+    CK(cudaGetDevice(&dev));
+    Staging &st = g_stmap[std::make_pair(dev, (uintptr_t)stream)];
+    if (st.base && st.cap >= bytes && st.layout == layout) { *out = st.base; return SNTRUP_OK; }
+    for (cudaStream_t cs : g_copy_streams) CK(cudaStreamSynchronize(cs));   // copies still reading it
+    if (st.base && st.cap < bytes) {
+        cudaFree(st.base);
+        st.base = nullptr;
+        st.cap = 0;
+    }
+    if (!st.base) {
+        if (cudaMalloc(&st.base, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            st.base = nullptr;
+            return SNTRUP_E_WORKSPACE;
+        }
+        st.cap = bytes;
+    }
+    st.layout = layout;
+    *out = st.base;
+    return SNTRUP_OK;
+}
+
 template <class T>
 T *ws_take(size_t count) {
     size_t bytes = (count * sizeof(T) + 255) & ~(size_t)255;
@@ -413,6 +470,9 @@ T *ws_take(size_t count) {
     g_ws->used += bytes;
     return p;
 }
+
+// every ws_take of a call stayed inside the reservation (checked before the first launch)
+bool ws_fits() { return g_ws && g_ws->used <= g_ws->cap; }
 
 size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
@@ -495,6 +555,9 @@ int launch_tc_impl(const MulArgs &a, cudaStream_t s) {
     long long grid = (long long)it->second * dev_info().sms;
     if (grid > a.n_out) grid = a.n_out;
     g_cur_kind = PK_I8;
+    // per work item: NKS K steps x LA A-limbs, each MMA reading an MM x 32-byte A tile and an
+    // NB x 32-byte B tile from shared memory
+    g_cur_smem = (double)a.n_out * G::NKS * LA * (double)(MM * 32 + G::NB * 32);
     kern<<<(unsigned)grid, NT, SMEM, s>>>(a);
     LAUNCHED();
     return SNTRUP_OK;
@@ -534,6 +597,9 @@ int launch_tc4_impl(const MulArgs &a, cudaStream_t s) {
     long long grid = (long long)it->second * dev_info().sms;
     if (grid > a.n_out) grid = a.n_out;
     g_cur_kind = PK_F4;
+    // per work item: NKS MMAs, each an 128 x 32-byte A tile (64 fp4 K-elements; none for the K
+    // steps whose A is in TMEM) and an NB x 32-byte B tile
+    g_cur_smem = (double)a.n_out * ((double)(G::NKS - G::NTA) * 128 * 32 + (double)G::NKS * G::NB * 32);
     kern<<<(unsigned)grid, 128, G::SMEM, s>>>(a);
     LAUNCHED();
     return SNTRUP_OK;
@@ -559,15 +625,9 @@ int launch_mul(MulArgs a, cudaStream_t s, int la = 2, int lb = 2) {
     if (a.n_out <= 0) return SNTRUP_OK;
     const int impl = (g_mul_impl >= 7) ? 0 : g_mul_impl;   // 7, 8, 9: as 0 except u / pipelining / TMEM A
     const bool pipe = g_mul_impl == 8;
-    // algorithmic ops: tensor path = 2 p^2 int8 multiply-add ops per limb-pair product (the
-    // limb-decomposed schoolbook contraction); schoolbook path = 2 p^2 int32 ops per product
-    // (fp4 path: digit pairs = LB base-9 digits of the big operand x 1)
-    const bool small_op = (M == 3) || la == 1 || lb == 1;
-    int limb_pairs = (impl == 1 || M == 3) ? 1 : la * lb;
-    if ((impl == 0 || impl == 5 || impl == 6) && small_op && M != 3) limb_pairs = (la == 1 && lb == 1) ? 1 : 2;
-    if (impl == 4 && small_op && M != 3) limb_pairs = (la == 1 && lb == 1) ? 1 : digits9(M);
-    ProfScope ps_(M == 3 ? PC_MUL_R3 : PC_MUL_RQ, (double)a.n_out, s,
-                  2.0 * PS::P * PS::P * limb_pairs * (double)a.n_out);
+    // algorithmic ops: the method's work, 2 p^2 (p^2 multiply-adds) per ring product whatever the
+    // implementation (limbs, digits, padding and the zero triangles are implementation overhead)
+    ProfScope ps_(M == 3 ? PC_MUL_R3 : PC_MUL_RQ, (double)a.n_out, s, 2.0 * PS::P * PS::P * (double)a.n_out);
     if (impl == 1) {
         const int threads = (PS::P8 / 8 + 31) / 32 * 32;
         long long grid = a.n_out;
@@ -817,6 +877,43 @@ int lane_join_events(LaneJoin **out) {
     return SNTRUP_OK;
 }
 
+// Shape of a keygen call: chunking, lanes, and the exact device bytes it reserves -- one helper
+// for keygen_impl and sntrup_keygen_workspace_bytes, so the query is what a call takes.
+struct KeygenShape {
+    uint64_t chunk;
+    size_t pkb, skb;
+    int nl, nbuf;
+    size_t ws_need;      // workspace (cached per stream, or the caller's)
+    size_t stage_need;   // host-output staging (own allocation; 0 without SNTRUP_OPT_HOST_OUTPUT)
+};
+
+template <class PS>
+KeygenShape keygen_shape(uint64_t n, int B, uint32_t flags, uint64_t chunk_keys, size_t pk_bytes) {
+    KeygenShape k{};
+    uint64_t chunk = chunk_keys ? chunk_keys : 65536;
+    chunk = (chunk + B - 1) / B * B;
+    if (chunk > n) chunk = (n + B - 1) / B * B;
+    k.chunk = chunk;
+    k.pkb = pk_bytes;
+    k.skb = 2 * PS::SKH;
+    const uint64_t nchunks = (n + chunk - 1) / chunk;
+    const int nlmax = (flags & SNTRUP_OPT_SERIAL) ? 1 : (flags & SNTRUP_OPT_LANES4) ? 4 : 2;
+    k.nl = (int)(nchunks < (uint64_t)nlmax ? nchunks : nlmax);
+    k.nbuf = k.nl >= 2 ? k.nl : 2;          // host-output staging buffers (lane-owned if nl >= 2)
+    // per lane, exactly the ws_take calls of keygen_impl (each rounded up to 256 bytes)
+    const TreePlan tp = make_plan((long long)chunk, B);
+    size_t per_lane = 3 * align256(chunk * PS::P16) + align256(chunk);           // G, F, Ginv, attempts
+    for (int l = 1; l <= tp.L; l++)
+        per_lane += 2 * align256(tp.cnt[l] * PS::P16) + 2 * align256(tp.cnt[l] * PS::P8 * 2);
+    per_lane += 3 * align256(chunk * PS::P8 * 2);                                // Fbar, H, U
+    per_lane += 2 * align256(tp.cnt[tp.L]);                                      // root ok flags
+    per_lane += align256(sizeof(unsigned long long)) + align256(sizeof(int));    // counters
+    k.ws_need = (size_t)k.nl * per_lane;
+    k.stage_need = (flags & SNTRUP_OPT_HOST_OUTPUT)
+                       ? (size_t)k.nbuf * (align256(chunk * k.pkb) + align256(chunk * k.skb)) : 0;
+    return k;
+}
+
 template <class PS>
 int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
                 const sntrup_keygen_opts &o) {
@@ -829,29 +926,17 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
     const int B = o.batch_size ? (int)o.batch_size : 32;
     if (B < 1 || B > 4096 || (B & (B - 1))) return SNTRUP_E_ARG;
     const bool host_out = (o.flags & SNTRUP_OPT_HOST_OUTPUT) != 0;
-    uint64_t chunk = o.chunk_keys ? o.chunk_keys : 65536;
-    chunk = (chunk + B - 1) / B * B;
-    if (chunk > n) chunk = (n + B - 1) / B * B;
-    const size_t pkb = tb->enc.pk_bytes, skb = 2 * PS::SKH;
-    const uint64_t nchunks = (n + chunk - 1) / chunk;
-    const int nlmax = (o.flags & SNTRUP_OPT_LANES4) ? 4 : 2;
-    const int nl = (int)(nchunks < (uint64_t)nlmax ? nchunks : nlmax);
-    const int nbuf = nl >= 2 ? nl : 2;          // host-output staging buffers (lane-owned if nl >= 2)
-
-    // workspace: one chunk's buffers per lane (+ shared host-output staging)
+    const KeygenShape ks = keygen_shape<PS>(n, B, o.flags, o.chunk_keys, tb->enc.pk_bytes);
+    const uint64_t chunk = ks.chunk;
+    const size_t pkb = ks.pkb, skb = ks.skb;
+    const int nl = ks.nl, nbuf = ks.nbuf;
     const TreePlan tpmax = make_plan((long long)chunk, B);
-    const long long inner = tpmax.inner_rows();
-    size_t per_lane = 0;
-    per_lane += 3 * align256(chunk * PS::P16);                  // G, F, Ginv
-    per_lane += align256(chunk);                                 // attempts
-    per_lane += 2 * (inner * PS::P16 + 256 * (tpmax.L + 1)) + 2 * 256 * (tpmax.L + 1);  // R/3 levels + inverses
-    per_lane += 2 * (inner * PS::P8 * 2 + 256 * (tpmax.L + 1)) + 2 * 256 * (tpmax.L + 1); // R/q levels + inverses
-    per_lane += 3 * align256(chunk * PS::P8 * 2);                // Fbar, H, U
-    per_lane += 2 * align256(tpmax.cnt[tpmax.L]);                // root ok flags
-    per_lane += 2 * 256;                                         // counters
-    size_t need = nl * per_lane + 4096;
-    if (host_out) need += nbuf * (align256(chunk * pkb) + align256(chunk * skb));
-    if ((rc = ws_reserve(need, s0))) return rc;
+    if ((rc = ws_reserve(ks.ws_need, s0, o.workspace, o.workspace_bytes))) return rc;
+    char *stage_base = nullptr;
+    if (host_out) {
+        const uint64_t layout = ((uint64_t)PS::P << 48) ^ (chunk << 8) ^ (uint64_t)(nbuf << 4) ^ (uint64_t)nl;
+        if ((rc = staging_reserve(ks.stage_need, layout, s0, &stage_base))) return rc;
+    }
     Lane lanes[MAX_LANES];
     const bool prio = (o.flags & SNTRUP_OPT_LANE_PRIORITY) != 0;
     const int l0 = prio ? 0 : 1;           // first lane on an internal stream (forked from s0)
@@ -883,15 +968,16 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
         L.okq = ws_take<uint8_t>(tpmax.cnt[tpmax.L]);
         L.repaired = ws_take<unsigned long long>(1);
         L.err = ws_take<int>(1);
-        if (o.flags & SNTRUP_OPT_RING_STREAMS)
+        if ((o.flags & SNTRUP_OPT_RING_STREAMS) && !(o.flags & SNTRUP_OPT_SERIAL))
             if ((rc = ring_stream(li, pr, &L.r3))) return rc;
     }
+    if (!ws_fits()) return SNTRUP_E_INTERNAL;    // keygen_shape and the takes above disagree
     uint8_t *pk_stage[MAX_LANES] = {}, *sk_stage[MAX_LANES] = {};
     CopyStream *csl[MAX_LANES] = {};               // one copy stream per lane: copies follow readiness
     if (host_out) {
         for (int i = 0; i < nbuf; i++) {
-            pk_stage[i] = ws_take<uint8_t>(chunk * pkb);
-            sk_stage[i] = ws_take<uint8_t>(chunk * skb);
+            pk_stage[i] = (uint8_t *)stage_base + i * (align256(chunk * pkb) + align256(chunk * skb));
+            sk_stage[i] = pk_stage[i] + align256(chunk * pkb);
         }
         for (int li = 0; li < nl; li++)
             if ((rc = copy_stream(&csl[li], li, prio ? li : -1))) return rc;
@@ -966,6 +1052,7 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
         const TreeJob<PS, PS::Q> jq{tp, rows8(Fc, PS::P16, 3), L.Fbar, 2, PS::P8, L.lq, L.iq, L.okq, true};
         const bool utrick = tp.L >= 1;
         const bool rings = L.r3 != nullptr;      // R/3 chain on its own stream
+        const bool serial = (o.flags & SNTRUP_OPT_SERIAL) != 0;
         AuxStream *ax = L.ax;
         const cudaStream_t s3 = rings ? L.r3->s : s;  // stream of the R/3 chain
         if (rings) {
@@ -1009,7 +1096,22 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
         }
         if ((rc = jq.up(s, &n_rq, fused_u ? 2 : 1))) return rc;
         if (stagger && ci + 1 < (uint64_t)nl) CK(cudaEventRecord(lj->upd[ci], s));
-        if (utrick && !fused_u) {
+        if (utrick && !fused_u && serial) {
+            // SNTRUP_OPT_SERIAL (measurement): the u products on the chunk's own stream, so every
+            // kernel of the call runs alone and its CUDA-event time is its own
+            MulArgs a{};
+            a.mode = MUL_SIB;
+            a.n_out = (long long)m;
+            a.cnt_in = (long long)m;
+            a.X = rows8(Gc, PS::P16);
+            a.Y = rows8(Fc, PS::P16, 3);
+            a.out = L.U;
+            a.out_stride = PS::P8;
+            a.out_bytes = 2;
+            a.periodic = 0;
+            if ((rc = launch_mul<PS, PS::Q>(a, s, 1, 1))) return rc;
+            CK(cudaEventRecord(ax->done, s));
+        } else if (utrick && !fused_u) {
             CK(cudaEventRecord(ax->go, s));
             CK(cudaStreamWaitEvent(ax->s, ax->go, 0));
             MulArgs a{};
@@ -1025,9 +1127,9 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
             if ((rc = launch_mul<PS, PS::Q>(a, ax->s, 1, 1))) return rc;
             CK(cudaEventRecord(ax->done, ax->s));
         }
-        if (rings) {
+        if (rings || serial) {
             // each ring's roots on its own chain: one ring's latency-bound inversion overlaps the
-            // other ring's products
+            // other ring's products (serial: one after the other, separately timed)
             if ((rc = launch_divstep<PS, 3>(j3.roots(), s3))) return rc;
             if ((rc = launch_divstep<PS, PS::Q>(jq.roots(), s))) return rc;
         } else {
@@ -1232,7 +1334,9 @@ __global__ void __launch_bounds__(128) r3_prepare_kernel(const int8_t *g, int8_t
 
 // r3: finalize.  Trees whose root inverted: ok = ok_small (zero rows that were substituted).
 // Trees whose root failed: exact per-element divstep on the original input.
-template <class PS>
+// OUT = false (r3_is_invertible_batch): only ok[] is final; `out` is scratch written only for the
+// rows of failed trees.
+template <class PS, bool OUT = true>
 __global__ void __launch_bounds__(128) r3_finalize_kernel(const int8_t *g, int8_t *out, uint8_t *ok,
                                                           long long n, int B, const uint8_t *root_ok) {
     const int lane = threadIdx.x & 31;
@@ -1240,7 +1344,7 @@ __global__ void __launch_bounds__(128) r3_finalize_kernel(const int8_t *g, int8_
     if (row >= n) return;
     int8_t *orow = out + row * PS::P16;
     if (root_ok[row / B]) {
-        if (!ok[row])
+        if (OUT && !ok[row])
             for (int k = lane; k < PS::P16; k += 32) orow[k] = 0;
         return;
     }
@@ -1276,6 +1380,43 @@ int r3_recip_impl(uint64_t n, const int8_t *g, int8_t *out, uint8_t *ok, uint32_
     if ((rc = batch_inverse<PS, 3>(tp, rows8(gp, PS::P16), out, 1, PS::P16, l3, i3, rok, false, s, &np)))
         return rc;
     r3_finalize_kernel<PS><<<(unsigned)((n + 3) / 4), 128, 0, s>>>(g, out, ok, (long long)n, B, rok);
+    LAUNCHED();
+    CK(cudaStreamSynchronize(s));
+    return SNTRUP_OK;
+}
+
+// isInvertible without the reciprocals: the small-factor residues decide the small
+// factors; a tree's root (the product of its prepared leaves) is invertible iff every leaf is
+// prime to the big factors, so only the up-sweep and the root divsteps run, and the leaves of a
+// failed tree get their own divstep (invertibility only).  No down-sweep, no allocation.
+template <class PS>
+int r3_isinv_impl(uint64_t n, const int8_t *g, uint8_t *ok, cudaStream_t s) {
+    int dev;
+    CK(cudaGetDevice(&dev));
+    DevTables *tb;
+    int rc = build_tables(dev, PS::P, PS::WT, &tb);
+    if (rc) return rc;
+    const int B = 32;
+    const TreePlan tp = make_plan((long long)n, B);
+    size_t need = 2 * align256(n * PS::P16) + align256(tp.cnt[tp.L]);
+    for (int l = 1; l <= tp.L; l++) need += 2 * align256(tp.cnt[l] * PS::P16);
+    if ((rc = ws_reserve(need, s))) return rc;
+    int8_t *gp = ws_take<int8_t>(n * PS::P16);
+    int8_t *scratch = ws_take<int8_t>(n * PS::P16);
+    std::vector<void *> l3(tp.L + 1, nullptr), i3(tp.L + 1, nullptr);
+    for (int l = 1; l <= tp.L; l++) {
+        l3[l] = ws_take<int8_t>(tp.cnt[l] * PS::P16);
+        i3[l] = ws_take<int8_t>(tp.cnt[l] * PS::P16);
+    }
+    uint8_t *rok = ws_take<uint8_t>(tp.cnt[tp.L]);
+    if (!ws_fits()) return SNTRUP_E_INTERNAL;
+    r3_prepare_kernel<PS><<<(unsigned)((n + 3) / 4), 128, 0, s>>>(g, gp, ok, (long long)n, tb->T, tb->masks, tb->nf);
+    LAUNCHED();
+    const TreeJob<PS, 3> j{tp, rows8(gp, PS::P16), scratch, 1, PS::P16, l3, i3, rok, false};
+    uint64_t np = 0;
+    if ((rc = j.up(s, &np))) return rc;
+    if ((rc = launch_divstep<PS, 3>(j.roots(), s))) return rc;
+    r3_finalize_kernel<PS, false><<<(unsigned)((n + 3) / 4), 128, 0, s>>>(g, scratch, ok, (long long)n, B, rok);
     LAUNCHED();
     CK(cudaStreamSynchronize(s));
     return SNTRUP_OK;
@@ -1364,16 +1505,32 @@ int sntrup_batch_keygen(int param_set, uint64_t n_keys, uint64_t seed, uint8_t *
 }
 
 size_t sntrup_keygen_workspace_bytes(int param_set, uint64_t n_keys, uint32_t batch_size) {
+    return sntrup_keygen_workspace_bytes_ex(param_set, n_keys, batch_size, 0, 0);
+}
+
+size_t sntrup_keygen_workspace_bytes_ex(int param_set, uint64_t n_keys, uint32_t batch_size, uint32_t flags,
+                                        uint64_t chunk_keys) {
     ParamInfo pi;
     if (!param_info(param_set, &pi) || n_keys == 0) return 0;
     const int B = batch_size ? (int)batch_size : 32;
-    uint64_t chunk = 65536;
-    chunk = (chunk + B - 1) / B * B;
-    if (chunk > n_keys) chunk = (n_keys + B - 1) / B * B;
-    const TreePlan tp = make_plan((long long)chunk, B);
-    const long long inner = tp.inner_rows();
-    return 3 * align256(chunk * pi.p16) + align256(chunk) + 2 * align256(inner * pi.p16) +
-           2 * align256(inner * pi.p8 * 2) + 2 * align256(chunk * pi.p8 * 2) + 4096;
+    if (B < 1 || B > 4096 || (B & (B - 1))) return 0;
+    SNTRUP_DISPATCH(param_set, {
+        const KeygenShape k = keygen_shape<PS>(n_keys, B, flags, chunk_keys, pi.pk);
+        return k.ws_need;
+    });
+    return 0;
+}
+
+size_t sntrup_workspace_reserved_bytes(void *stream, int which) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    if (which == 1) {
+        auto it = g_stmap.find(std::make_pair(dev, (uintptr_t)stream));
+        return it == g_stmap.end() ? 0 : it->second.cap;
+    }
+    auto it = g_wsmap.find(std::make_pair(dev, (uintptr_t)stream));
+    return it == g_wsmap.end() ? 0 : it->second.cap;
 }
 
 int rq_mul_batch(int param_set, uint64_t n, const int16_t *a, const int16_t *b, int16_t *c,
@@ -1479,6 +1636,21 @@ int sntrup_sample_short_batch(int param_set, uint64_t n, uint64_t seed, uint64_t
     return SNTRUP_E_PARAM;
 }
 
+int sntrup_sample_uniform_rq_batch(int param_set, uint64_t n, uint64_t seed, uint64_t first_key_index,
+                                    uint64_t domain, int16_t *a_out, void *stream) {
+    ParamInfo pi;
+    if (!param_info(param_set, &pi)) return SNTRUP_E_PARAM;
+    if (n == 0 || !a_out) return SNTRUP_E_ARG;
+    SNTRUP_DISPATCH(param_set, {
+        const uint64_t threads = n * (uint64_t)(PS::P8 / 2);
+        uniform_rq_kernel<PS><<<(unsigned)((threads + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+            seed, first_key_index, n, domain, a_out);
+        LAUNCHED();
+        return SNTRUP_OK;
+    });
+    return SNTRUP_E_PARAM;
+}
+
 int sntrup_encap_core_batch(int param_set, uint64_t n, const int16_t *h, const int8_t *r, int16_t *c,
                             void *stream) {
     ParamInfo pi;
@@ -1577,11 +1749,9 @@ int r3_is_invertible_batch(int param_set, uint64_t n, const int8_t *g, uint8_t *
     ParamInfo pi;
     if (!param_info(param_set, &pi)) return SNTRUP_E_PARAM;
     if (n == 0 || !g || !ok) return SNTRUP_E_ARG;
-    int8_t *scratch = nullptr;
-    CK(cudaMalloc(&scratch, n * pi.p16));
-    int rc = r3_recip_batch(param_set, n, g, scratch, ok, 32, stream);
-    cudaFree(scratch);
-    return rc;
+    std::lock_guard<std::mutex> lk(g_mu);
+    SNTRUP_DISPATCH(param_set, return r3_isinv_impl<PS>(n, g, ok, (cudaStream_t)stream));
+    return SNTRUP_E_PARAM;
 }
 
 int rq_encode_batch(int param_set, uint64_t n, const int16_t *h, uint8_t *pk, void *stream) {
@@ -1616,8 +1786,94 @@ void sntrup_release_workspace(void) {
         kv.second.base = nullptr;
         kv.second.cap = 0;
     }
+    for (cudaStream_t cs : g_copy_streams) cudaStreamSynchronize(cs);
+    for (auto &kv : g_stmap) {
+        if (!kv.second.base) continue;
+        cudaSetDevice(kv.first.first);
+        cudaFree(kv.second.base);
+        kv.second.base = nullptr;
+        kv.second.cap = 0;
+    }
     cudaSetDevice(cur);
     g_ws = nullptr;
+}
+
+int sntrup_release_stream_workspace(void *stream) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    const auto key = std::make_pair(dev, (uintptr_t)stream);
+    CK(cudaStreamSynchronize((cudaStream_t)stream));
+    for (cudaStream_t cs : g_copy_streams) CK(cudaStreamSynchronize(cs));
+    auto it = g_wsmap.find(key);
+    if (it != g_wsmap.end() && it->second.base) {
+        // the workspace held secret f, 1/g and tree rows: erase before freeing
+        CK(cudaMemset(it->second.base, 0, it->second.cap));
+        CK(cudaFree(it->second.base));
+        if (g_ws == &it->second) g_ws = nullptr;
+        g_wsmap.erase(it);
+    }
+    auto st = g_stmap.find(key);
+    if (st != g_stmap.end() && st->second.base) {
+        CK(cudaMemset(st->second.base, 0, st->second.cap));
+        CK(cudaFree(st->second.base));
+        g_stmap.erase(st);
+    }
+    return SNTRUP_OK;
+}
+
+int sntrup_measure_int_peak(int op, double *lane_ops_per_clk_sm, double *lane_ops_per_s) {
+    if (op < 0 || op >= IOP_N) return SNTRUP_E_ARG;
+    std::lock_guard<std::mutex> lk(g_mu);
+    constexpr int CH = 8, ITER = 2048, NT = 256;
+    const int sms = dev_info().sms, nb = sms * 8;
+    uint32_t *sink = nullptr;
+    IntPeakRec *rec = nullptr;
+    CK(cudaMalloc(&sink, NT * sizeof(uint32_t)));
+    CK(cudaMalloc(&rec, nb * sizeof(IntPeakRec)));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    auto launch = [&](cudaStream_t s) {
+        switch (op) {
+        case IOP_IMAD: int_peak_kernel<IOP_IMAD, CH, ITER><<<nb, NT, 0, s>>>(7u, sink, rec); break;
+        case IOP_IADD3: int_peak_kernel<IOP_IADD3, CH, ITER><<<nb, NT, 0, s>>>(7u, sink, rec); break;
+        case IOP_LOP3: int_peak_kernel<IOP_LOP3, CH, ITER><<<nb, NT, 0, s>>>(7u, sink, rec); break;
+        default: int_peak_kernel<IOP_SHF, CH, ITER><<<nb, NT, 0, s>>>(7u, sink, rec); break;
+        }
+    };
+    launch(0);                                   // warm-up (clocks up)
+    LAUNCHED();
+    CK(cudaEventRecord(e0, 0));
+    launch(0);
+    LAUNCHED();
+    CK(cudaEventRecord(e1, 0));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    std::vector<IntPeakRec> h(nb);
+    CK(cudaMemcpy(h.data(), rec, nb * sizeof(IntPeakRec), cudaMemcpyDeviceToHost));
+    cudaFree(sink);
+    cudaFree(rec);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    const double per_block = (double)NT * ITER * 8 * CH;
+    std::map<unsigned, std::tuple<unsigned long long, unsigned long long, int>> sm;   // smid -> t0, t1, blocks
+    for (auto &r : h) {
+        auto it = sm.find(r.smid);
+        if (it == sm.end()) sm[r.smid] = std::make_tuple(r.t0, r.t1, 1);
+        else {
+            auto &t = it->second;
+            if (r.t0 < std::get<0>(t)) std::get<0>(t) = r.t0;
+            if (r.t1 > std::get<1>(t)) std::get<1>(t) = r.t1;
+            std::get<2>(t) += 1;
+        }
+    }
+    double rate = 0;
+    for (auto &kv : sm) rate += per_block * std::get<2>(kv.second) / (double)(std::get<1>(kv.second) - std::get<0>(kv.second));
+    if (lane_ops_per_clk_sm) *lane_ops_per_clk_sm = sm.empty() ? 0 : rate / sm.size();
+    if (lane_ops_per_s) *lane_ops_per_s = per_block * nb / (ms * 1e-3);
+    return SNTRUP_OK;
 }
 
 uint64_t sntrup_kernel_launch_count(void) { return g_launches.load(); }
@@ -1629,6 +1885,22 @@ int sntrup_profile_read_kinds(int reset, double *ms, double *ops, uint64_t *laun
         if (ms) ms[i] = g_kagg[i].ms;
         if (ops) ops[i] = g_kagg[i].ops;
         if (launches) launches[i] = g_kagg[i].launches;
+    }
+    if (reset)
+        for (int i = 0; i < PK_N; i++) g_kagg[i] = ProfAgg{};
+    return PK_N;
+}
+
+int sntrup_profile_read_kinds_ex(int reset, double *ms, double *ops, uint64_t *launches, double *products,
+                                 double *smem_bytes) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    prof_drain();
+    for (int i = 0; i < PK_N; i++) {
+        if (ms) ms[i] = g_kagg[i].ms;
+        if (ops) ops[i] = g_kagg[i].ops;
+        if (launches) launches[i] = g_kagg[i].launches;
+        if (products) products[i] = g_kagg[i].units;
+        if (smem_bytes) smem_bytes[i] = g_kagg[i].smem;
     }
     if (reset)
         for (int i = 0; i < PK_N; i++) g_kagg[i] = ProfAgg{};

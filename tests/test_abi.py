@@ -170,3 +170,35 @@ def test_compute_calls_reject_host_tensors(lib):
     a = torch.zeros((4, 768), dtype=torch.int16)
     with pytest.raises((ValueError, RuntimeError, AssertionError)):
         S.rq_mul_batch(761, a, a.clone())
+
+
+def test_workspace_query_host_only(lib):
+    import paper_2106_08759_b200 as S
+    L = S._lib
+    assert L.sntrup_keygen_workspace_bytes(700, 10, 32) == 0
+    assert L.sntrup_keygen_workspace_bytes(761, 0, 32) == 0
+    assert L.sntrup_keygen_workspace_bytes_ex(761, 100, 3, 0, 0) == 0          # B not a power of two
+    a = S.keygen_workspace_bytes(761, 65536, 1024, 0, 32768)
+    b = S.keygen_workspace_bytes(761, 65536, 1024, S.OPT_LANES4, 16384)
+    assert a > 0 and b > 0
+    # one lane per chunk up to the lane count: 2 lanes of 32768 keys vs 4 lanes of 16384 keys
+    # hold the same number of keys' buffers (+ per-level rounding)
+    assert abs(a - b) < 0.01 * a
+    # the plain query is the _ex query with default options
+    assert L.sntrup_keygen_workspace_bytes(761, 5000, 64) == S.keygen_workspace_bytes(761, 5000, 64)
+    # host outputs do not enlarge the workspace (staging is a separate allocation)
+    assert S.keygen_workspace_bytes(761, 65536, 1024, S.OPT_HOST_OUTPUT, 32768) == a
+
+
+def test_binding_checks_caller_outputs_without_gpu(lib):
+    # outputs supplied by the caller are checked (shape, dtype, placement) before any
+    # library call; host-output keygen wants host tensors
+    import torch
+    import paper_2106_08759_b200 as S
+    bad = torch.zeros((4, 100), dtype=torch.uint8)
+    sk = torch.zeros((4, 382), dtype=torch.uint8)
+    with pytest.raises(ValueError):
+        S.batch_keygen(761, 4, 1, flags=S.OPT_HOST_OUTPUT, pk_out=bad, sk_out=sk)
+    with pytest.raises(ValueError):
+        S.batch_keygen(761, 4, 1, flags=S.OPT_HOST_OUTPUT, pk_out=torch.zeros((4, 1158), dtype=torch.int16),
+                       sk_out=sk)

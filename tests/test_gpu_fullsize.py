@@ -1,0 +1,206 @@
+"""GPU parity at the north-star size: EVERY key of BASELINE.json configs[1], configs[3] and
+configs[4], and EVERY pair of configs[2], against the oracle -- in the launch configuration bench.py
+times.
+
+The oracle's outputs at these sizes (2.8 GB for configs[4]) are too large to commit, so
+scripts/gen_oracle_digests.py (which calls only oracle/) stored per-group SHA-256 digests under
+tests/golden/oracle_digests/; these tests hash the CUDA path's outputs group by group the same way.
+A mismatching group is then re-checked key by key against the oracle to name the first bad key.
+North star: "bit-exact sntrup761 batch keygen (pk/sk bytes) versus the CPU oracle at >= 2^16 keys
+per call"; SURVEY.md 8(d) cfg2-cfg5 parity columns.
+"""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2106_08759_b200 as S  # noqa: E402
+
+DIG = os.path.join(os.path.dirname(__file__), "golden", "oracle_digests")
+
+# bench.py's launch configurations (bench.py DEFAULT_B / DEFAULT_CHUNK / flags; other_configs())
+BENCH_KEYGEN = dict(batch_size=1024, chunk_keys=32768, flags=S.OPT_ASYNC | S.OPT_RING_STREAMS)
+BENCH_1277 = dict(batch_size=1024, chunk_keys=65536, flags=S.OPT_ASYNC | S.OPT_RING_STREAMS)
+
+
+def load(name):
+    path = os.path.join(DIG, name + ".json")
+    d = json.load(open(path))
+    return d
+
+
+def first_bad_key(O, param, seed, pk, sk, g0, G):
+    ref = O.keygen_many(param, seed, np.arange(g0, g0 + G))
+    bad = np.nonzero((pk != ref["pk"]).any(1) | (sk != ref["sk"]).any(1))[0]
+    return int(g0 + bad[0]) if len(bad) else None
+
+
+def check_keygen_digests(O, name, run_kwargs):
+    d = load(name)
+    param, seed, n, G = d["param"], d["seed"], d["n_keys"], d["group"]
+    assert len(d["groups"]) == n // G, "digest file %s incomplete" % name
+    P = S.params(param)
+    assert (d["pk_bytes"], d["sk_bytes"]) == (P["pk_bytes"], P["sk_bytes"])
+    res = S.batch_keygen(param, n, seed, **run_kwargs)
+    torch.cuda.synchronize()
+    pk, sk = res["pk"].cpu().numpy(), res["sk"].cpu().numpy()
+    bad = []
+    for g, e in enumerate(d["groups"]):
+        s = slice(g * G, (g + 1) * G)
+        if hashlib.sha256(pk[s].tobytes() + sk[s].tobytes()).hexdigest() != e["kv"]:
+            bad.append(g)
+    if bad:
+        g = bad[0]
+        k = first_bad_key(O, param, seed, pk[g * G:(g + 1) * G], sk[g * G:(g + 1) * G], g * G, G)
+        pytest.fail("%s: %d of %d key groups differ from the oracle; first bad key %s"
+                    % (name, len(bad), len(d["groups"]), k))
+    return d, res
+
+
+def check_attempts(d, param, seed, run_kwargs, pk_ref):
+    """Per-key g-draw counts (rejections) against the oracle's, through the debug outputs; the
+    keys of this run must equal the bench-configuration run's."""
+    n, G = d["n_keys"], d["group"]
+    res = S.batch_keygen(param, n, seed, debug=True, **run_kwargs)
+    torch.cuda.synchronize()
+    att = res["attempts"].cpu().numpy().astype(np.uint8)
+    for g, e in enumerate(d["groups"]):
+        s = slice(g * G, (g + 1) * G)
+        assert hashlib.sha256(att[s].tobytes()).hexdigest() == e["att"], "attempts group %d" % g
+    assert int(att.astype(np.int64).sum()) - n == sum(e["rej"] for e in d["groups"])
+    assert torch.equal(res["pk"], pk_ref)
+
+
+def test_cfg1_every_key_bench_config(O):
+    # BASELINE configs[1]: all 65,536 sntrup761 keys of seed 2, at bench.py's launch configuration
+    d, res = check_keygen_digests(O, "cfg1_761", BENCH_KEYGEN)
+    check_attempts(d, 761, 2, BENCH_KEYGEN, res["pk"])
+
+
+@pytest.mark.parametrize("B", [32, 128, 512, 2048])
+def test_cfg1_every_key_batch_size_sweep(O, B):
+    # configs[1]'s Montgomery batch-size sweep: every key at every B (C0: the tree shape cannot
+    # change any byte)
+    check_keygen_digests(O, "cfg1_761", dict(batch_size=B))
+
+
+def test_cfg1_every_key_plain_entry_point(O):
+    # the north-star call itself: sntrup_batch_keygen(param_set, n_keys, seed, pk_out, sk_out)
+    # (B = 32, internal chunking, synchronous), all 65,536 keys
+    d = load("cfg1_761")
+    P = S.params(761)
+    n = d["n_keys"]
+    pk = torch.empty((n, P["pk_bytes"]), dtype=torch.uint8, device="cuda")
+    sk = torch.empty((n, P["sk_bytes"]), dtype=torch.uint8, device="cuda")
+    torch.cuda.synchronize()
+    rc = S._lib.sntrup_batch_keygen(761, n, d["seed"], S._ptr(pk), S._ptr(sk))
+    assert rc == S.SNTRUP_OK
+    pkn, skn, G = pk.cpu().numpy(), sk.cpu().numpy(), d["group"]
+    for g, e in enumerate(d["groups"]):
+        s = slice(g * G, (g + 1) * G)
+        assert hashlib.sha256(pkn[s].tobytes() + skn[s].tobytes()).hexdigest() == e["kv"], g
+
+
+@pytest.mark.parametrize("param", [653, 857, 953, 1013])
+def test_cfg3_every_key_bench_config(O, param):
+    # BASELINE configs[3]: all 65,536 keys per set, seed 4, bench.py's configs[3] launch shape;
+    # per-key attempt counts (the rejection path is hot for 653/953/1013) equal the oracle's
+    name = "cfg3_%d" % param
+    d, res = check_keygen_digests(O, name, BENCH_KEYGEN)
+    check_attempts(d, param, 4, BENCH_KEYGEN, res["pk"])
+
+
+def test_cfg4_every_key_bench_config(O):
+    # BASELINE configs[4]: all 2^20 sntrup1277 keys of seed 5, B = 1024, 65,536-key chunks
+    d, res = check_keygen_digests(O, "cfg4_1277", BENCH_1277)
+    del res
+    torch.cuda.empty_cache()
+
+
+def test_cfg4_attempts_every_key(O):
+    d = load("cfg4_1277")
+    n, G = d["n_keys"], d["group"]
+    res = S.batch_keygen(1277, n, d["seed"], debug=True, **BENCH_1277)
+    torch.cuda.synchronize()
+    att = res["attempts"].cpu().numpy().astype(np.uint8)
+    for g, e in enumerate(d["groups"]):
+        s = slice(g * G, (g + 1) * G)
+        assert hashlib.sha256(att[s].tobytes()).hexdigest() == e["att"], "attempts group %d" % g
+    # SURVEY 8(c) "Rejections": 54,614 +- 240 expected extra draws at 2^20 keys
+    assert abs(sum(e["rej"] for e in d["groups"]) - 54614) < 6 * 240
+
+
+def c12_inputs(param, seed, first, n):
+    """configs[2] inputs, generated on the GPU by the library's own C12 samplers."""
+    a = S.sample_uniform_rq_batch(param, n, seed, first_key_index=first, domain=0)
+    b = S.sample_short_batch(param, n, seed, first_key_index=first, domain=1)
+    return a, b
+
+
+def test_cfg2_every_pair_bench_config(O):
+    # BASELINE configs[2]: 2^20 R/q products uniform x Short(286), seed 3, through
+    # rq_mul_small_batch at the full launch size (persistent grid: every CTA loops over ~1,000
+    # work items with the next item prefetched); inputs by C12 on both sides
+    d = load("cfg2_761")
+    param, seed, n, G = d["param"], d["seed"], d["n_pairs"], d["group"]
+    assert len(d["groups"]) == n // G
+    P = S.params(param)
+    p = P["p"]
+    a, b = c12_inputs(param, seed, 0, n)
+    c = S.rq_mul_small_batch(param, a, b)
+    torch.cuda.synchronize()
+    an, bn, cn = a.cpu().numpy(), b.cpu().numpy(), c.cpu().numpy()
+    assert not an[:, p:].any() and not bn[:, p:].any() and not cn[:, p:].any()
+    for g, e in enumerate(d["groups"]):
+        s = slice(g * G, (g + 1) * G)
+        assert hashlib.sha256(np.ascontiguousarray(an[s, :p]).tobytes()).hexdigest() == e["a"], "a group %d" % g
+        assert hashlib.sha256(np.ascontiguousarray(bn[s, :p]).tobytes()).hexdigest() == e["b"], "b group %d" % g
+        if hashlib.sha256(np.ascontiguousarray(cn[s, :p]).tobytes()).hexdigest() != e["c"]:
+            ref = O.mul_many(p, P["q"], an[s], bn[s].astype(np.int16))
+            i = int(np.nonzero((ref[:, :p] != cn[s, :p]).any(1))[0][0])
+            pytest.fail("configs[2] pair %d differs from the oracle" % (g * G + i))
+
+
+def test_cfg2_big_x_big_full_launch(O):
+    # the big x big path (rq_mul_batch, the tree's int8 2 x 2-limb kernel) at the 2^20-pair launch
+    # shape: a stride of 65,536 pairs compared one by one with the oracle, the rest by the
+    # identity a*b = b*a (both orders run the same multi-item persistent loop)
+    P = S.params(761)
+    n, p = 1 << 20, P["p"]
+    a = S.sample_uniform_rq_batch(761, n, 3, domain=0)
+    b = S.sample_uniform_rq_batch(761, n, 3, domain=2)
+    c = S.rq_mul_batch(761, a, b)
+    c2 = S.rq_mul_batch(761, b, a)
+    torch.cuda.synchronize()
+    assert torch.equal(c, c2)
+    idx = np.arange(0, n, 16)
+    ref = O.mul_many(p, P["q"], a[idx].cpu().numpy(), b[idx].cpu().numpy())
+    assert np.array_equal(c[idx].cpu().numpy(), ref)
+
+
+def test_c12_sampler_matches_oracle(O):
+    # the GPU's C12 uniform sampler against the oracle's (ragged n, several domains and offsets)
+    for param in (761, 1277, 653):
+        P = S.params(param)
+        p, q = P["p"], P["q"]
+        a = S.sample_uniform_rq_batch(param, 37, 3, first_key_index=1000, domain=5)
+        an = a.cpu().numpy()
+        assert not an[:, p:].any()
+        for i in range(37):
+            ref = O.uniform_from_words(p, q, O.stream_words(3, 1000 + i, 5, p))
+            assert np.array_equal(an[i, :p], ref)
+    # C14 golden: pair 0 of configs[2]
+    a, b = c12_inputs(761, 3, 0, 1)
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "survey_c14.json")))["config3_pair0_seed3"]
+    assert list(map(int, a[0, :6].cpu())) == g["a0_5"]
+    assert list(map(int, np.nonzero(b[0].cpu().numpy())[0][:4])) == g["b_first_nonzero"]
+    c = S.rq_mul_small_batch(761, a, b)
+    assert list(map(int, c[0, :6].cpu())) == g["c0_5"]
