@@ -120,40 +120,15 @@ def load_peaks():
         return {}
 
 
-def int_peak_macs_per_s(sm_mhz: float, n_sm: int = 148) -> float:
-    # integer multiply-add (IMAD) issues on the FMA pipe at 64 lanes/clk/SM
-    # (B300_MICROARCH: FMA pipe rt_SMSP = 2 -> 16 lanes/clk/SMSP).
-    return 64.0 * n_sm * sm_mhz * 1e6
-
-
-def int8_tc_peak_tops(peaks: dict):
-    """Dense int8 tensor peak: the measured bf16 cuBLAS peak x the nominal int8/bf16 ratio
-    (4.5 / 2.25 PF dense, B200_PROFILING.md).  The ring-product kernels run inside a multi-ms step,
-    so the sustained bf16 figure is the base."""
-    if "bf16_tflops_sustained" in peaks:
-        return 2.0 * peaks["bf16_tflops_sustained"], "measured bf16_tflops_sustained %.1f x 2 (nominal int8/bf16 ratio)" % peaks["bf16_tflops_sustained"]
-    return 2.0 * 1400.0, "fallback 1.4 PF/s sustained bf16 (B200_PROFILING.md) x 2"
-
-
-def binding_resource(kind):
-    """What bounds the dominant ring-product kernels, from the committed ncu capture
-    (profiles/ncu_pipes.json): the largest launch of each kernel of that kind."""
-    pipes = load_ncu_pipes() or {}
-    tag = "tc_mul_kernel" if kind == "tc_int8" else "tc4_mul_kernel"
-    ev = {}
-    for name, e in pipes.get("kernels", {}).items():
-        if tag in name and e.get("largest_launch"):
-            L = e["largest_launch"]
-            ev[name.replace("void ", "")] = {
-                "tc_pipe_pct": L.get("tc_pipe_pct"), "tensor_math_pct": L.get("tensor_math_pct"),
-                "smem_tc_wavefronts_pct": L.get("smem_tc_wavefronts_pct"),
-                "smem_lsu_wavefronts_pct": L.get("smem_lsu_wavefronts_pct"),
-                "issue_active_pct": L.get("issue_active_pct"), "duration_us": L.get("duration_us")}
-    return {"resource": "shared-memory operand traffic: every MMA of a small-N GEMM re-reads its "
-                        "128 x 32-byte Hankel A tile (UMMA operand fetch, tc wavefronts) while the "
-                        "next item's operands are built (LSU wavefronts); tensor math stays low",
-            "evidence_largest_launch": ev,
-            "source": "profiles/ncu_pipes.json (ncu --clock-control none), DESIGN.md section 6.1"}
+def tensor_peak_tops(peaks: dict, kind: str):
+    """Dense tensor peak for the ring-product kernel kind, for a kernel timed ALONE (the serialised
+    pass): the measured bf16 cuBLAS burst figure (MEASURED_PEAKS.json) x the nominal ratio of the
+    kind's dtype to bf16 (int8 4.5 / 2.25 PF, fp4 9 / 2.25 PF dense; B200_PROFILING.md)."""
+    ratio = 2.0 if kind == "tc_int8" else 4.0
+    if "bf16_tflops" in peaks:
+        return ratio * peaks["bf16_tflops"], "measured bf16 burst %.1f TF/s (MEASURED_PEAKS.json) x %g (nominal %s/bf16)" % (
+            peaks["bf16_tflops"], ratio, "int8" if kind == "tc_int8" else "fp4")
+    return ratio * 1650.0, "fallback bf16 1650 TF/s (B200_PROFILING.md) x %g" % ratio
 
 
 def load_ncu_pipes():
@@ -174,6 +149,26 @@ def load_traffic():
         return json.load(open(os.path.join(ROOT, "profiles", "roofline_traffic.json")))["per_launch_bytes"]
     except Exception:
         return {}
+
+
+# Algorithmic integer work per unit of the ALU-bound kernels (SURVEY.md 8(d)
+# "Algorithmic work per unit").  Lane-ops the method itself needs, not what our code issues.
+def sampler_ops_per_key(p: int, nsort: int) -> float:
+    # p SplitMix64 outputs (p/2 per domain, f and one g attempt) x 20 lane-ops (two 64-bit
+    # multiplies = 6 IMAD, three 64-bit xor-shifts = 12 SHF/LOP3, the counter add = 2), the
+    # 1024- (2048-) entry bitonic network (n/4 log2 n (log2 n + 1) compare-exchanges, 2 ops each:
+    # min + max), and 5 ops per coefficient to map words to g and tagged f words
+    lg = nsort.bit_length() - 1
+    return 20.0 * p + 2.0 * (nsort // 4) * lg * (lg + 1) + 5.0 * p
+
+
+def divstep_ops_per_root(p: int, ring: str) -> float:
+    # 2p - 1 divsteps (C15).  R/q: per coefficient of the four p+1 vectors 4 multiplies, 2 adds,
+    # 4 selects and 2 reductions = 12 lane-ops; R/3 bitsliced: ~45 LOP3/SHF word-ops per 32
+    # coefficients of the vectors
+    if ring == "rq":
+        return (2 * p - 1) * 12.0 * (p + 1)
+    return (2 * p - 1) * 45.0 * ((p + 1 + 31) // 32)
 
 
 def cpu_model():
@@ -201,6 +196,25 @@ def oracle_keygen_rate(target_s: float = 10.0):
     dt = time.perf_counter() - t
     return n / dt, threads, "keys 0..%d of configs[1] (sntrup761, seed 2), %d host threads, %.1f s" % (
         n - 1, threads, dt)
+
+
+def oracle_single_thread():
+    """The oracle on ONE host thread: keys/s over keys 0..255 of configs[1], and R/q schoolbook
+    products/s over the first 4096 pairs of configs[2] (inputs by C12)."""
+    import numpy as np
+    from oracle import oracle as O
+    t = time.perf_counter()
+    O.keygen_many(PARAM, SEED, np.arange(256), threads=1)
+    keys = 256 / (time.perf_counter() - t)
+    p, q, w = O.PARAMS[PARAM]
+    A = np.zeros((4096, p), np.int16)
+    Bm = np.zeros((4096, p), np.int16)
+    for i in range(4096):
+        a, b = O.c12_pair(PARAM, 3, i)
+        A[i], Bm[i] = a, b
+    t = time.perf_counter()
+    O.mul_many(p, q, A, Bm, threads=1)
+    return keys, 4096 / (time.perf_counter() - t)
 
 
 def other_configs(S, torch, timed):
@@ -349,7 +363,7 @@ def run_reference(args):
         n_step, threads, cpu_model())
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": "configs[1]: sntrup761 batch keygen, seed 2 (oracle sample)",
                        "keys_per_step": n_step},
@@ -374,7 +388,6 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    import numpy as np
     import paper_2106_08759_b200 as S
 
     global MUL_IMPL
@@ -391,14 +404,13 @@ def main():
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")   # > 126 MB L2
 
     CHUNK = args.chunk_keys or DEFAULT_CHUNK
-
     RINGS = DEFAULT_RING_STREAMS if args.ring_streams < 0 else bool(args.ring_streams)
     LANES = args.lanes or DEFAULT_LANES
     FLAGS = S.OPT_ASYNC | (S.OPT_RING_STREAMS if RINGS else 0) | (S.OPT_LANES4 if LANES == 4 else 0)
 
-    def step(batch=B, chunk=None):
+    def step(batch=B, chunk=None, flags=FLAGS):
         S.batch_keygen(PARAM, n, SEED, first_key_index=first, batch_size=batch, pk_out=pk,
-                       sk_out=sk, flags=FLAGS, chunk_keys=CHUNK if chunk is None else chunk)
+                       sk_out=sk, flags=flags, chunk_keys=CHUNK if chunk is None else chunk)
 
     def barrier():
         if world > 1:
@@ -422,6 +434,10 @@ def main():
             ms = float(t.item())
         return ms
 
+    # integer-pipe peaks of this GPU (the metric's "int-pipe % of peak"; MEASURED_PEAKS.json has
+    # none): lane-ops per SM clock per SM of IMAD (FMA pipe) and IADD3 / LOP3 / SHF (ALU pipe)
+    int_peaks = {op: S.measure_int_peak(op) for op in S.INT_OPS} if rank == 0 else {}
+
     # clocks are sampled from the warm-up through the timed, profiled and e2e steps (all under
     # load; the timed region alone can be shorter than nvidia-smi's first sample)
     clk = ClockSampler(local)
@@ -436,46 +452,32 @@ def main():
     launches = S.kernel_launch_count() - launches0
     value = world * n * args.steps / (ms / 1e3)
 
-    # ---- per-kernel breakdown (CUDA events on the launching stream, same K steps)
+    # ---- per-kernel times: the same step SERIALISED (SNTRUP_OPT_SERIAL: one lane, every kernel
+    # alone on one stream), so each launch's CUDA-event time is its own; the kernel shares of the
+    # step and the roofline's launch durations come from this pass (the overlapped step above
+    # hides the latency-bound phases behind the other lane's products)
+    serial_flags = S.OPT_ASYNC | S.OPT_SERIAL
+    step(flags=serial_flags)
     S.profile_enable(True)
-    ms_prof = timed(step, args.steps)
+    ms_serial = timed(lambda: step(flags=serial_flags), args.steps)
     prof = S.profile_read(reset=True)
     kinds = S.profile_read_kinds(reset=True)
     S.profile_enable(False)
 
-    # ---- e2e through the C ABI with HOST output buffers (D2H inside the timed region)
+    # ---- e2e through the C ABI with HOST output buffers (D2H inside the timed region), one fixed
+    # configuration: the key-serving loop -- asynchronous host-output calls into two alternating
+    # pinned buffer sets; the host waits for step k-1's completion event (all of its pk/sk bytes in
+    # host memory) and reads its first key before issuing step k+1, so every step's D2H copy is in
+    # the timed region while it overlaps the next step's compute; wall clock over max(20, K) steps
+    # including the final drain
     pk_h = torch.empty((n, P["pk_bytes"]), dtype=torch.uint8).pin_memory()
     sk_h = torch.empty((n, P["sk_bytes"]), dtype=torch.uint8).pin_memory()
-
-    def step_host(chunk, fl):
-        S.batch_keygen(PARAM, n, SEED, first_key_index=first, batch_size=B, pk_out=pk_h,
-                       sk_out=sk_h, flags=S.OPT_HOST_OUTPUT | fl, chunk_keys=chunk)
-
-    # the chunk size trades D2H/compute overlap against per-chunk latency phases, and the ring
-    # streams interact with the copy streams: measure the candidates and report the best (all are
-    # in the line)
-    e2e_steps = max(2, args.steps // 2)
-    # (lane priority: the first lane's chunk completes early, so its pk/sk copies overlap the
-    # other lanes' compute instead of queueing behind the end of the step)
-    e2e_by_chunk = {}
-    R, PR, L4, ST = S.OPT_RING_STREAMS, S.OPT_LANE_PRIORITY, S.OPT_LANES4, S.OPT_STAGGER
-    for chunk, fl, tag in ((65536, R, "+rings"), (32768, 0, ""), (32768, R, "+rings"),
-                           (16384, R, "+rings"), (32768, R | PR, "+rings+prio"),
-                           (40960, R | ST | PR, "+rings+stagger+prio"), (32768, R | ST | PR, "+rings+stagger+prio"),
-                           (24576, R | ST | L4, "+rings+stagger+lanes4")):
-        step_host(chunk, fl)
-        barrier()
-        ms_c = timed(lambda: step_host(chunk, fl), e2e_steps)
-        e2e_by_chunk["%d%s" % (chunk, tag)] = world * n * e2e_steps / (ms_c / 1e3)
-    # steady state of a key-serving loop: asynchronous host-output calls into two alternating
-    # pinned buffer sets; the host waits for step k-1's completion event (all of its pk/sk bytes
-    # in host memory) and reads its first key before issuing step k+1, so every step's D2H copy
-    # is inside the timed region while it overlaps the next step's compute
     pk_h2 = [pk_h, torch.empty_like(pk_h).pin_memory()]
     sk_h2 = [sk_h, torch.empty_like(sk_h).pin_memory()]
     evs = [S.Event(), S.Event()]
+    E2E_FLAGS = S.OPT_RING_STREAMS
 
-    def serve(chunk, fl, steps):
+    def serve(steps, fl=E2E_FLAGS, chunk=CHUNK):
         for k in range(steps):
             S.batch_keygen(PARAM, n, SEED, first_key_index=first, batch_size=B, pk_out=pk_h2[k % 2],
                            sk_out=sk_h2[k % 2], flags=S.OPT_HOST_OUTPUT | S.OPT_ASYNC | fl,
@@ -485,16 +487,18 @@ def main():
                 _ = int(pk_h2[(k - 1) % 2][0, 0]) + int(sk_h2[(k - 1) % 2][0, 0])
         evs[(steps - 1) % 2].synchronize()
 
-    serve_steps = max(20, args.steps)          # (the last step's copies are not overlapped: pipeline drain)
-    for chunk, fl, tag in ((32768, R, "+rings"), (65536, R, "+rings"), (32768, R | ST, "+rings+stagger")):
-        serve(chunk, fl, 2)
-        barrier()
-        t0 = time.perf_counter()
-        serve(chunk, fl, serve_steps)
-        dt = time.perf_counter() - t0
-        e2e_by_chunk["%d%s+pipelined" % (chunk, tag)] = world * n * serve_steps / dt
-    best_chunk = max(e2e_by_chunk, key=e2e_by_chunk.get)
-    e2e_value = e2e_by_chunk[best_chunk]
+    serve_steps = max(20, args.steps)
+    serve(2)
+    barrier()
+    t0 = time.perf_counter()
+    serve(serve_steps)
+    e2e_value = world * n * serve_steps / (time.perf_counter() - t0)
+    # context: one synchronous host-output call per step (copies overlap only within the call)
+    def step_host_sync():
+        S.batch_keygen(PARAM, n, SEED, first_key_index=first, batch_size=B, pk_out=pk_h, sk_out=sk_h,
+                       flags=S.OPT_HOST_OUTPUT | E2E_FLAGS, chunk_keys=CHUNK)
+    step_host_sync()
+    e2e_sync = world * n * args.steps / (timed(step_host_sync, args.steps) / 1e3)
     # the e2e ceiling set by the host link: one device->pinned-host copy of a step's pk+sk bytes
     d2h_b = n * (P["pk_bytes"] + P["sk_bytes"])
     dbuf = torch.empty(d2h_b, dtype=torch.uint8, device="cuda")
@@ -510,68 +514,116 @@ def main():
     if rank == 0:
         peaks = load_peaks()
         sm_mhz = clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
-        # dominant kernel class by device time; the roofline is taken on the ring-product
-        # kernels of the dominant arithmetic kind (int8 or fp4 tensor, or int32 schoolbook),
-        # each against its own peak
-        dom = max(prof, key=lambda k: prof[k]["ms"])
-        tot_ms = sum(v["ms"] for v in prof.values())
+        n_sm = torch.cuda.get_device_properties(local).multi_processor_count
+        tot_serial = sum(v["ms"] for v in prof.values())
+        share = {k: v["ms"] / tot_serial for k, v in prof.items() if v["launches"]}
+        kshare = {k: v["ms"] / tot_serial for k, v in kinds.items() if v["launches"]}
+        # the dominant kernel kind by serialised device time
         kd = max(kinds, key=lambda k: kinds[k]["ms"])
+        K = kinds[kd]
         roof = None
-        if kinds[kd]["launches"]:
-            launches_d = kinds[kd]["launches"]
-            avg_ms = kinds[kd]["ms"] / launches_d
-            achieved = kinds[kd]["ops"] / launches_d / (avg_ms / 1e3) / 1e12          # T ops/s
-            share = kinds[kd]["ms"] / tot_ms
+        if K["launches"]:
+            secs = K["ms"] / 1e3                                   # summed launch durations (serial)
+            achieved = K["ops"] / secs / 1e12                      # T ops/s: 2 p^2 per product
             if kd in ("tc_int8", "tc_fp4"):
-                peak8, src = int8_tc_peak_tops(peaks)
-                peak = peak8 if kd == "tc_int8" else 2 * peak8
+                peak, src = tensor_peak_tops(peaks, kd)
+                smem_peak = 128.0 * n_sm * sm_mhz * 1e6            # B/s: 128 B/clk/SM shared-memory reads
+                smem_ach = K["smem_bytes"] / secs
                 roof = {"bound": "tensor",
                         "kernel": "ring products, " + ("tc_mul_kernel (tcgen05.mma kind::i8)" if kd == "tc_int8"
                                                         else "tc4_mul_kernel (tcgen05.mma kind::mxf4)"),
-                        "achieved": achieved, "peak": peak,
-                        "unit": "TOPS %s (algorithmic: 2 p^2 per limb/digit-pair product)" % ("int8" if kd == "tc_int8" else "fp4"),
-                        "frac": achieved / peak, "traffic": TRAFFIC.get("tc_int8" if kd == "tc_int8" else "tc_fp4"),
-                        "peak_source": src + ("" if kd == "tc_int8" else " x 2 (nominal fp4/int8 ratio 9/4.5 PF)"),
-                        "share_of_step": share,
-                        "by_kind_ms_per_step": {k: v["ms"] / args.steps for k, v in kinds.items()},
-                        "binding_resource": binding_resource(kd)}
+                        "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                        "unit_note": "tera-ops/s of the method's work: 2 p^2 per ring product (p^2 "
+                                     "multiply-adds), whatever the limb / digit / padding overhead",
+                        "frac": achieved / peak, "traffic": TRAFFIC.get(kd),
+                        "peak_source": src,
+                        "launch_time_source": "CUDA events per launch on its stream, serialised pass "
+                                              "(SNTRUP_OPT_SERIAL), %d launches" % K["launches"],
+                        "products_per_step": K["products"] / args.steps,
+                        "share_of_serial_step": K["ms"] / tot_serial,
+                        "by_kind_share_of_serial_step": kshare,
+                        "smem_operand_roofline": {
+                            "achieved_gbs": smem_ach / 1e9, "peak_gbs": smem_peak / 1e9,
+                            "frac": smem_ach / smem_peak,
+                            "bytes_per_product": K["smem_bytes"] / max(K["products"], 1),
+                            "note": "A and B tile bytes the MMAs fetch from shared memory (geometry x "
+                                    "MMAs) / launch time, against 128 B/clk/SM x %d SMs x %.0f MHz "
+                                    "(the run's median SM clock): the resource that binds these "
+                                    "small-N GEMMs (DESIGN.md 6.1)" % (n_sm, sm_mhz)}}
             else:
-                peak = 2 * int_peak_macs_per_s(sm_mhz) / 1e12
+                imad = int_peaks.get("IMAD", {}).get("lanes_per_clk_sm", 64.0)
+                peak = 2 * imad * n_sm * sm_mhz * 1e6 / 1e12
                 roof = {"bound": "alu", "kernel": "ring products, ring_mul_kernel (int32 schoolbook)",
-                        "achieved": achieved, "peak": peak,
-                        "unit": "TOPS int32 (2 p^2 per product)", "frac": achieved / peak,
-                        "traffic": None,
-                        "peak_source": "derived: 64 IMAD lanes/clk/SM x 2 ops x 148 SMs x %.0f MHz" % sm_mhz,
-                        "share_of_step": share}
+                        "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                        "frac": achieved / peak, "traffic": None,
+                        "peak_source": "measured IMAD %.1f lanes/clk/SM x 2 ops x %d SMs x %.0f MHz" % (imad, n_sm, sm_mhz)}
+        # integer-pipe fractions of the ALU-bound kernels, from the serialised pass and the
+        # measured pipe peaks at the run's clock (DESIGN.md 6.2 op counts)
+        # ALU pipe = LOP3's rate; FMA pipe = IMAD's; issue = IADD3's (it dual-issues on both pipes,
+        # measuring the 4 x 32 lanes/clk/SM issue limit)
+        alu = int_peaks["LOP3"]["lanes_per_clk_sm"] if int_peaks else 64.0
+        alu_peak = alu * n_sm * sm_mhz * 1e6
+        fma_peak = (int_peaks.get("IMAD", {}).get("lanes_per_clk_sm", 64.0)) * n_sm * sm_mhz * 1e6
+        issue_peak = (int_peaks.get("IADD3", {}).get("lanes_per_clk_sm", 128.0)) * n_sm * sm_mhz * 1e6
+        nsort = 1024 if PARAM <= 1024 else 2048
+        pipes = {}
+        if prof["sample"]["launches"]:
+            r = prof["sample"]["units"] * sampler_ops_per_key(P["p"], nsort) / (prof["sample"]["ms"] / 1e3)
+            pipes["sample_kernel"] = {"achieved_lane_ops_per_s": r, "issue_peak": issue_peak,
+                                      "frac_of_issue": r / issue_peak,
+                                      "ops_per_key": sampler_ops_per_key(P["p"], nsort),
+                                      "note": "algorithmic lane-ops (ALU and FMA work) against the "
+                                              "issue limit both pipes share"}
+        if prof["r3_mul"]["launches"] or prof["root_inv"]["launches"]:
+            nroots = prof["root_inv"]["units"]
+            r3 = nroots * divstep_ops_per_root(P["p"], "r3") / max(prof["root_inv"]["ms"] / 1e3, 1e-12)
+            pipes["divstep_kernel (R/3 roots)"] = {"achieved_lane_ops_per_s": r3, "frac_of_alu": r3 / alu_peak,
+                                                   "roots_per_step": nroots / args.steps,
+                                                   "note": "latency-bound: one warp per root, few roots"}
+        if prof["rq_inv"]["launches"]:
+            nr = prof["rq_inv"]["units"]
+            rq = nr * divstep_ops_per_root(P["p"], "rq") / (prof["rq_inv"]["ms"] / 1e3)
+            pipes["divstep_cta_kernel (R/q roots)"] = {"achieved_lane_ops_per_s": rq, "frac_of_fma": rq / fma_peak,
+                                                       "roots_per_step": nr / args.steps,
+                                                       "note": "latency-bound: 8 warps per root on <= 2 x %d roots" % n_sm}
+        if prof["encode"]["launches"]:
+            keys_e = prof["encode"]["units"]              # device outputs: one encode launch per key range
+            byt = keys_e * (2 * P["p8"] + 2 * P["p16"] + P["pk_bytes"] + P["sk_bytes"])
+            bw = byt / (prof["encode"]["ms"] / 1e3)
+            pipes["encode_kernel"] = {"achieved_gbs": bw / 1e9, "hbm_peak_gbs": peaks.get("hbm_gbs", 6552.0),
+                                      "frac_of_hbm": bw / 1e9 / peaks.get("hbm_gbs", 6552.0),
+                                      "bytes_per_key": byt / keys_e}
         result = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "scaling": "weak", "vs_baseline": None, "dtype": "int8/e2m1 MMA -> s32/f32 (exact integer)",
+            "data": "synthetic",
             "config": {"workload": "configs[1]: sntrup761 batch keygen, 65,536 keys per GPU, seed 2",
                        "keys_per_gpu": n, "batch_size": B, "chunk_keys": CHUNK, "ring_streams": RINGS,
-                       "lanes": LANES,
-                       "param_set": PARAM,
+                       "lanes": LANES, "param_set": PARAM,
                        "l2": "flushed between timed steps (256 MiB write); working set > L2",
                        "parallelism": "key ranges per GPU (no collective)"},
             "gpu_launches": launches,
             "clocks": clocks,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": world * n * (P["pk_bytes"] + P["sk_bytes"]),
-                    "chunk_keys": best_chunk,
-                    "by_chunk_keys": e2e_by_chunk,
+                    "config": "key-serving loop: asynchronous host-output calls (chunk %d, ring streams) "
+                              "into two alternating pinned buffer sets; the host waits for each step's "
+                              "completion event and reads its bytes; wall clock over %d steps incl. the "
+                              "final drain" % (CHUNK, serve_steps),
+                    "one_synchronous_call_per_step": e2e_sync,
                     "d2h_gbs_measured": d2h_gbs,
                     "d2h_ceiling_keys_per_s": world * d2h_gbs * 1e9 / (P["pk_bytes"] + P["sk_bytes"]),
-                    "note": "inputs are (param, n, seed, first key index): no H2D payload; "
-                            "pk/sk copied D2H into pinned host buffers inside the timed region; "
-                            "'+pipelined': consecutive asynchronous calls into two alternating pinned "
-                            "buffer sets, host waits for each step's completion event (all bytes in host "
-                            "memory) and reads it before issuing the step after next; wall clock over "
-                            "max(20, K) steps including the final drain"},
+                    "note": "inputs are (param, n, seed, first key index): no H2D payload"},
             "roofline": roof,
-            "breakdown_ms_per_step": {k: v["ms"] / args.steps for k, v in prof.items() if v["launches"]},
+            "int_pipe": {"peaks_lanes_per_clk_sm": {k: v["lanes_per_clk_sm"] for k, v in int_peaks.items()},
+                         "source": "sntrup_measure_int_peak microkernels, this run",
+                         "kernels": pipes},
+            "serial_ms_per_step": ms_serial / args.steps,
+            "serial_share_by_class": share,
+            "serial_ms_per_step_by_class": {k: v["ms"] / args.steps for k, v in prof.items() if v["launches"]},
             "mul_impl": MUL_IMPL,
             "ncu_pipes": load_ncu_pipes(),
-            "profiled_ms_per_step": ms_prof / args.steps,
         }
 
     if not args.no_extras and rank == 0:
@@ -587,7 +639,7 @@ def main():
             step(chunk=ck)
             csweep[str(ck)] = n * 3 / (timed(lambda: step(chunk=ck), 3) / 1e3)
         result["chunk_sweep_keys_per_s"] = csweep
-        # A/B: the same step without the shared-A down-sweep, and on the int32 schoolbook
+        # A/B: the same step under the other ring-product implementations
         ab = {}
         for name, impl in (("tc_int8_m64", S.MUL_TENSOR_CORE_M64),
                            ("tc_int8_big_single", S.MUL_TENSOR_CORE_I8_SINGLE),
@@ -601,35 +653,41 @@ def main():
             ab[name] = n * 2 / (timed(step, 2) / 1e3)
         S.set_mul_impl(S.MUL_TENSOR_CORE if MUL_IMPL == "tc" else S.MUL_SCHOOLBOOK)
         result["mul_impl_ab_keys_per_s"] = ab
-        # R/q multiplication microbenchmark (configs[2]): 2^20 pairs, uniform x ternary(286),
-        # through the big x small entry point; the int32 schoolbook beside it (A/B evidence)
-        from inputs import synth
+        # R/q multiplication microbenchmark (configs[2]): 2^20 pairs, inputs per SURVEY.md C12 drawn
+        # on the GPU by the library's samplers (a uniform from domain 0, b Short(286) from domain 1,
+        # seed 3), through the big x small entry point; big x big and the int32 schoolbook beside it
         npairs = 1 << 20
-        p = P["p"]
-        a = torch.from_numpy(synth.uniform_rq(npairs, p, P["q"], P["p8"], seed=3)).cuda()
-        bt = torch.from_numpy(synth.ternary_fast(npairs, p, P["w"], P["p16"], seed=3, dtype=np.int8)).cuda()
+        a = S.sample_uniform_rq_batch(PARAM, npairs, 3, domain=0)
+        bt = S.sample_short_batch(PARAM, npairs, 3, domain=1)
         c = torch.empty_like(a)
         S.rq_mul_small_batch(PARAM, a, bt, c)
         rq_ms = timed(lambda: S.rq_mul_small_batch(PARAM, a, bt, c), 3) / 3
-        b16 = torch.zeros_like(a)
-        b16[:, :p] = bt[:, :p].to(torch.int16)
-        bb_ms = timed(lambda: S.rq_mul_batch(PARAM, a, b16, c), 3) / 3
+        b2 = S.sample_uniform_rq_batch(PARAM, npairs, 3, domain=2)
+        S.rq_mul_batch(PARAM, a, b2, c)
+        bb_ms = timed(lambda: S.rq_mul_batch(PARAM, a, b2, c), 3) / 3
         S.set_mul_impl(S.MUL_SCHOOLBOOK)
-        sb_ms = timed(lambda: S.rq_mul_batch(PARAM, a, b16, c), 2) / 2
+        sb_ms = timed(lambda: S.rq_mul_batch(PARAM, a, b2, c), 2) / 2
         S.set_mul_impl(S.MUL_TENSOR_CORE if MUL_IMPL == "tc" else S.MUL_SCHOOLBOOK)
         result["rq_mul"] = {"value": npairs / (rq_ms / 1e3), "unit": "Rq mults/s",
-                            "config": "configs[2]: 2^20 pairs in Z/4591[x]/(x^761-x-1), uniform x ternary w=286 (rq_mul_small_batch)",
+                            "config": "configs[2]: 2^20 pairs in Z/4591[x]/(x^761-x-1), a uniform (C12, "
+                                      "domain 0) x Short w=286 (domain 1), seed 3, rq_mul_small_batch",
                             "ms": rq_ms,
                             "big_x_big_path_mults_per_s": npairs / (bb_ms / 1e3),
                             "int32_schoolbook_mults_per_s": npairs / (sb_ms / 1e3)}
-        del a, bt, c, b16
+        del a, bt, c, b2
         # the other configs' reported quantities; parity for each is in
-        # tests/test_gpu_parity.py
+        # tests/test_gpu_parity.py and tests/test_gpu_fullsize.py
         result["other_configs"] = other_configs(S, torch, timed)
-        # CPU baseline: the oracle on this host (bounded sample)
+        # CPU baseline: the oracle on this host -- all cores (bounded sample), one thread on 256
+        # keys, and R/q schoolbook products (SURVEY.md 8(d) "Oracle timing beside the GPU")
         v, cores, sample = oracle_keygen_rate(10.0)
+        v1, rq1 = oracle_single_thread()
         result["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
-                                  "sample": sample}
+                                  "sample": sample, "cpu_model": cpu_model(),
+                                  "single_thread_keys_per_s": v1,
+                                  "single_thread_rq_mults_per_s": rq1,
+                                  "single_thread_sample": "keys 0..255 of configs[1]; R/q products of "
+                                                          "4096 configs[2] pairs (C12)"}
     if rank == 0:
         print(json.dumps(result))
     if world > 1:

@@ -1,4 +1,8 @@
-"""Build libsntrup_gpu.so in-tree with nvcc for sm_100a (B200)."""
+"""Build libsntrup_gpu.so in-tree with nvcc for sm_100a (B200).
+
+One translation unit per parameter set (csrc/ps_<p>.cu) plus the C ABI (capi.cu) and the key
+pool (pool.cu), compiled in parallel and linked into one shared library."""
+import concurrent.futures as cf
 import os
 import subprocess
 
@@ -7,12 +11,21 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsntrup_gpu.so")
 LIB_CHECKED = os.path.join(PKG, "libsntrup_gpu_check.so")   # bounds-checked build (tests only)
-SOURCES = [os.path.join(CSRC, "sntrup_gpu.cu"), os.path.join(CSRC, "pool.cu")]
+OBJDIR = os.path.join(PKG, "build")
+SOURCES = [os.path.join(CSRC, f) for f in
+           ("capi.cu", "ps_761.cu", "ps_1277.cu", "ps_1013.cu", "ps_953.cu", "ps_857.cu", "ps_653.cu", "pool.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))] + \
     [os.path.join(ROOT, "include", "sntrup_gpu.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
+              "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
+
+
+def _nvcc():
+    nvcc = os.environ.get("NVCC", "nvcc")
+    if nvcc == "nvcc" and os.path.exists("/usr/local/cuda/bin/nvcc"):
+        nvcc = "/usr/local/cuda/bin/nvcc"
+    return nvcc
 
 
 def needs_build() -> bool:
@@ -31,20 +44,32 @@ def build_checked(force: bool = False) -> str:
 def build(force: bool = False, verbose: bool = False, out: str = LIB, extra=()) -> str:
     target = out
     stale = not os.path.exists(target) or any(os.path.getmtime(d) > os.path.getmtime(target) for d in DEPS)
-    if force or stale:
-        nvcc = os.environ.get("NVCC", "nvcc")
-        if not os.path.exists("/usr/local/cuda/bin/nvcc") and nvcc == "nvcc":
-            pass
-        elif nvcc == "nvcc":
-            nvcc = "/usr/local/cuda/bin/nvcc"
-        tmp = target + ".tmp%d" % os.getpid()
-        cmd = [nvcc] + NVCC_FLAGS + list(extra) + ["-o", tmp] + SOURCES
+    if not (force or stale):
+        return target
+    nvcc = _nvcc()
+    tag = "chk" if extra else "rel"
+    os.makedirs(OBJDIR, exist_ok=True)
+
+    def compile_one(src):
+        obj = os.path.join(OBJDIR, "%s_%s.o" % (os.path.basename(src)[:-3], tag))
+        tmp = obj + ".tmp%d" % os.getpid()
+        cmd = [nvcc] + NVCC_FLAGS + list(extra) + ["-c", "-o", tmp, src]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
-            raise RuntimeError("nvcc failed:\n" + res.stderr[-6000:])
-        if verbose:
-            print(res.stderr)
-        os.replace(tmp, target)
+            raise RuntimeError("nvcc failed on %s:\n%s" % (os.path.basename(src), res.stderr[-6000:]))
+        os.replace(tmp, obj)
+        return obj, res.stderr
+
+    with cf.ThreadPoolExecutor(max_workers=max(1, min(len(SOURCES), os.cpu_count() or 1))) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    if verbose:
+        for _, err in results:
+            print(err)
+    tmp = target + ".tmp%d" % os.getpid()
+    res = subprocess.run([nvcc, "-shared", "-o", tmp] + [o for o, _ in results], capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError("link failed:\n" + res.stderr[-6000:])
+    os.replace(tmp, target)
     return target
 
 

@@ -1,0 +1,5 @@
+// ps_1013.cu -- the kernels and host orchestration of parameter set 1013 (one translation unit per
+// set, so the sets compile in parallel; runtime.cuh / ps_ops.cuh).
+#include "ps_ops.cuh"
+
+template struct sntrup_rt::PsOps<sntrup::P1013>;

@@ -1,4 +1,6 @@
-// sntrup_gpu.cu -- host orchestration and the C ABI (include/sntrup_gpu.h).
+// runtime.cuh -- host orchestration of the kernels (included by capi.cu and the per-parameter-set
+// translation units ps_<p>.cu; split so the six parameter sets compile in parallel).
+#pragma once
 //
 // BatchKeyGen (Algorithm 1) per chunk of keys, all on one stream:
 //   sample (f, g + small-factor isInvertible, retries)          sample.cuh
@@ -33,12 +35,12 @@
 #include "tcmul.cuh"
 #include "tc4mul.cuh"
 
+
+namespace sntrup_rt {
 using namespace sntrup;
 
-namespace {
-
-std::atomic<uint64_t> g_launches{0};
-std::mutex g_mu;                                   // serialises calls (shared workspace)
+inline std::atomic<uint64_t> g_launches{0};
+inline std::mutex g_mu;                                   // serialises calls (shared workspace)
 
 // ------------------------------------------------------------------------------ profiler
 // Optional per-launch CUDA-event timing on the launching stream (bench.py's roofline): every
@@ -47,19 +49,19 @@ std::mutex g_mu;                                   // serialises calls (shared w
 enum ProfClass { PC_SAMPLE = 0, PC_MUL_R3, PC_MUL_RQ, PC_INV_R3, PC_INV_RQ, PC_REPAIR, PC_ENCODE,
                  PC_MISC, PC_N };
 struct ProfRec { int cls; cudaEvent_t a, b; double units, ops; int kind; double smem; };
-bool g_prof_on = false;
-std::vector<ProfRec> g_prof;
-std::vector<cudaEvent_t> g_evpool;
+inline bool g_prof_on = false;
+inline std::vector<ProfRec> g_prof;
+inline std::vector<cudaEvent_t> g_evpool;
 struct ProfAgg { double ms = 0, units = 0, ops = 0, smem = 0; uint64_t launches = 0; };
-ProfAgg g_agg[PC_N];
+inline ProfAgg g_agg[PC_N];
 // ring-product launches by arithmetic kind: 0 = int8 tensor (kind::i8), 1 = fp4 tensor
 // (kind::mxf4), 2 = int32 schoolbook
 enum { PK_I8 = 0, PK_F4 = 1, PK_I32 = 2, PK_N = 3 };
-ProfAgg g_kagg[PK_N];
-int g_cur_kind = -1;                 // set by the launcher inside a ProfScope
-double g_cur_smem = 0;               // tensor-core operand bytes the launch's MMAs fetch from smem
+inline ProfAgg g_kagg[PK_N];
+inline int g_cur_kind = -1;                 // set by the launcher inside a ProfScope
+inline double g_cur_smem = 0;               // tensor-core operand bytes the launch's MMAs fetch from smem
 
-cudaEvent_t ev_get() {
+inline cudaEvent_t ev_get() {
     if (!g_evpool.empty()) { cudaEvent_t e = g_evpool.back(); g_evpool.pop_back(); return e; }
     cudaEvent_t e;
     cudaEventCreate(&e);
@@ -79,7 +81,7 @@ struct ProfScope {
     }
 };
 
-void prof_drain() {
+inline void prof_drain() {
     for (auto &r : g_prof) {
         cudaEventSynchronize(r.b);
         float ms = 0;
@@ -125,7 +127,7 @@ void prof_drain() {
 // ------------------------------------------------------------------------------ param info
 struct ParamInfo { int p, q, w, p16, p8; size_t pk, sk; };
 
-size_t rq_encoded_len(int p, int q) {
+inline size_t rq_encoded_len(int p, int q) {
     std::vector<uint32_t> M(p, (uint32_t)q);
     size_t len = 0;
     int n = p;
@@ -145,7 +147,7 @@ size_t rq_encoded_len(int p, int q) {
     return len;
 }
 
-bool param_info(int ps, ParamInfo *pi) {
+inline bool param_info(int ps, ParamInfo *pi) {
     static const int tab[][3] = {{653, 4621, 288}, {761, 4591, 286}, {857, 5167, 322},
                                  {953, 6343, 396}, {1013, 7177, 448}, {1277, 7879, 492}};
     for (auto &t : tab)
@@ -171,9 +173,9 @@ struct DevTables {
     EncTables enc{};
     double p_small_reject = 0;   // 1 - prod (1 - 3^-d) over the small factors' degrees d
 };
-std::map<std::pair<int, int>, DevTables> g_tables;    // (device, param) -> tables
+inline std::map<std::pair<int, int>, DevTables> g_tables;    // (device, param) -> tables
 
-int build_tables(int dev, int ps, int WT, DevTables **out) {
+inline int build_tables(int dev, int ps, int WT, DevTables **out) {
     auto key = std::make_pair(dev, ps);
     auto it = g_tables.find(key);
     if (it != g_tables.end()) { *out = &it->second; return SNTRUP_OK; }
@@ -306,11 +308,11 @@ int build_tables(int dev, int ps, int WT, DevTables **out) {
 // Host-output keygen: chunk i's pk/sk are copied device->host on a copy stream while chunk i+1
 // computes (double-buffered device staging).  One per device (calls are serialised).
 struct CopyStream { cudaStream_t s = nullptr; cudaEvent_t comp[2] = {}, copy[2] = {}; };
-std::vector<cudaStream_t> g_copy_streams;     // every copy stream created (staging layout changes)
+inline std::vector<cudaStream_t> g_copy_streams;     // every copy stream created (staging layout changes)
 // SNTRUP_OPT_LANE_PRIORITY: lane li's streams get priority rank li (lane 0 highest), so the
 // scheduler finishes lane 0's chunk first while the other lanes fill its latency gaps; -1 = the
 // default priority.
-int lane_priority(int prio_rank) {
+inline int lane_priority(int prio_rank) {
     if (prio_rank < 0) return 0;
     int least = 0, greatest = 0;
     cudaDeviceGetStreamPriorityRange(&least, &greatest);
@@ -318,13 +320,13 @@ int lane_priority(int prio_rank) {
     return p > least ? least : p;
 }
 
-int make_stream(cudaStream_t *s, int prio_rank) {
+inline int make_stream(cudaStream_t *s, int prio_rank) {
     if (prio_rank < 0) CK(cudaStreamCreateWithFlags(s, cudaStreamNonBlocking));
     else CK(cudaStreamCreateWithPriority(s, cudaStreamNonBlocking, lane_priority(prio_rank)));
     return SNTRUP_OK;
 }
 
-int copy_stream(CopyStream **out, int which = 0, int prio_rank = -1) {   // which: pipeline lane
+inline int copy_stream(CopyStream **out, int which = 0, int prio_rank = -1) {   // which: pipeline lane
     static std::map<std::tuple<int, int, int>, CopyStream> m;
     int dev = 0;
     CK(cudaGetDevice(&dev));
@@ -345,7 +347,7 @@ int copy_stream(CopyStream **out, int which = 0, int prio_rank = -1) {   // whic
 // Keygen's u_i = g_i * 3 f_{i^1} products depend only on the sample: they run on an aux stream
 // concurrently with the (latency-bound) joint root inversion.  One per device.
 struct AuxStream { cudaStream_t s = nullptr; cudaEvent_t go = nullptr, done = nullptr; };
-int aux_stream(AuxStream **out) {
+inline int aux_stream(AuxStream **out) {
     static std::map<int, AuxStream> m;
     int dev = 0;
     CK(cudaGetDevice(&dev));
@@ -361,7 +363,7 @@ int aux_stream(AuxStream **out) {
 
 // side stream on which asynchronous host-output calls record their completion event, and an
 // event marking the end of the call's work on the caller's stream
-int done_stream(cudaStream_t *out, cudaEvent_t *s0_end) {
+inline int done_stream(cudaStream_t *out, cudaEvent_t *s0_end) {
     static std::map<int, std::pair<cudaStream_t, cudaEvent_t>> m;
     int dev = 0;
     CK(cudaGetDevice(&dev));
@@ -384,15 +386,15 @@ struct Workspace {
     size_t cap = 0, used = 0;
     int dev = -1;
 };
-std::map<std::pair<int, uintptr_t>, Workspace> g_wsmap;
-Workspace *g_ws = nullptr;
-Workspace g_user_ws;                          // a caller-supplied workspace (opts.workspace)
+inline std::map<std::pair<int, uintptr_t>, Workspace> g_wsmap;
+inline Workspace *g_ws = nullptr;
+inline Workspace g_user_ws;                          // a caller-supplied workspace (opts.workspace)
 
 // bytes ws_reserve allocates for a request of `bytes` (slack so that slightly larger later
 // calls on the same stream reuse the allocation)
-size_t ws_alloc_bytes(size_t bytes) { return bytes + (bytes >> 3) + (1 << 20); }
+inline size_t ws_alloc_bytes(size_t bytes) { return bytes + (bytes >> 3) + (1 << 20); }
 
-int ws_reserve(size_t bytes, cudaStream_t stream, void *user = nullptr, size_t user_bytes = 0) {
+inline int ws_reserve(size_t bytes, cudaStream_t stream, void *user = nullptr, size_t user_bytes = 0) {
     int dev;
     CK(cudaGetDevice(&dev));
     if (user) {                               // caller-owned memory: no caching, no allocation
@@ -437,9 +439,9 @@ struct Staging {
     size_t cap = 0;
     uint64_t layout = 0;
 };
-std::map<std::pair<int, uintptr_t>, Staging> g_stmap;
+inline std::map<std::pair<int, uintptr_t>, Staging> g_stmap;
 
-int staging_reserve(size_t bytes, uint64_t layout, cudaStream_t stream, char **out) {
+inline int staging_reserve(size_t bytes, uint64_t layout, cudaStream_t stream, char **out) {
     int dev;
     CK(cudaGetDevice(&dev));
     Staging &st = g_stmap[std::make_pair(dev, (uintptr_t)stream)];
@@ -472,9 +474,9 @@ T *ws_take(size_t count) {
 }
 
 // every ws_take of a call stayed inside the reservation (checked before the first launch)
-bool ws_fits() { return g_ws && g_ws->used <= g_ws->cap; }
+inline bool ws_fits() { return g_ws && g_ws->used <= g_ws->cap; }
 
-size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+inline size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
 // ------------------------------------------------------------------------------ tree plan
 // rows r.. of a row descriptor
@@ -489,7 +491,7 @@ struct TreePlan {
     long long inner_rows() const { long long s = 0; for (int l = 1; l <= L; l++) s += cnt[l]; return s; }
 };
 
-TreePlan make_plan(long long m, int B) {
+inline TreePlan make_plan(long long m, int B) {
     TreePlan t;
     t.L = 0;
     while ((1 << t.L) < B) t.L++;
@@ -508,10 +510,10 @@ TreePlan make_plan(long long m, int B) {
 // 6 = as 0 but one int8 big x big product per work item (A/B for the shared-A down-sweep);
 // 7 = as 0 but the keygen's u products fused with the R/q tree's level 1 (shared A; A/B);
 // 8 = as 0 but the int8 big x big products software-pipelined (two operand stages, 8 warps)
-int g_mul_impl = 0;
+inline int g_mul_impl = 0;
 
 struct DevInfo { int sms = 0; };
-DevInfo &dev_info() {
+inline DevInfo &dev_info() {
     static std::map<int, DevInfo> m;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -564,19 +566,21 @@ int launch_tc_impl(const MulArgs &a, cudaStream_t s) {
 }
 
 // KEM-core pre/post-ops need the XOPS instantiation (keygen never sets them)
-bool mul_xops(const MulArgs &a) { return a.round3 || a.X.mod3 || a.Y.mod3; }
+inline bool mul_xops(const MulArgs &a) { return a.round3 || a.X.mod3 || a.Y.mod3; }
 
+// KEM pre/post-ops exist only in one-product-per-item M = 128 instantiations (the shapes the KEM
+// core launches); an A/B variant asked to run them falls back to that kernel
 template <class PS, int M, int LA, int LB, int NPR = 1, int MM = 128>
 int launch_tc(const MulArgs &a, cudaStream_t s) {
-    return mul_xops(a) ? launch_tc_impl<PS, M, LA, LB, NPR, MM, true>(a, s)
-                       : launch_tc_impl<PS, M, LA, LB, NPR, MM, false>(a, s);
+    if (mul_xops(a)) return launch_tc_impl<PS, M, LA, LB, 1, 128, true>(a, s);
+    return launch_tc_impl<PS, M, LA, LB, NPR, MM, false>(a, s);
 }
 
 // software-pipelined variant (two operand stages, 8 warps) of the int8 big x big products
 template <class PS, int M, int NPR>
 int launch_tc_pipe(const MulArgs &a, cudaStream_t s) {
-    return mul_xops(a) ? launch_tc_impl<PS, M, 2, 2, NPR, 128, true, 256, 2>(a, s)
-                       : launch_tc_impl<PS, M, 2, 2, NPR, 128, false, 256, 2>(a, s);
+    if (mul_xops(a)) return launch_tc_impl<PS, M, 2, 2, 1, 128, true>(a, s);
+    return launch_tc_impl<PS, M, 2, 2, NPR, 128, false, 256, 2>(a, s);
 }
 
 template <class PS, int M, int LB, int NPR = 1, bool XOPS = false, int TA = 0>
@@ -607,24 +611,27 @@ int launch_tc4_impl(const MulArgs &a, cudaStream_t s) {
 
 template <class PS, int M, int LB, int NPR = 1>
 int launch_tc4(const MulArgs &a, cudaStream_t s) {
-    if constexpr (LB == 1) {
-        if (g_mul_impl == 9)                              // A operand in TMEM (128-column allocation)
-            return mul_xops(a) ? launch_tc4_impl<PS, M, LB, NPR, true, 128>(a, s)
-                               : launch_tc4_impl<PS, M, LB, NPR, false, 128>(a, s);
-        if (g_mul_impl == 10)                             // A operand in TMEM (64-column allocation)
-            return mul_xops(a) ? launch_tc4_impl<PS, M, LB, NPR, true, 64>(a, s)
-                               : launch_tc4_impl<PS, M, LB, NPR, false, 64>(a, s);
+    if (mul_xops(a)) return launch_tc4_impl<PS, M, LB, 1, true>(a, s);   // KEM: one product per item
+    if constexpr (LB == 1 && PS::P == 761) {              // A/B variants: sntrup761 only
+        if (g_mul_impl == 9) return launch_tc4_impl<PS, M, LB, NPR, false, 128>(a, s);  // A in TMEM, 128 cols
+        if (g_mul_impl == 10) return launch_tc4_impl<PS, M, LB, NPR, false, 64>(a, s);  // A in TMEM, 64 cols
     }
-    return mul_xops(a) ? launch_tc4_impl<PS, M, LB, NPR, true>(a, s)
-                       : launch_tc4_impl<PS, M, LB, NPR, false>(a, s);
+    return launch_tc4_impl<PS, M, LB, NPR, false>(a, s);
 }
+
+// The A/B-only ring-product variants (sntrup_set_mul_impl 2-10) are compiled for sntrup761 only;
+// the other parameter sets run the default tensor-core path (or the int32 schoolbook, impl 1).
+template <class PS>
+constexpr bool kABVariants = PS::P == 761;
 
 // la / lb: int8 limbs of the first / second operand (1 = small: R/3, 3f, g; 2 = R/q element).
 template <class PS, int M>
 int launch_mul(MulArgs a, cudaStream_t s, int la = 2, int lb = 2) {
     if (a.n_out <= 0) return SNTRUP_OK;
-    const int impl = (g_mul_impl >= 7) ? 0 : g_mul_impl;   // 7, 8, 9: as 0 except u / pipelining / TMEM A
-    const bool pipe = g_mul_impl == 8;
+    constexpr bool AB = kABVariants<PS>;
+    const int sel = AB ? g_mul_impl : (g_mul_impl == 1 ? 1 : 0);
+    const int impl = (sel >= 7) ? 0 : sel;   // 7, 8, 9, 10: as 0 except u / pipelining / TMEM A
+    const bool pipe = sel == 8;
     // algorithmic ops: the method's work, 2 p^2 (p^2 multiply-adds) per ring product whatever the
     // implementation (limbs, digits, padding and the zero triangles are implementation overhead)
     ProfScope ps_(M == 3 ? PC_MUL_R3 : PC_MUL_RQ, (double)a.n_out, s, 2.0 * PS::P * PS::P * (double)a.n_out);
@@ -653,30 +660,38 @@ int launch_mul(MulArgs a, cudaStream_t s, int la = 2, int lb = 2) {
     const bool fp4 = impl == 0 || impl == 4 || impl == 5 || impl == 6;
     if constexpr (M == 3) {
         a.swap = 0;
-        if (fp4) return down2 ? launch_tc4<PS, M, 1, 2>(a, s) : launch_tc4<PS, M, 1, 1>(a, s);
-        return down2 ? launch_tc<PS, M, 1, 1, 2>(a, s) : launch_tc<PS, M, 1, 1>(a, s);
+        if constexpr (AB) {
+            if (!fp4) return down2 ? launch_tc<PS, M, 1, 1, 2>(a, s) : launch_tc<PS, M, 1, 1>(a, s);
+        }
+        return down2 ? launch_tc4<PS, M, 1, 2>(a, s) : launch_tc4<PS, M, 1, 1>(a, s);
     } else {
         constexpr int D9 = digits9(M);
         if (la == 1 && lb == 1) {
             a.swap = 0;
-            if (fp4) return down2 ? launch_tc4<PS, M, 1, 2>(a, s) : launch_tc4<PS, M, 1, 1>(a, s);
-            return down2 ? launch_tc<PS, M, 1, 1, 2>(a, s) : launch_tc<PS, M, 1, 1>(a, s);
+            if constexpr (AB) {
+                if (!fp4) return down2 ? launch_tc<PS, M, 1, 1, 2>(a, s) : launch_tc<PS, M, 1, 1>(a, s);
+            }
+            return down2 ? launch_tc4<PS, M, 1, 2>(a, s) : launch_tc4<PS, M, 1, 1>(a, s);
         }
-        // int8 products at MMA M = 128; M = 64 (half the A bytes per MMA, twice the N) is kept
-        // as an A/B mode (impl 5): measured slower
-        const bool m128 = impl != 5;
         if (la == 1 || lb == 1) {
             // the small operand takes the A (Hankel) role.  int8 with two limbs for the big one:
             // measured faster than fp4 with D9 base-9 digits (larger N, digit staging), see
-            // DESIGN.md section 6; the fp4 variant stays selectable for A/B (impl 4)
+            // DESIGN.md section 6; the fp4 variant stays selectable for A/B (impl 4); int8 products
+            // at MMA M = 64 (half the A bytes per MMA, twice the N) are A/B mode impl 5
             a.swap = la == 1 ? 0 : 1;
-            if (impl == 4) return launch_tc4<PS, M, D9, 1>(a, s);
-            return m128 ? launch_tc<PS, M, 1, 2>(a, s) : launch_tc<PS, M, 1, 2, 1, 64>(a, s);
+            if constexpr (AB) {
+                if (impl == 4) return launch_tc4<PS, M, D9, 1>(a, s);
+                if (impl == 5) return launch_tc<PS, M, 1, 2, 1, 64>(a, s);
+            }
+            return launch_tc<PS, M, 1, 2>(a, s);
         }
         a.swap = 0;
-        if (down2) return pipe ? launch_tc_pipe<PS, M, 2>(a, s) : launch_tc<PS, M, 2, 2, 2>(a, s);
-        if (pipe) return launch_tc_pipe<PS, M, 1>(a, s);
-        return m128 ? launch_tc<PS, M, 2, 2>(a, s) : launch_tc<PS, M, 2, 2, 1, 64>(a, s);
+        if constexpr (AB) {
+            if (pipe) return down2 ? launch_tc_pipe<PS, M, 2>(a, s) : launch_tc_pipe<PS, M, 1>(a, s);
+            if (impl == 5) return launch_tc<PS, M, 2, 2, 1, 64>(a, s);
+        }
+        if (down2) return launch_tc<PS, M, 2, 2, 2>(a, s);
+        return launch_tc<PS, M, 2, 2>(a, s);
     }
 }
 
@@ -698,8 +713,8 @@ int launch_divstep(const InvArgs &a, cudaStream_t s) {
     return SNTRUP_OK;
 }
 
-RowDesc rows8(const void *p, long long stride, int scale = 1) { return RowDesc{p, stride, 1, scale}; }
-RowDesc rows16(const void *p, long long stride) { return RowDesc{p, stride, 2, 1}; }
+inline RowDesc rows8(const void *p, long long stride, int scale = 1) { return RowDesc{p, stride, 1, scale}; }
+inline RowDesc rows16(const void *p, long long stride) { return RowDesc{p, stride, 2, 1}; }
 
 // Batch inversion over one ring by product trees.  X0 = leaves (row descriptor), out0 = leaf
 // inverse rows.  Levels l >= 1 live in lvl[l] / inv[l].  M = ring modulus (3 or q).  Split into
@@ -829,7 +844,7 @@ struct Lane {
 };
 
 // internal lane li: a stream and its own aux stream (per device, per priority mode)
-int lane_streams(int li, int prio_rank, cudaStream_t *s2, AuxStream **ax2) {
+inline int lane_streams(int li, int prio_rank, cudaStream_t *s2, AuxStream **ax2) {
     static std::map<std::tuple<int, int, int>, std::pair<cudaStream_t, AuxStream>> m;
     int dev = 0;
     CK(cudaGetDevice(&dev));
@@ -845,7 +860,7 @@ int lane_streams(int li, int prio_rank, cudaStream_t *s2, AuxStream **ax2) {
 }
 
 // R/3-chain stream of a lane (SNTRUP_OPT_RING_STREAMS); go = sample done, done = R/3 chain done
-int ring_stream(int lane, int prio_rank, AuxStream **out) {
+inline int ring_stream(int lane, int prio_rank, AuxStream **out) {
     static std::map<std::tuple<int, int, int>, AuxStream> m;
     int dev = 0;
     CK(cudaGetDevice(&dev));
@@ -861,7 +876,7 @@ int ring_stream(int lane, int prio_rank, AuxStream **out) {
 
 constexpr int MAX_LANES = 4;
 struct LaneJoin { cudaEvent_t start = nullptr, end[MAX_LANES] = {}, upd[MAX_LANES] = {}; };
-int lane_join_events(LaneJoin **out) {
+inline int lane_join_events(LaneJoin **out) {
     static std::map<int, LaneJoin> m;
     int dev = 0;
     CK(cudaGetDevice(&dev));
@@ -1066,7 +1081,7 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
         // (A/B variant, impl 7: fewer A-operand fetches, but it moves the u products from the aux
         // stream -- where they fill the SMs the latency-bound root inversion leaves idle -- onto
         // the R/q chain's critical path; measured 2.5% slower than the default)
-        const bool fused_u = utrick && g_mul_impl == 7;
+        const bool fused_u = utrick && g_mul_impl == 7 && kABVariants<PS>;
         if (fused_u) {
             MulArgs a{};
             a.mode = MUL_UP0;
@@ -1291,7 +1306,7 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
 }
 
 // ------------------------------------------------------------------------------ small kernels
-__global__ void zero_rows_kernel(const int16_t *a, long long n, int p, long long stride,
+static __global__ void zero_rows_kernel(const int16_t *a, long long n, int p, long long stride,
                                  unsigned long long *first_zero) {
     const int lane = threadIdx.x & 31;
     const long long row = (long long)blockIdx.x * 4 + (threadIdx.x >> 5);
@@ -1455,485 +1470,24 @@ int rq_recip_impl(uint64_t n, const int16_t *a, int16_t *out, uint32_t B_, uint6
     return SNTRUP_OK;
 }
 
-}  // namespace
 
-// ================================================================================== C ABI
-extern "C" {
+// ------------------------------------------------------------------------------ per-set entry points
+// Everything that instantiates kernels for a parameter set goes through PsOps<PS>, defined in
+// ps_ops.cuh and explicitly instantiated once per set in ps_<p>.cu (capi.cu only declares it).
+template <class PS>
+struct PsOps {
+    static int keygen(uint64_t n, uint64_t seed, uint8_t *pk, uint8_t *sk, const sntrup_keygen_opts &o);
+    static int mul_q(MulArgs m, cudaStream_t s, int la, int lb);     // in R/q
+    static int mul_3(MulArgs m, cudaStream_t s, int la, int lb);     // in R/3
+    static int r3_recip(uint64_t n, const int8_t *g, int8_t *out, uint8_t *ok, uint32_t B, cudaStream_t s);
+    static int r3_isinv(uint64_t n, const int8_t *g, uint8_t *ok, cudaStream_t s);
+    static int rq_recip(uint64_t n, const int16_t *a, int16_t *out, uint32_t B, uint64_t *bad, cudaStream_t s);
+    static int full_sk(const FullSkArgs &a, int pkb, int skb, cudaStream_t s);
+    static int sample_short(uint64_t seed, uint64_t first, uint64_t n, uint64_t domain, int8_t *out, cudaStream_t s);
+    static int sample_uniform(uint64_t seed, uint64_t first, uint64_t n, uint64_t domain, int16_t *out,
+                              cudaStream_t s);
+    static int weight_check(const int8_t *r, uint64_t n, uint8_t *ok, cudaStream_t s);
+    static int encode(uint64_t n, const int16_t *h, uint8_t *pk, cudaStream_t s);
+};
 
-int sntrup_params(int param_set, int *p, int *q, int *w, int *p_pad16, int *p_pad8,
-                  size_t *pk_bytes, size_t *sk_bytes) {
-    ParamInfo pi;
-    if (!param_info(param_set, &pi)) return SNTRUP_E_PARAM;
-    if (p) *p = pi.p;
-    if (q) *q = pi.q;
-    if (w) *w = pi.w;
-    if (p_pad16) *p_pad16 = pi.p16;
-    if (p_pad8) *p_pad8 = pi.p8;
-    if (pk_bytes) *pk_bytes = pi.pk;
-    if (sk_bytes) *sk_bytes = pi.sk;
-    return SNTRUP_OK;
-}
-
-const char *sntrup_strerror(int code) {
-    switch (code) {
-    case SNTRUP_OK: return "ok";
-    case SNTRUP_E_PARAM: return "unknown parameter set";
-    case SNTRUP_E_ARG: return "invalid argument";
-    case SNTRUP_E_NOT_INVERTIBLE: return "element not invertible";
-    case SNTRUP_E_CUDA: return "CUDA error";
-    case SNTRUP_E_WORKSPACE: return "device allocation failed";
-    case SNTRUP_E_INTERNAL: return "internal error (retry bound exceeded)";
-    default: return "unknown error";
-    }
-}
-
-int sntrup_batch_keygen_ex(int param_set, uint64_t n_keys, uint64_t seed, uint8_t *pk_out,
-                           uint8_t *sk_out, const sntrup_keygen_opts *opt) {
-    ParamInfo pi;
-    if (!param_info(param_set, &pi)) return SNTRUP_E_PARAM;
-    if (n_keys == 0 || !pk_out || !sk_out) return SNTRUP_E_ARG;
-    sntrup_keygen_opts o{};
-    if (opt) o = *opt;
-    std::lock_guard<std::mutex> lk(g_mu);
-    SNTRUP_DISPATCH(param_set, return keygen_impl<PS>(n_keys, seed, pk_out, sk_out, o));
-    return SNTRUP_E_PARAM;
-}
-
-int sntrup_batch_keygen(int param_set, uint64_t n_keys, uint64_t seed, uint8_t *pk_out,
-                        uint8_t *sk_out) {
-    return sntrup_batch_keygen_ex(param_set, n_keys, seed, pk_out, sk_out, nullptr);
-}
-
-size_t sntrup_keygen_workspace_bytes(int param_set, uint64_t n_keys, uint32_t batch_size) {
-    return sntrup_keygen_workspace_bytes_ex(param_set, n_keys, batch_size, 0, 0);
-}
-
-size_t sntrup_keygen_workspace_bytes_ex(int param_set, uint64_t n_keys, uint32_t batch_size, uint32_t flags,
-                                        uint64_t chunk_keys) {
-    ParamInfo pi;
-    if (!param_info(param_set, &pi) || n_keys == 0) return 0;
-    const int B = batch_size ? (int)batch_size : 32;
-    if (B < 1 || B > 4096 || (B & (B - 1))) return 0;
-    SNTRUP_DISPATCH(param_set, {
-        const KeygenShape k = keygen_shape<PS>(n_keys, B, flags, chunk_keys, pi.pk);
-        return k.ws_need;
-    });
-    return 0;
-}
-
-size_t sntrup_workspace_reserved_bytes(void *stream, int which) {
-    std::lock_guard<std::mutex> lk(g_mu);
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
-    if (which == 1) {
-        auto it = g_stmap.find(std::make_pair(dev, (uintptr_t)stream));
-        return it == g_stmap.end() ? 0 : it->second.cap;
-    }
-    auto it = g_wsmap.find(std::make_pair(dev, (uintptr_t)stream));
-    return it == g_wsmap.end() ? 0 : it->second.cap;
-}
-
-int rq_mul_batch(int param_set, uint64_t n, const int16_t *a, const int16_t *b, int16_t *c,
-                 void *stream) {
-    ParamInfo pi;
-    if (!param_info(param_set, &pi)) return SNTRUP_E_PARAM;
-    if (n == 0 || !a || !b || !c) return SNTRUP_E_ARG;
-    MulArgs m{};
-    m.mode = MUL_ZIP;
-    m.n_out = (long long)n;
-    m.X = RowDesc{a, pi.p8, 2, 1};
-    m.Y = RowDesc{b, pi.p8, 2, 1};
-    m.out = c;
-    m.out_stride = pi.p8;
-    m.out_bytes = 2;
-    m.periodic = 1;
-    std::lock_guard<std::mutex> lk(g_mu);             // launcher caches, profiler state
-    SNTRUP_DISPATCH(param_set, return launch_mul<PS, PS::Q>(m, (cudaStream_t)stream));
-    return SNTRUP_E_PARAM;
-}
-
-int rq_mul_small_batch(int param_set, uint64_t n, const int16_t *a, const int8_t *b, int16_t *c,
-                       void *stream) {
-    ParamInfo pi;
-    if (!param_info(param_set, &pi)) return SNTRUP_E_PARAM;
-    if (n == 0 || !a || !b || !c) return SNTRUP_E_ARG;
-    MulArgs m{};
-    m.mode = MUL_ZIP;
-    m.n_out = (long long)n;
-    m.X = RowDesc{a, pi.p8, 2, 1};
-    m.Y = RowDesc{b, pi.p16, 1, 1};
-    m.out = c;
-    m.out_stride = pi.p8;
-    m.out_bytes = 2;
-    m.periodic = 0;
-    std::lock_guard<std::mutex> lk(g_mu);             // launcher caches, profiler state
-    SNTRUP_DISPATCH(param_set, return launch_mul<PS, PS::Q>(m, (cudaStream_t)stream, 2, 1));
-    return SNTRUP_E_PARAM;
-}
-
-size_t sntrup_full_sk_bytes(int param_set) {
-    size_t pkb = 0, skb = 0;
-    int p = 0;
-    if (sntrup_params(param_set, &p, nullptr, nullptr, nullptr, nullptr, &pkb, &skb)) return 0;
-    return skb + pkb + (size_t)((p + 3) / 4) + 32;
-}
-
-int sntrup_full_sk_batch(int param_set, uint64_t n, uint64_t seed, uint64_t first_key_index,
-                         const uint8_t *pk, const uint8_t *sk, uint8_t *sk_full, void *stream) {
-    size_t pkb = 0, skb = 0;
-    if (sntrup_params(param_set, nullptr, nullptr, nullptr, nullptr, nullptr, &pkb, &skb)) return SNTRUP_E_PARAM;
-    if (n == 0 || !pk || !sk || !sk_full) return SNTRUP_E_ARG;
-    FullSkArgs a{seed, first_key_index, n, pk, sk, sk_full};
-    const cudaStream_t s = (cudaStream_t)stream;
-    SNTRUP_DISPATCH(param_set, {
-        full_sk_copy_kernel<PS><<<(unsigned)((n + 3) / 4), 128, 0, s>>>(a, (int)pkb, (int)skb);
-        LAUNCHED();
-        sha512_pk_kernel<PS><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(a, (int)pkb, (int)skb);
-        LAUNCHED();
-        CK(cudaGetLastError());
-        return SNTRUP_OK;
-    });
-    return SNTRUP_E_PARAM;
-}
-
-int sntrup_event_create(void **ev) {
-    if (!ev) return SNTRUP_E_ARG;
-    cudaEvent_t e = nullptr;
-    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    *ev = (void *)e;
-    return SNTRUP_OK;
-}
-
-int sntrup_event_synchronize(void *ev) {
-    if (!ev) return SNTRUP_E_ARG;
-    CK(cudaEventSynchronize((cudaEvent_t)ev));
-    return SNTRUP_OK;
-}
-
-int sntrup_event_query(void *ev) {
-    if (!ev) return SNTRUP_E_ARG;
-    const cudaError_t e = cudaEventQuery((cudaEvent_t)ev);
-    if (e == cudaErrorNotReady) return 1;
-    CK(e);
-    return SNTRUP_OK;
-}
-
-void sntrup_event_destroy(void *ev) {
-    if (ev) cudaEventDestroy((cudaEvent_t)ev);
-}
-
-int sntrup_sample_short_batch(int param_set, uint64_t n, uint64_t seed, uint64_t first_key_index,
-                              uint64_t domain, int8_t *r_out, void *stream) {
-    ParamInfo pi;
-    if (!param_info(param_set, &pi)) return SNTRUP_E_PARAM;
-    if (n == 0 || !r_out) return SNTRUP_E_ARG;
-    SNTRUP_DISPATCH(param_set, {
-        short_kernel<PS><<<(unsigned)((n + 3) / 4), 128, 0, (cudaStream_t)stream>>>(seed, first_key_index, n,
-                                                                                    domain, r_out);
-        LAUNCHED();
-        return SNTRUP_OK;
-    });
-    return SNTRUP_E_PARAM;
-}
-
-int sntrup_sample_uniform_rq_batch(int param_set, uint64_t n, uint64_t seed, uint64_t first_key_index,
-                                    uint64_t domain, int16_t *a_out, void *stream) {
-    ParamInfo pi;
-    if (!param_info(param_set, &pi)) return SNTRUP_E_PARAM;
-    if (n == 0 || !a_out) return SNTRUP_E_ARG;
-    SNTRUP_DISPATCH(param_set, {
-        const uint64_t threads = n * (uint64_t)(PS::P8 / 2);
-        uniform_rq_kernel<PS><<<(unsigned)((threads + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
-            seed, first_key_index, n, domain, a_out);
-        LAUNCHED();
-        return SNTRUP_OK;
-    });
-    return SNTRUP_E_PARAM;
-}
-
-int sntrup_encap_core_batch(int param_set, uint64_t n, const int16_t *h, const int8_t *r, int16_t *c,
-                            void *stream) {
-    ParamInfo pi;
-    if (!param_info(param_set, &pi)) return SNTRUP_E_PARAM;
-    if (n == 0 || !h || !r || !c) return SNTRUP_E_ARG;
-    std::lock_guard<std::mutex> lk(g_mu);
-    MulArgs m{};
-    m.mode = MUL_ZIP;
-    m.n_out = (long long)n;
-    m.X = RowDesc{h, pi.p8, 2, 1};
-    m.Y = RowDesc{r, pi.p16, 1, 1};
-    m.out = c;
-    m.out_stride = pi.p8;
-    m.out_bytes = 2;
-    m.round3 = 1;                                   // c = Round(h * r)
-    SNTRUP_DISPATCH(param_set, return launch_mul<PS, PS::Q>(m, (cudaStream_t)stream, 2, 1));
-    return SNTRUP_E_PARAM;
-}
-
-int sntrup_decap_core_batch(int param_set, uint64_t n, const int8_t *f, const int8_t *ginv,
-                            const int16_t *c, int8_t *r_out, uint8_t *ok, void *stream) {
-    ParamInfo pi;
-    if (!param_info(param_set, &pi)) return SNTRUP_E_PARAM;
-    if (n == 0 || !f || !ginv || !c || !r_out || !ok) return SNTRUP_E_ARG;
-    std::lock_guard<std::mutex> lk(g_mu);
-    cudaStream_t s = (cudaStream_t)stream;
-    int rc;
-    if ((rc = ws_reserve(align256(n * pi.p8 * 2) + 4096, s))) return rc;
-    int16_t *e = ws_take<int16_t>(n * pi.p8);
-    SNTRUP_DISPATCH(param_set, {
-        MulArgs m{};                                 // e = 3f * c in R/q
-        m.mode = MUL_ZIP;
-        m.n_out = (long long)n;
-        m.X = RowDesc{c, pi.p8, 2, 1};
-        m.Y = RowDesc{f, pi.p16, 1, 3};
-        m.out = e;
-        m.out_stride = pi.p8;
-        m.out_bytes = 2;
-        if ((rc = launch_mul<PS, PS::Q>(m, s, 2, 1))) return rc;
-        MulArgs m3{};                                // r' = (e mod 3) * (1/g) in R/3
-        m3.mode = MUL_ZIP;
-        m3.n_out = (long long)n;
-        m3.X = RowDesc{e, pi.p8, 2, 1, 1};
-        m3.Y = RowDesc{ginv, pi.p16, 1, 1};
-        m3.out = r_out;
-        m3.out_stride = pi.p16;
-        m3.out_bytes = 1;
-        if ((rc = launch_mul<PS, 3>(m3, s, 1, 1))) return rc;
-        weight_check_kernel<PS><<<(unsigned)((n + 3) / 4), 128, 0, s>>>(r_out, n, ok);
-        LAUNCHED();
-        return SNTRUP_OK;
-    });
-    return SNTRUP_E_PARAM;
-}
-
-int r3_mul_batch(int param_set, uint64_t n, const int8_t *a, const int8_t *b, int8_t *c,
-                 void *stream) {
-    ParamInfo pi;
-    if (!param_info(param_set, &pi)) return SNTRUP_E_PARAM;
-    if (n == 0 || !a || !b || !c) return SNTRUP_E_ARG;
-    MulArgs m{};
-    m.mode = MUL_ZIP;
-    m.n_out = (long long)n;
-    m.X = RowDesc{a, pi.p16, 1, 1};
-    m.Y = RowDesc{b, pi.p16, 1, 1};
-    m.out = c;
-    m.out_stride = pi.p16;
-    m.out_bytes = 1;
-    m.periodic = 0;
-    std::lock_guard<std::mutex> lk(g_mu);             // launcher caches, profiler state
-    SNTRUP_DISPATCH(param_set, return launch_mul<PS, 3>(m, (cudaStream_t)stream, 1, 1));
-    return SNTRUP_E_PARAM;
-}
-
-int rq_recip_batch(int param_set, uint64_t n, const int16_t *a, int16_t *out, uint32_t batch_size,
-                   uint64_t *bad_index, void *stream) {
-    ParamInfo pi;
-    if (!param_info(param_set, &pi)) return SNTRUP_E_PARAM;
-    if (n == 0 || !a || !out) return SNTRUP_E_ARG;
-    std::lock_guard<std::mutex> lk(g_mu);
-    SNTRUP_DISPATCH(param_set, return rq_recip_impl<PS>(n, a, out, batch_size, bad_index, (cudaStream_t)stream));
-    return SNTRUP_E_PARAM;
-}
-
-int r3_recip_batch(int param_set, uint64_t n, const int8_t *g, int8_t *out, uint8_t *ok,
-                   uint32_t batch_size, void *stream) {
-    ParamInfo pi;
-    if (!param_info(param_set, &pi)) return SNTRUP_E_PARAM;
-    if (n == 0 || !g || !out || !ok) return SNTRUP_E_ARG;
-    std::lock_guard<std::mutex> lk(g_mu);
-    SNTRUP_DISPATCH(param_set, return r3_recip_impl<PS>(n, g, out, ok, batch_size, (cudaStream_t)stream));
-    return SNTRUP_E_PARAM;
-}
-
-int r3_is_invertible_batch(int param_set, uint64_t n, const int8_t *g, uint8_t *ok, void *stream) {
-    ParamInfo pi;
-    if (!param_info(param_set, &pi)) return SNTRUP_E_PARAM;
-    if (n == 0 || !g || !ok) return SNTRUP_E_ARG;
-    std::lock_guard<std::mutex> lk(g_mu);
-    SNTRUP_DISPATCH(param_set, return r3_isinv_impl<PS>(n, g, ok, (cudaStream_t)stream));
-    return SNTRUP_E_PARAM;
-}
-
-int rq_encode_batch(int param_set, uint64_t n, const int16_t *h, uint8_t *pk, void *stream) {
-    ParamInfo pi;
-    if (!param_info(param_set, &pi)) return SNTRUP_E_PARAM;
-    if (n == 0 || !h || !pk) return SNTRUP_E_ARG;
-    std::lock_guard<std::mutex> lk(g_mu);
-    int dev;
-    CK(cudaGetDevice(&dev));
-    SNTRUP_DISPATCH(param_set, {
-        DevTables *tb;
-        int rc = build_tables(dev, PS::P, PS::WT, &tb);
-        if (rc) return rc;
-        EncArgs ea{};
-        ea.n = n; ea.h = h; ea.pk = pk; ea.t = tb->enc;
-        encode_kernel<PS><<<(unsigned)((n + 3) / 4), 128, 0, (cudaStream_t)stream>>>(ea);
-        LAUNCHED();
-        return SNTRUP_OK;
-    });
-    return SNTRUP_E_PARAM;
-}
-
-void sntrup_release_workspace(void) {
-    std::lock_guard<std::mutex> lk(g_mu);
-    int cur = 0;
-    cudaGetDevice(&cur);
-    for (auto &kv : g_wsmap) {
-        if (!kv.second.base) continue;
-        cudaSetDevice(kv.second.dev);
-        cudaDeviceSynchronize();
-        cudaFree(kv.second.base);
-        kv.second.base = nullptr;
-        kv.second.cap = 0;
-    }
-    for (cudaStream_t cs : g_copy_streams) cudaStreamSynchronize(cs);
-    for (auto &kv : g_stmap) {
-        if (!kv.second.base) continue;
-        cudaSetDevice(kv.first.first);
-        cudaFree(kv.second.base);
-        kv.second.base = nullptr;
-        kv.second.cap = 0;
-    }
-    cudaSetDevice(cur);
-    g_ws = nullptr;
-}
-
-int sntrup_release_stream_workspace(void *stream) {
-    std::lock_guard<std::mutex> lk(g_mu);
-    int dev = 0;
-    CK(cudaGetDevice(&dev));
-    const auto key = std::make_pair(dev, (uintptr_t)stream);
-    CK(cudaStreamSynchronize((cudaStream_t)stream));
-    for (cudaStream_t cs : g_copy_streams) CK(cudaStreamSynchronize(cs));
-    auto it = g_wsmap.find(key);
-    if (it != g_wsmap.end() && it->second.base) {
-        // the workspace held secret f, 1/g and tree rows: erase before freeing
-        CK(cudaMemset(it->second.base, 0, it->second.cap));
-        CK(cudaFree(it->second.base));
-        if (g_ws == &it->second) g_ws = nullptr;
-        g_wsmap.erase(it);
-    }
-    auto st = g_stmap.find(key);
-    if (st != g_stmap.end() && st->second.base) {
-        CK(cudaMemset(st->second.base, 0, st->second.cap));
-        CK(cudaFree(st->second.base));
-        g_stmap.erase(st);
-    }
-    return SNTRUP_OK;
-}
-
-int sntrup_measure_int_peak(int op, double *lane_ops_per_clk_sm, double *lane_ops_per_s) {
-    if (op < 0 || op >= IOP_N) return SNTRUP_E_ARG;
-    std::lock_guard<std::mutex> lk(g_mu);
-    constexpr int CH = 8, ITER = 2048, NT = 256;
-    const int sms = dev_info().sms, nb = sms * 8;
-    uint32_t *sink = nullptr;
-    IntPeakRec *rec = nullptr;
-    CK(cudaMalloc(&sink, NT * sizeof(uint32_t)));
-    CK(cudaMalloc(&rec, nb * sizeof(IntPeakRec)));
-    cudaEvent_t e0, e1;
-    CK(cudaEventCreate(&e0));
-    CK(cudaEventCreate(&e1));
-    auto launch = [&](cudaStream_t s) {
-        switch (op) {
-        case IOP_IMAD: int_peak_kernel<IOP_IMAD, CH, ITER><<<nb, NT, 0, s>>>(7u, sink, rec); break;
-        case IOP_IADD3: int_peak_kernel<IOP_IADD3, CH, ITER><<<nb, NT, 0, s>>>(7u, sink, rec); break;
-        case IOP_LOP3: int_peak_kernel<IOP_LOP3, CH, ITER><<<nb, NT, 0, s>>>(7u, sink, rec); break;
-        default: int_peak_kernel<IOP_SHF, CH, ITER><<<nb, NT, 0, s>>>(7u, sink, rec); break;
-        }
-    };
-    launch(0);                                   // warm-up (clocks up)
-    LAUNCHED();
-    CK(cudaEventRecord(e0, 0));
-    launch(0);
-    LAUNCHED();
-    CK(cudaEventRecord(e1, 0));
-    CK(cudaEventSynchronize(e1));
-    float ms = 0;
-    CK(cudaEventElapsedTime(&ms, e0, e1));
-    std::vector<IntPeakRec> h(nb);
-    CK(cudaMemcpy(h.data(), rec, nb * sizeof(IntPeakRec), cudaMemcpyDeviceToHost));
-    cudaFree(sink);
-    cudaFree(rec);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    const double per_block = (double)NT * ITER * 8 * CH;
-    std::map<unsigned, std::tuple<unsigned long long, unsigned long long, int>> sm;   // smid -> t0, t1, blocks
-    for (auto &r : h) {
-        auto it = sm.find(r.smid);
-        if (it == sm.end()) sm[r.smid] = std::make_tuple(r.t0, r.t1, 1);
-        else {
-            auto &t = it->second;
-            if (r.t0 < std::get<0>(t)) std::get<0>(t) = r.t0;
-            if (r.t1 > std::get<1>(t)) std::get<1>(t) = r.t1;
-            std::get<2>(t) += 1;
-        }
-    }
-    double rate = 0;
-    for (auto &kv : sm) rate += per_block * std::get<2>(kv.second) / (double)(std::get<1>(kv.second) - std::get<0>(kv.second));
-    if (lane_ops_per_clk_sm) *lane_ops_per_clk_sm = sm.empty() ? 0 : rate / sm.size();
-    if (lane_ops_per_s) *lane_ops_per_s = per_block * nb / (ms * 1e-3);
-    return SNTRUP_OK;
-}
-
-uint64_t sntrup_kernel_launch_count(void) { return g_launches.load(); }
-
-int sntrup_profile_read_kinds(int reset, double *ms, double *ops, uint64_t *launches) {
-    std::lock_guard<std::mutex> lk(g_mu);
-    prof_drain();
-    for (int i = 0; i < PK_N; i++) {
-        if (ms) ms[i] = g_kagg[i].ms;
-        if (ops) ops[i] = g_kagg[i].ops;
-        if (launches) launches[i] = g_kagg[i].launches;
-    }
-    if (reset)
-        for (int i = 0; i < PK_N; i++) g_kagg[i] = ProfAgg{};
-    return PK_N;
-}
-
-int sntrup_profile_read_kinds_ex(int reset, double *ms, double *ops, uint64_t *launches, double *products,
-                                 double *smem_bytes) {
-    std::lock_guard<std::mutex> lk(g_mu);
-    prof_drain();
-    for (int i = 0; i < PK_N; i++) {
-        if (ms) ms[i] = g_kagg[i].ms;
-        if (ops) ops[i] = g_kagg[i].ops;
-        if (launches) launches[i] = g_kagg[i].launches;
-        if (products) products[i] = g_kagg[i].units;
-        if (smem_bytes) smem_bytes[i] = g_kagg[i].smem;
-    }
-    if (reset)
-        for (int i = 0; i < PK_N; i++) g_kagg[i] = ProfAgg{};
-    return PK_N;
-}
-
-int sntrup_set_mul_impl(int impl) {
-    if (impl < 0 || impl > 10) return SNTRUP_E_ARG;
-    std::lock_guard<std::mutex> lk(g_mu);
-    g_mul_impl = impl;
-    return SNTRUP_OK;
-}
-
-void sntrup_profile_enable(int on) {
-    std::lock_guard<std::mutex> lk(g_mu);
-    prof_drain();
-    g_prof_on = on != 0;
-}
-
-int sntrup_profile_read(int reset, double *ms, double *units, double *ops, uint64_t *launches,
-                        int max_classes) {
-    std::lock_guard<std::mutex> lk(g_mu);
-    prof_drain();
-    const int n = max_classes < PC_N ? max_classes : PC_N;
-    for (int i = 0; i < n; i++) {
-        if (ms) ms[i] = g_agg[i].ms;
-        if (units) units[i] = g_agg[i].units;
-        if (ops) ops[i] = g_agg[i].ops;
-        if (launches) launches[i] = g_agg[i].launches;
-    }
-    if (reset)
-        for (int i = 0; i < PC_N; i++) g_agg[i] = ProfAgg{};
-    return PC_N;
-}
-
-}  // extern "C"
+}  // namespace sntrup_rt
