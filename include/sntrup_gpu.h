@@ -258,6 +258,11 @@ int sntrup_release_stream_workspace(void *stream);
    whole GPU's lane-ops/s at the clock of this run (CUDA events).  Synchronous; device 0-stream. */
 int sntrup_measure_int_peak(int op, double *lane_ops_per_clk_sm, double *lane_ops_per_s);
 
+/* Role timing of the warp-specialised ring-product kernels: only in a build with
+   -DSNTRUP_WS_TRACE (scripts/ws_trace.py); returns the number of counters (160 SM slots x 16
+   roles' summed cycles) or 0 in a normal build.  The first call allocates the buffer. */
+int sntrup_ws_trace_read(int reset, uint64_t *out, int n);
+
 /* Number of kernels this library launched since load (device work only; for bench accounting). */
 uint64_t sntrup_kernel_launch_count(void);
 

@@ -438,6 +438,7 @@ MUL_TENSOR_CORE_U_FUSED = 7       # keygen u products fused with the R/q level 1
 MUL_TENSOR_CORE_PIPELINED = 8     # int8 big x big products software-pipelined (2 stages, 8 warps)
 MUL_TENSOR_CORE_TMEM_A = 9        # fp4 products: first K steps of the Hankel A operand in TMEM (128 cols)
 MUL_TENSOR_CORE_TMEM_A64 = 10     # as 9 with a 64-column TMEM allocation
+MUL_TENSOR_CORE_WS = 11           # warp-specialised persistent kernels, Hankel A written to TMEM
 
 
 def set_mul_impl(impl: int):

@@ -11,6 +11,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsntrup_gpu.so")
 LIB_CHECKED = os.path.join(PKG, "libsntrup_gpu_check.so")   # bounds-checked build (tests only)
+LIB_TRACE = os.path.join(PKG, "libsntrup_gpu_trace.so")     # role-timing build (scripts/ws_trace.py)
 OBJDIR = os.path.join(PKG, "build")
 SOURCES = [os.path.join(CSRC, f) for f in
            ("capi.cu", "ps_761.cu", "ps_1277.cu", "ps_1013.cu", "ps_953.cu", "ps_857.cu", "ps_653.cu", "pool.cu")]
@@ -41,13 +42,18 @@ def build_checked(force: bool = False) -> str:
     return build(force, out=LIB_CHECKED, extra=["-DSNTRUP_BOUNDS_CHECK"])
 
 
+def build_trace(force: bool = False) -> str:
+    """The library with the warp-specialised kernels' role timing compiled in (SNTRUP_WS_TRACE)."""
+    return build(force, out=LIB_TRACE, extra=["-DSNTRUP_WS_TRACE"])
+
+
 def build(force: bool = False, verbose: bool = False, out: str = LIB, extra=()) -> str:
     target = out
     stale = not os.path.exists(target) or any(os.path.getmtime(d) > os.path.getmtime(target) for d in DEPS)
     if not (force or stale):
         return target
     nvcc = _nvcc()
-    tag = "chk" if extra else "rel"
+    tag = {(): "rel", ("-DSNTRUP_BOUNDS_CHECK",): "chk"}.get(tuple(extra), "trc")
     os.makedirs(OBJDIR, exist_ok=True)
 
     def compile_one(src):

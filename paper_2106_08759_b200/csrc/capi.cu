@@ -402,6 +402,26 @@ int sntrup_measure_int_peak(int op, double *lane_ops_per_clk_sm, double *lane_op
     return SNTRUP_OK;
 }
 
+int sntrup_ws_trace_read(int reset, uint64_t *out, int n) {
+#ifdef SNTRUP_WS_TRACE
+    std::lock_guard<std::mutex> lk(g_mu);
+    constexpr size_t NB = 160 * 16 * sizeof(unsigned long long);
+    if (!g_ws_trace) {
+        CK(cudaMalloc(&g_ws_trace, NB));
+        CK(cudaMemset(g_ws_trace, 0, NB));
+    }
+    CK(cudaDeviceSynchronize());
+    static unsigned long long h[160 * 16];
+    CK(cudaMemcpy(h, g_ws_trace, NB, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < n && i < 160 * 16; i++) out[i] = h[i];
+    if (reset) CK(cudaMemset(g_ws_trace, 0, NB));
+    return 160 * 16;
+#else
+    (void)reset; (void)out; (void)n;
+    return 0;
+#endif
+}
+
 uint64_t sntrup_kernel_launch_count(void) { return g_launches.load(); }
 
 int sntrup_profile_read_kinds(int reset, double *ms, double *ops, uint64_t *launches) {
@@ -434,7 +454,7 @@ int sntrup_profile_read_kinds_ex(int reset, double *ms, double *ops, uint64_t *l
 }
 
 int sntrup_set_mul_impl(int impl) {
-    if (impl < 0 || impl > 10) return SNTRUP_E_ARG;
+    if (impl < 0 || impl > 11) return SNTRUP_E_ARG;
     std::lock_guard<std::mutex> lk(g_mu);
     g_mul_impl = impl;
     return SNTRUP_OK;

@@ -41,6 +41,7 @@ struct MulArgs {
     int round3;             // post-op: each output coefficient to the nearest multiple of 3
     void *out2;             // MUL_UP0: second product's output rows (stride out2_stride)
     long long out2_stride;
+    unsigned long long *trace;   // SNTRUP_WS_TRACE builds: role timing of the warp-specialised kernels
 };
 
 template <int NP>

@@ -34,6 +34,7 @@
 #include "sample.cuh"
 #include "tcmul.cuh"
 #include "tc4mul.cuh"
+#include "tc4w.cuh"
 
 
 namespace sntrup_rt {
@@ -511,6 +512,7 @@ inline TreePlan make_plan(long long m, int B) {
 // 7 = as 0 but the keygen's u products fused with the R/q tree's level 1 (shared A; A/B);
 // 8 = as 0 but the int8 big x big products software-pipelined (two operand stages, 8 warps)
 inline int g_mul_impl = 0;
+inline unsigned long long *g_ws_trace = nullptr;   // SNTRUP_WS_TRACE: device [160][16] role cycles
 
 struct DevInfo { int sms = 0; };
 inline DevInfo &dev_info() {
@@ -609,9 +611,38 @@ int launch_tc4_impl(const MulArgs &a, cudaStream_t s) {
     return SNTRUP_OK;
 }
 
+// warp-specialised fp4 products with the Hankel A operand in TMEM (tc4w.cuh): one persistent CTA
+// of 13 warps per SM
+template <class PS, int M, int NPR>
+int launch_tc4w(const MulArgs &a, cudaStream_t s) {
+    using W = Tc4wGeom<PS, NPR>;
+    auto kern = tc4w_mul_kernel<PS, M, NPR>;
+    static std::map<int, bool> init;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    if (!init[dev]) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, W::SMEM));
+        init[dev] = true;
+    }
+    long long grid = (long long)W::CTAS * dev_info().sms;            // CTAS resident per SM
+    if (grid > a.n_out) grid = a.n_out;
+    g_cur_kind = PK_F4;
+    g_cur_smem = (double)a.n_out * (double)W::G::NKS * W::G::NB * 32;   // B tiles only: A is in TMEM
+    MulArgs b = a;
+    b.trace = g_ws_trace;
+    kern<<<(unsigned)grid, W::THREADS, W::SMEM, s>>>(b);
+    LAUNCHED();
+    return SNTRUP_OK;
+}
+
 template <class PS, int M, int LB, int NPR = 1>
 int launch_tc4(const MulArgs &a, cudaStream_t s) {
     if (mul_xops(a)) return launch_tc4_impl<PS, M, LB, 1, true>(a, s);   // KEM: one product per item
+    if constexpr (LB == 1) {
+        // (int8 operand rows only: the kernel bulk-copies raw rows)
+        if (g_mul_impl == 11 && a.mode != MUL_UP0 && a.X.bytes == 1 && (a.Y.bytes == 1 || a.mode == MUL_PAIRS))
+            return launch_tc4w<PS, M, NPR>(a, s);
+    }
     if constexpr (LB == 1 && PS::P == 761) {              // A/B variants: sntrup761 only
         if (g_mul_impl == 9) return launch_tc4_impl<PS, M, LB, NPR, false, 128>(a, s);  // A in TMEM, 128 cols
         if (g_mul_impl == 10) return launch_tc4_impl<PS, M, LB, NPR, false, 64>(a, s);  // A in TMEM, 64 cols
@@ -630,7 +661,7 @@ int launch_mul(MulArgs a, cudaStream_t s, int la = 2, int lb = 2) {
     if (a.n_out <= 0) return SNTRUP_OK;
     constexpr bool AB = kABVariants<PS>;
     const int sel = AB ? g_mul_impl : (g_mul_impl == 1 ? 1 : 0);
-    const int impl = (sel >= 7) ? 0 : sel;   // 7, 8, 9, 10: as 0 except u / pipelining / TMEM A
+    const int impl = (sel >= 7) ? 0 : sel;   // 7-11: as 0 except u / pipelining / TMEM A
     const bool pipe = sel == 8;
     // algorithmic ops: the method's work, 2 p^2 (p^2 multiply-adds) per ring product whatever the
     // implementation (limbs, digits, padding and the zero triangles are implementation overhead)

@@ -143,6 +143,26 @@ __device__ __forceinline__ void umma_mxf4(uint32_t tmem_d, uint64_t adesc, uint6
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(tsf), "r"(tsf));
 }
 
+__device__ __forceinline__ void umma_mxf4_w(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate, uint32_t tsf) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(tsf), "r"(tsf));
+}
+
+__device__ __forceinline__ void umma_mxf4_ta_w(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t accumulate, uint32_t tsf) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], [%1], %2, %3, [%5], [%6], p;\n\t}\n" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(tsf), "r"(tsf));
+}
+
 // A operand in TMEM ([a-tmem] form; scripts/probe/tmem_a_probe.cu)
 __device__ __forceinline__ void umma_mxf4_ta(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
                                              uint32_t accumulate, uint32_t tsf) {
@@ -432,7 +452,7 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
         fence_async_smem();
         tc_fence_before();
         __syncthreads();
-        if (tid == 0) {
+        if (warp == 0) {                                  // one elected lane of a converged warp
             tc_fence_after();
             const uint64_t bd0 = umma_desc(smem_u32(sB), G::BLD * 16, 128);
             const uint64_t ad0 = umma_desc(smem_u32(sA) + 16, 512, 128);
@@ -440,10 +460,10 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
             for (int ks = 0; ks < G::NKS; ks++) {
                 const uint64_t bd = bd0 + (uint64_t)((ks * 32 * G::BLD) >> 4);
                 const uint64_t ad = ad0 + (uint64_t)((ks * 1024) >> 4);
-                if (ks < G::NTA) umma_mxf4_ta(tmem, tmem + G::ACOL + 8 * ks, bd, IDESC, ks > 0 ? 1u : 0u, tmem + G::SFCOL);
-                else umma_mxf4(tmem, ad, bd, IDESC, ks > 0 ? 1u : 0u, tmem + G::SFCOL);
+                if (ks < G::NTA) umma_mxf4_ta_w(tmem, tmem + G::ACOL + 8 * ks, bd, IDESC, ks > 0 ? 1u : 0u, tmem + G::SFCOL);
+                else umma_mxf4_w(tmem, ad, bd, IDESC, ks > 0 ? 1u : 0u, tmem + G::SFCOL);
             }
-            umma_commit(bar);
+            umma_commit_w(bar);
         }
         const TcWork<NPR> nxt = wn;
         int fnx[NPR];

@@ -70,6 +70,29 @@ __device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t adesc, uint64_
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
+// Warp-collective forms (_w): the whole warp calls them converged and one elected lane issues.
+// A tcgen05.mma issued by a lone thread of a diverged warp costs ~46 cycles of issue; from a
+// converged warp through elect.sync the MMAs stream at the tensor core's own rate (16.9 cycles
+// for M128 N32 K32 i8 = the 128 N / 256 floor; scripts/probe/mma_issue_probe.cu).
+__device__ __forceinline__ void umma_i8_w(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit_w(uint64_t *bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+
 __device__ __forceinline__ void umma_commit(uint64_t *bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                      smem_u32(bar))
@@ -538,7 +561,7 @@ __global__ void __launch_bounds__(NT, (ST == 1 ? TcGeom<PS, LA, LB, NPR, MM>::MI
         fence_async_smem();
     };
 
-    // ---- MMAs of stage b (one thread) into accumulator set b; descriptors advance by adding to
+    // ---- MMAs of stage b (warp 0, one elected lane) into accumulator set b; descriptors advance by adding to
     //      the start-address field
     auto issue = [&](int b) {
         tc_fence_after();
@@ -551,10 +574,10 @@ __global__ void __launch_bounds__(NT, (ST == 1 ? TcGeom<PS, LA, LB, NPR, MM>::MI
 #pragma unroll
             for (int l = 0; l < LA; l++) {
                 const uint64_t ad = ad0 + (uint64_t)((l * G::A_BYTES + ks * 512) >> 4);
-                umma_i8(acc + l * G::NB, ad, bd, IDESC, ks > 0 ? 1u : 0u);
+                umma_i8_w(acc + l * G::NB, ad, bd, IDESC, ks > 0 ? 1u : 0u);
             }
         }
-        umma_commit(bar + b);
+        umma_commit_w(bar + b);
     };
 
     // ---- epilogue of accumulator set b: thread = TMEM lane = coefficient r of every block;
@@ -641,7 +664,7 @@ __global__ void __launch_bounds__(NT, (ST == 1 ? TcGeom<PS, LA, LB, NPR, MM>::MI
             build(0);
             tc_fence_before();
             __syncthreads();
-            if (tid == 0) issue(0);
+            if (warp == 0) issue(0);
             prefetch(it + gridDim.x);
             if (tid == 0) mbar_wait(bar, phases & 1u);
             phases ^= 1u;
@@ -664,7 +687,7 @@ __global__ void __launch_bounds__(NT, (ST == 1 ? TcGeom<PS, LA, LB, NPR, MM>::MI
                 build(0);
                 tc_fence_before();
                 __syncthreads();                          // operands built; staging area free
-                if (tid == 0) issue(0);
+                if (warp == 0) issue(0);
                 const TcWork<NPR> nxt = wn;
                 int fnx[NPR];
 #pragma unroll
@@ -695,7 +718,7 @@ __global__ void __launch_bounds__(NT, (ST == 1 ? TcGeom<PS, LA, LB, NPR, MM>::MI
             build(0);
             tc_fence_before();
             __syncthreads();
-            if (tid == 0) issue(0);
+            if (warp == 0) issue(0);
             prefetch(it + gridDim.x);
             int b = 0;
             for (; it < a.n_out; it += gridDim.x) {
@@ -720,7 +743,7 @@ __global__ void __launch_bounds__(NT, (ST == 1 ? TcGeom<PS, LA, LB, NPR, MM>::MI
                 tc_fence_after();
                 // issue item nx's MMAs before this item's epilogue (thread 0 may block in the
                 // issue until the tensor pipe accepts them; the other warps go on)
-                if (tid == 0 && nx < a.n_out) issue(b ^ 1);
+                if (warp == 0 && nx < a.n_out) issue(b ^ 1);
                 epilogue(b, cur, fcur);
                 tc_fence_before();
                 cur = nxt;

@@ -48,8 +48,8 @@ def main():
     c3 = torch.empty_like(g)
     impls = {"tc": [S.MUL_TENSOR_CORE], "school": [S.MUL_SCHOOLBOOK]}.get(
         args.impl, [S.MUL_TENSOR_CORE, S.MUL_SCHOOLBOOK])
-    if args.impl.isdigit():
-        impls = [int(args.impl)]
+    if args.impl.replace(",", "").isdigit():
+        impls = [int(x) for x in args.impl.split(",")]
     for impl in impls:
         S.set_mul_impl(impl)
         name = {S.MUL_TENSOR_CORE: "tc", S.MUL_SCHOOLBOOK: "schoolbook"}.get(impl, "impl%d" % impl)
