@@ -1368,7 +1368,8 @@ __global__ void __launch_bounds__(128) r3_prepare_kernel(const int8_t *g, int8_t
 #pragma unroll
     for (int s = 0; s < NBL; s++) zero = zero && !(pl[s] | mi[s]);
     zero = __all_sync(FULL, zero);
-    const bool ok = !zero && small_factor_check<PS, NBL>(pl, mi, T, masks, nf, lane);
+    const bool sf = small_factor_check<PS, NBL>(pl, mi, T, masks, nf, lane);   // (always: constant time)
+    const bool ok = !zero && sf;
 #pragma unroll
     for (int s = 0; s < NBL; s++) {
         const int b = lane + 32 * s;
@@ -1456,7 +1457,10 @@ int r3_isinv_impl(uint64_t n, const int8_t *g, uint8_t *ok, cudaStream_t s) {
     }
     uint8_t *rok = ws_take<uint8_t>(tp.cnt[tp.L]);
     if (!ws_fits()) return SNTRUP_E_INTERNAL;
-    r3_prepare_kernel<PS><<<(unsigned)((n + 3) / 4), 128, 0, s>>>(g, gp, ok, (long long)n, tb->T, tb->masks, tb->nf);
+    {
+        ProfScope ps_(PC_MISC, (double)n, s);              // (timed separately: tests of constant time)
+        r3_prepare_kernel<PS><<<(unsigned)((n + 3) / 4), 128, 0, s>>>(g, gp, ok, (long long)n, tb->T, tb->masks, tb->nf);
+    }
     LAUNCHED();
     const TreeJob<PS, 3> j{tp, rows8(gp, PS::P16), scratch, 1, PS::P16, l3, i3, rok, false};
     uint64_t np = 0;

@@ -263,6 +263,9 @@ __device__ __forceinline__ void load_block_int8(const int8_t *row, int b, uint32
 // Small-factor residue test (warp).  T: [P][WT] uint2 rows (x^j mod f_i concatenated over the
 // small factors, bitsliced); masks: [nf][WT] words selecting each factor's trits.  Blocks are
 // distributed over lanes (block b on lane b % 32).  Returns true iff no small factor divides g.
+// Constant time in g (reading Z19: only the attempt count may vary): every coefficient
+// j < p adds T[j] selected by masks (+T[j] for g_j = 1, -T[j] for g_j = -1, 0 otherwise) -- the
+// trip counts and every load address depend only on p, never on g.
 template <class PS, int NBL>
 __device__ __forceinline__ bool small_factor_check(const uint32_t (&pl)[NBL], const uint32_t (&mi)[NBL],
                                                    const uint2 *__restrict__ T,
@@ -272,22 +275,20 @@ __device__ __forceinline__ bool small_factor_check(const uint32_t (&pl)[NBL], co
     uint32_t ap[WT], am[WT];
 #pragma unroll
     for (int w = 0; w < WT; w++) { ap[w] = 0; am[w] = 0; }
+    // lane L takes coefficients j = 32 c + L of every block c: the warp's T loads are coalesced
+    // (consecutive rows), and block c's two planes are broadcast from its lane by two shuffles
 #pragma unroll
-    for (int s = 0; s < NBL; s++) {
-        const int b = lane + 32 * s;
-        uint32_t bp = pl[s], bm = mi[s];
-        while (bp | bm) {
-            const uint32_t any = bp | bm;
-            const int c = __ffs(any) - 1;
-            const bool neg = (bm >> c) & 1u;
-            bm &= ~(1u << c);                                 // clear bit c in both planes
-            bp &= ~(1u << c);
-            const int j = 32 * b + c;
+    for (int c = 0; c < PS::NB32; c++) {
+        const uint32_t bp = __shfl_sync(FULL, pl[c >> 5], c & 31);
+        const uint32_t bm = __shfl_sync(FULL, mi[c >> 5], c & 31);
+        const int j = 32 * c + lane;
+        if (j < PS::P) {                                     // public: depends on p and the lane
+            const uint32_t mp = 0u - ((bp >> lane) & 1u), mm = 0u - ((bm >> lane) & 1u);
 #pragma unroll
             for (int w = 0; w < WT; w++) {
                 const uint2 t = __ldg(&T[(size_t)j * WT + w]);
-                if (neg) gf3_add(ap[w], am[w], t.y, t.x);
-                else gf3_add(ap[w], am[w], t.x, t.y);
+                // g_j T[j]: T[j] if g_j = 1, its negation (planes swapped) if g_j = -1, else 0
+                gf3_add(ap[w], am[w], (t.x & mp) | (t.y & mm), (t.y & mp) | (t.x & mm));
             }
         }
     }
@@ -299,14 +300,15 @@ __device__ __forceinline__ bool small_factor_check(const uint32_t (&pl)[NBL], co
             const uint32_t om = __shfl_xor_sync(FULL, am[w], off);
             gf3_add(ap[w], am[w], op, om);
         }
-    bool ok = true;
+    // every factor's verdict computed (no early exit), combined without branches
+    uint32_t all_ok = 1u;
     for (int f = 0; f < nf; f++) {
         uint32_t nz = 0;
 #pragma unroll
         for (int w = 0; w < WT; w++) nz |= (ap[w] | am[w]) & masks[f * WT + w];
-        ok = ok && (nz != 0);
+        all_ok &= (uint32_t)(nz != 0);
     }
-    return ok;
+    return all_ok != 0;
 }
 
 // ---------------------------------------------------------------------------------------------

@@ -118,3 +118,30 @@ def test_binding_rejects_short_outputs():
     ref = S.batch_keygen(761, 4, 1)
     torch.cuda.synchronize()
     assert torch.equal(r["pk"], ref["pk"].cpu())
+
+
+@pytest.mark.parametrize("param", [1013, 1277])
+def test_small_factor_check_is_constant_time(param):
+    # ADVICE r1 / DESIGN.md Z19: the small-factor residue test (isInvertible for factors of degree
+    # <= 64) must not depend on g -- every coefficient's residue row is loaded and added under
+    # masks.  Time the kernel that runs it (r3_is_invertible_batch's prepare step, profiler class
+    # "other") on very sparse and on dense inputs of equal shape: a weight-dependent loop would run
+    # ~50x longer on the dense rows.
+    P = S.params(param)
+    p, n = P["p"], 1 << 16
+    dense = torch.from_numpy(synth.small(n, p, P["p16"], seed=3)).cuda()
+    sparse = torch.zeros_like(dense)
+    sparse[:, 0] = 1
+    sparse[:, 5] = -1
+    times = {}
+    for name, g in (("sparse", sparse), ("dense", dense), ("sparse2", sparse), ("dense2", dense)):
+        S.r3_is_invertible_batch(param, g)               # warm
+        torch.cuda.synchronize()
+        S.profile_enable(True)
+        for _ in range(3):
+            S.r3_is_invertible_batch(param, g)
+        prof = S.profile_read(reset=True)
+        S.profile_enable(False)
+        times[name] = prof["other"]["ms"] / 3
+    ts, td = min(times["sparse"], times["sparse2"]), min(times["dense"], times["dense2"])
+    assert abs(td - ts) <= 0.15 * max(td, ts), times
