@@ -251,6 +251,12 @@ void sntrup_release_workspace(void);
    f, 1/g and tree rows).  SNTRUP_OK or SNTRUP_E_CUDA. */
 int sntrup_release_stream_workspace(void *stream);
 
+/* Measurement hook: n ring products at p' = 383 --
+   one sub-product of a one-level Karatsuba split of a 761 product -- through the same tensor-core
+   kernels as the 761 products.  kind 0: R/3 (int8 rows of 384, fp4 MMAs); kind 1: R/q big x big
+   mod 4591 (int16 rows of 384, int8 2 x 2 limbs).  Device pointers; stream-ordered. */
+int sntrup_probe_half_mul(int kind, uint64_t n, const void *a, const void *b, void *c, void *stream);
+
 /* Integer-pipe peak (measurement for bench.py's roofline; BASELINE metric "int-pipe % of peak"):
    op 0 = IMAD (FMA pipe), 1 = IADD3, 2 = LOP3, 3 = SHF (ALU pipe).  A full-occupancy kernel of 8
    independent chains per thread of that one instruction; *lane_ops_per_clk_sm = lane-ops per SM

@@ -85,6 +85,7 @@ _lib.sntrup_profile_read_kinds.argtypes = [_i32, _vp, _vp, _vp]
 _lib.sntrup_profile_read_kinds_ex.restype = _i32
 _lib.sntrup_profile_read_kinds_ex.argtypes = [_i32, _vp, _vp, _vp, _vp, _vp]
 _lib.sntrup_measure_int_peak.argtypes = [_i32, _vp, _vp]
+_lib.sntrup_probe_half_mul.argtypes = [_i32, _u64, _vp, _vp, _vp, _vp]
 _lib.sntrup_pool_create.argtypes = [_i32, _u64, _u64, _u64, _u64, _u32, ctypes.POINTER(_vp)]
 _lib.sntrup_pool_take.argtypes = [_vp, _vp, _vp, ctypes.POINTER(ctypes.c_uint64)]
 _lib.sntrup_pool_stats.argtypes = [_vp] + [ctypes.POINTER(ctypes.c_uint64)] * 4
@@ -110,7 +111,7 @@ EXPORTED = ("sntrup_params", "sntrup_strerror", "sntrup_batch_keygen", "sntrup_b
             "r3_recip_batch", "r3_is_invertible_batch", "rq_encode_batch",
             "sntrup_release_workspace", "sntrup_release_stream_workspace", "sntrup_kernel_launch_count", "sntrup_set_mul_impl",
             "sntrup_profile_enable", "sntrup_profile_read_kinds", "sntrup_profile_read_kinds_ex",
-            "sntrup_measure_int_peak", "sntrup_pool_create",
+            "sntrup_measure_int_peak", "sntrup_probe_half_mul", "sntrup_pool_create",
             "sntrup_pool_take", "sntrup_pool_stats", "sntrup_pool_destroy",
             "sntrup_sample_short_batch", "sntrup_sample_uniform_rq_batch", "sntrup_encap_core_batch", "sntrup_decap_core_batch",
             "sntrup_profile_read", "sntrup_full_sk_bytes", "sntrup_full_sk_batch",
@@ -502,6 +503,17 @@ def profile_read_kinds(reset: bool = True) -> dict:
 
 
 INT_OPS = ("IMAD", "IADD3", "LOP3", "SHF")
+
+
+def probe_half_mul(kind: int, a, b, c, stream=None):
+    """Measurement hook: ring products at p' = 383 (one Karatsuba sub-product of a 761 product);
+    kind 0 = R/3 (int8 [n][384]), 1 = R/q big x big (int16 [n][384])."""
+    n = a.shape[0]
+    dt, w = (torch.int8, 384) if kind == 0 else (torch.int16, 384)
+    for t, nm in ((a, "a"), (b, "b"), (c, "c")):
+        _need(t, dt, (n, w), nm)
+    _check(_lib.sntrup_probe_half_mul(kind, n, _ptr(a), _ptr(b), _ptr(c), _stream(stream)), "sntrup_probe_half_mul")
+    return c
 
 
 def measure_int_peak(op: str) -> dict:

@@ -14,7 +14,8 @@ LIB_CHECKED = os.path.join(PKG, "libsntrup_gpu_check.so")   # bounds-checked bui
 LIB_TRACE = os.path.join(PKG, "libsntrup_gpu_trace.so")     # role-timing build (scripts/ws_trace.py)
 OBJDIR = os.path.join(PKG, "build")
 SOURCES = [os.path.join(CSRC, f) for f in
-           ("capi.cu", "ps_761.cu", "ps_1277.cu", "ps_1013.cu", "ps_953.cu", "ps_857.cu", "ps_653.cu", "pool.cu")]
+           ("capi.cu", "ps_761.cu", "ps_1277.cu", "ps_1013.cu", "ps_953.cu", "ps_857.cu", "ps_653.cu", "pool.cu",
+            "probe_split.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))] + \
     [os.path.join(ROOT, "include", "sntrup_gpu.h")]
 
