@@ -288,8 +288,12 @@ uint64_t sntrup_kernel_launch_count(void);
        (two operand stages: item k+1 built and issued before item k's epilogue);
    9 = as 0, with the first K steps of the fp4 products' Hankel A operand written to TMEM
        (tcgen05.st) and read by the MMAs from there instead of from shared memory (128-column
-       TMEM allocation per CTA); 10 = as 9 with 64 columns (fewer K steps in TMEM, more CTAs).
-   All are exact.  Returns SNTRUP_OK or SNTRUP_E_ARG. */
+       TMEM allocation per CTA); 10 = as 9 with 64 columns (fewer K steps in TMEM, more CTAs);
+   11 = as 0, with the small x small (fp4) products on the warp-specialised persistent kernel
+       whose Hankel A operand is built in registers and written to TMEM (csrc/tc4w.cuh).
+   All are exact.  Variants 2-10 are compiled for sntrup761 only (other sets run 0, or 1 / 11);
+   KEM pre/post-op calls always use the default kernel of their shape.  Returns SNTRUP_OK or
+   SNTRUP_E_ARG. */
 int sntrup_set_mul_impl(int impl);
 
 /* Measurement hooks (bench.py).  When enabled, every kernel launch is bracketed by CUDA events
