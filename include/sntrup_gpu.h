@@ -296,6 +296,10 @@ uint64_t sntrup_kernel_launch_count(void);
    SNTRUP_E_ARG. */
 int sntrup_set_mul_impl(int impl);
 
+/* A/B knob (measurement): threads per CTA of the R/q root inversion (one CTA per root, used when
+   the roots are few): 128, 256 (default), 512 or 768; sntrup761 only.  SNTRUP_OK / SNTRUP_E_ARG. */
+int sntrup_set_divstep_threads(int nt);
+
 /* Measurement hooks (bench.py).  When enabled, every kernel launch is bracketed by CUDA events
    recorded on its launching stream.  sntrup_profile_read() waits for the recorded events and
    returns, per kernel class, the summed device milliseconds, the summed work units, the summed

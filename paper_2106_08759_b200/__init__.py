@@ -76,6 +76,7 @@ _lib.sntrup_release_workspace.restype = None
 _lib.sntrup_release_stream_workspace.argtypes = [_vp]
 _lib.sntrup_kernel_launch_count.restype = _u64
 _lib.sntrup_set_mul_impl.argtypes = [_i32]
+_lib.sntrup_set_divstep_threads.argtypes = [_i32]
 _lib.sntrup_profile_enable.restype = None
 _lib.sntrup_profile_enable.argtypes = [_i32]
 _lib.sntrup_profile_read.restype = _i32
@@ -109,7 +110,7 @@ EXPORTED = ("sntrup_params", "sntrup_strerror", "sntrup_batch_keygen", "sntrup_b
             "sntrup_keygen_workspace_bytes", "sntrup_keygen_workspace_bytes_ex",
             "sntrup_workspace_reserved_bytes", "rq_mul_batch", "rq_mul_small_batch", "r3_mul_batch", "rq_recip_batch",
             "r3_recip_batch", "r3_is_invertible_batch", "rq_encode_batch",
-            "sntrup_release_workspace", "sntrup_release_stream_workspace", "sntrup_kernel_launch_count", "sntrup_set_mul_impl",
+            "sntrup_release_workspace", "sntrup_release_stream_workspace", "sntrup_kernel_launch_count", "sntrup_set_mul_impl", "sntrup_set_divstep_threads",
             "sntrup_profile_enable", "sntrup_profile_read_kinds", "sntrup_profile_read_kinds_ex",
             "sntrup_measure_int_peak", "sntrup_probe_half_mul", "sntrup_pool_create",
             "sntrup_pool_take", "sntrup_pool_stats", "sntrup_pool_destroy",

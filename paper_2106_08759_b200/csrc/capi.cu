@@ -453,6 +453,13 @@ int sntrup_profile_read_kinds_ex(int reset, double *ms, double *ops, uint64_t *l
     return PK_N;
 }
 
+int sntrup_set_divstep_threads(int nt) {
+    if (nt != 128 && nt != 256 && nt != 512 && nt != 768) return SNTRUP_E_ARG;
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_divstep_threads = nt;
+    return SNTRUP_OK;
+}
+
 int sntrup_set_mul_impl(int impl) {
     if (impl < 0 || impl > 11) return SNTRUP_E_ARG;
     std::lock_guard<std::mutex> lk(g_mu);

@@ -512,6 +512,7 @@ inline TreePlan make_plan(long long m, int B) {
 // 7 = as 0 but the keygen's u products fused with the R/q tree's level 1 (shared A; A/B);
 // 8 = as 0 but the int8 big x big products software-pipelined (two operand stages, 8 warps)
 inline int g_mul_impl = 0;
+inline int g_divstep_threads = 256;                // R/q root CTA size (A/B knob; sntrup761 only)
 inline unsigned long long *g_ws_trace = nullptr;   // SNTRUP_WS_TRACE: device [160][16] role cycles
 
 struct DevInfo { int sms = 0; };
@@ -736,7 +737,17 @@ int launch_divstep(const InvArgs &a, cudaStream_t s) {
         // few roots: latency bound -> one CTA of 8 warps per root; many roots: throughput bound
         // -> one warp per root (less per-step overhead in total)
         if (a.n < 2LL * dev_info().sms)
-            divstep_cta_kernel<PS, M, 256><<<(unsigned)a.n, 256, 0, s>>>(a);
+        {
+            // threads per root (A/B knob, sntrup_set_divstep_threads; default 256 = 8 warps)
+            if constexpr (PS::P == 761) {
+                if (g_divstep_threads == 128) { divstep_cta_kernel<PS, M, 128><<<(unsigned)a.n, 128, 0, s>>>(a); }
+                else if (g_divstep_threads == 512) { divstep_cta_kernel<PS, M, 512><<<(unsigned)a.n, 512, 0, s>>>(a); }
+                else if (g_divstep_threads == 768) { divstep_cta_kernel<PS, M, 768><<<(unsigned)a.n, 768, 0, s>>>(a); }
+                else divstep_cta_kernel<PS, M, 256><<<(unsigned)a.n, 256, 0, s>>>(a);
+            } else {
+                divstep_cta_kernel<PS, M, 256><<<(unsigned)a.n, 256, 0, s>>>(a);
+            }
+        }
         else
             divstep_kernel<PS, M><<<(unsigned)((a.n + 3) / 4), 128, 0, s>>>(a);
     }

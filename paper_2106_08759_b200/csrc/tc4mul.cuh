@@ -72,7 +72,10 @@ struct Tc4Geom {
     static constexpr int NT = (P + 127) / 128;                // output blocks (folded B, tcmul.cuh)
     static constexpr int NL = (NT + 1 + 7) / 8 * 8;           // B rows per digit (+ the fix row)
     static constexpr int PCOL = LB * NL;                      // D columns per product (multiple of 8)
-    static constexpr int NB = (NPR * PCOL + 15) / 16 * 16;   // N of the MMA: the products' rows packed
+    // N of the MMA: the products' rows packed (multiple of 8: one product of 8 rows -- the
+    // up-sweep and u items -- no longer fetches 8 rows of zero padding per MMA)
+    static constexpr int NB = (NPR * PCOL + 7) / 8 * 8;
+    static constexpr int NBL = (NB + 15) / 16;                // 16-column TMEM loads in the epilogue
     // window rows: the descriptor starts at row 1 and reads rows up to 127 + 32*(2*NKS-1) + 32
     static constexpr int AROWS = 64 * NKS + 128;             // multiple of 8
     static constexpr int A_BYTES = AROWS * 16;
@@ -483,9 +486,12 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
         tc_fence_after();
         // ---- epilogue: thread tid = TMEM lane = coefficient r of every block, straight to HBM
         const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
-        int v[G::NB / 16][16];                            // every product's columns, one load
+        int v[G::NBL][16];                                // every product's columns, one load
 #pragma unroll
-        for (int c16 = 0; c16 < G::NB / 16; c16++) tmem_ld16(lane_addr + 16 * c16, v[c16]);
+        for (int c16 = 0; c16 < G::NBL; c16++) {
+            if (16 * c16 + 16 <= G::NB) tmem_ld16(lane_addr + 16 * c16, v[c16]);
+            else tmem_ld8(lane_addr + 16 * c16, v[c16]);          // (columns 8..15 unused)
+        }
         tmem_ld_wait();
 #pragma unroll
         for (int pp = 0; pp < NPR; pp++) {

@@ -412,9 +412,12 @@ __global__ void __launch_bounds__(Tc4wGeom<PS, NPR>::THREADS, Tc4wGeom<PS, NPR>:
             WS_WAIT(7, accfull + ab, (uint32_t)((j >> 2) & 1));
             tc_fence_after();
             const uint32_t lane_addr = tmem + ((uint32_t)(q * 32) << 16) + W::COL_ACC + ab * G::NB;
-            int v[G::NB / 16][16];
+            int v[G::NBL][16];
 #pragma unroll
-            for (int c16 = 0; c16 < G::NB / 16; c16++) tmem_ld16(lane_addr + 16 * c16, v[c16]);
+            for (int c16 = 0; c16 < G::NBL; c16++) {
+                if (16 * c16 + 16 <= G::NB) tmem_ld16(lane_addr + 16 * c16, v[c16]);
+                else tmem_ld8(lane_addr + 16 * c16, v[c16]);
+            }
             tmem_ld_wait();
             tc_fence_before();
             __syncwarp();
