@@ -121,6 +121,12 @@ typedef struct {
     size_t workspace_bytes;
 } sntrup_keygen_opts;
 
+/* Error status of the last keygen call on `stream` (device pointers / SNTRUP_OPT_ASYNC calls do
+   not read their device error flags before returning): synchronises `stream`, then
+   SNTRUP_E_INTERNAL if that call hit the g retry bound, else SNTRUP_OK.  Valid until the next
+   call on the stream. */
+int sntrup_async_error(void *stream);
+
 /* Completion events for asynchronous host-output calls (opaque cudaEvent_t). */
 int sntrup_event_create(void **ev);
 int sntrup_event_synchronize(void *ev);       /* blocks until the event completed */

@@ -101,6 +101,7 @@ _lib.sntrup_full_sk_bytes.argtypes = [_i32]
 _lib.sntrup_full_sk_bytes.restype = ctypes.c_size_t
 _lib.sntrup_full_sk_batch.argtypes = [_i32, _u64, _u64, _u64, _vp, _vp, _vp, _vp]
 _lib.sntrup_event_create.argtypes = [ctypes.POINTER(_vp)]
+_lib.sntrup_async_error.argtypes = [_vp]
 _lib.sntrup_event_synchronize.argtypes = [_vp]
 _lib.sntrup_event_query.argtypes = [_vp]
 _lib.sntrup_event_destroy.argtypes = [_vp]
@@ -116,7 +117,7 @@ EXPORTED = ("sntrup_params", "sntrup_strerror", "sntrup_batch_keygen", "sntrup_b
             "sntrup_pool_take", "sntrup_pool_stats", "sntrup_pool_destroy",
             "sntrup_sample_short_batch", "sntrup_sample_uniform_rq_batch", "sntrup_encap_core_batch", "sntrup_decap_core_batch",
             "sntrup_profile_read", "sntrup_full_sk_bytes", "sntrup_full_sk_batch",
-            "sntrup_event_create", "sntrup_event_synchronize", "sntrup_event_query", "sntrup_event_destroy")
+            "sntrup_async_error", "sntrup_event_create", "sntrup_event_synchronize", "sntrup_event_query", "sntrup_event_destroy")
 
 PROFILE_CLASSES = ("sample", "r3_mul", "rq_mul", "root_inv", "rq_inv", "repair", "encode", "other")
 
@@ -415,6 +416,11 @@ def keygen_workspace_bytes(param_set: int, n_keys: int, batch_size: int = 32, fl
 def workspace_reserved_bytes(stream=None, staging: bool = False) -> int:
     """Bytes the library holds for `stream` (the cached workspace, or the host-output staging)."""
     return int(_lib.sntrup_workspace_reserved_bytes(_stream(stream), 1 if staging else 0))
+
+
+def async_error(stream=None):
+    """Raise if the last keygen call on `stream` (e.g. an OPT_ASYNC one) hit the g retry bound."""
+    _check(_lib.sntrup_async_error(_stream(stream)), "sntrup_async_error")
 
 
 def release_workspace():

@@ -453,6 +453,21 @@ int sntrup_profile_read_kinds_ex(int reset, double *ms, double *ops, uint64_t *l
     return PK_N;
 }
 
+int sntrup_async_error(void *stream) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    auto it = g_async_err.find(std::make_pair(dev, (uintptr_t)stream));
+    if (it == g_async_err.end()) return SNTRUP_OK;
+    CK(cudaStreamSynchronize((cudaStream_t)stream));
+    for (int *e : it->second) {
+        int h = 0;
+        CK(cudaMemcpy(&h, e, sizeof(int), cudaMemcpyDeviceToHost));
+        if (h) return SNTRUP_E_INTERNAL;
+    }
+    return SNTRUP_OK;
+}
+
 int sntrup_set_divstep_threads(int nt) {
     if (nt != 128 && nt != 256 && nt != 512 && nt != 768) return SNTRUP_E_ARG;
     std::lock_guard<std::mutex> lk(g_mu);

@@ -137,6 +137,8 @@ int sntrup_pool_take(sntrup_pool *p, uint8_t *pk, uint8_t *sk, uint64_t *key_ind
         } else if ((rc = pool_ck(q))) {
             goto done;
         }
+        // the refill was asynchronous: check its device error flags (g retry bound) now
+        if ((rc = sntrup_async_error(p->st))) goto done;
         s->state = sntrup_pool::READY;
     }
     {

@@ -512,7 +512,10 @@ inline TreePlan make_plan(long long m, int B) {
 // 7 = as 0 but the keygen's u products fused with the R/q tree's level 1 (shared A; A/B);
 // 8 = as 0 but the int8 big x big products software-pipelined (two operand stages, 8 warps)
 inline int g_mul_impl = 0;
-inline int g_divstep_threads = 256;                // R/q root CTA size (A/B knob; sntrup761 only)
+inline int g_divstep_threads = 256;
+// per (device, caller stream): the device error flags of the last keygen call (asynchronous calls
+// do not read them; sntrup_async_error does, once the call's work has completed)
+inline std::map<std::pair<int, uintptr_t>, std::vector<int *>> g_async_err;                // R/q root CTA size (A/B knob; sntrup761 only)
 inline unsigned long long *g_ws_trace = nullptr;   // SNTRUP_WS_TRACE: device [160][16] role cycles
 
 struct DevInfo { int sms = 0; };
@@ -1325,6 +1328,11 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
         for (int li = 0; li < nl; li++)
             for (int i = 0; i < 2; i++) CK(cudaStreamWaitEvent(ds, csl[li]->copy[i], 0));
         CK(cudaEventRecord((cudaEvent_t)o.done_event, ds));
+    }
+    {   // where this call's error flags live, for sntrup_async_error(stream) after an async call
+        auto &e = g_async_err[std::make_pair(dev, (uintptr_t)s0)];
+        e.assign(nl, nullptr);
+        for (int li = 0; li < nl; li++) e[li] = lanes[li].err;
     }
     const bool sync = !(o.flags & SNTRUP_OPT_ASYNC) || (host_out && !async_host) || o.stats_out;
     if (sync) {

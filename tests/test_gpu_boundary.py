@@ -145,3 +145,13 @@ def test_small_factor_check_is_constant_time(param):
         times[name] = prof["other"]["ms"] / 3
     ts, td = min(times["sparse"], times["sparse2"]), min(times["dense"], times["dense2"])
     assert abs(td - ts) <= 0.15 * max(td, ts), times
+
+
+def test_async_error_status():
+    # asynchronous calls do not read their device error flags before returning; the status of the
+    # last call on a stream is available afterwards (the key pool checks it per refill)
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        S.batch_keygen(653, 4096, 4, batch_size=512, flags=S.OPT_ASYNC, stream=st)
+    S.async_error(st)                                 # no retry-bound hit: returns quietly
+    assert S._lib.sntrup_async_error(S._stream(st)) == S.SNTRUP_OK
