@@ -296,8 +296,10 @@ uint64_t sntrup_kernel_launch_count(void);
        (tcgen05.st) and read by the MMAs from there instead of from shared memory (128-column
        TMEM allocation per CTA); 10 = as 9 with 64 columns (fewer K steps in TMEM, more CTAs);
    11 = as 0, with the small x small (fp4) products on the warp-specialised persistent kernel
-       whose Hankel A operand is built in registers and written to TMEM (csrc/tc4w.cuh).
-   All are exact.  Variants 2-10 are compiled for sntrup761 only (other sets run 0, or 1 / 11);
+       whose Hankel A operand is built in registers and written to TMEM (csrc/tc4w.cuh);
+   12 = as 0, with every K step of the fp4 products' A operand streamed through a 64-column TMEM
+       window in rounds (no shared-memory A at all; 8 CTAs per SM).
+   All are exact.  Variants 2-10 and 12 are compiled for sntrup761 only (other sets run 0, or 1 / 11);
    KEM pre/post-op calls always use the default kernel of their shape.  Returns SNTRUP_OK or
    SNTRUP_E_ARG. */
 int sntrup_set_mul_impl(int impl);

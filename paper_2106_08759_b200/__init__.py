@@ -447,6 +447,7 @@ MUL_TENSOR_CORE_PIPELINED = 8     # int8 big x big products software-pipelined (
 MUL_TENSOR_CORE_TMEM_A = 9        # fp4 products: first K steps of the Hankel A operand in TMEM (128 cols)
 MUL_TENSOR_CORE_TMEM_A64 = 10     # as 9 with a 64-column TMEM allocation
 MUL_TENSOR_CORE_WS = 11           # warp-specialised persistent kernels, Hankel A written to TMEM
+MUL_TENSOR_CORE_TMEM_RING = 12    # fp4: every K step's A rows through a 64-column TMEM window in rounds
 
 
 def set_mul_impl(impl: int):

@@ -589,10 +589,10 @@ int launch_tc_pipe(const MulArgs &a, cudaStream_t s) {
     return launch_tc_impl<PS, M, 2, 2, NPR, 128, false, 256, 2>(a, s);
 }
 
-template <class PS, int M, int LB, int NPR = 1, bool XOPS = false, int TA = 0>
+template <class PS, int M, int LB, int NPR = 1, bool XOPS = false, int TA = 0, bool RING = false>
 int launch_tc4_impl(const MulArgs &a, cudaStream_t s) {
     using G = Tc4Geom<PS, LB, NPR, TA>;
-    auto kern = tc4_mul_kernel<PS, M, LB, NPR, XOPS, TA>;
+    auto kern = tc4_mul_kernel<PS, M, LB, NPR, XOPS, TA, RING>;
     static std::map<int, int> per_sm;
     int dev = 0;
     CK(cudaGetDevice(&dev));
@@ -609,7 +609,7 @@ int launch_tc4_impl(const MulArgs &a, cudaStream_t s) {
     g_cur_kind = PK_F4;
     // per work item: NKS MMAs, each an 128 x 32-byte A tile (64 fp4 K-elements; none for the K
     // steps whose A is in TMEM) and an NB x 32-byte B tile
-    g_cur_smem = (double)a.n_out * ((double)(G::NKS - G::NTA) * 128 * 32 + (double)G::NKS * G::NB * 32);
+    g_cur_smem = (double)a.n_out * ((double)(RING ? 0 : G::NKS - G::NTA) * 128 * 32 + (double)G::NKS * G::NB * 32);
     kern<<<(unsigned)grid, 128, G::SMEM, s>>>(a);
     LAUNCHED();
     return SNTRUP_OK;
@@ -650,6 +650,7 @@ int launch_tc4(const MulArgs &a, cudaStream_t s) {
     if constexpr (LB == 1 && PS::P == 761) {              // A/B variants: sntrup761 only
         if (g_mul_impl == 9) return launch_tc4_impl<PS, M, LB, NPR, false, 128>(a, s);  // A in TMEM, 128 cols
         if (g_mul_impl == 10) return launch_tc4_impl<PS, M, LB, NPR, false, 64>(a, s);  // A in TMEM, 64 cols
+        if (g_mul_impl == 12) return launch_tc4_impl<PS, M, LB, NPR, false, 64, true>(a, s);  // all A via TMEM
     }
     return launch_tc4_impl<PS, M, LB, NPR, false>(a, s);
 }

@@ -200,9 +200,13 @@ __device__ __forceinline__ void digits_rev8(const int (&vals)[8], uint32_t (&dw)
 // M = modulus; A = one digit (the small operand); LB digits for the B operand; NPR products per A.
 // The B operand is folded (bt of tcmul.cuh): LB = 1 sums stay in {0, +-s, +-2s} (s = 1 or 3:
 // e2m1-exact up to 6); LB > 1 sums are reduced mod M before their base-9 digits.
-template <class PS, int M, int LB, int NPR, bool XOPS = false, int TA = 0>
+// RING (with TA > 0): every K step's A rows go through the TA-column TMEM window in rounds of
+// NTA K steps (build rows -> tcgen05.st -> MMAs from TMEM -> wait -> next round); no A windows in
+// shared memory at all, so the shared-memory traffic per item is only the B operand and staging.
+template <class PS, int M, int LB, int NPR, bool XOPS = false, int TA = 0, bool RING = false>
 __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
     using G = Tc4Geom<PS, LB, NPR, TA>;
+    static_assert(!RING || TA > 0, "RING streams A through TMEM");
     constexpr int P = PS::P;
     constexpr int CH = G::CH;
     constexpr int PD = G::PD;
@@ -389,7 +393,7 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
             stage(w, fixab);
         }
         __syncthreads();
-        if constexpr (TA) {
+        if constexpr (TA && !RING) {
             // ---- A rows into TMEM: lane r, K step ks = nibbles [1 + r + 64 ks, +64) of hA (the row the
             // shared-memory descriptor below starts at), 8 columns of 8 nibbles
             tc_fence_after();
@@ -414,7 +418,7 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
         }
         // ---- A windows: row rho = nibbles [rho, rho+32); rows 4m..4m+3 share word base m/2
 #pragma unroll
-        for (int kw = 0; kw < (G::AROWS / 4 - 16 * G::NTA + 127) / 128; kw++) {
+        for (int kw = 0; kw < (RING ? 0 : (G::AROWS / 4 - 16 * G::NTA + 127) / 128); kw++) {
             const int m = 16 * G::NTA + tid + 128 * kw;          // rows >= 64 NTA: the K steps >= NTA
             if (m >= G::AROWS / 4) break;
             SNTRUP_CHECK(4 * ((m >> 1) + 5) <= G::HA_BYTES && 64 * (m + 1) <= G::A_BYTES);
@@ -453,6 +457,56 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
             }
         }
         fence_async_smem();
+        if constexpr (RING) {
+            // ---- A through the TMEM window in rounds of NTA K steps; the B rows above are built
+            constexpr int NR = (G::NKS + G::NTA - 1) / G::NTA;
+            const int r1 = tid + 1, g = (r1 >> 3) - 4 * warp;             // hA copy 0..4
+            const uint32_t sh = 4u * (uint32_t)(r1 & 7);
+            const uint4 *src = reinterpret_cast<const uint4 *>(reinterpret_cast<const uint8_t *>(sHA) +
+                                                               g * G::HA_CSTRIDE) + warp;
+            const uint32_t la = tmem + ((uint32_t)(warp * 32) << 16) + G::ACOL;
+            const uint64_t bd0 = umma_desc(smem_u32(sB), G::BLD * 16, 128);
+#pragma unroll 1
+            for (int rr = 0; rr < NR; rr++) {
+                if (rr > 0) {                                 // the window's previous MMAs are done
+                    mbar_wait(bar, phase);
+                    phase ^= 1;
+                    tc_fence_after();
+                }
+                uint4 q0 = src[2 * G::NTA * rr];
+#pragma unroll
+                for (int kk = 0; kk < G::NTA; kk++) {
+                    const int ks = G::NTA * rr + kk;
+                    if (ks < G::NKS) {
+                        const uint4 q1 = src[2 * ks + 1], q2 = src[2 * ks + 2];
+                        const uint32_t x[9] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x};
+                        uint32_t o[8];
+#pragma unroll
+                        for (int i = 0; i < 8; i++) o[i] = __funnelshift_r(x[i], x[i + 1], sh);
+                        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
+                                         la + 8 * kk),
+                                     "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3]), "r"(o[4]), "r"(o[5]), "r"(o[6]),
+                                     "r"(o[7]));
+                        q0 = q2;
+                    }
+                }
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                tc_fence_before();
+                __syncthreads();
+                if (warp == 0) {
+                    tc_fence_after();
+#pragma unroll
+                    for (int kk = 0; kk < G::NTA; kk++) {
+                        const int ks = G::NTA * rr + kk;
+                        if (ks < G::NKS) {
+                            const uint64_t bd = bd0 + (uint64_t)((ks * 32 * G::BLD) >> 4);
+                            umma_mxf4_ta_w(tmem, tmem + G::ACOL + 8 * kk, bd, IDESC, ks > 0 ? 1u : 0u, tmem + G::SFCOL);
+                        }
+                    }
+                    umma_commit_w(bar);
+                }
+            }
+        } else {
         tc_fence_before();
         __syncthreads();
         if (warp == 0) {                                  // one elected lane of a converged warp
@@ -467,6 +521,7 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
                 else umma_mxf4_w(tmem, ad, bd, IDESC, ks > 0 ? 1u : 0u, tmem + G::SFCOL);
             }
             umma_commit_w(bar);
+        }
         }
         const TcWork<NPR> nxt = wn;
         int fnx[NPR];
