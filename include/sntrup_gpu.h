@@ -308,6 +308,15 @@ int sntrup_set_mul_impl(int impl);
    the roots are few): 128, 256 (default), 512 or 768; sntrup761 only.  SNTRUP_OK / SNTRUP_E_ARG. */
 int sntrup_set_divstep_threads(int nt);
 
+/* A/B knob (measurement): the root inversions used when the roots are few (fewer than two per
+   SM): 0 (default) = jump-divsteps in both rings (App. D "jump-div-step"): 31-step
+   transition matrices decided by one warp on a 32-coefficient window, applied to (f, g) by the
+   rest of that CTA and to (v, r) by a second CTA of a 2-CTA cluster (csrc/jump.cuh); 1 = one
+   divstep at a time (R/q: 8 warps per root, one CTA barrier per step, sntrup_set_divstep_threads;
+   R/3: one bitsliced warp per root); 2 = jump-divsteps for R/q, bitsliced steps for R/3.  All are
+   constant-time and exact.  Returns SNTRUP_OK or SNTRUP_E_ARG. */
+int sntrup_set_root_impl(int impl);
+
 /* Measurement hooks (bench.py).  When enabled, every kernel launch is bracketed by CUDA events
    recorded on its launching stream.  sntrup_profile_read() waits for the recorded events and
    returns, per kernel class, the summed device milliseconds, the summed work units, the summed

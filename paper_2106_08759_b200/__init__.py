@@ -77,6 +77,7 @@ _lib.sntrup_release_stream_workspace.argtypes = [_vp]
 _lib.sntrup_kernel_launch_count.restype = _u64
 _lib.sntrup_set_mul_impl.argtypes = [_i32]
 _lib.sntrup_set_divstep_threads.argtypes = [_i32]
+_lib.sntrup_set_root_impl.argtypes = [_i32]
 _lib.sntrup_profile_enable.restype = None
 _lib.sntrup_profile_enable.argtypes = [_i32]
 _lib.sntrup_profile_read.restype = _i32
@@ -112,6 +113,7 @@ EXPORTED = ("sntrup_params", "sntrup_strerror", "sntrup_batch_keygen", "sntrup_b
             "sntrup_workspace_reserved_bytes", "rq_mul_batch", "rq_mul_small_batch", "r3_mul_batch", "rq_recip_batch",
             "r3_recip_batch", "r3_is_invertible_batch", "rq_encode_batch",
             "sntrup_release_workspace", "sntrup_release_stream_workspace", "sntrup_kernel_launch_count", "sntrup_set_mul_impl", "sntrup_set_divstep_threads",
+            "sntrup_set_root_impl",
             "sntrup_profile_enable", "sntrup_profile_read_kinds", "sntrup_profile_read_kinds_ex",
             "sntrup_measure_int_peak", "sntrup_probe_half_mul", "sntrup_pool_create",
             "sntrup_pool_take", "sntrup_pool_stats", "sntrup_pool_destroy",
@@ -453,6 +455,16 @@ MUL_TENSOR_CORE_TMEM_RING = 12    # fp4: every K step's A rows through a 64-colu
 def set_mul_impl(impl: int):
     """0 = tcgen05 int8 Hankel-GEMM ring product (default), 1 = int32 schoolbook (v1)."""
     _check(_lib.sntrup_set_mul_impl(int(impl)), "sntrup_set_mul_impl")
+
+
+ROOT_JUMP = 0       # root inversions by jump-divsteps, both rings (default)
+ROOT_STEP = 1       # one divstep at a time (R/q: per CTA barrier; R/3: bitsliced warp)
+ROOT_JUMP_RQ = 2    # jump-divsteps for R/q only
+
+
+def set_root_impl(impl: int):
+    """Root inversions when the roots are few: ROOT_JUMP (default), ROOT_STEP or ROOT_JUMP_RQ."""
+    _check(_lib.sntrup_set_root_impl(int(impl)), "sntrup_set_root_impl")
 
 
 def profile_enable(on: bool = True):

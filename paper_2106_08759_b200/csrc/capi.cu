@@ -475,6 +475,13 @@ int sntrup_set_divstep_threads(int nt) {
     return SNTRUP_OK;
 }
 
+int sntrup_set_root_impl(int impl) {
+    if (impl < 0 || impl > 2) return SNTRUP_E_ARG;
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_root_impl = impl;
+    return SNTRUP_OK;
+}
+
 int sntrup_set_mul_impl(int impl) {
     if (impl < 0 || impl > 12) return SNTRUP_E_ARG;
     std::lock_guard<std::mutex> lk(g_mu);

@@ -26,6 +26,7 @@
 #include "../../include/sntrup_gpu.h"
 #include "common.cuh"
 #include "divstep.cuh"
+#include "jump.cuh"
 #include "encode.cuh"
 #include "factor_tables.h"
 #include "fullsk.cuh"
@@ -513,6 +514,10 @@ inline TreePlan make_plan(long long m, int B) {
 // 8 = as 0 but the int8 big x big products software-pipelined (two operand stages, 8 warps)
 inline int g_mul_impl = 0;
 inline int g_divstep_threads = 256;
+// root inversions when the roots are few (sntrup_set_root_impl): 0 = jump-divsteps (jump.cuh) in
+// both rings; 1 = one divstep per barrier (R/q: divstep_cta_kernel) / per warp step (R/3: the
+// bitsliced divstep_kernel); 2 = jump-divsteps for R/q, bitsliced steps for R/3
+inline int g_root_impl = 0;
 // per (device, caller stream): the device error flags of the last keygen call (asynchronous calls
 // do not read them; sntrup_async_error does, once the call's work has completed)
 inline std::map<std::pair<int, uintptr_t>, std::vector<int *>> g_async_err;                // R/q root CTA size (A/B knob; sntrup761 only)
@@ -736,11 +741,17 @@ int launch_divstep(const InvArgs &a, cudaStream_t s) {
     if (a.n <= 0) return SNTRUP_OK;
     ProfScope ps_(M == 3 ? PC_INV_R3 : PC_INV_RQ, (double)a.n, s);
     if constexpr (M == 3) {
-        divstep_kernel<PS, M><<<(unsigned)((a.n + 3) / 4), 128, 0, s>>>(a);      // bitsliced, warp/root
+        if (a.n < 2LL * dev_info().sms && g_root_impl == 0) {
+            CK((launch_jump_roots<PS, M>(a, s)));                                  // few roots: jump-divsteps
+        } else {
+            divstep_kernel<PS, M><<<(unsigned)((a.n + 3) / 4), 128, 0, s>>>(a);  // bitsliced, warp/root
+        }
     } else {
         // few roots: latency bound -> one CTA of 8 warps per root; many roots: throughput bound
         // -> one warp per root (less per-step overhead in total)
-        if (a.n < 2LL * dev_info().sms)
+        if (a.n < 2LL * dev_info().sms && g_root_impl != 1) {
+            CK((launch_jump_roots<PS, M>(a, s)));
+        } else if (a.n < 2LL * dev_info().sms)
         {
             // threads per root (A/B knob, sntrup_set_divstep_threads; default 256 = 8 warps)
             if constexpr (PS::P == 761) {

@@ -364,6 +364,48 @@ def test_rq_recip(O, param, B):
         assert ok and np.array_equal(out[i, :p], inv) and not out[i, p:].any()
 
 
+def rq_root_cases(p, q, p8, n, seed):
+    """Uniform rows plus the shapes that drive the divstep decisions to their extremes: 1, x^k
+    (long runs of g_0 = 0 in the reversed input, delta climbing), 1 + x^(p-1), sparse rows and a
+    row of all (q-1)/2."""
+    a = synth.uniform_rq(n, p, q, p8, seed=seed)
+    rng = np.random.default_rng(seed)
+    a[0] = 0; a[0, 0] = 1
+    a[1] = 0; a[1, p - 1] = 1
+    a[2] = 0; a[2, 1] = -1
+    a[3] = 0; a[3, 0] = 1; a[3, p - 1] = 1
+    a[4] = 0; a[4, :p] = (q - 1) // 2
+    for i in range(5, 12):
+        a[i] = 0
+        idx = rng.choice(p, size=1 + i % 4, replace=False)
+        a[i, idx] = rng.integers(-(q - 1) // 2, (q + 1) // 2, size=len(idx))
+        if not a[i].any():
+            a[i, 0] = 1
+    return a
+
+
+@pytest.mark.parametrize("param", PSETS)
+def test_rq_root_jump_vs_step(O, param):
+    # the jump-divstep root (default) and the one-step-per-barrier root against the oracle's
+    # Euclid inversion, one chain per row (B = 1)
+    P = S.params(param)
+    p, q, p8 = P["p"], P["q"], P["p8"]
+    a = rq_root_cases(p, q, p8, 40, seed=param)
+    outs = {}
+    try:
+        for impl in (S.ROOT_JUMP, S.ROOT_STEP):
+            S.set_root_impl(impl)
+            outs[impl] = S.rq_recip_batch(param, torch.from_numpy(a).cuda(), batch_size=1).cpu().numpy()
+    finally:
+        S.set_root_impl(S.ROOT_JUMP)
+    for i in range(len(a)):
+        ok, inv = O.poly_inv(p, q, a[i, :p])
+        assert ok
+        assert np.array_equal(outs[S.ROOT_JUMP][i, :p], inv), i
+        assert not outs[S.ROOT_JUMP][i, p:].any()
+    assert np.array_equal(outs[S.ROOT_JUMP], outs[S.ROOT_STEP])
+
+
 def test_rq_recip_zero_reports_index():
     P = S.params(761)
     a = synth.uniform_rq(50, 761, 4591, P["p8"], seed=7)
@@ -402,6 +444,33 @@ def test_r3_recip(O, param, B):
         assert bool(ok[i]) == rok, i
         assert np.array_equal(out[i, :p], inv if rok else np.zeros(p)), i
         assert not out[i, p:].any()
+
+
+@pytest.mark.parametrize("param", PSETS)
+def test_r3_root_jump_vs_step(O, param):
+    # R/3 roots one chain per row (B = 1): jump-divsteps (default) and the bitsliced one-step warp
+    # against the oracle's Euclid inversion, non-invertible rows included
+    P = S.params(param)
+    p, p16 = P["p"], P["p16"]
+    g = crafted_r3(O, p, p16, 40, seed=param + 7)
+    g[7] = 0; g[7, p - 1] = 1                     # x^(p-1): long run of g_0 = 0 in the reversed input
+    g[8] = 0; g[8, 0] = -1
+    outs = {}
+    try:
+        for impl in (S.ROOT_JUMP, S.ROOT_STEP):
+            S.set_root_impl(impl)
+            o, ok = S.r3_recip_batch(param, torch.from_numpy(g).cuda(), batch_size=1)
+            outs[impl] = (o.cpu().numpy(), ok.cpu().numpy())
+    finally:
+        S.set_root_impl(S.ROOT_JUMP)
+    out, ok = outs[S.ROOT_JUMP]
+    for i in range(len(g)):
+        rok, inv = O.poly_inv(p, 3, g[i, :p])
+        assert bool(ok[i]) == rok, i
+        assert np.array_equal(out[i, :p], inv if rok else np.zeros(p)), i
+        assert not out[i, p:].any()
+    assert np.array_equal(outs[S.ROOT_JUMP][0], outs[S.ROOT_STEP][0])
+    assert np.array_equal(outs[S.ROOT_JUMP][1], outs[S.ROOT_STEP][1])
 
 
 def test_r3_recip_big_factor_multiple(O):
