@@ -308,12 +308,16 @@ int sntrup_set_mul_impl(int impl);
    the roots are few): 128, 256 (default), 512 or 768; sntrup761 only.  SNTRUP_OK / SNTRUP_E_ARG. */
 int sntrup_set_divstep_threads(int nt);
 
-/* A/B knob (measurement): the root inversions used when the roots are few (fewer than two per
-   SM): 0 (default) = jump-divsteps in both rings (App. D "jump-div-step"): 31-step
+/* Knob: the root inversions used when the roots are few (fewer than two per SM).  0 (default) =
+   automatic: jump-divsteps (App. D "jump-div-step"; csrc/jump.cuh: 31-step
    transition matrices decided by one warp on a 32-coefficient window, applied to (f, g) by the
-   rest of that CTA and to (v, r) by a second CTA of a 2-CTA cluster (csrc/jump.cuh); 1 = one
-   divstep at a time (R/q: 8 warps per root, one CTA barrier per step, sntrup_set_divstep_threads;
-   R/3: one bitsliced warp per root); 2 = jump-divsteps for R/q, bitsliced steps for R/3.  All are
+   rest of that CTA and to (v, r) by the second CTA of a 2-CTA cluster) for the standalone
+   reciprocal calls (rq_recip_batch, r3_recip_batch, r3_is_invertible_batch) and keygen calls of
+   at most 4096 keys, whose time is the roots' latency; one divstep at a time inside larger keygen
+   calls, where the roots overlap the other ring's products and the smaller SM footprint wins.  1 = one divstep at a time everywhere (R/q: 8 warps
+   per root, one CTA barrier per step, sntrup_set_divstep_threads; R/3: one bitsliced warp per
+   root); 2 = jump-divsteps everywhere.  + 4 (with 0 or 2): the jump CTAs reserve only the shared
+   memory they use instead of more than half an SM each (measurement).  All variants are
    constant-time and exact.  Returns SNTRUP_OK or SNTRUP_E_ARG. */
 int sntrup_set_root_impl(int impl);
 

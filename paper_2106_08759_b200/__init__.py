@@ -457,13 +457,14 @@ def set_mul_impl(impl: int):
     _check(_lib.sntrup_set_mul_impl(int(impl)), "sntrup_set_mul_impl")
 
 
-ROOT_JUMP = 0       # root inversions by jump-divsteps, both rings (default)
+ROOT_AUTO = 0       # jump-divsteps for standalone reciprocals and keygen calls <= 4096 keys, else per-step
 ROOT_STEP = 1       # one divstep at a time (R/q: per CTA barrier; R/3: bitsliced warp)
-ROOT_JUMP_RQ = 2    # jump-divsteps for R/q only
+ROOT_JUMP = 2       # jump-divsteps everywhere
+ROOT_SHARED_SM = 4  # (+) jump CTAs reserve only the shared memory they use
 
 
 def set_root_impl(impl: int):
-    """Root inversions when the roots are few: ROOT_JUMP (default), ROOT_STEP or ROOT_JUMP_RQ."""
+    """Root inversions when the roots are few: ROOT_AUTO (default), ROOT_STEP, ROOT_JUMP (+ ROOT_SHARED_SM)."""
     _check(_lib.sntrup_set_root_impl(int(impl)), "sntrup_set_root_impl")
 
 

@@ -476,7 +476,7 @@ int sntrup_set_divstep_threads(int nt) {
 }
 
 int sntrup_set_root_impl(int impl) {
-    if (impl < 0 || impl > 2) return SNTRUP_E_ARG;
+    if (impl < 0 || impl > 7 || (impl & 3) == 3) return SNTRUP_E_ARG;
     std::lock_guard<std::mutex> lk(g_mu);
     g_root_impl = impl;
     return SNTRUP_OK;

@@ -411,7 +411,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(RqJump<PS, M>::NT, 1
 }
 
 template <class PS, int M>
-cudaError_t launch_jump_roots(const InvArgs &a, cudaStream_t s) {
+cudaError_t launch_jump_roots(const InvArgs &a, cudaStream_t s, bool reserve_sm = true) {
     using JS = RqJump<PS, M>;
     static unsigned long long attr_set = 0;         // per device (bit)
     int dev = 0;
@@ -422,7 +422,7 @@ cudaError_t launch_jump_roots(const InvArgs &a, cudaStream_t s) {
         if (e != cudaSuccess) return e;
         attr_set |= 1ull << (dev & 63);
     }
-    jump_cluster_kernel<PS, M><<<(unsigned)(2 * a.n), JS::NT, JS::SMEM, s>>>(a);
+    jump_cluster_kernel<PS, M><<<(unsigned)(2 * a.n), JS::NT, reserve_sm ? JS::SMEM : JS::SMEM_USED, s>>>(a);
     return cudaGetLastError();
 }
 

@@ -514,9 +514,12 @@ inline TreePlan make_plan(long long m, int B) {
 // 8 = as 0 but the int8 big x big products software-pipelined (two operand stages, 8 warps)
 inline int g_mul_impl = 0;
 inline int g_divstep_threads = 256;
-// root inversions when the roots are few (sntrup_set_root_impl): 0 = jump-divsteps (jump.cuh) in
-// both rings; 1 = one divstep per barrier (R/q: divstep_cta_kernel) / per warp step (R/3: the
-// bitsliced divstep_kernel); 2 = jump-divsteps for R/q, bitsliced steps for R/3
+// root inversions when the roots are few (sntrup_set_root_impl): 0 = automatic (jump-divsteps,
+// jump.cuh, for the standalone reciprocal calls and keygen calls of <= 4096 keys; one divstep at
+// a time inside larger keygen calls), 1 = one
+// divstep at a time everywhere (R/q: divstep_cta_kernel, one CTA barrier per step; R/3: the
+// bitsliced warp divstep_kernel), 2 = jump-divsteps everywhere; + 4: the jump CTAs reserve only the
+// shared memory they use (other kernels' CTAs may share their SMs) instead of more than half an SM
 inline int g_root_impl = 0;
 // per (device, caller stream): the device error flags of the last keygen call (asynchronous calls
 // do not read them; sntrup_async_error does, once the call's work has completed)
@@ -737,20 +740,25 @@ int launch_mul(MulArgs a, cudaStream_t s, int la = 2, int lb = 2) {
 }
 
 template <class PS, int M>
-int launch_divstep(const InvArgs &a, cudaStream_t s) {
+int launch_divstep(const InvArgs &a, cudaStream_t s, bool bulk = false) {
     if (a.n <= 0) return SNTRUP_OK;
+    // jump-divsteps when the roots are few and the call waits on them (the standalone reciprocal
+    // calls, latency-sized keygen calls); inside a bulk keygen call the roots overlap the other
+    // ring's products, where the per-step kernels' smaller SM footprint wins
+    const int rmode = g_root_impl & 3;
+    const bool jump = a.n < 2LL * dev_info().sms && (rmode == 2 || (rmode == 0 && !bulk));
     ProfScope ps_(M == 3 ? PC_INV_R3 : PC_INV_RQ, (double)a.n, s);
     if constexpr (M == 3) {
-        if (a.n < 2LL * dev_info().sms && g_root_impl == 0) {
-            CK((launch_jump_roots<PS, M>(a, s)));                                  // few roots: jump-divsteps
+        if (jump) {
+            CK((launch_jump_roots<PS, M>(a, s, !(g_root_impl & 4))));                                  // few roots: jump-divsteps
         } else {
             divstep_kernel<PS, M><<<(unsigned)((a.n + 3) / 4), 128, 0, s>>>(a);  // bitsliced, warp/root
         }
     } else {
         // few roots: latency bound -> one CTA of 8 warps per root; many roots: throughput bound
         // -> one warp per root (less per-step overhead in total)
-        if (a.n < 2LL * dev_info().sms && g_root_impl != 1) {
-            CK((launch_jump_roots<PS, M>(a, s)));
+        if (jump) {
+            CK((launch_jump_roots<PS, M>(a, s, !(g_root_impl & 4))));
         } else if (a.n < 2LL * dev_info().sms)
         {
             // threads per root (A/B knob, sntrup_set_divstep_threads; default 256 = 8 warps)
@@ -1202,8 +1210,10 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
         if (rings || serial) {
             // each ring's roots on its own chain: one ring's latency-bound inversion overlaps the
             // other ring's products (serial: one after the other, separately timed)
-            if ((rc = launch_divstep<PS, 3>(j3.roots(), s3))) return rc;
-            if ((rc = launch_divstep<PS, PS::Q>(jq.roots(), s))) return rc;
+            // a latency-sized call (<= 4096 keys) waits on its roots: jump-divsteps (automatic policy)
+            const bool bulk = n > 4096;
+            if ((rc = launch_divstep<PS, 3>(j3.roots(), s3, bulk))) return rc;
+            if ((rc = launch_divstep<PS, PS::Q>(jq.roots(), s, bulk))) return rc;
         } else {
             if ((rc = launch_joint_roots<PS>(j3.roots(), jq.roots(), s))) return rc;
         }

@@ -44,7 +44,7 @@ for ps in [int(x) for x in (sys.argv[1:] or ["653", "761", "857", "953", "1013",
         S.set_root_impl(impl)
         outs[name] = S.rq_recip_batch(ps, a, batch_size=1).clone()
         r["rq_recip_B1_us_" + name] = timed(lambda: S.rq_recip_batch(ps, a, batch_size=1))
-    S.set_root_impl(S.ROOT_JUMP)
+    S.set_root_impl(S.ROOT_AUTO)
     r["rq_jump_equals_step"] = bool(torch.equal(outs["jump"], outs["step"]))
     res[ps] = r
     print(ps, json.dumps(r), flush=True)

@@ -85,6 +85,22 @@ def test_batch_size_invariance_ragged(O, B):
     assert res["stats"]["r3_products"] == prods
 
 
+@pytest.mark.parametrize("impl", ["jump", "jump_shared_sm", "step"])
+def test_keygen_root_impls(O, impl):
+    # keygen with each root-inversion implementation forced (the automatic policy runs per-step
+    # roots inside keygen): ragged trees, both rings' roots on their own streams, and configs[0]
+    m = {"jump": S.ROOT_JUMP, "jump_shared_sm": S.ROOT_JUMP | S.ROOT_SHARED_SM, "step": S.ROOT_STEP}[impl]
+    try:
+        S.set_root_impl(m)
+        res = S.batch_keygen(761, 300, 7, batch_size=8, debug=True, flags=S.OPT_RING_STREAMS)
+        lat = S.batch_keygen(761, 32, 1, batch_size=1, flags=S.OPT_RING_STREAMS, debug=True)
+        torch.cuda.synchronize()
+    finally:
+        S.set_root_impl(S.ROOT_AUTO)
+    check_keys(O, 761, 7, res, np.arange(300))
+    check_keys(O, 761, 1, lat, np.arange(32))
+
+
 def test_chunking_and_first_index(O):
     n, first = 200, 1000
     res = S.batch_keygen(761, n, 3, batch_size=16, chunk_keys=48, first_key_index=first, debug=True)
@@ -397,7 +413,7 @@ def test_rq_root_jump_vs_step(O, param):
             S.set_root_impl(impl)
             outs[impl] = S.rq_recip_batch(param, torch.from_numpy(a).cuda(), batch_size=1).cpu().numpy()
     finally:
-        S.set_root_impl(S.ROOT_JUMP)
+        S.set_root_impl(S.ROOT_AUTO)
     for i in range(len(a)):
         ok, inv = O.poly_inv(p, q, a[i, :p])
         assert ok
@@ -462,7 +478,7 @@ def test_r3_root_jump_vs_step(O, param):
             o, ok = S.r3_recip_batch(param, torch.from_numpy(g).cuda(), batch_size=1)
             outs[impl] = (o.cpu().numpy(), ok.cpu().numpy())
     finally:
-        S.set_root_impl(S.ROOT_JUMP)
+        S.set_root_impl(S.ROOT_AUTO)
     out, ok = outs[S.ROOT_JUMP]
     for i in range(len(g)):
         rok, inv = O.poly_inv(p, 3, g[i, :p])
