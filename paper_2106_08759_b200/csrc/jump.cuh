@@ -38,6 +38,17 @@
 #include "common.cuh"
 #include "divstep.cuh"
 
+#ifndef SNTRUP_JUMP_RF
+#define SNTRUP_JUMP_RF 2          // (f, g) outputs per applier item (2 or 4; A/B)
+#endif
+#ifndef SNTRUP_JUMP_CHUNKED
+#define SNTRUP_JUMP_CHUNKED 0     // appliers' tap loop rolled in chunks of 8 (A/B: not faster)
+#endif
+#ifndef SNTRUP_JUMP_UNROLL
+#define SNTRUP_JUMP_UNROLL 4      // decision-loop unroll factor: 4 (3.2k cycles per jump) beats full
+                                  // unrolling (4.0k: the 16 KB loop thrashes the instruction caches
+                                  // shared with the appliers) and 1 (3.6k)
+#endif
 #ifndef SNTRUP_JUMP_MODE
 #define SNTRUP_JUMP_MODE 0        // timing experiments: 1 = decisions only, 2 = applications only
 #endif
@@ -126,6 +137,8 @@ template <class PS, int M>
 struct RqJump {
     static constexpr int P = PS::P, P1 = P + 1, S = 2 * P - 1;
     static constexpr int J = 31;                               // steps per jump (U: 32 coefficients)
+    static constexpr int UNR = SNTRUP_JUMP_UNROLL;
+    static constexpr bool CHUNKED = SNTRUP_JUMP_CHUNKED;     // appliers' tap loop rolled in chunks of 8
     static constexpr int NJ = (S + J - 1) / J;
     static constexpr int NT = 512;
     static constexpr int NA0 = 384;                            // CTA 0 appliers: warps on SMSPs 1-3
@@ -171,7 +184,7 @@ struct RqJump {
                                                   float (&u)[4]) {
         float u00 = lane == 0 ? 1.0f : 0.0f, u01 = 0.0f, u10 = 0.0f, u11 = u00;
         float g0 = __shfl_sync(FULL, Gf, 0);
-#pragma unroll
+#pragma unroll (UNR)
         for (int t = 0; t < (SC ? SC : J); t++) {
             if (!SC && t >= s) break;
             const float D = mulsub(f0, Gf, g0, Ff);                     // f0 g - g0 f (pre-swap)
@@ -196,44 +209,119 @@ struct RqJump {
         u[0] = u00; u[1] = u01; u[2] = u10; u[3] = u11;
     }
 
-    // f, g application of jump k (CTA 0): outputs n, n+1
-    template <bool FULLJ>
+    // f, g application of jump k (CTA 0): outputs n .. n+RR-1 (RR = 2: 8-byte window loads, 4:
+    // 16-byte loads)
+    template <bool FULLJ, int RR>
     __device__ __forceinline__ static void apply_fg(const int *Fb, const int *Gb, int *Fo, int *Go,
                                                     const int4 *U, int n, int s) {
-        constexpr int WN = R + 32;                                  // window F[n+s-31 .. n+s+R]
+        constexpr int WN = RR + 32;                                 // window F[n+s-31 .. n+s+RR]
+        if constexpr (FULLJ && RR == 2 && CHUNKED) {
+            // taps in rolled chunks of 8 (small code: the decision warp's loop and this one stay
+            // in the instruction caches); window of chunk c: F[n + 24 - 8c .. n + 33 - 8c]
+            int aF0 = 0, aF1 = 0, aG0 = 0, aG1 = 0;
+#pragma unroll 1
+            for (int c = 0; c < 4; c++) {
+                int wF[10], wG[10];
+#pragma unroll
+                for (int w = 0; w < 10; w += 2) {
+                    const int2 x = *reinterpret_cast<const int2 *>(Fb + n + 24 - 8 * c + w);
+                    const int2 y = *reinterpret_cast<const int2 *>(Gb + n + 24 - 8 * c + w);
+                    wF[w] = x.x; wF[w + 1] = x.y; wG[w] = y.x; wG[w + 1] = y.y;
+                }
+#pragma unroll
+                for (int jj = 0; jj < 8; jj++) {
+                    const int4 w = U[8 * c + jj];
+                    aF0 += w.x * wF[7 - jj] + w.y * wG[7 - jj];
+                    aG0 += w.z * wF[7 - jj] + w.w * wG[7 - jj];
+                    aF1 += w.x * wF[8 - jj] + w.y * wG[8 - jj];
+                    aG1 += w.z * wF[8 - jj] + w.w * wG[8 - jj];
+                }
+            }
+            *reinterpret_cast<int2 *>(Fo + n) = make_int2(ired<M>(aF0), ired<M>(aF1));
+            *reinterpret_cast<int2 *>(Go + n) = make_int2(ired<M>(aG0), ired<M>(aG1));
+            return;
+        }
         int wF[WN], wG[WN];
         if (FULLJ) {                                                // s = 31: window starts at n
+            if constexpr (RR == 4) {
 #pragma unroll
-            for (int w = 0; w < WN; w += 2) {
-                const int2 x = *reinterpret_cast<const int2 *>(Fb + n + w);
-                const int2 y = *reinterpret_cast<const int2 *>(Gb + n + w);
-                wF[w] = x.x; wF[w + 1] = x.y; wG[w] = y.x; wG[w + 1] = y.y;
+                for (int w = 0; w < WN; w += 4) {
+                    const int4 x = *reinterpret_cast<const int4 *>(Fb + n + w);
+                    const int4 y = *reinterpret_cast<const int4 *>(Gb + n + w);
+                    wF[w] = x.x; wF[w + 1] = x.y; wF[w + 2] = x.z; wF[w + 3] = x.w;
+                    wG[w] = y.x; wG[w + 1] = y.y; wG[w + 2] = y.z; wG[w + 3] = y.w;
+                }
+            } else {
+#pragma unroll
+                for (int w = 0; w < WN; w += 2) {
+                    const int2 x = *reinterpret_cast<const int2 *>(Fb + n + w);
+                    const int2 y = *reinterpret_cast<const int2 *>(Gb + n + w);
+                    wF[w] = x.x; wF[w + 1] = x.y; wG[w] = y.x; wG[w + 1] = y.y;
+                }
             }
         } else {
 #pragma unroll
             for (int w = 0; w < WN; w++) { wF[w] = Fb[n + s - 31 + w]; wG[w] = Gb[n + s - 31 + w]; }
         }
-        int aF[R], aG[R];
+        int aF[RR], aG[RR];
 #pragma unroll
-        for (int m = 0; m < R; m++) { aF[m] = 0; aG[m] = 0; }
+        for (int m = 0; m < RR; m++) { aF[m] = 0; aG[m] = 0; }
 #pragma unroll
         for (int j = 0; j < 32; j++) {
             const int4 w = U[j];
 #pragma unroll
-            for (int m = 0; m < R; m++) {
+            for (int m = 0; m < RR; m++) {
                 const int fv = wF[m + 31 - j], gv = wG[m + 31 - j];
                 aF[m] += w.x * fv + w.y * gv;
                 aG[m] += w.z * fv + w.w * gv;
             }
         }
-        *reinterpret_cast<int2 *>(Fo + n) = make_int2(ired<M>(aF[0]), ired<M>(aF[1]));
-        *reinterpret_cast<int2 *>(Go + n) = make_int2(ired<M>(aG[0]), ired<M>(aG[1]));
+        if constexpr (RR == 4) {
+            *reinterpret_cast<int4 *>(Fo + n) = make_int4(ired<M>(aF[0]), ired<M>(aF[1]), ired<M>(aF[2]), ired<M>(aF[3]));
+            *reinterpret_cast<int4 *>(Go + n) = make_int4(ired<M>(aG[0]), ired<M>(aG[1]), ired<M>(aG[2]), ired<M>(aG[3]));
+        } else {
+            *reinterpret_cast<int2 *>(Fo + n) = make_int2(ired<M>(aF[0]), ired<M>(aF[1]));
+            *reinterpret_cast<int2 *>(Go + n) = make_int2(ired<M>(aG[0]), ired<M>(aG[1]));
+        }
     }
 
     // v, r application (CTA 1): v'[n+m] = sum u00[j] v[n+m-j] + u01[j] r[n+m+1-j],
     // r'[n+m] = sum u10[j] v[n+m-1-j] + u11[j] r[n+m-j]; windows from n - 32
     __device__ __forceinline__ static void apply_vr(const int *Vb, const int *Rb, int *Vo, int *Ro,
                                                     const int4 *U, int n) {
+        if constexpr (CHUNKED) {
+            // taps in rolled chunks of 8; chunk c: V[n - 8c - 8 .. n - 8c + 1], R[.. n - 8c + 3]
+            int aV0 = 0, aV1 = 0, aR0 = 0, aR1 = 0;
+#pragma unroll 1
+            for (int c = 0; c < 4; c++) {
+                int wV[10], wR[12];
+#pragma unroll
+                for (int w = 0; w < 12; w += 2) {
+                    const int2 y = *reinterpret_cast<const int2 *>(Rb + n - 8 * c - 8 + w);
+                    wR[w] = y.x; wR[w + 1] = y.y;
+                    if (w < 10) {
+                        const int2 x = *reinterpret_cast<const int2 *>(Vb + n - 8 * c - 8 + w);
+                        wV[w] = x.x; wV[w + 1] = x.y;
+                    }
+                }
+#pragma unroll
+                for (int jj = 0; jj < 8; jj++) {
+                    const int4 w = U[8 * c + jj];
+                    aV0 += w.x * wV[8 - jj] + w.y * wR[9 - jj];
+                    aR0 += w.z * wV[7 - jj] + w.w * wR[8 - jj];
+                    aV1 += w.x * wV[9 - jj] + w.y * wR[10 - jj];
+                    aR1 += w.z * wV[8 - jj] + w.w * wR[9 - jj];
+                }
+            }
+            if (n + 1 < P1) {
+                *reinterpret_cast<int2 *>(Vo + n) = make_int2(ired<M>(aV0), ired<M>(aV1));
+                *reinterpret_cast<int2 *>(Ro + n) = make_int2(ired<M>(aR0), ired<M>(aR1));
+            } else if (n < P1) {
+                Vo[n] = ired<M>(aV0);
+                Ro[n] = ired<M>(aR0);
+            }
+            return;
+        }
         constexpr int WV = R + 32, WR = R + 34;
         int wV[WV], wR[WR];
 #pragma unroll
@@ -273,6 +361,7 @@ template <class PS, int M>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(RqJump<PS, M>::NT, 1) jump_cluster_kernel(InvArgs a) {
     using JS = RqJump<PS, M>;
     constexpr int P = PS::P, NT = JS::NT, PAD = JS::PAD, LEN = JS::LEN, NJ = JS::NJ, R = JS::R;
+    constexpr int RF = SNTRUP_JUMP_RF;
     extern __shared__ __align__(16) uint8_t smem[];
     int *buf = reinterpret_cast<int *>(smem + JS::OFF_BUF);           // [parity][poly][LEN]
     int4 *Us = reinterpret_cast<int4 *>(smem + JS::OFF_U);
@@ -360,12 +449,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(RqJump<PS, M>::NT, 1
 #if SNTRUP_JUMP_MODE == 1
                 const int nit = 0;
 #else
-                const int nit = A / R;
+                const int nit = A / RF;
 #endif
 #pragma unroll 1
                 for (int it = ta; it < nit; it += JS::NA0) {
-                    if (s == JS::J) JS::template apply_fg<true>(B(b, 0), B(b, 1), B(o, 0), B(o, 1), U, R * it, s);
-                    else JS::template apply_fg<false>(B(b, 0), B(b, 1), B(o, 0), B(o, 1), U, R * it, s);
+                    if (s == JS::J) JS::template apply_fg<true, RF>(B(b, 0), B(b, 1), B(o, 0), B(o, 1), U, RF * it, s);
+                    else JS::template apply_fg<false, RF>(B(b, 0), B(b, 1), B(o, 0), B(o, 1), U, RF * it, s);
                 }
                 // beyond this jump's bound: clear what jump k-2 left in this buffer
                 for (int i = A + ta; i < Aold; i += JS::NA0) {
