@@ -41,13 +41,16 @@
 #ifndef SNTRUP_JUMP_RF
 #define SNTRUP_JUMP_RF 2          // (f, g) outputs per applier item (2 or 4; A/B)
 #endif
+#ifndef SNTRUP_JUMP_PREP4
+#define SNTRUP_JUMP_PREP4 1       // prep sums in 4 independent chains (3.1k vs 3.2k cycles per jump)
+#endif
 #ifndef SNTRUP_JUMP_CHUNKED
 #define SNTRUP_JUMP_CHUNKED 0     // appliers' tap loop rolled in chunks of 8 (A/B: not faster)
 #endif
 #ifndef SNTRUP_JUMP_UNROLL
-#define SNTRUP_JUMP_UNROLL 4      // decision-loop unroll factor: 4 (3.2k cycles per jump) beats full
-                                  // unrolling (4.0k: the 16 KB loop thrashes the instruction caches
-                                  // shared with the appliers) and 1 (3.6k)
+#define SNTRUP_JUMP_UNROLL 8      // decision-loop unroll factor: 4-8 (3.1-3.2k cycles per jump) beats
+                                  // full unrolling (4.0k: the 16 KB loop thrashes the instruction
+                                  // caches shared with the appliers) and 1 (3.6k)
 #endif
 #ifndef SNTRUP_JUMP_MODE
 #define SNTRUP_JUMP_MODE 0        // timing experiments: 1 = decisions only, 2 = applications only
@@ -423,6 +426,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(RqJump<PS, M>::NT, 1
                 if (k + 1 < NJ) {
                     // low 32 coefficients of the next f, g: f'[i] = sum_j u00[j] f[i+s-j] + u01[j] g[i+s-j]
                     const int *Fb = B(b, 0) + lane + s, *Gb = B(b, 1) + lane + s;
+#if SNTRUP_JUMP_PREP4
+                    int af[4] = {0, 0, 0, 0}, ag[4] = {0, 0, 0, 0};             // 4 chains each
+#pragma unroll
+                    for (int j = 0; j < 32; j++) {
+                        const int4 w = Us[b * 32 + j];
+                        const int fv = Fb[-j], gv = Gb[-j];
+                        af[j & 3] += w.x * fv + w.y * gv;
+                        ag[j & 3] += w.z * fv + w.w * gv;
+                    }
+                    Ff = (float)ired<M>((af[0] + af[1]) + (af[2] + af[3]));
+                    Gf = (float)ired<M>((ag[0] + ag[1]) + (ag[2] + ag[3]));
+#else
                     int af = 0, ag = 0;
 #pragma unroll
                     for (int j = 0; j < 32; j++) {
@@ -433,6 +448,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(RqJump<PS, M>::NT, 1
                     }
                     Ff = (float)ired<M>(af);
                     Gf = (float)ired<M>(ag);
+#endif
                 }
                 JTRACE(k, 3);
             }

@@ -574,7 +574,7 @@ __global__ void __launch_bounds__(NT, (ST == 1 ? TcGeom<PS, LA, LB, NPR, MM>::MI
         const uint64_t bd0 = umma_desc(smem_u32(sm + OFF_B + b * G::B_BYTES), G::BLD * 16, 128);
         const uint64_t ad0 = umma_desc(smem_u32(sm + b * ASTG) + 16, 256, 128);
         const uint32_t acc = tmem + (uint32_t)(b * LA * G::NB);
-#pragma unroll
+#pragma unroll 1
         for (int ks = 0; ks < G::NKS; ks++) {
             const uint64_t bd = bd0 + (uint64_t)((ks * 32 * G::BLD) >> 4);
 #pragma unroll
