@@ -227,25 +227,41 @@ def other_configs(S, torch, timed):
     P = S.params(761)
     pk = torch.empty((32, P["pk_bytes"]), dtype=torch.uint8, device="cuda")
     sk = torch.empty((32, P["sk_bytes"]), dtype=torch.uint8, device="cuda")
-    # latency-tuned: B = 1 (each key's reciprocals by its own divstep chain, all 32 in parallel:
-    # no tree levels on the critical path) with the R/3 and R/q chains on separate streams;
-    # the one-tree B = 32 configuration beside it (scripts/latency_sweep.py sweeps B)
+    # latency-tuned: B = 1 (each key's reciprocals by its own root chain -- jump-divsteps -- all 32
+    # in parallel: no tree levels on the critical path) with the R/3 and R/q chains on separate
+    # streams, replayed as a CUDA graph (SNTRUP_OPT_GRAPH: captured on the first call, seed and
+    # first key index patched per call); the same call without the graph and the one-tree B = 32
+    # configuration beside it (scripts/latency_sweep.py sweeps B)
+    st = torch.cuda.Stream()
+    l2flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
     def lat_of(B, fl):
-        for _ in range(5):
-            S.batch_keygen(761, 32, 1, batch_size=B, pk_out=pk, sk_out=sk, flags=fl)
-        torch.cuda.synchronize()
-        lat = []
-        for _ in range(20):
-            t0 = time.perf_counter()
-            S.batch_keygen(761, 32, 1, batch_size=B, pk_out=pk, sk_out=sk, flags=fl)   # synchronous call
-            lat.append((time.perf_counter() - t0) * 1e6)
-        dev_ms = timed(lambda: S.batch_keygen(761, 32, 1, batch_size=B, pk_out=pk, sk_out=sk,
-                                              flags=fl | S.OPT_ASYNC), 10) / 10
+        with torch.cuda.stream(st):
+            call = lambda f2: S.batch_keygen(761, 32, 1, batch_size=B, pk_out=pk, sk_out=sk, flags=f2, stream=st)
+            for _ in range(5):
+                call(fl)
+            torch.cuda.synchronize()
+            lat = []
+            for _ in range(20):
+                t0 = time.perf_counter()
+                call(fl)                                           # synchronous call
+                lat.append((time.perf_counter() - t0) * 1e6)
+            # device time on the call's stream, L2 flushed before each call (not timed)
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
+            for e0, e1 in ev:
+                l2flush.zero_()
+                e0.record(st)
+                call(fl | S.OPT_ASYNC)
+                e1.record(st)
+            torch.cuda.synchronize()
+            dev_ms = sum(e0.elapsed_time(e1) for e0, e1 in ev) / len(ev)
         return statistics.median(lat), dev_ms * 1e3
+    lg, dg = lat_of(1, S.OPT_RING_STREAMS | S.OPT_GRAPH)
     l1, d1 = lat_of(1, S.OPT_RING_STREAMS)
     l32, d32 = lat_of(32, 0)
-    out["configs[0]"] = {"workload": "sntrup761, 32 keys, seed 1, B = 1, ring streams (latency-tuned)",
-                         "latency_us_median": l1, "device_us": d1, "keys_per_s": 32 / (l1 / 1e6),
+    out["configs[0]"] = {"workload": "sntrup761, 32 keys, seed 1, B = 1, ring streams, CUDA graph (latency-tuned)",
+                         "latency_us_median": lg, "device_us": dg, "keys_per_s": 32 / (lg / 1e6),
+                         "without_graph": {"latency_us_median": l1, "device_us": d1},
                          "one_tree_B32": {"latency_us_median": l32, "device_us": d32}}
     # configs[3]: parameter sweep at 65,536 keys, seed 4
     sweep = {}

@@ -92,6 +92,18 @@ int sntrup_batch_keygen(int param_set, uint64_t n_keys, uint64_t seed,
 #define SNTRUP_OPT_LANE_PRIORITY  64u /* lanes on internal streams of decreasing priority: the
                                          first lane's chunk completes first (its D2H copies overlap
                                          the other lanes' compute); outputs identical */
+#define SNTRUP_OPT_GRAPH         512u /* replay the call as a CUDA graph: the first call of a shape
+                                         (param set, n, B, chunk, flags, stream, output / debug
+                                         pointers, workspace) runs normally and then captures its
+                                         launches on every stream of the call into a graph; later
+                                         calls of that shape patch the seed and first key index into
+                                         the captured sampler / repair kernels and launch the graph.
+                                         Device outputs on a non-default stream only (no host
+                                         outputs, stats or done_event: SNTRUP_E_ARG); the graph is
+                                         rebuilt when the stream's workspace is reallocated and
+                                         dropped by sntrup_release_[stream_]workspace.  Outputs
+                                         identical; for launch-bound calls (configs[0]) it removes
+                                         the host enqueue and inter-stream latency. */
 
 typedef struct {
     uint64_t first_key_index; /* keys first .. first+n-1 (chunked / resumable / multi-GPU runs) */

@@ -40,6 +40,7 @@ OPT_LANES4 = 32
 OPT_LANE_PRIORITY = 64
 OPT_STAGGER = 128
 OPT_SERIAL = 256
+OPT_GRAPH = 512         # replay the call as a CUDA graph (captured per call shape)
 
 PARAM_SETS = (653, 761, 857, 953, 1013, 1277)
 

@@ -322,6 +322,8 @@ void sntrup_release_workspace(void) {
     }
     cudaSetDevice(cur);
     g_ws = nullptr;
+    ++g_ws_epoch;
+    graphs_release();
 }
 
 int sntrup_release_stream_workspace(void *stream) {
@@ -331,6 +333,8 @@ int sntrup_release_stream_workspace(void *stream) {
     const auto key = std::make_pair(dev, (uintptr_t)stream);
     CK(cudaStreamSynchronize((cudaStream_t)stream));
     for (cudaStream_t cs : g_copy_streams) CK(cudaStreamSynchronize(cs));
+    graphs_release((uintptr_t)stream, false);
+    ++g_ws_epoch;
     auto it = g_wsmap.find(key);
     if (it != g_wsmap.end() && it->second.base) {
         // the workspace held secret f, 1/g and tree rows: erase before freeing

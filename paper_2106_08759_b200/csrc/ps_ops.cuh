@@ -7,6 +7,7 @@ namespace sntrup_rt {
 
 template <class PS>
 int PsOps<PS>::keygen(uint64_t n, uint64_t seed, uint8_t *pk, uint8_t *sk, const sntrup_keygen_opts &o) {
+    if (o.flags & SNTRUP_OPT_GRAPH) return keygen_graph<PS>(n, seed, pk, sk, o);
     return keygen_impl<PS>(n, seed, pk, sk, o);
 }
 template <class PS>

@@ -389,6 +389,9 @@ struct Workspace {
     int dev = -1;
 };
 inline std::map<std::pair<int, uintptr_t>, Workspace> g_wsmap;
+// bumped whenever a cached workspace is (re)allocated or released: captured keygen graphs
+// (SNTRUP_OPT_GRAPH) hold workspace pointers and are rebuilt when it changes
+inline uint64_t g_ws_epoch = 1;
 inline Workspace *g_ws = nullptr;
 inline Workspace g_user_ws;                          // a caller-supplied workspace (opts.workspace)
 
@@ -419,6 +422,7 @@ inline int ws_reserve(size_t bytes, cudaStream_t stream, void *user = nullptr, s
         w.cap = 0;
     }
     size_t cap = ws_alloc_bytes(bytes);
+    ++g_ws_epoch;
     if (cudaMalloc(&w.base, cap) != cudaSuccess) {
         cudaGetLastError();
         w.base = nullptr;
@@ -1375,6 +1379,168 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
         }
     }
     return SNTRUP_OK;
+}
+
+// ------------------------------------------------------------------------------ CUDA graphs
+// SNTRUP_OPT_GRAPH: a keygen call's launches (every stream of the call: lanes, ring and aux
+// streams fork from and join into the caller's stream) are captured once per call shape into a
+// CUDA graph and replayed; the seed and first key index -- the only per-call values the kernels
+// read besides the shape -- are patched into the captured sampler / repair kernel nodes.  For
+// launch-bound calls (configs[0]: 32 keys) this removes the host enqueue and the inter-stream
+// dependency latency from the call.
+struct GraphKey {
+    int dev, p;
+    uint64_t n, chunk;
+    uint32_t B, flags;
+    uintptr_t stream, pk, sk, h, g, f, ginv, att, ws;
+    size_t wsb;
+    auto tie() const { return std::tie(dev, p, n, chunk, B, flags, stream, pk, sk, h, g, f, ginv, att, ws, wsb); }
+    bool operator<(const GraphKey &o) const { return tie() < o.tie(); }
+};
+struct GraphArgNode {
+    cudaGraphNode_t node;
+    cudaKernelNodeParams prm;
+    int kind;                     // 1 sampler, 2 repair
+    uint64_t first_rel;           // the node's first key index - the call's
+    SampleArgs sa;
+    RepairArgs ra;
+};
+struct KeygenGraph {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    uint64_t epoch = 0;
+    uint64_t kernels = 0;
+    std::vector<GraphArgNode> nodes;
+    std::vector<int *> errs;
+};
+inline std::map<GraphKey, KeygenGraph> g_graphs;
+
+inline void graph_destroy(KeygenGraph &G) {
+    if (G.exec) cudaGraphExecDestroy(G.exec);
+    if (G.graph) cudaGraphDestroy(G.graph);
+    G.exec = nullptr;
+    G.graph = nullptr;
+}
+inline void graphs_release(uintptr_t stream = 0, bool all = true) {
+    for (auto it = g_graphs.begin(); it != g_graphs.end();) {
+        if (all || it->first.stream == stream) {
+            graph_destroy(it->second);
+            it = g_graphs.erase(it);
+        } else {
+            ++it;
+        }
+    }
+}
+
+// the synchronous tail of a keygen call (as keygen_impl's): the lanes' error flags
+inline int keygen_finish(const sntrup_keygen_opts &o, const std::vector<int *> &errs, cudaStream_t s0) {
+    if (o.flags & SNTRUP_OPT_ASYNC) return SNTRUP_OK;
+    int herr[MAX_LANES] = {};
+    for (size_t li = 0; li < errs.size() && li < (size_t)MAX_LANES; li++)
+        CK(cudaMemcpyAsync(&herr[li], errs[li], sizeof(int), cudaMemcpyDeviceToHost, s0));
+    CK(cudaStreamSynchronize(s0));
+    for (size_t li = 0; li < errs.size() && li < (size_t)MAX_LANES; li++)
+        if (herr[li]) return SNTRUP_E_INTERNAL;
+    return SNTRUP_OK;
+}
+
+template <class PS>
+int keygen_graph(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out, const sntrup_keygen_opts &o) {
+    // device outputs on a non-default stream; no per-call host state (stats, host outputs)
+    if ((o.flags & (SNTRUP_OPT_HOST_OUTPUT | SNTRUP_OPT_SERIAL)) || o.stats_out || o.done_event || !o.stream)
+        return SNTRUP_E_ARG;
+    int dev;
+    CK(cudaGetDevice(&dev));
+    const cudaStream_t s0 = (cudaStream_t)o.stream;
+    sntrup_keygen_opts oa = o;
+    oa.flags = (o.flags & ~SNTRUP_OPT_GRAPH) | SNTRUP_OPT_ASYNC;
+    const GraphKey key{dev, PS::P, n, o.chunk_keys, o.batch_size, o.flags, (uintptr_t)s0, (uintptr_t)pk_out,
+                       (uintptr_t)sk_out, (uintptr_t)o.h_out, (uintptr_t)o.g_out, (uintptr_t)o.f_out,
+                       (uintptr_t)o.ginv_out, (uintptr_t)o.attempts_out, (uintptr_t)o.workspace, o.workspace_bytes};
+    auto it = g_graphs.find(key);
+    if (it != g_graphs.end() && it->second.epoch != g_ws_epoch) {      // workspace moved: rebuild
+        graph_destroy(it->second);
+        g_graphs.erase(it);
+        it = g_graphs.end();
+    }
+    if (it == g_graphs.end()) {
+        // first call of this shape: run it (reserves the workspace, produces this call's keys),
+        // then capture the same enqueue sequence without executing it
+        int rc = keygen_impl<PS>(n, seed, pk_out, sk_out, oa);
+        if (rc) return rc;
+        const std::vector<int *> errs = g_async_err[std::make_pair(dev, (uintptr_t)s0)];
+        const uint64_t epoch = g_ws_epoch;
+        const uint64_t l0 = g_launches.load();
+        CK(cudaStreamBeginCapture(s0, cudaStreamCaptureModeThreadLocal));
+        const int rc2 = keygen_impl<PS>(n, seed, pk_out, sk_out, oa);
+        cudaGraph_t graph = nullptr;
+        const cudaError_t ce = cudaStreamEndCapture(s0, &graph);
+        g_launches.store(l0);
+        if (rc2 || ce != cudaSuccess || !graph || g_ws_epoch != epoch) {
+            if (graph) cudaGraphDestroy(graph);
+            cudaGetLastError();
+            return rc2 ? rc2 : SNTRUP_E_CUDA;
+        }
+        KeygenGraph G;
+        G.graph = graph;
+        G.epoch = epoch;
+        G.errs = errs;
+        if (cudaGraphInstantiate(&G.exec, graph, 0) != cudaSuccess) {
+            graph_destroy(G);
+            cudaGetLastError();
+            return SNTRUP_E_CUDA;
+        }
+        size_t nn = 0;
+        CK(cudaGraphGetNodes(graph, nullptr, &nn));
+        std::vector<cudaGraphNode_t> nodes(nn);
+        CK(cudaGraphGetNodes(graph, nodes.data(), &nn));
+        for (cudaGraphNode_t nd : nodes) {
+            cudaGraphNodeType t;
+            CK(cudaGraphNodeGetType(nd, &t));
+            if (t != cudaGraphNodeTypeKernel) continue;
+            G.kernels++;
+            GraphArgNode a{};
+            a.node = nd;
+            CK(cudaGraphKernelNodeGetParams(nd, &a.prm));
+            if (a.prm.func == (void *)sample_kernel<PS>) {
+                a.kind = 1;
+                a.sa = *(const SampleArgs *)a.prm.kernelParams[0];
+                if (a.sa.seed != seed) { graph_destroy(G); return SNTRUP_E_INTERNAL; }
+                a.first_rel = a.sa.first - o.first_key_index;
+            } else if (a.prm.func == (void *)repair_kernel<PS>) {
+                a.kind = 2;
+                a.ra = *(const RepairArgs *)a.prm.kernelParams[0];
+                if (a.ra.seed != seed) { graph_destroy(G); return SNTRUP_E_INTERNAL; }
+                a.first_rel = a.ra.first - o.first_key_index;
+            } else {
+                continue;
+            }
+            G.nodes.push_back(a);
+        }
+        g_graphs[key] = std::move(G);
+        return keygen_finish(o, errs, s0);
+    }
+    KeygenGraph &G = it->second;
+    for (GraphArgNode &a : G.nodes) {
+        void *args[1];
+        if (a.kind == 1) {
+            a.sa.seed = seed;
+            a.sa.first = o.first_key_index + a.first_rel;
+            args[0] = &a.sa;
+        } else {
+            a.ra.seed = seed;
+            a.ra.first = o.first_key_index + a.first_rel;
+            args[0] = &a.ra;
+        }
+        cudaKernelNodeParams prm = a.prm;
+        prm.kernelParams = args;
+        prm.extra = nullptr;
+        CK(cudaGraphExecKernelNodeSetParams(G.exec, a.node, &prm));
+    }
+    CK(cudaGraphLaunch(G.exec, s0));
+    g_launches.fetch_add(G.kernels, std::memory_order_relaxed);
+    g_async_err[std::make_pair(dev, (uintptr_t)s0)] = G.errs;
+    return keygen_finish(o, G.errs, s0);
 }
 
 // ------------------------------------------------------------------------------ small kernels

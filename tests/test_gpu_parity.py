@@ -101,6 +101,53 @@ def test_keygen_root_impls(O, impl):
     check_keys(O, 761, 1, lat, np.arange(32))
 
 
+def test_graph_mode_configs0(O):
+    # SNTRUP_OPT_GRAPH: first call of a shape runs and captures, later calls replay with the seed
+    # and first key index patched in; the stream's workspace release drops the graph (rebuilt)
+    P = S.params(761)
+    s = torch.cuda.Stream()
+    pk = torch.empty((32, P["pk_bytes"]), dtype=torch.uint8, device="cuda")
+    sk = torch.empty((32, P["sk_bytes"]), dtype=torch.uint8, device="cuda")
+    fl = S.OPT_RING_STREAMS | S.OPT_GRAPH
+    for seed, first in ((1, 0), (1, 0), (9, 0), (9, 1000), (3, 77)):
+        S.batch_keygen(761, 32, seed, batch_size=1, first_key_index=first, pk_out=pk, sk_out=sk, flags=fl,
+                       stream=s)
+        s.synchronize()
+        ref = oracle_keys(O, 761, seed, np.arange(first, first + 32))
+        assert np.array_equal(pk.cpu().numpy(), ref["pk"]) and np.array_equal(sk.cpu().numpy(), ref["sk"]), (seed, first)
+    S.release_stream_workspace(s)
+    S.batch_keygen(761, 32, 5, batch_size=1, pk_out=pk, sk_out=sk, flags=fl, stream=s)
+    s.synchronize()
+    ref = oracle_keys(O, 761, 5, np.arange(32))
+    assert np.array_equal(pk.cpu().numpy(), ref["pk"]) and np.array_equal(sk.cpu().numpy(), ref["sk"])
+
+
+def test_graph_mode_trees_and_repair(O):
+    # a graph with product trees, several chunks and the repair kernel (653 draws non-invertible
+    # g often enough with the small test off), replayed with new seeds
+    P = S.params(653)
+    s = torch.cuda.Stream()
+    n = 300
+    pk = torch.empty((n, P["pk_bytes"]), dtype=torch.uint8, device="cuda")
+    sk = torch.empty((n, P["sk_bytes"]), dtype=torch.uint8, device="cuda")
+    fl = S.OPT_RING_STREAMS | S.OPT_GRAPH | S.OPT_NO_SMALL_CHECK
+    for seed, first in ((4, 0), (4, 0), (6, 300), (8, 12345)):
+        S.batch_keygen(653, n, seed, batch_size=16, chunk_keys=128, first_key_index=first, pk_out=pk, sk_out=sk,
+                       flags=fl, stream=s)
+        s.synchronize()
+        ref = oracle_keys(O, 653, seed, np.arange(first, first + n))
+        assert np.array_equal(pk.cpu().numpy(), ref["pk"]) and np.array_equal(sk.cpu().numpy(), ref["sk"]), (seed, first)
+
+
+def test_graph_mode_rejects_host_outputs():
+    P = S.params(761)
+    s = torch.cuda.Stream()
+    pk = torch.empty((32, P["pk_bytes"]), dtype=torch.uint8).pin_memory()
+    sk = torch.empty((32, P["sk_bytes"]), dtype=torch.uint8).pin_memory()
+    with pytest.raises((S.SntrupError, ValueError)):
+        S.batch_keygen(761, 32, 1, pk_out=pk, sk_out=sk, flags=S.OPT_GRAPH | S.OPT_HOST_OUTPUT, stream=s)
+
+
 def test_chunking_and_first_index(O):
     n, first = 200, 1000
     res = S.batch_keygen(761, n, 3, batch_size=16, chunk_keys=48, first_key_index=first, debug=True)
