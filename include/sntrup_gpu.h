@@ -272,7 +272,9 @@ int sntrup_release_stream_workspace(void *stream);
 /* Measurement hook: n ring products at p' = 383 --
    one sub-product of a one-level Karatsuba split of a 761 product -- through the same tensor-core
    kernels as the 761 products.  kind 0: R/3 (int8 rows of 384, fp4 MMAs); kind 1: R/q big x big
-   mod 4591 (int16 rows of 384, int8 2 x 2 limbs).  Device pointers; stream-ordered. */
+   mod 4591 (int16 rows of 384, int8 2 x 2 limbs); kinds 2 / 3: R/3 at p' = 255 / 257 (int8 rows
+   of 256 / 272), the sub-product sizes of the paper's 5-way R/3 multiplier.  Device
+   pointers; stream-ordered.  SNTRUP_OK / SNTRUP_E_ARG. */
 int sntrup_probe_half_mul(int kind, uint64_t n, const void *a, const void *b, void *c, void *stream);
 
 /* Integer-pipe peak (measurement for bench.py's roofline; BASELINE metric "int-pipe % of peak"):

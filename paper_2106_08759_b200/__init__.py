@@ -529,9 +529,10 @@ INT_OPS = ("IMAD", "IADD3", "LOP3", "SHF")
 
 def probe_half_mul(kind: int, a, b, c, stream=None):
     """Measurement hook: ring products at p' = 383 (one Karatsuba sub-product of a 761 product);
-    kind 0 = R/3 (int8 [n][384]), 1 = R/q big x big (int16 [n][384])."""
+    kind 0 = R/3 (int8 [n][384]), 1 = R/q big x big (int16 [n][384]); kinds 2 / 3 = R/3 at
+    p' = 255 / 257 (int8 [n][256] / [n][272]: the 5-way R/3 multiplier's sub-products)."""
     n = a.shape[0]
-    dt, w = (torch.int8, 384) if kind == 0 else (torch.int16, 384)
+    dt, w = {0: (torch.int8, 384), 1: (torch.int16, 384), 2: (torch.int8, 256), 3: (torch.int8, 272)}[kind]
     for t, nm in ((a, "a"), (b, "b"), (c, "c")):
         _need(t, dt, (n, w), nm)
     _check(_lib.sntrup_probe_half_mul(kind, n, _ptr(a), _ptr(b), _ptr(c), _stream(stream)), "sntrup_probe_half_mul")

@@ -42,7 +42,20 @@ def main():
     t383 = timeit(lambda: S.probe_half_mul(0, g2, h2, c2))
     out["r3_fp4"] = {"ms_761_product": t761, "ms_383_product": t383,
                      "karatsuba_lower_bound_ms": 3 * t383, "ratio_karatsuba_over_direct": 3 * t383 / t761}
-    del g, h, c3, g2, h2, c2
+    # the paper's 5-way R/3 multiplier: 4 sub-products of <= 254 coefficients (run
+    # at p' = 255) and H(x) of 256 (p' = 257)
+    g5 = torch.from_numpy(synth.small(n, 255, 256, seed=8)).cuda()
+    h5 = torch.from_numpy(synth.small(n, 255, 256, seed=9)).cuda()
+    c5 = torch.empty_like(g5)
+    g7 = torch.from_numpy(synth.small(n, 257, 272, seed=10)).cuda()
+    h7 = torch.from_numpy(synth.small(n, 257, 272, seed=11)).cuda()
+    c7 = torch.empty_like(g7)
+    t255 = timeit(lambda: S.probe_half_mul(2, g5, h5, c5))
+    t257 = timeit(lambda: S.probe_half_mul(3, g7, h7, c7))
+    out["r3_fp4_5way"] = {"ms_761_product": t761, "ms_255_product": t255, "ms_257_product": t257,
+                          "five_way_lower_bound_ms": 4 * t255 + t257,
+                          "ratio_five_way_over_direct": (4 * t255 + t257) / t761}
+    del g, h, c3, g2, h2, c2, g5, h5, c5, g7, h7, c7
     a = torch.from_numpy(synth.uniform_rq(n, 761, 4591, P["p8"], seed=1)).cuda()
     b = torch.from_numpy(synth.uniform_rq(n, 761, 4591, P["p8"], seed=2)).cuda()
     c = torch.empty_like(a)
@@ -53,8 +66,9 @@ def main():
     t383 = timeit(lambda: S.probe_half_mul(1, a2, b2, c2))
     out["rq_int8_big_x_big"] = {"ms_761_product": t761, "ms_383_product": t383,
                                 "karatsuba_lower_bound_ms": 3 * t383, "ratio_karatsuba_over_direct": 3 * t383 / t761}
-    out["note"] = ("2^20 products each; one-level Karatsuba = 3 sub-products of 383 coefficients "
-                   "(+ elementwise pre-adds and recombination, not counted)")
+    out["note"] = ("2^20 products each; one-level Karatsuba = 3 sub-products of 383 coefficients; the 5-way "
+                   "R/3 split = 4 of <= 254 (run at 255) + 1 of 256 (run at 257); elementwise pre-adds, "
+                   "interpolation and the x^2-1 divisions not counted")
     print(json.dumps(out, indent=1))
 
 

@@ -469,6 +469,24 @@ def test_rq_root_jump_vs_step(O, param):
     assert np.array_equal(outs[S.ROOT_JUMP], outs[S.ROOT_STEP])
 
 
+@pytest.mark.parametrize("kind,p,q,stride", [(0, 383, 3, 384), (1, 383, 4591, 384), (2, 255, 3, 256),
+                                             (3, 257, 3, 272)])
+def test_probe_split_products(O, kind, p, q, stride):
+    # the split-multiplier probes time real products: p' = 383 (Karatsuba halves), 255 / 257 (the
+    # 5-way R/3 split) against the oracle's schoolbook product mod x^p' - x - 1
+    n = 300
+    if q == 3:
+        a = synth.small(n, p, stride, seed=kind + 1)
+        b = synth.small(n, p, stride, seed=kind + 2)
+    else:
+        a = synth.uniform_rq(n, p, q, stride, seed=kind + 1)
+        b = synth.uniform_rq(n, p, q, stride, seed=kind + 2)
+    c = S.probe_half_mul(kind, torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(),
+                         torch.empty((n, stride), dtype=torch.int8 if q == 3 else torch.int16, device="cuda"))
+    ref = O.mul_many(p, q, a[:, :p].astype(np.int16), b[:, :p].astype(np.int16))
+    assert np.array_equal(c.cpu().numpy()[:, :p].astype(np.int16), ref[:, :p])
+
+
 def test_rq_recip_zero_reports_index():
     P = S.params(761)
     a = synth.uniform_rq(50, 761, 4591, P["p8"], seed=7)
