@@ -203,11 +203,11 @@ __device__ __forceinline__ void digits_rev8(const int (&vals)[8], uint32_t (&dw)
 // RING (with TA > 0): every K step's A rows go through the TA-column TMEM window in rounds of
 // NTA K steps (build rows -> tcgen05.st -> MMAs from TMEM -> wait -> next round); no A windows in
 // shared memory at all, so the shared-memory traffic per item is only the B operand and staging.
-#ifndef SNTRUP_TC4_MINB
-#define SNTRUP_TC4_MINB 1
-#endif
+// (an explicit minimum of 8 CTAs per SM, i.e. <= 64 registers, measured slower: 320 -> 310 M R/3
+// products/s; note __launch_bounds__(128, 1) is NOT the same as (128): it let ptxas raise the
+// R/3 kernels to 80 / 95 registers, 6 / 5 CTAs per SM, and the step lost 5%)
 template <class PS, int M, int LB, int NPR, bool XOPS = false, int TA = 0, bool RING = false>
-__global__ void __launch_bounds__(128, (TA == 0 && !XOPS) ? SNTRUP_TC4_MINB : 1) tc4_mul_kernel(MulArgs a) {
+__global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
     using G = Tc4Geom<PS, LB, NPR, TA>;
     static_assert(!RING || TA > 0, "RING streams A through TMEM");
     constexpr int P = PS::P;
