@@ -652,7 +652,9 @@ int launch_tc4w(const MulArgs &a, cudaStream_t s) {
 }
 
 template <class PS, int M, int LB, int NPR = 1>
-int launch_tc4(const MulArgs &a, cudaStream_t s) {
+int launch_tc4(const MulArgs &a0, cudaStream_t s) {
+    MulArgs a = a0;
+    a.trace = g_ws_trace;                                 // phase timing in SNTRUP_WS_TRACE builds
     if (mul_xops(a)) return launch_tc4_impl<PS, M, LB, 1, true>(a, s);   // KEM: one product per item
     if constexpr (LB == 1) {
         // (int8 operand rows only: the kernel bulk-copies raw rows)

@@ -267,30 +267,36 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
         if (it >= a.n_out) return;
         TcWork<NPR> &w = wn;
         tc_work<NPR>(a, it, w);
+        const Opnd du = opnd_or_zero(w.du, w.unit_u);
 #pragma unroll
         for (int h = 0; h < CH; h++) {
             const int c = tid + 128 * h;
-            if (c < G::NCHK) pu[h] = w.unit_u ? make_uint4(0, 0, 0, 0) : load_chunk(w.du, c);
+            if (c < G::NCHK) pu[h] = load_chunk(du, c);
             const int cs = c == G::NCHK ? -1 : c;
 #pragma unroll
             for (int pp = 0; pp < NPR; pp++) {
-                const bool none = w.unit_v[pp] || (pp > 0 && w.orow[pp] < 0);
-                if (c < G::NCHK) pv[pp][h] = none ? make_uint4(0, 0, 0, 0) : load_chunk(w.dv[pp], c);
-                if (c <= G::NCHK && cs < G::NCHK - 1)
-                    pn[pp][h] = none ? make_uint4(0, 0, 0, 0) : load_chunk(w.dv[pp], cs + 1);
+                const Opnd dv = opnd_or_zero(w.dv[pp], w.unit_v[pp] || (pp > 0 && w.orow[pp] < 0));
+                if (c < G::NCHK) pv[pp][h] = load_chunk(dv, c);
+                if (c <= G::NCHK && cs < G::NCHK - 1) pn[pp][h] = load_chunk(dv, cs + 1);
             }
         }
-        if (tid == 0) {
-            pa1 = opnd_coef<XOPS>(w.du, w.unit_u, P - 1);
+        if (tid == 0) {                                   // raw: decoded when staged (coef_fin)
+            pa1 = load_raw(du, P - 1);
 #pragma unroll
             for (int pp = 0; pp < NPR; pp++)
-                pb1[pp] = (pp > 0 && w.orow[pp] < 0) ? 0 : opnd_coef<XOPS>(w.dv[pp], w.unit_v[pp], P - 1);
+                pb1[pp] = load_raw(opnd_or_zero(w.dv[pp], w.unit_v[pp] || (pp > 0 && w.orow[pp] < 0)), P - 1);
         }
     };
     // ---- stage digits of work item w (registers -> hA / Z staging, which the MMAs do not read)
     auto stage = [&](const TcWork<NPR> &w, int (&fixab)[NPR]) {
 #pragma unroll
         for (int pp = 0; pp < NPR; pp++) fixab[pp] = 0;
+        if (tid == 0) {                                   // the prefetched raw scalars u[p-1], v[p-1]
+            pa1 = coef_fin<XOPS>(w.du, w.unit_u, P - 1, pa1);
+#pragma unroll
+            for (int pp = 0; pp < NPR; pp++)
+                pb1[pp] = (pp > 0 && w.orow[pp] < 0) ? 0 : coef_fin<XOPS>(w.dv[pp], w.unit_v[pp], P - 1, pb1[pp]);
+        }
             // ---- stage digits: one 32-bit word (8 nibbles) per 8 coefficients
 #pragma unroll
             for (int h = 0; h < CH; h++) {
@@ -389,13 +395,23 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
         stage(w, fixab);
         prefetch(blockIdx.x + gridDim.x);
     }
+#ifdef SNTRUP_WS_TRACE
+    // phase timing (trace build): thread 0's clock between the loop's barriers, summed per CTA
+    unsigned long long tph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long tq = clock64();
+#define TC4_PH(i) do { if (tid == 0) { const long long t_ = clock64(); tph[i] += t_ - tq; tq = t_; } } while (0)
+#else
+#define TC4_PH(i) do { } while (0)
+#endif
     for (long long it = blockIdx.x; it < a.n_out; it += gridDim.x) {
         const long long nx = it + gridDim.x;
         if constexpr (!ES) {
             w = wn;
             stage(w, fixab);
         }
+        TC4_PH(0);
         __syncthreads();
+        TC4_PH(1);
         if constexpr (TA && !RING) {
             // ---- A rows into TMEM: lane r, K step ks = nibbles [1 + r + 64 ks, +64) of hA (the row the
             // shared-memory descriptor below starts at), 8 columns of 8 nibbles
@@ -526,6 +542,7 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
             umma_commit_w(bar);
         }
         }
+        TC4_PH(2);
         const TcWork<NPR> nxt = wn;
         int fnx[NPR];
 #pragma unroll
@@ -533,14 +550,18 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
         if constexpr (ES) {
             if (nx < a.n_out) {
                 stage(nxt, fnx);
+                TC4_PH(7);
                 prefetch(nx + gridDim.x);
             }
         } else {
             prefetch(nx);
         }
+        TC4_PH(3);
         if (tid == 0) mbar_wait(bar, phase);
+        TC4_PH(4);
         phase ^= 1;
         __syncthreads();
+        TC4_PH(5);
         tc_fence_after();
         // ---- epilogue: thread tid = TMEM lane = coefficient r of every block, straight to HBM
         const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
@@ -590,12 +611,21 @@ __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
             else store(reinterpret_cast<int8_t *>(orp));
         }
         tc_fence_before();
+        TC4_PH(6);
         if constexpr (ES) {
             w = nxt;
 #pragma unroll
             for (int pp = 0; pp < NPR; pp++) fixab[pp] = fnx[pp];
         }
     }
+#ifdef SNTRUP_WS_TRACE
+    if (tid == 0 && a.trace && TA == 0) {
+        unsigned long long *tr = a.trace + (blockIdx.x % 160) * 16;
+        for (int i = 0; i < 8; i++) atomicAdd(tr + 8 + i, tph[i]);
+        atomicAdd(tr, (unsigned long long)((a.n_out - blockIdx.x + gridDim.x - 1) / gridDim.x));
+    }
+#endif
+#undef TC4_PH
     tc_fence_before();
     __syncthreads();
     if (warp == 0)

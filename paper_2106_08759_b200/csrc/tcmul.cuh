@@ -248,6 +248,28 @@ __device__ __forceinline__ uint4 load_chunk(const Opnd &d, int c) {
     return make_uint4(v.x, v.y, 0, 0);
 }
 
+// Prefetch without waiting: the prefetches issue loads whose results are consumed an iteration
+// later, so nothing in them may depend on a loaded value.  An absent or unit operand (whose data
+// the decode ignores) loads from this zero row instead of selecting a zero VALUE after the load
+// (a select on the value made every prefetch wait for global-memory latency: 2.5k of 5.4k cycles
+// per fp4 item, scripts/tc4_phase_trace.py); the scalar coefficient is loaded raw and decoded
+// (unit, scale, mod-3) when staged.
+__device__ uint4 g_zero_rows[192];                       // 3 KB >= the longest row (1280 x int16)
+__device__ __forceinline__ Opnd opnd_or_zero(const Opnd &d, bool none) {
+    Opnd o = d;
+    o.row = none ? reinterpret_cast<const uint8_t *>(g_zero_rows) : d.row;
+    return o;
+}
+__device__ __forceinline__ int load_raw(const Opnd &d, int k) {
+    return d.bytes == 1 ? (int)((const int8_t *)d.row)[k] : (int)((const int16_t *)d.row)[k];
+}
+template <bool XOPS>
+__device__ __forceinline__ int coef_fin(const Opnd &d, bool unit, int k, int raw) {
+    if (unit) return k == 0 ? 1 : 0;
+    const int v = raw * d.scale;
+    return (XOPS && d.mod3) ? canon<3>(v) : v;
+}
+
 // coefficient k of an operand row (decoded: scale, optional mod-3 pre-op)
 template <bool XOPS>
 __device__ __forceinline__ int opnd_coef(const Opnd &d, bool unit, int k) {
@@ -417,24 +439,24 @@ __global__ void __launch_bounds__(NT, (ST == 1 ? TcGeom<PS, LA, LB, NPR, MM>::MI
         if (it >= a.n_out) return;
         TcWork<NPR> &w = wn;
         tc_work<NPR>(a, it, w);
+        const Opnd du = opnd_or_zero(w.du, w.unit_u);
 #pragma unroll
         for (int h = 0; h < CH; h++) {
             const int c = tid + NT * h;
-            if (c < G::NCHK) pu[h] = w.unit_u ? make_uint4(0, 0, 0, 0) : load_chunk(w.du, c);
+            if (c < G::NCHK) pu[h] = load_chunk(du, c);
             const int cs = c == G::NCHK ? -1 : c;                // thread NCHK: s-group -1
 #pragma unroll
             for (int pp = 0; pp < NPR; pp++) {
-                const bool none = w.unit_v[pp] || (pp > 0 && w.orow[pp] < 0);
-                if (c < G::NCHK) pv[pp][h] = none ? make_uint4(0, 0, 0, 0) : load_chunk(w.dv[pp], c);
-                if (c <= G::NCHK && cs < G::NCHK - 1)
-                    pn[pp][h] = none ? make_uint4(0, 0, 0, 0) : load_chunk(w.dv[pp], cs + 1);
+                const Opnd dv = opnd_or_zero(w.dv[pp], w.unit_v[pp] || (pp > 0 && w.orow[pp] < 0));
+                if (c < G::NCHK) pv[pp][h] = load_chunk(dv, c);
+                if (c <= G::NCHK && cs < G::NCHK - 1) pn[pp][h] = load_chunk(dv, cs + 1);
             }
         }
-        if (tid == 0) {
-            pa1 = opnd_coef<XOPS>(w.du, w.unit_u, P - 1);
+        if (tid == 0) {                                       // raw: decoded when staged (coef_fin)
+            pa1 = load_raw(du, P - 1);
 #pragma unroll
             for (int pp = 0; pp < NPR; pp++)
-                pb1[pp] = (pp > 0 && w.orow[pp] < 0) ? 0 : opnd_coef<XOPS>(w.dv[pp], w.unit_v[pp], P - 1);
+                pb1[pp] = load_raw(opnd_or_zero(w.dv[pp], w.unit_v[pp] || (pp > 0 && w.orow[pp] < 0)), P - 1);
         }
     };
 
@@ -443,6 +465,12 @@ __global__ void __launch_bounds__(NT, (ST == 1 ? TcGeom<PS, LA, LB, NPR, MM>::MI
     auto stage = [&](const TcWork<NPR> &w, int (&fixab)[NPR], int b) {
 #pragma unroll
         for (int pp = 0; pp < NPR; pp++) fixab[pp] = 0;
+        if (tid == 0) {                                       // the prefetched raw scalars u[p-1], v[p-1]
+            pa1 = coef_fin<XOPS>(w.du, w.unit_u, P - 1, pa1);
+#pragma unroll
+            for (int pp = 0; pp < NPR; pp++)
+                pb1[pp] = (pp > 0 && w.orow[pp] < 0) ? 0 : coef_fin<XOPS>(w.dv[pp], w.unit_v[pp], P - 1, pb1[pp]);
+        }
 #pragma unroll
         for (int h = 0; h < CH; h++) {
             const int c = tid + NT * h;
