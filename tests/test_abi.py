@@ -82,6 +82,27 @@ def test_argument_errors_without_gpu(lib):
     S.set_mul_impl(S.MUL_TENSOR_CORE)
 
 
+def test_root_impl_knob_without_gpu(lib):
+    # sntrup_set_root_impl: 0 automatic, 1 one divstep at a time, 2 jump-divsteps, + 4 shared SMs
+    import paper_2106_08759_b200 as S
+    for v in (S.ROOT_AUTO, S.ROOT_STEP, S.ROOT_JUMP, S.ROOT_AUTO | S.ROOT_SHARED_SM,
+              S.ROOT_JUMP | S.ROOT_SHARED_SM, S.ROOT_STEP | S.ROOT_SHARED_SM):
+        assert S._lib.sntrup_set_root_impl(v) == S.SNTRUP_OK, v
+    for v in (-1, 3, 7, 8):
+        assert S._lib.sntrup_set_root_impl(v) == S.SNTRUP_E_ARG, v
+    with pytest.raises(S.SntrupError):
+        S.set_root_impl(3)
+    S.set_root_impl(S.ROOT_AUTO)
+
+
+def test_graph_flag_value():
+    # SNTRUP_OPT_GRAPH in the binding matches the header
+    import paper_2106_08759_b200 as S
+    txt = open(HEADER).read()
+    m = re.search(r"#define SNTRUP_OPT_GRAPH\s+(\d+)u", txt)
+    assert m and int(m.group(1)) == S.OPT_GRAPH == 512
+
+
 def test_full_sk_sizes_host_query(lib):
     import paper_2106_08759_b200 as S
     # App. D key-pair storage: pk + full sk = 2512 / 2921 / 3321
