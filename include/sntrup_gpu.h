@@ -312,7 +312,10 @@ uint64_t sntrup_kernel_launch_count(void);
    11 = as 0, with the small x small (fp4) products on the warp-specialised persistent kernel
        whose Hankel A operand is built in registers and written to TMEM (csrc/tc4w.cuh);
    12 = as 0, with every K step of the fp4 products' A operand streamed through a 64-column TMEM
-       window in rounds (no shared-memory A at all; 8 CTAs per SM).
+       window in rounds (no shared-memory A at all; 8 CTAs per SM);
+   13 = as 0, with the int8 one-product items (R/q up-sweep, rq_mul_batch, rq_mul_small_batch) in
+       the transposed Hankel form (csrc/tcxmul.cuh): 16 output coefficients per accumulator row,
+       the folded operand read by the MMAs as a view of its staging array at MMA M = 64.
    All are exact.  Variants 2-10 and 12 are compiled for sntrup761 only (other sets run 0, or 1 / 11);
    KEM pre/post-op calls always use the default kernel of their shape.  Returns SNTRUP_OK or
    SNTRUP_E_ARG. */

@@ -165,9 +165,10 @@ def _need(t, dtype, shape, name, host: bool = False):
 def batch_keygen(param_set: int, n_keys: int, seed: int, *, first_key_index: int = 0,
                  batch_size: int = 32, chunk_keys: int = 0, flags: int = 0, pk_out=None,
                  sk_out=None, debug: bool = False, stream=None, stats: bool = False, done_event=None,
-                 workspace=None):
+                 workspace=None, attempts: bool = False):
     """Generate n_keys key pairs (global indices first_key_index ..).  Returns dict with pk, sk
-    (uint8 CUDA tensors) and, with debug=True, h/g/f/ginv/attempts.  With host outputs,
+    (uint8 CUDA tensors) and, with debug=True, h/g/f/ginv/attempts (attempts=True: only the
+    per-key number of g draws, uint8 CUDA tensor).  With host outputs,
     flags OPT_ASYNC and a done_event (Event), the call returns after enqueueing and the event
     completes when every output byte is in host memory."""
     P = params(param_set)
@@ -195,6 +196,9 @@ def batch_keygen(param_set: int, n_keys: int, seed: int, *, first_key_index: int
         out["attempts"] = torch.zeros(n_keys, dtype=torch.uint8, device=dev)
         o.h_out, o.g_out, o.f_out = out["h"].data_ptr(), out["g"].data_ptr(), out["f"].data_ptr()
         o.ginv_out, o.attempts_out = out["ginv"].data_ptr(), out["attempts"].data_ptr()
+    elif attempts:
+        out["attempts"] = torch.zeros(n_keys, dtype=torch.uint8, device=dev)
+        o.attempts_out = out["attempts"].data_ptr()
     st = (ctypes.c_uint64 * 4)()
     if stats:
         o.stats_out = ctypes.addressof(st)
@@ -450,6 +454,7 @@ MUL_TENSOR_CORE_PIPELINED = 8     # int8 big x big products software-pipelined (
 MUL_TENSOR_CORE_TMEM_A = 9        # fp4 products: first K steps of the Hankel A operand in TMEM (128 cols)
 MUL_TENSOR_CORE_TMEM_A64 = 10     # as 9 with a 64-column TMEM allocation
 MUL_TENSOR_CORE_WS = 11           # warp-specialised persistent kernels, Hankel A written to TMEM
+MUL_TENSOR_CORE_TRANSPOSED = 13   # int8 one-product items in the transposed Hankel form (tcxmul.cuh)
 MUL_TENSOR_CORE_TMEM_RING = 12    # fp4: every K step's A rows through a 64-column TMEM window in rounds
 
 

@@ -36,6 +36,7 @@
 #include "tcmul.cuh"
 #include "tc4mul.cuh"
 #include "tc4w.cuh"
+#include "tcxmul.cuh"
 
 
 namespace sntrup_rt {
@@ -50,7 +51,7 @@ inline std::mutex g_mu;                                   // serialises calls (s
 // inversions).  Read back with sntrup_profile_read().
 enum ProfClass { PC_SAMPLE = 0, PC_MUL_R3, PC_MUL_RQ, PC_INV_R3, PC_INV_RQ, PC_REPAIR, PC_ENCODE,
                  PC_MISC, PC_N };
-struct ProfRec { int cls; cudaEvent_t a, b; double units, ops; int kind; double smem; };
+struct ProfRec { int cls; cudaEvent_t a, b; double units, ops; int kind; double smem; cudaStream_t s; };
 inline bool g_prof_on = false;
 inline std::vector<ProfRec> g_prof;
 inline std::vector<cudaEvent_t> g_evpool;
@@ -77,17 +78,32 @@ struct ProfScope {
         if (g_prof_on) { a = ev_get(); cudaEventRecord(a, s); }
     }
     ~ProfScope() {
-        if (a) { cudaEvent_t b = ev_get(); cudaEventRecord(b, s); g_prof.push_back(ProfRec{cls, a, b, units, ops, g_cur_kind, g_cur_smem}); }
+        if (a) { cudaEvent_t b = ev_get(); cudaEventRecord(b, s); g_prof.push_back(ProfRec{cls, a, b, units, ops, g_cur_kind, g_cur_smem, s}); }
         g_cur_kind = -1;
         g_cur_smem = 0;
     }
 };
 
 inline void prof_drain() {
+    // SNTRUP_TIMELINE=<file> (diagnostic): append one line per launch -- class, arithmetic kind,
+    // units, stream, and the times (ms, from the drain's first record) at which the launch became
+    // runnable on its stream (start event) and finished (end event); scripts/timeline.py
+    FILE *tl = nullptr;
+    if (!g_prof.empty()) {
+        const char *tp = getenv("SNTRUP_TIMELINE");
+        if (tp && *tp) tl = fopen(tp, "a");
+    }
     for (auto &r : g_prof) {
         cudaEventSynchronize(r.b);
         float ms = 0;
         cudaEventElapsedTime(&ms, r.a, r.b);
+        if (tl) {
+            float t0 = 0;
+            cudaEventSynchronize(g_prof.front().a);
+            cudaEventElapsedTime(&t0, g_prof.front().a, r.a);
+            fprintf(tl, "%d,%d,%.0f,%llx,%.4f,%.4f\n", r.cls, r.kind, r.units, (unsigned long long)(uintptr_t)r.s,
+                    t0, t0 + ms);
+        }
         g_agg[r.cls].ms += ms;
         g_agg[r.cls].units += r.units;
         g_agg[r.cls].ops += r.ops;
@@ -102,6 +118,7 @@ inline void prof_drain() {
         g_evpool.push_back(r.a);
         g_evpool.push_back(r.b);
     }
+    if (tl) { fprintf(tl, "#\n"); fclose(tl); }
     g_prof.clear();
 }
 
@@ -583,11 +600,42 @@ int launch_tc_impl(const MulArgs &a, cudaStream_t s) {
     return SNTRUP_OK;
 }
 
+// transposed form (tcxmul.cuh): one product per item, u = window operand (LA limbs), v = Z operand
+template <class PS, int M, int LA, int LB, int NPR = 1, bool XOPS = false>
+int launch_tcx_impl(const MulArgs &a, cudaStream_t s) {
+    using G = TcxGeom<PS, LA, LB, NPR>;
+    auto kern = tcx_mul_kernel<PS, M, LA, LB, NPR, XOPS>;
+    static std::map<int, int> per_sm;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    auto it = per_sm.find(dev);
+    if (it == per_sm.end()) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        it = per_sm.emplace(dev, resident_ctas(kern, G::SMEM, G::TCOLS)).first;
+    }
+    long long grid = (long long)it->second * dev_info().sms;
+    if (grid > a.n_out) grid = a.n_out;
+    g_cur_kind = PK_I8;
+    // per work item: NKS K steps x LB chains, each MMA reading an MM x 32-byte Z tile and an
+    // NB x 32-byte window tile from shared memory
+    g_cur_smem = (double)a.n_out * G::NKS * NPR * LB * (double)(G::MM * 32 + G::NB * 32);
+    kern<<<(unsigned)grid, 128, G::SMEM, s>>>(a);
+    LAUNCHED();
+    return SNTRUP_OK;
+}
+
 // KEM-core pre/post-ops need the XOPS instantiation (keygen never sets them)
 inline bool mul_xops(const MulArgs &a) { return a.round3 || a.X.mod3 || a.Y.mod3; }
 
 // KEM pre/post-ops exist only in one-product-per-item M = 128 instantiations (the shapes the KEM
 // core launches); an A/B variant asked to run them falls back to that kernel
+template <class PS, int M, int LA, int LB, int NPR = 1>
+int launch_tcx(const MulArgs &a, cudaStream_t s) {
+    if (mul_xops(a)) return launch_tcx_impl<PS, M, LA, LB, 1, true>(a, s);
+    return launch_tcx_impl<PS, M, LA, LB, NPR, false>(a, s);
+}
+
 template <class PS, int M, int LA, int LB, int NPR = 1, int MM = 128>
 int launch_tc(const MulArgs &a, cudaStream_t s) {
     if (mul_xops(a)) return launch_tc_impl<PS, M, LA, LB, 1, 128, true>(a, s);
@@ -680,8 +728,9 @@ int launch_mul(MulArgs a, cudaStream_t s, int la = 2, int lb = 2) {
     if (a.n_out <= 0) return SNTRUP_OK;
     constexpr bool AB = kABVariants<PS>;
     const int sel = AB ? g_mul_impl : (g_mul_impl == 1 ? 1 : 0);
-    const int impl = (sel >= 7) ? 0 : sel;   // 7-11: as 0 except u / pipelining / TMEM A
+    const int impl = (sel >= 7) ? 0 : sel;   // 7-13: as 0 except u / pipelining / TMEM A / transposed
     const bool pipe = sel == 8;
+    const bool tcx = sel == 13;              // one-product int8 items in the transposed form (tcxmul.cuh)
     // algorithmic ops: the method's work, 2 p^2 (p^2 multiply-adds) per ring product whatever the
     // implementation (limbs, digits, padding and the zero triangles are implementation overhead)
     ProfScope ps_(M == 3 ? PC_MUL_R3 : PC_MUL_RQ, (double)a.n_out, s, 2.0 * PS::P * PS::P * (double)a.n_out);
@@ -730,6 +779,10 @@ int launch_mul(MulArgs a, cudaStream_t s, int la = 2, int lb = 2) {
             // at MMA M = 64 (half the A bytes per MMA, twice the N) are A/B mode impl 5
             a.swap = la == 1 ? 0 : 1;
             if constexpr (AB) {
+                if (tcx) {                   // the big operand takes the window role (2 limbs along N)
+                    a.swap = la == 1 ? 1 : 0;
+                    return launch_tcx<PS, M, 2, 1>(a, s);
+                }
                 if (impl == 4) return launch_tc4<PS, M, D9, 1>(a, s);
                 if (impl == 5) return launch_tc<PS, M, 1, 2, 1, 64>(a, s);
             }
@@ -739,6 +792,9 @@ int launch_mul(MulArgs a, cudaStream_t s, int la = 2, int lb = 2) {
         if constexpr (AB) {
             if (pipe) return down2 ? launch_tc_pipe<PS, M, 2>(a, s) : launch_tc_pipe<PS, M, 1>(a, s);
             if (impl == 5) return launch_tc<PS, M, 2, 2, 1, 64>(a, s);
+        }
+        if constexpr (AB) {
+            if (tcx) return down2 ? launch_tcx<PS, M, 2, 2, 2>(a, s) : launch_tcx<PS, M, 2, 2>(a, s);
         }
         if (down2) return launch_tc<PS, M, 2, 2, 2>(a, s);
         return launch_tc<PS, M, 2, 2>(a, s);
@@ -1412,10 +1468,15 @@ struct KeygenGraph {
     cudaGraphExec_t exec = nullptr;
     uint64_t epoch = 0;
     uint64_t kernels = 0;
+    uint64_t last_use = 0;                  // g_graph_tick of the last capture / replay (LRU eviction)
     std::vector<GraphArgNode> nodes;
     std::vector<int *> errs;
 };
 inline std::map<GraphKey, KeygenGraph> g_graphs;
+inline uint64_t g_graph_tick = 0;
+// A graph is cached per call shape INCLUDING the output pointers; a caller that rotates through many
+// output buffers would otherwise accumulate executable graphs without bound.
+constexpr size_t MAX_GRAPHS = 32;
 
 inline void graph_destroy(KeygenGraph &G) {
     if (G.exec) cudaGraphExecDestroy(G.exec);
@@ -1492,18 +1553,20 @@ int keygen_graph(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out, co
             cudaGetLastError();
             return SNTRUP_E_CUDA;
         }
+        // a failure past this point must not leak the instantiated graph
+#define GCK(x) do { if ((x) != cudaSuccess) { graph_destroy(G); cudaGetLastError(); return SNTRUP_E_CUDA; } } while (0)
         size_t nn = 0;
-        CK(cudaGraphGetNodes(graph, nullptr, &nn));
+        GCK(cudaGraphGetNodes(graph, nullptr, &nn));
         std::vector<cudaGraphNode_t> nodes(nn);
-        CK(cudaGraphGetNodes(graph, nodes.data(), &nn));
+        GCK(cudaGraphGetNodes(graph, nodes.data(), &nn));
         for (cudaGraphNode_t nd : nodes) {
             cudaGraphNodeType t;
-            CK(cudaGraphNodeGetType(nd, &t));
+            GCK(cudaGraphNodeGetType(nd, &t));
             if (t != cudaGraphNodeTypeKernel) continue;
             G.kernels++;
             GraphArgNode a{};
             a.node = nd;
-            CK(cudaGraphKernelNodeGetParams(nd, &a.prm));
+            GCK(cudaGraphKernelNodeGetParams(nd, &a.prm));
             if (a.prm.func == (void *)sample_kernel<PS>) {
                 a.kind = 1;
                 a.sa = *(const SampleArgs *)a.prm.kernelParams[0];
@@ -1519,10 +1582,23 @@ int keygen_graph(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out, co
             }
             G.nodes.push_back(a);
         }
+#undef GCK
+        if (g_graphs.size() >= MAX_GRAPHS) {                 // evict the least recently used shape
+            auto lru = g_graphs.begin();
+            for (auto jt = g_graphs.begin(); jt != g_graphs.end(); ++jt)
+                if (jt->second.last_use < lru->second.last_use) lru = jt;
+            // a replay of it may still be running (its exec must outlive the launch), and its
+            // stream may be gone by now: wait for the device, not for that stream
+            if (cudaDeviceSynchronize() != cudaSuccess) cudaGetLastError();
+            graph_destroy(lru->second);
+            g_graphs.erase(lru);
+        }
+        G.last_use = ++g_graph_tick;
         g_graphs[key] = std::move(G);
         return keygen_finish(o, errs, s0);
     }
     KeygenGraph &G = it->second;
+    G.last_use = ++g_graph_tick;
     for (GraphArgNode &a : G.nodes) {
         void *args[1];
         if (a.kind == 1) {

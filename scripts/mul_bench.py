@@ -60,6 +60,10 @@ def main():
         if "rqt" in w:
             ms = timeit(lambda: S.rq_mul_batch(args.param, a, t, c), args.iters)
             print("%-10s rq x ternary   %8.3f ms  %10.3f M mults/s  (rq_mul_batch treats both as big)" % (name, ms, n / ms / 1e3))
+        if "rqs" in w:        # big x small entry point (configs[2]'s path); t8 = the ternary rows as int8
+            t8 = t[:, :P["p16"]].to(torch.int8).contiguous() if P["p16"] <= t.shape[1] else torch.nn.functional.pad(t, (0, P["p16"] - t.shape[1])).to(torch.int8).contiguous()
+            ms = timeit(lambda: S.rq_mul_small_batch(args.param, a, t8, c), args.iters)
+            print("%-10s rq big x small %8.3f ms  %10.3f M mults/s" % (name, ms, n / ms / 1e3))
         if "r3" in w:
             ms = timeit(lambda: S.r3_mul_batch(args.param, g, h, c3), args.iters)
             print("%-10s r3             %8.3f ms  %10.3f M mults/s  %8.1f ns/product" % (name, ms, n / ms / 1e3, ms * 1e6 / n))

@@ -20,9 +20,10 @@ PSETS = [653, 761, 857, 953, 1013, 1277]
 @pytest.fixture(params=[S.MUL_TENSOR_CORE, S.MUL_TENSOR_CORE_INT8, S.MUL_TENSOR_CORE_FP4_ALL,
                         S.MUL_TENSOR_CORE_M64, S.MUL_TENSOR_CORE_I8_SINGLE, S.MUL_TENSOR_CORE_U_FUSED,
                         S.MUL_TENSOR_CORE_PIPELINED, S.MUL_TENSOR_CORE_TMEM_A, S.MUL_TENSOR_CORE_TMEM_A64,
-                        S.MUL_TENSOR_CORE_WS, S.MUL_TENSOR_CORE_TMEM_RING, S.MUL_SCHOOLBOOK],
+                        S.MUL_TENSOR_CORE_WS, S.MUL_TENSOR_CORE_TMEM_RING, S.MUL_TENSOR_CORE_TRANSPOSED,
+                        S.MUL_SCHOOLBOOK],
                 ids=["tc", "tc_int8", "tc_fp4_all", "tc_m64", "tc_i8_single", "tc_u_fused", "tc_pipe",
-                     "tc_tmem_a", "tc_tmem_a64", "tc_ws", "tc_tmem_ring", "schoolbook"])
+                     "tc_tmem_a", "tc_tmem_a64", "tc_ws", "tc_tmem_ring", "tc_transposed", "schoolbook"])
 def mul_impl(request):
     """Run a test under both ring-product implementations (tcgen05 Hankel GEMM, int32 schoolbook)."""
     S.set_mul_impl(request.param)
@@ -137,6 +138,36 @@ def test_graph_mode_trees_and_repair(O):
         s.synchronize()
         ref = oracle_keys(O, 653, seed, np.arange(first, first + n))
         assert np.array_equal(pk.cpu().numpy(), ref["pk"]) and np.array_equal(sk.cpu().numpy(), ref["sk"]), (seed, first)
+
+
+def test_graph_cache_is_bounded(O):
+    # a graph is cached per call shape including the output pointers: more distinct output buffers
+    # than the cache holds (32) evict the least recently used graphs; evicted shapes are rebuilt
+    # and every call stays exact
+    P = S.params(761)
+    s = torch.cuda.Stream()
+    fl = S.OPT_RING_STREAMS | S.OPT_GRAPH
+    bufs = [(torch.empty((8, P["pk_bytes"]), dtype=torch.uint8, device="cuda"),
+             torch.empty((8, P["sk_bytes"]), dtype=torch.uint8, device="cuda")) for _ in range(36)]
+    ref = {seed: oracle_keys(O, 761, seed, np.arange(8)) for seed in (1, 2)}
+    for seed in (1, 2):                          # second pass: the first buffers were evicted
+        for pk, sk in bufs:
+            S.batch_keygen(761, 8, seed, batch_size=1, pk_out=pk, sk_out=sk, flags=fl, stream=s)
+        s.synchronize()
+        for pk, sk in bufs:
+            assert np.array_equal(pk.cpu().numpy(), ref[seed]["pk"])
+            assert np.array_equal(sk.cpu().numpy(), ref[seed]["sk"])
+    S.release_stream_workspace(s)
+
+
+def test_attempts_only_output(O):
+    # attempts=True: only the per-key number of g draws (bench.py's rejection totals)
+    res = S.batch_keygen(653, 400, 4, batch_size=16, attempts=True)
+    torch.cuda.synchronize()
+    assert set(res) == {"pk", "sk", "attempts"}
+    ref = oracle_keys(O, 653, 4, np.arange(400))
+    assert np.array_equal(res["attempts"].cpu().numpy(), ref["attempts"])
+    assert int(res["attempts"].sum()) > 400      # 653 rejects ~3.7% of the draws
 
 
 def test_graph_mode_rejects_host_outputs():
