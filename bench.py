@@ -301,7 +301,7 @@ def other_configs(S, torch, timed):
     out["configs[4]"] = {"workload": "sntrup1277, 2^20 keys, seed 5, B = 1024, 65,536-key chunks, ring streams",
                          "keys_per_s": n / (ms / 1e3), "ms": ms,
                          "rejected_g_draws": int(att.to(torch.int64).sum().item()) - n,
-                         "rejected_g_draws_note": "the oracle's count for these 2^20 keys is 54,589 (every key's "
+                         "rejected_g_draws_note": "the oracle's count for these 2^20 keys is 54,600 (tests/golden/oracle_digests/cfg4_1277.json; every key's "
                                                   "attempt count is compared in tests/test_gpu_fullsize.py)"}
     del pk, sk, att
     # KEM core: 65,536 encapsulations (r from the encapsulation stream
