@@ -315,8 +315,12 @@ uint64_t sntrup_kernel_launch_count(void);
        window in rounds (no shared-memory A at all; 8 CTAs per SM);
    13 = as 0, with the int8 one-product items (R/q up-sweep, rq_mul_batch, rq_mul_small_batch) in
        the transposed Hankel form (csrc/tcxmul.cuh): 16 output coefficients per accumulator row,
-       the folded operand read by the MMAs as a view of its staging array at MMA M = 64.
-   All are exact.  Variants 2-10 and 12 are compiled for sntrup761 only (other sets run 0, or 1 / 11);
+       the folded operand read by the MMAs as a view of its staging array at MMA M = 64;
+   14 = as 0, with the int8 big x big two-product items (R/q down-sweep, h) built and multiplied over
+       the whole K range at once (72 KB of shared memory per CTA at p = 761, 3 CTAs per SM) instead of
+       in two parts through half-size operand buffers (the default: 43 KB, 5 CTAs per SM);
+   15 = as 0 with three parts; 16 = as 0 with the one-product int8 big x big items in two parts too.
+   All are exact.  Variants 2-10 and 12-16 are compiled for sntrup761 only (other sets run 0, or 1 / 11);
    KEM pre/post-op calls always use the default kernel of their shape.  Returns SNTRUP_OK or
    SNTRUP_E_ARG. */
 int sntrup_set_mul_impl(int impl);

@@ -455,6 +455,9 @@ MUL_TENSOR_CORE_TMEM_A = 9        # fp4 products: first K steps of the Hankel A 
 MUL_TENSOR_CORE_TMEM_A64 = 10     # as 9 with a 64-column TMEM allocation
 MUL_TENSOR_CORE_WS = 11           # warp-specialised persistent kernels, Hankel A written to TMEM
 MUL_TENSOR_CORE_TRANSPOSED = 13   # int8 one-product items in the transposed Hankel form (tcxmul.cuh)
+MUL_TENSOR_CORE_ONE_PART = 14     # int8 big x big two-product items over the whole K range at once (default: two parts)
+MUL_TENSOR_CORE_3PARTS = 15       # ... in three parts
+MUL_TENSOR_CORE_PARTS_ALL = 16    # one-product int8 big x big items in two parts too
 MUL_TENSOR_CORE_TMEM_RING = 12    # fp4: every K step's A rows through a 64-column TMEM window in rounds
 
 

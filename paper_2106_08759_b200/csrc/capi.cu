@@ -487,7 +487,7 @@ int sntrup_set_root_impl(int impl) {
 }
 
 int sntrup_set_mul_impl(int impl) {
-    if (impl < 0 || impl > 13) return SNTRUP_E_ARG;
+    if (impl < 0 || impl > 16) return SNTRUP_E_ARG;
     std::lock_guard<std::mutex> lk(g_mu);
     g_mul_impl = impl;
     return SNTRUP_OK;

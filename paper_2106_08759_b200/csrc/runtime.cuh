@@ -573,11 +573,12 @@ int resident_ctas(F kern, int smem, int tcols, int threads = 128) {
     return nb < 1 ? 1 : nb;
 }
 
-template <class PS, int M, int LA, int LB, int NPR = 1, int MM = 128, bool XOPS = false, int NT = 128, int ST = 1>
+template <class PS, int M, int LA, int LB, int NPR = 1, int MM = 128, bool XOPS = false, int NT = 128, int ST = 1,
+          int NH = 1>
 int launch_tc_impl(const MulArgs &a, cudaStream_t s) {
     using G = TcGeom<PS, LA, LB, NPR, MM>;
-    constexpr int SMEM = tc_smem_bytes<G, LA, LB, NPR, ST>();
-    auto kern = tc_mul_kernel<PS, M, LA, LB, NPR, MM, XOPS, NT, ST>;
+    constexpr int SMEM = tc_smem_bytes<G, LA, LB, NPR, ST, MM, NH>();
+    auto kern = tc_mul_kernel<PS, M, LA, LB, NPR, MM, XOPS, NT, ST, NH>;
     static std::map<int, int> per_sm;                 // device -> resident CTAs per SM
     int dev = 0;
     CK(cudaGetDevice(&dev));
@@ -728,9 +729,11 @@ int launch_mul(MulArgs a, cudaStream_t s, int la = 2, int lb = 2) {
     if (a.n_out <= 0) return SNTRUP_OK;
     constexpr bool AB = kABVariants<PS>;
     const int sel = AB ? g_mul_impl : (g_mul_impl == 1 ? 1 : 0);
-    const int impl = (sel >= 7) ? 0 : sel;   // 7-13: as 0 except u / pipelining / TMEM A / transposed
+    const int impl = (sel >= 7) ? 0 : sel;   // 7-16: as 0 except u / pipelining / TMEM A / transposed
     const bool pipe = sel == 8;
     const bool tcx = sel == 13;              // one-product int8 items in the transposed form (tcxmul.cuh)
+    // int8 big x big items with the K range in parts (default: two-product items in 2 parts):
+    // 14 = one part (the former default), 15 = 3 parts, 16 = one-product items in 2 parts too
     // algorithmic ops: the method's work, 2 p^2 (p^2 multiply-adds) per ring product whatever the
     // implementation (limbs, digits, padding and the zero triangles are implementation overhead)
     ProfScope ps_(M == 3 ? PC_MUL_R3 : PC_MUL_RQ, (double)a.n_out, s, 2.0 * PS::P * PS::P * (double)a.n_out);
@@ -747,9 +750,10 @@ int launch_mul(MulArgs a, cudaStream_t s, int la = 2, int lb = 2) {
     // inverse as the A operand (one work item per parent), halving the A-operand fetch that
     // bounds the tensor-core products.  int8 big x big at M = 128 too since the folded B operand
     // halved N (3 CTAs/SM); impl 6 keeps one big x big product per item for A/B.
-    // (only where two such CTAs still fit an SM: at p = 1277 the stacked B rows would leave one)
+    // (only where two such CTAs fit an SM; with the operands in two K parts that holds for every set,
+    // p = 1277 included: 12.1 vs 10.95 M keys/s there, profiles/r02s3/kparts_1277.log)
     const bool big2 = la == 2 && lb == 2 && impl != 5 && impl != 6 &&
-                      TcGeom<PS, 2, 2, 2>::MINB >= 2;
+                      TcParts<TcGeom<PS, 2, 2, 2>, 2, 2, 2, 128, 2>::BY_SMEM >= 2;
     const bool down2 = (a.mode == MUL_DOWN || a.mode == MUL_DOWNH) && (M == 3 || (la == 1 && lb == 1) || big2) &&
                        impl != 2;
     if (down2) {
@@ -796,6 +800,16 @@ int launch_mul(MulArgs a, cudaStream_t s, int la = 2, int lb = 2) {
         if constexpr (AB) {
             if (tcx) return down2 ? launch_tcx<PS, M, 2, 2, 2>(a, s) : launch_tcx<PS, M, 2, 2>(a, s);
         }
+        if constexpr (AB) {
+            if (down2 && !mul_xops(a)) {
+                if (sel == 14) return launch_tc_impl<PS, M, 2, 2, 2>(a, s);                                  // one part
+                if (sel == 15) return launch_tc_impl<PS, M, 2, 2, 2, 128, false, 128, 1, 3>(a, s);
+            }
+            if (sel == 16 && !down2 && !mul_xops(a)) return launch_tc_impl<PS, M, 2, 2, 1, 128, false, 128, 1, 2>(a, s);
+        }
+        // two-product items: operands built and multiplied in two parts of the K range (half-size
+        // buffers: 43 instead of 72 KB per CTA at p = 761, 5 resident CTAs per SM instead of 3)
+        if (down2 && !mul_xops(a)) return launch_tc_impl<PS, M, 2, 2, 2, 128, false, 128, 1, 2>(a, s);
         if (down2) return launch_tc<PS, M, 2, 2, 2>(a, s);
         return launch_tc<PS, M, 2, 2>(a, s);
     }

@@ -373,18 +373,43 @@ __device__ __forceinline__ void tc_work(const MulArgs &a, long long it, TcWork<N
 // per SM overlap one CTA's operand build with another's MMAs; ST = 2 (NT = 256, one or two CTAs
 // per SM) software-pipelines inside the CTA: item k+1's operands are built in the second stage and
 // its MMAs issued before item k's epilogue, which then overlaps them.
-template <class PS, int M, int LA, int LB, int NPR, int MM = 128, bool XOPS = false, int NT = 128, int ST = 1>
-__global__ void __launch_bounds__(NT, (ST == 1 ? TcGeom<PS, LA, LB, NPR, MM>::MINB : 1)) tc_mul_kernel(MulArgs a) {
+// NH > 1 (big x big, ST = 1): the K range is processed in NH parts through operand buffers sized
+// for one part (A windows and B rows of KH = ceil(NKS / NH) K steps; each part's MMAs accumulate
+// into the same TMEM columns and are waited for before the next part is built), which cuts the
+// shared memory per CTA from 72 KB to 43 KB (NH = 2, two products per item) -- more resident CTAs
+// per SM, at the same per-item chain length.
+template <class G, int LA, int LB, int NPR, int MM, int NH>
+struct TcParts {
+    static constexpr int KH = (G::NKS + NH - 1) / NH;         // K steps per part
+    static constexpr int AROWS = 32 * KH + MM - 15;
+    static constexpr int A_BYTES = NH == 1 ? G::A_BYTES : (AROWS + 7) / 8 * 128;
+    static constexpr int AROWS4 = NH == 1 ? G::AROWS4 : (AROWS + 3) / 4;
+    static constexpr int B_BYTES = NH == 1 ? G::B_BYTES : 2 * KH * G::BLD * 16;
+    static constexpr int ZUN = G::ZUN - G::NCHB + 2 * KH;    // Z units feeding one part's chunks
+    static constexpr int UITEMS = NPR * LB * ZUN;
+    static constexpr int SMEM = LA * A_BYTES + B_BYTES + LA * G::HA_LEN + NPR * LB * G::Z_LEN + 128;
+    static constexpr int BY_SMEM = (227 * 1024) / (SMEM + 1024);
+    static constexpr int CAPB = NH == 2 && NPR == 2 ? 5 : 6;  // register cap: 65536 / (128 CAPB) per thread
+    static constexpr int MINB = NH == 1 ? G::MINB : (BY_SMEM < CAPB ? BY_SMEM : CAPB);
+    static_assert(4 * AROWS4 * 16 <= A_BYTES, "A part too short");
+    static_assert(4 * (8 * KH * (NH - 1) + AROWS4 + 5) <= G::HA_LEN + 64, "hA reads");
+};
+
+template <class PS, int M, int LA, int LB, int NPR, int MM = 128, bool XOPS = false, int NT = 128, int ST = 1, int NH = 1>
+__global__ void __launch_bounds__(NT, (ST == 1 ? TcParts<TcGeom<PS, LA, LB, NPR, MM>, LA, LB, NPR, MM, NH>::MINB : 1))
+tc_mul_kernel(MulArgs a) {
     using G = TcGeom<PS, LA, LB, NPR, MM>;
+    using H = TcParts<G, LA, LB, NPR, MM, NH>;
     static_assert(ST == 1 || (ST == 2 && MM == 128 && NT == 256), "pipelined variant: M = 128, 8 warps");
     static_assert(ST == 2 || NT == 128, "plain variant: 4 warps");
+    static_assert(NH == 1 || (ST == 1 && LA == 2 && LB == 2), "K parts: the big x big plain variant");
     constexpr int P = PS::P;
     constexpr int PD = G::PD;
     constexpr int CH = (G::NCHK + 1 + NT - 1) / NT;           // staging chunks per thread (+ s-group -1)
-    constexpr int UPER = (G::UITEMS + NT - 1) / NT;
-    constexpr int ASTG = LA * G::A_BYTES;                     // one stage's A windows
+    constexpr int UPER = (H::UITEMS + NT - 1) / NT;
+    constexpr int ASTG = LA * H::A_BYTES;                     // one stage's A windows
     constexpr int OFF_B = ST * ASTG;                          // B of stage b at OFF_B + b B_BYTES
-    constexpr int OFF_HA = OFF_B + ST * G::B_BYTES;
+    constexpr int OFF_HA = OFF_B + ST * H::B_BYTES;
     constexpr int OFF_ZR = OFF_HA + LA * G::HA_LEN;
     constexpr int OFF_BAR = OFF_ZR + NPR * LB * G::Z_LEN;
     constexpr int TCU = ST * LA * G::NB;                      // accumulators of every stage
@@ -547,21 +572,22 @@ __global__ void __launch_bounds__(NT, (ST == 1 ? TcGeom<PS, LA, LB, NPR, MM>::MI
     // ---- operands of stage b: A sliding windows (row rho = hA[rho .. rho+15], the descriptor
     //      starts at row 1; each work item builds rows 4m .. 4m+3 from 5 words) and B rows
     //      (row pp*PCOL + l*NL + t, K-chunk c = 16-byte unit c of the row's Z window)
-    auto build = [&](int b) {
+    auto build = [&](int b, int h = 0) {
         uint8_t *sA = sm + b * ASTG;
-        uint8_t *sB = sm + OFF_B + b * G::B_BYTES;
+        uint8_t *sB = sm + OFF_B + b * H::B_BYTES;
 #pragma unroll
         for (int l = 0; l < LA; l++) {
 #pragma unroll
-            for (int kw = 0; kw < (G::AROWS4 + NT - 1) / NT; kw++) {
+            for (int kw = 0; kw < (H::AROWS4 + NT - 1) / NT; kw++) {
                 const int m = tid + NT * kw;
-                if (m >= G::AROWS4) break;
-                SNTRUP_CHECK(4 * (m + 5) <= G::HA_LEN && 64 * (m + 1) <= G::A_BYTES);
-                const uint32_t *src = reinterpret_cast<const uint32_t *>(sHA + l * G::HA_LEN) + m;
+                if (m >= H::AROWS4) break;
+                const int mg = m + 8 * H::KH * h;               // window rows 4 mg .. of the whole operand
+                SNTRUP_CHECK(4 * (mg + 5) <= G::HA_LEN && 64 * (m + 1) <= H::A_BYTES);
+                const uint32_t *src = reinterpret_cast<const uint32_t *>(sHA + l * G::HA_LEN) + mg;
                 uint32_t wd[5];
 #pragma unroll
                 for (int i = 0; i < 5; i++) wd[i] = src[i];
-                uint4 *dst = reinterpret_cast<uint4 *>(sA + l * G::A_BYTES) + 4 * m;
+                uint4 *dst = reinterpret_cast<uint4 *>(sA + l * H::A_BYTES) + 4 * m;
 #pragma unroll
                 for (int i = 0; i < 4; i++) {
                     uint4 o;
@@ -573,22 +599,26 @@ __global__ void __launch_bounds__(NT, (ST == 1 ? TcGeom<PS, LA, LB, NPR, MM>::MI
                 }
             }
         }
-        // each Z unit read once and stored into every row window that covers it
+        // each Z unit read once and stored into every row window that covers it (part h: the
+        // chunks 2 KH h .. of every row)
+        const int c0 = 2 * H::KH * h;
 #pragma unroll
-        for (int h = 0; h < UPER; h++) {
-            const int w = tid + NT * h;
-            if (w >= G::UITEMS) break;
-            const int pl = w / G::ZUN, u = G::ZU0 + (w - pl * G::ZUN);          // pl = pp * LB + l
+        for (int hh = 0; hh < UPER; hh++) {
+            const int w = tid + NT * hh;
+            if (w >= H::UITEMS) break;
+            const int pl = w / H::ZUN, u = G::ZU0 + c0 + (w - pl * H::ZUN);     // pl = pp * LB + l
             const int pp = pl / LB, l = pl - pp * LB;
+            if (NH > 1 && u >= G::ZU1) continue;
             SNTRUP_CHECK(pl * (G::Z_LEN / 16) + u < NPR * LB * G::Z_LEN / 16);
             const uint4 z = reinterpret_cast<const uint4 *>(sZR)[pl * (G::Z_LEN / 16) + u];
             uint4 *dst = reinterpret_cast<uint4 *>(sB) + pp * G::PCOL + l * G::NL;
 #pragma unroll
             for (int t = 0; t < G::NROWS; t++) {
                 const int c = u - G::zrow(t) / 16;
-                if (c >= 0 && c < G::NCHB) {
-                    // in range by construction: base + t < NPR PCOL <= NB < BLD and c < NCHB
-                    dst[c * G::BLD + t] = z;
+                const int cl = c - c0;
+                if (cl >= 0 && cl < 2 * H::KH && c < G::NCHB) {
+                    // in range by construction: base + t < NPR PCOL <= NB < BLD and cl < 2 KH
+                    dst[cl * G::BLD + t] = z;
                 }
             }
         }
@@ -597,18 +627,19 @@ __global__ void __launch_bounds__(NT, (ST == 1 ? TcGeom<PS, LA, LB, NPR, MM>::MI
 
     // ---- MMAs of stage b (warp 0, one elected lane) into accumulator set b; descriptors advance by adding to
     //      the start-address field
-    auto issue = [&](int b) {
+    auto issue = [&](int b, int h = 0) {
         tc_fence_after();
-        const uint64_t bd0 = umma_desc(smem_u32(sm + OFF_B + b * G::B_BYTES), G::BLD * 16, 128);
+        const uint64_t bd0 = umma_desc(smem_u32(sm + OFF_B + b * H::B_BYTES), G::BLD * 16, 128);
         const uint64_t ad0 = umma_desc(smem_u32(sm + b * ASTG) + 16, 256, 128);
         const uint32_t acc = tmem + (uint32_t)(b * LA * G::NB);
+        const int ksn = (G::NKS - h * H::KH) < H::KH ? (G::NKS - h * H::KH) : H::KH;
 #pragma unroll 1
-        for (int ks = 0; ks < G::NKS; ks++) {
+        for (int ks = 0; ks < ksn; ks++) {
             const uint64_t bd = bd0 + (uint64_t)((ks * 32 * G::BLD) >> 4);
 #pragma unroll
             for (int l = 0; l < LA; l++) {
-                const uint64_t ad = ad0 + (uint64_t)((l * G::A_BYTES + ks * 512) >> 4);
-                umma_i8_w(acc + l * G::NB, ad, bd, IDESC, ks > 0 ? 1u : 0u);
+                const uint64_t ad = ad0 + (uint64_t)((l * H::A_BYTES + ks * 512) >> 4);
+                umma_i8_w(acc + l * G::NB, ad, bd, IDESC, (ks > 0 || h > 0) ? 1u : 0u);
             }
         }
         umma_commit_w(bar + b);
@@ -717,11 +748,21 @@ __global__ void __launch_bounds__(NT, (ST == 1 ? TcGeom<PS, LA, LB, NPR, MM>::MI
             prefetch(it + gridDim.x);
             for (; it < a.n_out; it += gridDim.x) {
                 const long long nx = it + gridDim.x;
+#pragma unroll 1
+                for (int h = 0; h < NH - 1; h++) {        // all parts but the last: build, MMAs, wait
+                    __syncthreads();                      // staging complete / previous part's MMAs done
+                    build(0, h);
+                    tc_fence_before();
+                    __syncthreads();
+                    if (warp == 0) issue(0, h);
+                    if (tid == 0) mbar_wait(bar, phases & 1u);
+                    phases ^= 1u;
+                }
                 __syncthreads();                          // staging of item it complete
-                build(0);
+                build(0, NH - 1);
                 tc_fence_before();
                 __syncthreads();                          // operands built; staging area free
-                if (warp == 0) issue(0);
+                if (warp == 0) issue(0, NH - 1);
                 const TcWork<NPR> nxt = wn;
                 int fnx[NPR];
 #pragma unroll
@@ -794,9 +835,10 @@ __global__ void __launch_bounds__(NT, (ST == 1 ? TcGeom<PS, LA, LB, NPR, MM>::MI
 }
 
 // shared memory of a tc_mul_kernel instantiation (ST operand stages)
-template <class G, int LA, int LB, int NPR, int ST>
+template <class G, int LA, int LB, int NPR, int ST, int MM = 128, int NH = 1>
 constexpr int tc_smem_bytes() {
-    return ST * (LA * G::A_BYTES + G::B_BYTES) + LA * G::HA_LEN + NPR * LB * G::Z_LEN + 128;
+    using H = TcParts<G, LA, LB, NPR, MM, NH>;
+    return ST * (LA * H::A_BYTES + H::B_BYTES) + LA * G::HA_LEN + NPR * LB * G::Z_LEN + 128;
 }
 template <class G, int LA, int ST>
 constexpr int tc_tmem_cols() {

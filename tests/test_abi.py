@@ -67,7 +67,7 @@ def test_argument_errors_without_gpu(lib):
     assert S._lib.sntrup_batch_keygen(700, 5, 1, None, None) == S.SNTRUP_E_PARAM
     assert S._lib.rq_mul_batch(761, 0, None, None, None, None) == S.SNTRUP_E_ARG
     assert S._lib.sntrup_strerror(S.SNTRUP_E_NOT_INVERTIBLE) == b"element not invertible"
-    assert S._lib.sntrup_set_mul_impl(14) == S.SNTRUP_E_ARG
+    assert S._lib.sntrup_set_mul_impl(17) == S.SNTRUP_E_ARG
     assert S._lib.sntrup_set_mul_impl(12) == S.SNTRUP_OK
     assert S._lib.sntrup_set_mul_impl(11) == S.SNTRUP_OK
     assert S._lib.sntrup_set_mul_impl(10) == S.SNTRUP_OK

@@ -20,10 +20,11 @@ PSETS = [653, 761, 857, 953, 1013, 1277]
 @pytest.fixture(params=[S.MUL_TENSOR_CORE, S.MUL_TENSOR_CORE_INT8, S.MUL_TENSOR_CORE_FP4_ALL,
                         S.MUL_TENSOR_CORE_M64, S.MUL_TENSOR_CORE_I8_SINGLE, S.MUL_TENSOR_CORE_U_FUSED,
                         S.MUL_TENSOR_CORE_PIPELINED, S.MUL_TENSOR_CORE_TMEM_A, S.MUL_TENSOR_CORE_TMEM_A64,
-                        S.MUL_TENSOR_CORE_WS, S.MUL_TENSOR_CORE_TMEM_RING, S.MUL_TENSOR_CORE_TRANSPOSED,
+                        S.MUL_TENSOR_CORE_WS, S.MUL_TENSOR_CORE_TMEM_RING, S.MUL_TENSOR_CORE_TRANSPOSED, S.MUL_TENSOR_CORE_ONE_PART, S.MUL_TENSOR_CORE_3PARTS,
+                        S.MUL_TENSOR_CORE_PARTS_ALL,
                         S.MUL_SCHOOLBOOK],
                 ids=["tc", "tc_int8", "tc_fp4_all", "tc_m64", "tc_i8_single", "tc_u_fused", "tc_pipe",
-                     "tc_tmem_a", "tc_tmem_a64", "tc_ws", "tc_tmem_ring", "tc_transposed", "schoolbook"])
+                     "tc_tmem_a", "tc_tmem_a64", "tc_ws", "tc_tmem_ring", "tc_transposed", "tc_one_part", "tc_3parts", "tc_parts_all", "schoolbook"])
 def mul_impl(request):
     """Run a test under both ring-product implementations (tcgen05 Hankel GEMM, int32 schoolbook)."""
     S.set_mul_impl(request.param)
