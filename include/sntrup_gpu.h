@@ -342,6 +342,18 @@ int sntrup_set_divstep_threads(int nt);
    constant-time and exact.  Returns SNTRUP_OK or SNTRUP_E_ARG. */
 int sntrup_set_root_impl(int impl);
 
+/* Knob: scheduling of the tree tops inside bulk keygen calls (more than 4096 keys, ring streams).
+   The top levels of the product trees (Algorithm 1 lines 10-11: batchInv) and the root
+   inversions are chains of small launches; on their lane's stream they wait behind the other lane's
+   bulk ring-product kernels, whose persistent CTAs hold the SMs' shared memory until the launch
+   ends.  top_items > 0: ring-product launches of at most top_items products and the root
+   inversions run on a high-priority companion stream of their chain (ordered with it by an event
+   at each switch).  items_cap > 0: a ring-product launch uses at least ceil(work items /
+   items_cap) CTAs, so a CTA retires after items_cap work items and a waiting high-priority CTA
+   takes its place.  (0, 0) = off.  Outputs do not depend on it.  Returns SNTRUP_OK or
+   SNTRUP_E_ARG (negative values). */
+int sntrup_set_sched(long long top_items, long long items_cap);
+
 /* Measurement hooks (bench.py).  When enabled, every kernel launch is bracketed by CUDA events
    recorded on its launching stream.  sntrup_profile_read() waits for the recorded events and
    returns, per kernel class, the summed device milliseconds, the summed work units, the summed

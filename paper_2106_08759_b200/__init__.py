@@ -79,6 +79,7 @@ _lib.sntrup_kernel_launch_count.restype = _u64
 _lib.sntrup_set_mul_impl.argtypes = [_i32]
 _lib.sntrup_set_divstep_threads.argtypes = [_i32]
 _lib.sntrup_set_root_impl.argtypes = [_i32]
+_lib.sntrup_set_sched.argtypes = [ctypes.c_longlong, ctypes.c_longlong]
 _lib.sntrup_profile_enable.restype = None
 _lib.sntrup_profile_enable.argtypes = [_i32]
 _lib.sntrup_profile_read.restype = _i32
@@ -114,7 +115,7 @@ EXPORTED = ("sntrup_params", "sntrup_strerror", "sntrup_batch_keygen", "sntrup_b
             "sntrup_workspace_reserved_bytes", "rq_mul_batch", "rq_mul_small_batch", "r3_mul_batch", "rq_recip_batch",
             "r3_recip_batch", "r3_is_invertible_batch", "rq_encode_batch",
             "sntrup_release_workspace", "sntrup_release_stream_workspace", "sntrup_kernel_launch_count", "sntrup_set_mul_impl", "sntrup_set_divstep_threads",
-            "sntrup_set_root_impl",
+            "sntrup_set_root_impl", "sntrup_set_sched",
             "sntrup_profile_enable", "sntrup_profile_read_kinds", "sntrup_profile_read_kinds_ex",
             "sntrup_measure_int_peak", "sntrup_probe_half_mul", "sntrup_pool_create",
             "sntrup_pool_take", "sntrup_pool_stats", "sntrup_pool_destroy",
@@ -475,6 +476,12 @@ ROOT_SHARED_SM = 4  # (+) jump CTAs reserve only the shared memory they use
 def set_root_impl(impl: int):
     """Root inversions when the roots are few: ROOT_AUTO (default), ROOT_STEP, ROOT_JUMP (+ ROOT_SHARED_SM)."""
     _check(_lib.sntrup_set_root_impl(int(impl)), "sntrup_set_root_impl")
+
+
+def set_sched(top_items: int = 0, items_cap: int = 0):
+    """Tree tops of bulk keygen calls on high-priority streams (launches of <= top_items products and
+    the roots); ring-product CTAs retire after items_cap work items.  (0, 0) = off."""
+    _check(_lib.sntrup_set_sched(int(top_items), int(items_cap)), "sntrup_set_sched")
 
 
 def profile_enable(on: bool = True):

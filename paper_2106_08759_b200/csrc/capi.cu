@@ -486,6 +486,14 @@ int sntrup_set_root_impl(int impl) {
     return SNTRUP_OK;
 }
 
+int sntrup_set_sched(long long top_items, long long items_cap) {
+    if (top_items < 0 || items_cap < 0) return SNTRUP_E_ARG;
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_top_items = top_items;
+    g_items_cap = items_cap;
+    return SNTRUP_OK;
+}
+
 int sntrup_set_mul_impl(int impl) {
     if (impl < 0 || impl > 16) return SNTRUP_E_ARG;
     std::lock_guard<std::mutex> lk(g_mu);

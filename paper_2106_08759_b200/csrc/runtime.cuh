@@ -345,6 +345,57 @@ inline int make_stream(cudaStream_t *s, int prio_rank) {
     return SNTRUP_OK;
 }
 
+// ------------------------------------------------------------------------------ tree-top routing
+// Inside a bulk keygen call the tree tops (levels of a few hundred work items) and the root
+// inversions are a chain of small, latency-bound launches.  On the lane's own stream they queue
+// behind the other lane's bulk kernels, whose persistent CTAs hold every shared-memory slot of the
+// SMs until their launch ends.  With routing on (sntrup_set_sched: top_items > 0), a launch of
+// <= top_items work items goes to a high-priority companion stream of its chain (ordered with the
+// chain by an event at every switch), and with items_cap > 0 a bulk launch's grid grows to
+// ceil(items / items_cap) CTAs, so CTAs retire after items_cap items and the block scheduler
+// hands the freed slot to a waiting high-priority CTA first.
+struct TopRoute { cudaStream_t hi = nullptr; cudaEvent_t ev = nullptr; bool on_hi = false; };
+inline bool g_route_on = false;             // set for the duration of a bulk keygen call
+inline long long g_top_items = 0;           // sntrup_set_sched
+inline long long g_items_cap = 0;
+inline std::map<std::pair<int, uintptr_t>, TopRoute> g_routes;
+
+inline int route_stream(cudaStream_t s, bool top, cudaStream_t *out) {
+    *out = s;
+    if (!g_route_on) return SNTRUP_OK;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    TopRoute &r = g_routes[std::make_pair(dev, (uintptr_t)s)];
+    if (!r.hi) {
+        if (!top) return SNTRUP_OK;
+        CK(cudaStreamCreateWithPriority(&r.hi, cudaStreamNonBlocking, lane_priority(0)));
+        CK(cudaEventCreateWithFlags(&r.ev, cudaEventDisableTiming));
+    }
+    if (top != r.on_hi) {
+        CK(cudaEventRecord(r.ev, r.on_hi ? r.hi : s));
+        CK(cudaStreamWaitEvent(r.on_hi ? s : r.hi, r.ev, 0));
+        r.on_hi = top;
+    }
+    *out = top ? r.hi : s;
+    return SNTRUP_OK;
+}
+// back onto the chain's own stream (before anything but a ring product / root launch touches it)
+inline int route_flush(cudaStream_t s) {
+    cudaStream_t t;
+    return route_stream(s, false, &t);
+}
+inline bool stream_capturing(cudaStream_t s) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    return cudaStreamIsCapturing(s, &st) != cudaSuccess || st != cudaStreamCaptureStatusNone;
+}
+inline long long capped_grid(long long grid, long long items) {
+    if (g_items_cap > 0) {
+        const long long g2 = (items + g_items_cap - 1) / g_items_cap;
+        if (g2 > grid) grid = g2;
+    }
+    return grid;
+}
+
 inline int copy_stream(CopyStream **out, int which = 0, int prio_rank = -1) {   // which: pipeline lane
     static std::map<std::tuple<int, int, int>, CopyStream> m;
     int dev = 0;
@@ -590,7 +641,7 @@ int launch_tc_impl(const MulArgs &a, cudaStream_t s) {
         nb = resident_ctas(kern, SMEM, tc_tmem_cols<G, LA, ST>(), NT);
         it = per_sm.emplace(dev, nb).first;
     }
-    long long grid = (long long)it->second * dev_info().sms;
+    long long grid = capped_grid((long long)it->second * dev_info().sms, a.n_out);
     if (grid > a.n_out) grid = a.n_out;
     g_cur_kind = PK_I8;
     // per work item: NKS K steps x LA A-limbs, each MMA reading an MM x 32-byte A tile and an
@@ -615,7 +666,7 @@ int launch_tcx_impl(const MulArgs &a, cudaStream_t s) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         it = per_sm.emplace(dev, resident_ctas(kern, G::SMEM, G::TCOLS)).first;
     }
-    long long grid = (long long)it->second * dev_info().sms;
+    long long grid = capped_grid((long long)it->second * dev_info().sms, a.n_out);
     if (grid > a.n_out) grid = a.n_out;
     g_cur_kind = PK_I8;
     // per work item: NKS K steps x LB chains, each MMA reading an MM x 32-byte Z tile and an
@@ -665,7 +716,7 @@ int launch_tc4_impl(const MulArgs &a, cudaStream_t s) {
         nb = resident_ctas(kern, G::SMEM, G::TCOLS);
         it = per_sm.emplace(dev, nb).first;
     }
-    long long grid = (long long)it->second * dev_info().sms;
+    long long grid = capped_grid((long long)it->second * dev_info().sms, a.n_out);
     if (grid > a.n_out) grid = a.n_out;
     g_cur_kind = PK_F4;
     // per work item: NKS MMAs, each an 128 x 32-byte A tile (64 fp4 K-elements; none for the K
@@ -727,6 +778,11 @@ constexpr bool kABVariants = PS::P == 761;
 template <class PS, int M>
 int launch_mul(MulArgs a, cudaStream_t s, int la = 2, int lb = 2) {
     if (a.n_out <= 0) return SNTRUP_OK;
+    if (g_route_on) {                        // tree tops on the chain's high-priority stream
+        cudaStream_t t;
+        if (int rc = route_stream(s, a.n_out <= g_top_items, &t)) return rc;
+        s = t;
+    }
     constexpr bool AB = kABVariants<PS>;
     const int sel = AB ? g_mul_impl : (g_mul_impl == 1 ? 1 : 0);
     const int impl = (sel >= 7) ? 0 : sel;   // 7-16: as 0 except u / pipelining / TMEM A / transposed
@@ -818,6 +874,11 @@ int launch_mul(MulArgs a, cudaStream_t s, int la = 2, int lb = 2) {
 template <class PS, int M>
 int launch_divstep(const InvArgs &a, cudaStream_t s, bool bulk = false) {
     if (a.n <= 0) return SNTRUP_OK;
+    if (g_route_on) {                        // roots: with the tree tops
+        cudaStream_t t;
+        if (int rc = route_stream(s, true, &t)) return rc;
+        s = t;
+    }
     // jump-divsteps when the roots are few and the call waits on them (the standalone reciprocal
     // calls, latency-sized keygen calls); inside a bulk keygen call the roots overlap the other
     // ring's products, where the per-step kernels' smaller SM footprint wins
@@ -1094,6 +1155,13 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
         if ((rc = staging_reserve(ks.stage_need, layout, s0, &stage_base))) return rc;
     }
     Lane lanes[MAX_LANES];
+    // tree tops and roots on high-priority companion streams (sntrup_set_sched): bulk calls with
+    // ring streams only; not under graph capture or the serialised measurement pass
+    struct RouteGuard {
+        RouteGuard(bool on) { g_route_on = on; }
+        ~RouteGuard() { g_route_on = false; }
+    } route_guard(g_top_items > 0 && n > 4096 && (o.flags & SNTRUP_OPT_RING_STREAMS) &&
+                  !(o.flags & SNTRUP_OPT_SERIAL) && !stream_capturing(s0));
     const bool prio = (o.flags & SNTRUP_OPT_LANE_PRIORITY) != 0;
     const int l0 = prio ? 0 : 1;           // first lane on an internal stream (forked from s0)
     for (int li = 0; li < nl; li++) {
@@ -1294,6 +1362,7 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
             if ((rc = launch_joint_roots<PS>(j3.roots(), jq.roots(), s))) return rc;
         }
         if ((rc = j3.down(s3, &n_r3))) return rc;
+        if ((rc = route_flush(s3))) return rc;
         if (utrick) CK(cudaStreamWaitEvent(s3, ax->done, 0));    // repair may rewrite u rows
         RepairArgs ra{};
         ra.seed = seed; ra.first = first; ra.n = m; ra.B = B; ra.root_ok = L.ok3;
@@ -1338,6 +1407,7 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
         const bool grouped = host_out && utrick && nroots >= nsub;
         const int SG = tp.L < 5 ? tp.L : 5;
         if ((rc = jq.down(s, &n_rq, grouped ? SG + 1 : (utrick ? 2 : 1)))) return rc;
+        if ((rc = route_flush(s))) return rc;
         if (utrick) n_rq += m;                                     // the u products replace level 1
         n_inv += 2 * tp.cnt[tp.L];
         for (int j = 0; j < nsub; j++) {
@@ -1345,6 +1415,7 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
             if (grouped) {
                 const long long ra = nroots * j / nsub, rb = nroots * (j + 1) / nsub;
                 if ((rc = jq.down_group(s, &n_rq, SG, 2, ra, rb))) return rc;
+                if ((rc = route_flush(s))) return rc;
                 r0 = (uint64_t)ra << tp.L;
                 r1 = (uint64_t)rb << tp.L;
                 if (r1 > m) r1 = m;
@@ -1389,6 +1460,7 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
                     if ((rc = launch_mul<PS, PS::Q>(a, s, 1, 2))) return rc;   // g small, fbar big
                 }
             }
+            if ((rc = route_flush(s))) return rc;
             {
                 EncArgs ea{};
                 ea.n = rows; ea.h = Hc + r0 * PS::P8; ea.pk = pkc + r0 * pkb; ea.t = tb->enc;
@@ -1405,6 +1477,7 @@ int keygen_impl(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out,
         }
         n_rq += m;
         if (host_out) CK(cudaEventRecord(cs->copy[buf], cs->s));
+        if ((rc = route_flush(s)) || (rc = route_flush(s3))) return rc;
         }
     for (int li = l0; li < nl; li++) {     // join the lanes into the caller's stream
         CK(cudaEventRecord(lj->end[li], lanes[li].s));

@@ -20,6 +20,8 @@ R = S.OPT_RING_STREAMS
 ST, L4 = S.OPT_STAGGER, S.OPT_LANES4
 cfgs = [(1024, 32768, R), (1024, 32768, R | ST), (1024, 16384, R | ST | L4), (1024, 16384, ST | L4),
         (1024, 24576, R | ST), (1024, 16384, R | L4)]
+if len(sys.argv) > 1:      # B:chunk:flags ...
+    cfgs = [tuple(int(x) for x in a.split(":")) for a in sys.argv[1:]]
 res = {c: [] for c in cfgs}
 for rnd in range(6):
     for c in cfgs:

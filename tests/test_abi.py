@@ -93,6 +93,11 @@ def test_root_impl_knob_without_gpu(lib):
     with pytest.raises(S.SntrupError):
         S.set_root_impl(3)
     S.set_root_impl(S.ROOT_AUTO)
+    # sntrup_set_sched: tree-top routing threshold and items-per-CTA cap, both >= 0
+    assert S._lib.sntrup_set_sched(1024, 4) == S.SNTRUP_OK
+    assert S._lib.sntrup_set_sched(-1, 0) == S.SNTRUP_E_ARG
+    assert S._lib.sntrup_set_sched(0, -2) == S.SNTRUP_E_ARG
+    S.set_sched(0, 0)
 
 
 def test_graph_flag_value():

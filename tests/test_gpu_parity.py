@@ -256,6 +256,34 @@ def test_host_output_grouped_tail(O, B, chunk, flags):
     assert np.array_equal(pk.numpy()[idx], r["pk"]) and np.array_equal(sk.numpy()[idx], r["sk"])
 
 
+@pytest.mark.parametrize("top,cap,flags", [(1024, 0, S.OPT_RING_STREAMS), (1024, 4, S.OPT_RING_STREAMS),
+                                           (256, 8, S.OPT_RING_STREAMS | S.OPT_STAGGER),
+                                           (0, 16, S.OPT_RING_STREAMS),
+                                           (1 << 20, 2, S.OPT_RING_STREAMS | S.OPT_LANES4)])
+def test_tree_top_scheduling_knob(O, top, cap, flags):
+    # sntrup_set_sched: tree tops and roots on high-priority companion streams, ring-product CTAs
+    # retiring after `cap` items -- a scheduling change only: byte-identical to the default call
+    # (host outputs too), and to the oracle on a sample; (1 << 20: every product launch routed)
+    n = 40000
+    P = S.params(761)
+    ref = S.batch_keygen(761, n, 29, batch_size=512, chunk_keys=16384, flags=flags)
+    torch.cuda.synchronize()
+    S.set_sched(top, cap)
+    try:
+        res = S.batch_keygen(761, n, 29, batch_size=512, chunk_keys=16384, flags=flags)
+        pk = torch.empty((n, P["pk_bytes"]), dtype=torch.uint8).pin_memory()
+        sk = torch.empty((n, P["sk_bytes"]), dtype=torch.uint8).pin_memory()
+        S.batch_keygen(761, n, 29, batch_size=512, chunk_keys=16384, pk_out=pk, sk_out=sk,
+                       flags=flags | S.OPT_HOST_OUTPUT)
+        torch.cuda.synchronize()
+    finally:
+        S.set_sched(0, 0)
+    assert torch.equal(res["pk"], ref["pk"]) and torch.equal(res["sk"], ref["sk"])
+    assert torch.equal(pk, ref["pk"].cpu()) and torch.equal(sk, ref["sk"].cpu())
+    idx = np.unique(np.concatenate([np.arange(0, n, 211), np.arange(n - 8, n), np.arange(16380, 16390)]))
+    check_keys(O, 761, 29, res, idx)
+
+
 def test_cfg2_full_size_sampled(O):
     # BASELINE configs[1]: 65,536 keys, seed 2, in the launch configuration bench.py times;
     # compared on a sample the oracle computes one by one: first and last trees, every 97th key.
