@@ -392,7 +392,8 @@ struct TcParts {
     static constexpr int CAPB = NH == 2 && NPR == 2 ? 5 : 6;  // register cap: 65536 / (128 CAPB) per thread
     static constexpr int MINB = NH == 1 ? G::MINB : (BY_SMEM < CAPB ? BY_SMEM : CAPB);
     static_assert(4 * AROWS4 * 16 <= A_BYTES, "A part too short");
-    static_assert(4 * (8 * KH * (NH - 1) + AROWS4 + 5) <= G::HA_LEN + 64, "hA reads");
+    // (the build skips window rows past the whole operand's AROWS4 groups, so its hA reads stay
+    // inside HA_LEN also when NKS is not a multiple of NH)
 };
 
 template <class PS, int M, int LA, int LB, int NPR, int MM = 128, bool XOPS = false, int NT = 128, int ST = 1, int NH = 1>
@@ -582,6 +583,7 @@ tc_mul_kernel(MulArgs a) {
                 const int m = tid + NT * kw;
                 if (m >= H::AROWS4) break;
                 const int mg = m + 8 * H::KH * h;               // window rows 4 mg .. of the whole operand
+                if (NH > 1 && mg >= G::AROWS4) break;           // last part of an odd NKS: rows no MMA reads
                 SNTRUP_CHECK(4 * (mg + 5) <= G::HA_LEN && 64 * (m + 1) <= H::A_BYTES);
                 const uint32_t *src = reinterpret_cast<const uint32_t *>(sHA + l * G::HA_LEN) + mg;
                 uint32_t wd[5];
