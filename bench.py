@@ -506,23 +506,37 @@ def main():
     sk_h2 = [sk_h, torch.empty_like(sk_h).pin_memory()]
     evs = [S.Event(), S.Event()]
     E2E_FLAGS = S.OPT_RING_STREAMS
+    serve_stream = torch.cuda.Stream()
 
-    def serve(steps, fl=E2E_FLAGS, chunk=CHUNK):
+    def serve(steps, fl=E2E_FLAGS, chunk=CHUNK, graph=True):
+        # graph=True: each call replays the keygen as one CUDA graph on a side stream and copies
+        # the whole call's pk/sk afterwards (SNTRUP_OPT_GRAPH | SNTRUP_OPT_HOST_OUTPUT); while the
+        # previous call's bytes cross PCIe, ~90 separately enqueued launches each start later
+        # (the plain asynchronous call, graph=False: reported beside it)
         for k in range(steps):
             S.batch_keygen(PARAM, n, SEED, first_key_index=first, batch_size=B, pk_out=pk_h2[k % 2],
-                           sk_out=sk_h2[k % 2], flags=S.OPT_HOST_OUTPUT | S.OPT_ASYNC | fl,
-                           chunk_keys=chunk, done_event=evs[k % 2])
+                           sk_out=sk_h2[k % 2], chunk_keys=chunk, done_event=evs[k % 2],
+                           flags=S.OPT_HOST_OUTPUT | S.OPT_ASYNC | fl | (S.OPT_GRAPH if graph else 0),
+                           stream=serve_stream if graph else None)
             if k >= 1:
                 evs[(k - 1) % 2].synchronize()
                 _ = int(pk_h2[(k - 1) % 2][0, 0]) + int(sk_h2[(k - 1) % 2][0, 0])
         evs[(steps - 1) % 2].synchronize()
 
     serve_steps = max(20, args.steps)
-    serve(2)
-    barrier()
-    t0 = time.perf_counter()
-    serve(serve_steps)
-    e2e_value = world * n * serve_steps / (time.perf_counter() - t0)
+    e2e_by_mode = {}
+    for graph in (False, True):
+        serve(3, graph=graph)
+        barrier()
+        t0 = time.perf_counter()
+        serve(serve_steps, graph=graph)
+        dt = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([dt], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        e2e_by_mode[graph] = world * n * serve_steps / dt
+    e2e_value = e2e_by_mode[True]
     # context: one synchronous host-output call per step (copies overlap only within the call)
     def step_host_sync():
         S.batch_keygen(PARAM, n, SEED, first_key_index=first, batch_size=B, pk_out=pk_h, sk_out=sk_h,
@@ -637,10 +651,13 @@ def main():
             "clocks": clocks,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": world * n * (P["pk_bytes"] + P["sk_bytes"]),
-                    "config": "key-serving loop: asynchronous host-output calls (chunk %d, ring streams) "
+                    "config": "key-serving loop: asynchronous host-output calls (chunk %d, ring streams), "
+                              "each a CUDA-graph replay of the keygen on a side stream followed by the "
+                              "D2H copies of its pk/sk (SNTRUP_OPT_GRAPH | SNTRUP_OPT_HOST_OUTPUT), "
                               "into two alternating pinned buffer sets; the host waits for each step's "
                               "completion event and reads its bytes; wall clock over %d steps incl. the "
                               "final drain" % (CHUNK, serve_steps),
+                    "plain_async_calls_no_graph": e2e_by_mode[False],
                     "one_synchronous_call_per_step": e2e_sync,
                     "d2h_gbs_measured": d2h_gbs,
                     "d2h_ceiling_keys_per_s": world * d2h_gbs * 1e9 / (P["pk_bytes"] + P["sk_bytes"]),

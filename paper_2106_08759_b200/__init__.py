@@ -237,7 +237,7 @@ class Event:
         return rc == 0
 
     def __del__(self):
-        if getattr(self, "handle", None):
+        if getattr(self, "handle", None) and _lib is not None:     # (_lib is None at interpreter exit)
             _lib.sntrup_event_destroy(ctypes.c_void_p(self.handle))
             self.handle = None
 

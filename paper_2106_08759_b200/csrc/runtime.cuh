@@ -1128,6 +1128,9 @@ KeygenShape keygen_shape(uint64_t n, int B, uint32_t flags, uint64_t chunk_keys,
     k.ws_need = (size_t)k.nl * per_lane;
     k.stage_need = (flags & SNTRUP_OPT_HOST_OUTPUT)
                        ? (size_t)k.nbuf * (align256(chunk * k.pkb) + align256(chunk * k.skb)) : 0;
+    // graph replay with host outputs: two whole-call device output sets (keygen_graph_host)
+    if ((flags & SNTRUP_OPT_HOST_OUTPUT) && (flags & SNTRUP_OPT_GRAPH))
+        k.stage_need = 2 * (align256(n * k.pkb) + align256(n * k.skb));
     return k;
 }
 
@@ -1595,9 +1598,13 @@ inline int keygen_finish(const sntrup_keygen_opts &o, const std::vector<int *> &
 }
 
 template <class PS>
+int keygen_graph_host(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out, const sntrup_keygen_opts &o);
+
+template <class PS>
 int keygen_graph(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out, const sntrup_keygen_opts &o) {
+    if (o.flags & SNTRUP_OPT_HOST_OUTPUT) return keygen_graph_host<PS>(n, seed, pk_out, sk_out, o);
     // device outputs on a non-default stream; no per-call host state (stats, host outputs)
-    if ((o.flags & (SNTRUP_OPT_HOST_OUTPUT | SNTRUP_OPT_SERIAL)) || o.stats_out || o.done_event || !o.stream)
+    if ((o.flags & SNTRUP_OPT_SERIAL) || o.stats_out || o.done_event || !o.stream)
         return SNTRUP_E_ARG;
     int dev;
     CK(cudaGetDevice(&dev));
@@ -1706,6 +1713,57 @@ int keygen_graph(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out, co
     g_launches.fetch_add(G.kernels, std::memory_order_relaxed);
     g_async_err[std::make_pair(dev, (uintptr_t)s0)] = G.errs;
     return keygen_finish(o, G.errs, s0);
+}
+
+// SNTRUP_OPT_GRAPH | SNTRUP_OPT_HOST_OUTPUT | SNTRUP_OPT_ASYNC with a done event (the key-serving
+// loop): the call is the graph replay of the device-output keygen into one of two whole-call
+// output sets in device memory, followed by that set's two D2H copies on a copy stream, which
+// then records the caller's event.  Why: while the previous call's 100 MB of pk/sk cross PCIe,
+// every separately enqueued launch of this call starts later (the GPU fetches its commands over
+// the same link: 2.55 -> 2.80 ms per 65,536-key call, scripts/serve_probe3.py); a graph launch is
+// one submission and keeps 2.58 ms.  The copies of call k overlap the compute of call k+1 (two
+// sets), not the call's own tail -- this mode is for back-to-back asynchronous calls.
+struct GraphHost { cudaStream_t cs = nullptr; cudaEvent_t ready[2] = {}, copied[2] = {}; unsigned calls = 0; };
+inline std::map<std::pair<int, uintptr_t>, GraphHost> g_graph_host;
+
+template <class PS>
+int keygen_graph_host(uint64_t n, uint64_t seed, uint8_t *pk_out, uint8_t *sk_out, const sntrup_keygen_opts &o) {
+    if (!(o.flags & SNTRUP_OPT_ASYNC) || (o.flags & SNTRUP_OPT_SERIAL) || !o.done_event || o.stats_out || !o.stream)
+        return SNTRUP_E_ARG;
+    int dev;
+    CK(cudaGetDevice(&dev));
+    DevTables *tb;
+    int rc = build_tables(dev, PS::P, PS::WT, &tb);
+    if (rc) return rc;
+    const size_t pkb = tb->enc.pk_bytes, skb = 2 * PS::SKH;
+    const size_t set = align256(n * pkb) + align256(n * skb);
+    const cudaStream_t s0 = (cudaStream_t)o.stream;
+    GraphHost &gh = g_graph_host[std::make_pair(dev, (uintptr_t)s0)];
+    if (!gh.cs) {
+        if (make_stream(&gh.cs, -1)) return SNTRUP_E_CUDA;
+        g_copy_streams.push_back(gh.cs);
+        for (int i = 0; i < 2; i++) {
+            CK(cudaEventCreateWithFlags(&gh.ready[i], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&gh.copied[i], cudaEventDisableTiming));
+        }
+    }
+    char *base = nullptr;
+    const uint64_t layout = ((uint64_t)PS::P << 48) ^ (n << 8) ^ 0xF;       // (the lanes' layouts end in nbuf, nl)
+    if ((rc = staging_reserve(2 * set, layout, s0, &base))) return rc;
+    const unsigned par = gh.calls++ & 1u;
+    uint8_t *dpk = (uint8_t *)base + par * set, *dsk = dpk + align256(n * pkb);
+    CK(cudaStreamWaitEvent(s0, gh.copied[par], 0));        // this set's previous copies (two calls ago)
+    sntrup_keygen_opts od = o;
+    od.flags = o.flags & ~SNTRUP_OPT_HOST_OUTPUT;
+    od.done_event = nullptr;
+    if ((rc = keygen_graph<PS>(n, seed, dpk, dsk, od))) return rc;
+    CK(cudaEventRecord(gh.ready[par], s0));
+    CK(cudaStreamWaitEvent(gh.cs, gh.ready[par], 0));
+    CK(cudaMemcpyAsync(sk_out, dsk, n * skb, cudaMemcpyDeviceToHost, gh.cs));
+    CK(cudaMemcpyAsync(pk_out, dpk, n * pkb, cudaMemcpyDeviceToHost, gh.cs));
+    CK(cudaEventRecord(gh.copied[par], gh.cs));
+    CK(cudaEventRecord((cudaEvent_t)o.done_event, gh.cs));
+    return SNTRUP_OK;
 }
 
 // ------------------------------------------------------------------------------ small kernels

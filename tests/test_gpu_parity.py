@@ -171,13 +171,63 @@ def test_attempts_only_output(O):
     assert int(res["attempts"].sum()) > 400      # 653 rejects ~3.7% of the draws
 
 
-def test_graph_mode_rejects_host_outputs():
+def test_graph_mode_rejects_synchronous_host_outputs():
+    # graph replay with host outputs is the asynchronous serving mode only: without OPT_ASYNC or a
+    # done event (or on the default stream) the call is refused
     P = S.params(761)
     s = torch.cuda.Stream()
     pk = torch.empty((32, P["pk_bytes"]), dtype=torch.uint8).pin_memory()
     sk = torch.empty((32, P["sk_bytes"]), dtype=torch.uint8).pin_memory()
     with pytest.raises((S.SntrupError, ValueError)):
         S.batch_keygen(761, 32, 1, pk_out=pk, sk_out=sk, flags=S.OPT_GRAPH | S.OPT_HOST_OUTPUT, stream=s)
+    with pytest.raises((S.SntrupError, ValueError)):
+        S.batch_keygen(761, 32, 1, pk_out=pk, sk_out=sk, stream=s,
+                       flags=S.OPT_GRAPH | S.OPT_HOST_OUTPUT | S.OPT_ASYNC)          # no done_event
+    with pytest.raises((S.SntrupError, ValueError)):
+        S.batch_keygen(761, 32, 1, pk_out=pk, sk_out=sk, done_event=S.Event(),
+                       flags=S.OPT_GRAPH | S.OPT_HOST_OUTPUT | S.OPT_ASYNC)          # default stream
+
+
+@pytest.mark.parametrize("n,B,chunk", [(600, 16, 128), (40000, 512, 16384)])
+def test_graph_host_output_serving_loop(O, n, B, chunk):
+    # SNTRUP_OPT_GRAPH | SNTRUP_OPT_HOST_OUTPUT | SNTRUP_OPT_ASYNC: graph replay into two device
+    # output sets, D2H copies on a copy stream, done event after the last byte.  Back-to-back
+    # calls with different seeds / first indices into two alternating pinned buffer sets (the
+    # serving loop of bench.py's e2e): each call's bytes equal the plain device-output call's, and
+    # the oracle's on a sample; a plain host-output call in between (other staging layout) and a
+    # workspace release do not disturb it.
+    P = S.params(761)
+    s = torch.cuda.Stream()
+    fl = S.OPT_RING_STREAMS | S.OPT_GRAPH | S.OPT_HOST_OUTPUT | S.OPT_ASYNC
+    pk = [torch.empty((n, P["pk_bytes"]), dtype=torch.uint8).pin_memory() for _ in range(2)]
+    sk = [torch.empty((n, P["sk_bytes"]), dtype=torch.uint8).pin_memory() for _ in range(2)]
+    evs = [S.Event(), S.Event()]
+    calls = [(31, 0), (32, 5), (31, 0), (33, n), (34, 7), (31, 0)]
+    got = []
+    for k, (seed, first) in enumerate(calls):
+        if k >= 2:
+            evs[k % 2].synchronize()
+            got.append((pk[k % 2].clone(), sk[k % 2].clone()))
+        if k == 3:                                  # a plain host-output call on the same stream
+            S.batch_keygen(761, 64, 9, batch_size=16, stream=s, flags=S.OPT_HOST_OUTPUT)
+        if k == 4:
+            evs[(k - 1) % 2].synchronize()
+            S.release_stream_workspace(s)           # drops the graphs and the staging
+        S.batch_keygen(761, n, seed, first_key_index=first, batch_size=B, chunk_keys=chunk, pk_out=pk[k % 2],
+                       sk_out=sk[k % 2], flags=fl, stream=s, done_event=evs[k % 2])
+    for k in (len(calls) - 2, len(calls) - 1):
+        evs[k % 2].synchronize()
+        got.append((pk[k % 2].clone(), sk[k % 2].clone()))
+    S.async_error(s)                                # raises if a lane hit the g retry bound
+    idx = np.unique(np.concatenate([np.arange(0, n, 97), np.arange(n - 4, n)]))
+    for (seed, first), (gpk, gsk) in zip(calls, got):
+        ref = S.batch_keygen(761, n, seed, first_key_index=first, batch_size=B, chunk_keys=chunk,
+                             flags=S.OPT_RING_STREAMS)
+        torch.cuda.synchronize()
+        assert torch.equal(gpk, ref["pk"].cpu()) and torch.equal(gsk, ref["sk"].cpu()), (seed, first)
+        r = oracle_keys(O, 761, seed, first + idx)
+        assert np.array_equal(gpk.numpy()[idx], r["pk"]) and np.array_equal(gsk.numpy()[idx], r["sk"])
+    S.release_stream_workspace(s)
 
 
 def test_chunking_and_first_index(O):
