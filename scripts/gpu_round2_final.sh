@@ -22,8 +22,10 @@ if [ "${PROFILE:-1}" = "1" ]; then
     echo "$k rc=$?"
     ncu -i /tmp/prof_${T}_$k.ncu-rep --page raw --csv > gpurun_out/${T}_pipes_$k.csv
   done
-  # one full capture of the dominant kernel (int8 ring products): the largest launch of the step
-  timeout 900 ncu -f --set full --clock-control none --import-source on -k regex:tc_mul_kernel --launch-skip 6 -c 1 \
+  # one full capture (source page) of the dominant kernel's largest launch: the int8 two-product
+  # kernel's h launch (16,384 work items; the 10th launch of that kernel in a chunk)
+  timeout 900 ncu -f --set full --clock-control none --import-source on --kernel-name-base demangled \
+      -k 'regex:tc_mul_kernel.*int.1, .int.2>' --launch-skip 9 -c 1 \
       -o gpurun_out/${T}_full_tc_mul python bench.py --steps 1 --warmup 3 --no-extras > gpurun_out/${T}_ncu_full.log 2>&1
   echo "full rc=$?"
   ncu -i gpurun_out/${T}_full_tc_mul.ncu-rep --page raw --csv > gpurun_out/${T}_full_tc_mul_raw.csv 2>&1
