@@ -472,6 +472,13 @@ def main():
     # load; the timed region alone can be shorter than nvidia-smi's first sample)
     clk = ClockSampler(local)
     clk.start()
+    # settle phase before the W warm-up steps: the first ~30 steps of a fresh process run 1-4%
+    # slower (SM clocks ramping from idle, first touches of the workspace; scripts/gpu_warm.sh,
+    # profiles/r02s4/warm_ab.log) -- a serving process is past this; disclosed in config.settle
+    SETTLE_STEPS = 40
+    for _ in range(SETTLE_STEPS):
+        step()
+    torch.cuda.synchronize()
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
@@ -646,6 +653,7 @@ def main():
                        "keys_per_gpu": n, "batch_size": B, "chunk_keys": CHUNK, "ring_streams": RINGS,
                        "lanes": LANES, "param_set": PARAM,
                        "l2": "flushed between timed steps (256 MiB write); working set > L2",
+                       "settle": "%d untimed steps before the W warm-up steps (clocks from idle, first touches)" % SETTLE_STEPS,
                        "parallelism": "key ranges per GPU (no collective)"},
             "gpu_launches": launches,
             "clocks": clocks,
