@@ -85,6 +85,40 @@ def test_cfg1_every_key_bench_config(O):
     check_attempts(d, 761, 2, BENCH_KEYGEN, res["pk"])
 
 
+def test_cfg1_every_key_e2e_serving_loop(O):
+    # bench.py's e2e configuration: asynchronous host-output calls, each a CUDA-graph replay on a
+    # side stream (SNTRUP_OPT_GRAPH | SNTRUP_OPT_HOST_OUTPUT | SNTRUP_OPT_ASYNC, 32,768-key chunks,
+    # ring streams) into two alternating pinned buffer sets.  Every key of three back-to-back
+    # steps (the first builds the graph, the others replay it into either device output set)
+    # against the oracle's digests.
+    d = load("cfg1_761")
+    n, G = d["n_keys"], d["group"]
+    P = S.params(761)
+    s = torch.cuda.Stream()
+    pk = [torch.zeros((n, P["pk_bytes"]), dtype=torch.uint8).pin_memory() for _ in range(2)]
+    sk = [torch.zeros((n, P["sk_bytes"]), dtype=torch.uint8).pin_memory() for _ in range(2)]
+    evs = [S.Event(), S.Event()]
+    fl = S.OPT_HOST_OUTPUT | S.OPT_ASYNC | S.OPT_RING_STREAMS | S.OPT_GRAPH
+
+    def check(k):
+        evs[k % 2].synchronize()
+        pkn, skn = pk[k % 2].numpy(), sk[k % 2].numpy()
+        for g, e in enumerate(d["groups"]):
+            sl = slice(g * G, (g + 1) * G)
+            assert hashlib.sha256(pkn[sl].tobytes() + skn[sl].tobytes()).hexdigest() == e["kv"], (k, g)
+        pk[k % 2].zero_()
+        sk[k % 2].zero_()
+
+    for k in range(4):
+        S.batch_keygen(761, n, d["seed"], batch_size=1024, chunk_keys=32768, pk_out=pk[k % 2], sk_out=sk[k % 2],
+                       flags=fl, stream=s, done_event=evs[k % 2])
+        if k >= 1:
+            check(k - 1)
+    check(3)
+    S.async_error(s)
+    S.release_stream_workspace(s)
+
+
 @pytest.mark.parametrize("B", [32, 128, 512, 2048])
 def test_cfg1_every_key_batch_size_sweep(O, B):
     # configs[1]'s Montgomery batch-size sweep: every key at every B (C0: the tree shape cannot
