@@ -205,7 +205,10 @@ __device__ __forceinline__ void digits_rev8(const int (&vals)[8], uint32_t (&dw)
 // shared memory at all, so the shared-memory traffic per item is only the B operand and staging.
 // (an explicit minimum of 8 CTAs per SM, i.e. <= 64 registers, measured slower: 320 -> 310 M R/3
 // products/s; note __launch_bounds__(128, 1) is NOT the same as (128): it let ptxas raise the
-// R/3 kernels to 80 / 95 registers, 6 / 5 CTAs per SM, and the step lost 5%)
+// R/3 kernels to 80 / 95 registers, 6 / 5 CTAs per SM, and the step lost 5%; session 4: the
+// two-product kernel alone at (128, 8) -- 64 registers without spills instead of 72, 8 CTAs per SM
+// instead of 7 -- made the keygen step 0.4% slower in three alternating rounds,
+// profiles/r02s4/libab_tc4minb8.log)
 template <class PS, int M, int LB, int NPR, bool XOPS = false, int TA = 0, bool RING = false>
 __global__ void __launch_bounds__(128) tc4_mul_kernel(MulArgs a) {
     using G = Tc4Geom<PS, LB, NPR, TA>;
