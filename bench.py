@@ -505,7 +505,7 @@ def main():
     # configuration: the key-serving loop -- asynchronous host-output calls into two alternating
     # pinned buffer sets; the host waits for step k-1's completion event (all of its pk/sk bytes in
     # host memory) and reads its first key before issuing step k+1, so every step's D2H copy is in
-    # the timed region while it overlaps the next step's compute; wall clock over max(20, K) steps
+    # the timed region while it overlaps the next step's compute; wall clock over max(50, K) steps
     # including the final drain
     pk_h = torch.empty((n, P["pk_bytes"]), dtype=torch.uint8).pin_memory()
     sk_h = torch.empty((n, P["sk_bytes"]), dtype=torch.uint8).pin_memory()
@@ -530,7 +530,9 @@ def main():
                 _ = int(pk_h2[(k - 1) % 2][0, 0]) + int(sk_h2[(k - 1) % 2][0, 0])
         evs[(steps - 1) % 2].synchronize()
 
-    serve_steps = max(20, args.steps)
+    # (the last step's 1.8 ms of D2H copies cannot overlap a next step: over 50 steps that drain is
+    # 1.4% of the wall clock, over 20 it was 3.5%)
+    serve_steps = max(50, args.steps)
     e2e_by_mode = {}
     for graph in (False, True):
         serve(3, graph=graph)
