@@ -457,7 +457,9 @@ def main():
             fn()
             e1.record(stream)
         barrier()
-        ms = sum(e0.elapsed_time(e1) for e0, e1 in ev)
+        per_step = [e0.elapsed_time(e1) for e0, e1 in ev]
+        timed.last = per_step                       # this rank's per-step device times
+        ms = sum(per_step)
         if world > 1:
             t = torch.tensor([ms], device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -487,6 +489,7 @@ def main():
     launches0 = S.kernel_launch_count()
     ms = timed(step, args.steps)
     launches = S.kernel_launch_count() - launches0
+    step_ms = sorted(timed.last)
     value = world * n * args.steps / (ms / 1e3)
 
     # ---- per-kernel times: the same step SERIALISED (SNTRUP_OPT_SERIAL: one lane, every kernel
@@ -676,6 +679,7 @@ def main():
             "int_pipe": {"peaks_lanes_per_clk_sm": {k: v["lanes_per_clk_sm"] for k, v in int_peaks.items()},
                          "source": "sntrup_measure_int_peak microkernels, this run",
                          "kernels": pipes},
+            "step_ms_min_median_max": [step_ms[0], step_ms[len(step_ms) // 2], step_ms[-1]],
             "serial_ms_per_step": ms_serial / args.steps,
             "serial_share_by_class": share,
             "serial_ms_per_step_by_class": {k: v["ms"] / args.steps for k, v in prof.items() if v["launches"]},
