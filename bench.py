@@ -420,6 +420,8 @@ def main():
     # rendezvous variables are present and BENCH_FORCE_DIST is set (a 1-GPU check of the N > 1 path)
     use_dist = world > 1 or (os.environ.get("BENCH_FORCE_DIST") == "1" and "MASTER_ADDR" in os.environ)
     if use_dist:
+        # (the GPU boxes export NCCL_DEBUG=VERSION: NCCL's one-line version banner precedes the JSON
+        # line on stdout; left as the launcher set it)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2106_08759_b200 as S
 
